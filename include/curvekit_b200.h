@@ -1,0 +1,101 @@
+/* C-ABI of the B200 multi-modular resultant engine (libcurvekit_b200.so).
+ *
+ * The reference (arXiv 1201.1548 artifact, package `curvekit`) is pure
+ * Python; its hot path is pkg/src/curvekit/modpoly.py.  Each entry point below
+ * replaces one reference function or loop; the Python drop-in
+ * (paper_1201_1548_b200/modpoly.py) binds them with ctypes, keeping the
+ * reference's names, argument meaning and exceptions.
+ *
+ * Conventions: plain pointers and sizes; all host buffers are caller-owned and
+ * never retained after return; device memory belongs to one process-global
+ * context (ckb_init); calls are serialised by a mutex (ctypes releases the
+ * GIL).  Integers cross the boundary as little-endian two's-complement 32-bit
+ * limbs.  Primes must be odd with 3 <= p < 2^31 and pairwise distinct.
+ * Return: 0 ok, > 0 recoverable (CKB_STATUS_*), < 0 failure (ckb_last_error()).
+ */
+#ifndef CURVEKIT_B200_H
+#define CURVEKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKB_ABI_VERSION 1
+#define CKB_STATUS_REPLAN 1 /* a prime had no admissible evaluation points: re-plan without it */
+
+int ckb_abi_version(void);
+const char* ckb_last_error(void);
+int ckb_init(int device);
+int ckb_shutdown(void);
+unsigned long long ckb_launch_count(void);
+
+/* res_y(f, g) in Z[x] — replaces curvekit.modpoly.biv_resultant
+ * (pkg/src/curvekit/modpoly.py:348-394) after its degenerate branches.
+ *   limbs  [C][L]  f's dense grid f[j][i] (coefficient of x^i y^j, j <= m,
+ *                  i <= dfx) followed by g's grid (j <= n, i <= dgx);
+ *                  C = (m+1)(dfx+1) + (n+1)(dgx+1)
+ *   degs   [m+n+2] trimmed x-degree of each y-coefficient (-1 = zero)
+ *   primes/gens [K] primes and a generator of large order for each
+ *   N      evaluation points per prime (N > deg_x res)
+ *   out    [N][LW] coefficients of res (low degree first), two's complement;
+ *          requires prod(primes) > 2 * (coefficient bound) and 2^(32 LW) > prod
+ *   status bit 0: some prime had no admissible point set (CKB_STATUS_REPLAN)
+ *   device_ms (optional) CUDA-event time of the device work incl. copies */
+int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
+                      const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, uint32_t* out,
+                      uint32_t* status, float* device_ms);
+
+/* K1: residues of every coefficient mod every prime — replaces
+ * `[[c % p for c in cf] for cf in fc]` (modpoly.py:376-377).
+ *   limbs [C][L] -> out [K][C] */
+int ckb_reduce(const uint32_t* limbs, int C, int L, const uint32_t* primes, int K, uint32_t* out);
+
+/* Batch of univariate resultants mod p — replaces _zp_resultant / zp_resultant_uni
+ * (modpoly.py:132-161).  fa, gb [B][W] low-first residues (< p), da/db their
+ * trimmed degrees (-1 = zero polynomial -> result 0), pidx [B] index into
+ * primes [P].  W - 1 <= 64. */
+int ckb_uni_resultant_batch(const uint32_t* fa, const int32_t* da, const uint32_t* gb, const int32_t* db, int W,
+                            const uint32_t* primes, int P, const int32_t* pidx, int B, uint32_t* out);
+
+/* The planned evaluation points x_t = q^t (t < N) for each prime. */
+int ckb_interp_plan_points(const uint32_t* primes, const uint32_t* gens, int K, int N, uint32_t* xpts);
+
+/* Interpolation at the planned points — replaces _zp_interp (modpoly.py:164-185)
+ * on the pipeline's point set.  values [K][N] at x_t = q^t -> coeffs [K][N]. */
+int ckb_interp_geometric(const uint32_t* values, const uint32_t* primes, const uint32_t* gens, int K, int N,
+                         uint32_t* coeffs);
+
+/* Mixed-radix CRT + symmetric lift — replaces _CrtAccumulator.add/symmetric and
+ * crt_reconstruct (modpoly.py:264-300).  residues [K][N] -> out [N][LW]. */
+int ckb_crt_lift(const uint32_t* residues, int K, int N, const uint32_t* primes, int LW, uint32_t* out);
+
+/* Batch of monic gcds mod p — replaces _zp_gcd (modpoly.py:115-122), the
+ * per-prime step of int_gcd_uni (:307-341).  fa [B][Wf], gb [B][Wg] low-first
+ * residues with trimmed degrees da/db (-1 = zero); out [B][Wo] monic gcd,
+ * odeg [B] its degree (-1 if both inputs are zero). */
+int ckb_gcd_mod_batch(const uint32_t* fa, const int32_t* da, int Wf, const uint32_t* gb, const int32_t* db, int Wg,
+                      const uint32_t* primes, int P, const int32_t* pidx, int B, uint32_t* out, int Wo,
+                      int32_t* odeg);
+
+/* Interpolation at arbitrary distinct points — replaces _zp_interp /
+ * zp_interpolate (modpoly.py:164-189).  xs, vs [B][W] (points reduced mod p),
+ * ns [B] point counts (<= W <= 4096) -> out [B][W] coefficients (low first). */
+int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const uint32_t* primes, int P,
+                      const int32_t* pidx, int B, uint32_t* out);
+
+/* Device-pointer stages for the multi-GPU driver (one process per GPU).
+ * stream: a cudaStream_t or NULL for the context stream.
+ * modular_images: limbs/degs on device (h_degs: host copy) -> d_coeffs [K][N]
+ * residues of res's coefficients for this rank's primes. */
+int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
+                           int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* d_gens, int K, int N,
+                           uint32_t* d_coeffs, uint32_t* d_status, void* stream);
+int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, int LW, uint32_t* d_out,
+                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,43 @@
+"""B200-native multi-modular resultant / gcd engine (drop-in for curvekit.modpoly).
+
+Reference: arXiv 1201.1548 artifact ``curvekit`` (pure Python); hot path
+pkg/src/curvekit/modpoly.py.  See DESIGN.md.
+"""
+
+__version__ = "0.1.0"
+
+
+def install():
+    """Rebind the reference's hot-path names to the B200 implementations.
+
+    Rebinds ``curvekit.modpoly.{biv_resultant, int_gcd_uni, zp_resultant_uni,
+    zp_interpolate, zp_gcd_sylvester, crt_reconstruct}`` and the names
+    ``curvekit.bisolve`` bound at import (bisolve.py:26).  ``upoly`` and
+    ``bivpoly`` import ``int_gcd_uni`` lazily (upoly.py:258,372,538,569;
+    bivpoly.py:186,268), so they pick up the GPU gcd through the first rebinding.
+    Returns the previous bindings (pass them to ``uninstall``).
+    """
+    import importlib
+
+    from . import modpoly as ours
+    ref = importlib.import_module("curvekit.modpoly")
+    saved = {}
+    for name in ("biv_resultant", "int_gcd_uni", "zp_resultant_uni", "zp_interpolate",
+                 "zp_gcd_sylvester", "crt_reconstruct"):
+        saved[("curvekit.modpoly", name)] = getattr(ref, name)
+        setattr(ref, name, getattr(ours, name))
+    try:
+        bis = importlib.import_module("curvekit.bisolve")
+    except ImportError:  # bisolve needs mpmath
+        bis = None
+    if bis is not None:
+        for name in ("biv_resultant", "int_gcd_uni"):
+            saved[("curvekit.bisolve", name)] = getattr(bis, name)
+            setattr(bis, name, getattr(ours, name))
+    return saved
+
+
+def uninstall(saved):
+    import importlib
+    for (mod, name), fn in saved.items():
+        setattr(importlib.import_module(mod), name, fn)

@@ -1,0 +1,92 @@
+"""ctypes binding of libcurvekit_b200.so (the C-ABI in include/curvekit_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is usable, every entry point raises ``RuntimeError`` (loudly, by design).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcurvekit_b200.so")
+
+# every symbol include/curvekit_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "ckb_abi_version", "ckb_last_error", "ckb_init", "ckb_shutdown", "ckb_launch_count",
+    "ckb_biv_resultant", "ckb_reduce", "ckb_uni_resultant_batch", "ckb_interp_plan_points",
+    "ckb_interp_geometric", "ckb_crt_lift", "ckb_dev_modular_images", "ckb_dev_crt",
+    "ckb_interp_points", "ckb_gcd_mod_batch",
+)
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_U32P = ctypes.POINTER(ctypes.c_uint32)
+
+_lock = threading.Lock()
+_lib = None
+_ready = False
+
+
+class CkbError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load the library (no device work).  Raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise CkbError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                       "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    lib.ckb_last_error.restype = ctypes.c_char_p
+    lib.ckb_abi_version.restype = _I
+    lib.ckb_launch_count.restype = ctypes.c_ulonglong
+    for name in EXPORTS:
+        getattr(lib, name)  # raises AttributeError if not exported
+    _lib = lib
+    return lib
+
+
+def _device_index() -> int:
+    for var in ("CKB_DEVICE", "LOCAL_RANK"):
+        v = os.environ.get(var)
+        if v is not None and v != "":
+            return int(v)
+    return 0
+
+
+def lib():
+    """The initialised library (lazily binds a CUDA device)."""
+    global _ready
+    lb = load()
+    if not _ready:
+        with _lock:
+            if not _ready:
+                rc = lb.ckb_init(_device_index())
+                if rc != 0:
+                    raise CkbError("ckb_init failed: " + lb.ckb_last_error().decode())
+                _ready = True
+    return lb
+
+
+def check(rc: int, what: str) -> int:
+    if rc < 0:
+        raise CkbError(f"{what} failed: {_lib.ckb_last_error().decode()}")
+    return rc
+
+
+def ptr(a: np.ndarray):
+    """ctypes pointer to a C-contiguous numpy array."""
+    assert a.flags["C_CONTIGUOUS"], "array must be C-contiguous"
+    return a.ctypes.data_as(_P)
+
+
+def launch_count() -> int:
+    return int(lib().ckb_launch_count())

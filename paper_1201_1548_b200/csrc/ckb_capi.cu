@@ -1,0 +1,643 @@
+// C-ABI boundary of the B200 modular symbolic engine (declared in
+// include/curvekit_b200.h).  Plain pointers and sizes only; every host buffer
+// is caller-owned and never retained; device memory is owned by a
+// process-global context; calls are serialised by a mutex.  Return value:
+// 0 ok, > 0 recoverable (see CKB_STATUS_*), < 0 CUDA/usage failure with the
+// message in ckb_last_error().
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/curvekit_b200.h"
+#include "ckb_kernels.cuh"
+
+using namespace ckb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::string& msg, int code = -1) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(std::string(#call) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + \
+                  ":" + std::to_string(__LINE__));                                        \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+struct CrtEntry {
+  std::vector<uint32_t> primes;
+  int LW = 0;
+  Prime* d_primes = nullptr;
+  uint32_t* d_Wm = nullptr;
+  uint32_t* d_invm = nullptr;
+  uint32_t* d_Pl = nullptr;
+  uint64_t last_use = 0;
+};
+
+struct Ctx {
+  bool ready = false;
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::map<std::string, Buf> dev;
+  std::map<std::string, Buf> host;  // pinned staging
+  std::vector<CrtEntry> crt;
+  uint64_t tick = 0;
+  uint64_t launches = 0;
+};
+
+Ctx g;
+std::mutex g_mu;
+
+int dev_buf(const char* name, size_t bytes, void** out) {
+  Buf& b = g.dev[name];
+  if (b.n < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    CK(cudaMalloc(&b.p, want));
+    b.n = want;
+  }
+  *out = b.p;
+  return 0;
+}
+
+int host_buf(const char* name, size_t bytes, void** out) {
+  Buf& b = g.host[name];
+  if (b.n < bytes) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    CK(cudaMallocHost(&b.p, want));
+    b.n = want;
+  }
+  *out = b.p;
+  return 0;
+}
+
+template <typename T>
+int dbuf(const char* name, size_t count, T** out) {
+  void* p;
+  int rc = dev_buf(name, count * sizeof(T) + 16, &p);
+  *out = (T*)p;
+  return rc;
+}
+
+// ---- host arithmetic for the tables ----------------------------------------
+uint32_t h_inv32(uint32_t p) {
+  uint32_t x = p;
+  for (int i = 0; i < 5; ++i) x *= 2u - p * x;
+  return x;
+}
+uint32_t h_powmod(uint64_t a, uint64_t e, uint32_t p) {
+  uint64_t r = 1 % p;
+  a %= p;
+  while (e) {
+    if (e & 1) r = r * a % p;
+    a = a * a % p;
+    e >>= 1;
+  }
+  return (uint32_t)r;
+}
+Prime h_prime(uint32_t p) {
+  Prime P;
+  P.p = p;
+  P.pinv = h_inv32(p);
+  uint64_t r1 = (1ull << 32) % p;
+  P.r2 = (uint32_t)(r1 * r1 % p);
+  return P;
+}
+uint32_t h_mont(uint64_t x, uint32_t p) { return (uint32_t)(((x % p) << 32) % p); }
+
+int check_primes(const uint32_t* primes, int K) {
+  for (int i = 0; i < K; ++i) {
+    uint32_t p = primes[i];
+    if (p < 3 || !(p & 1u) || p >= 0x80000000u) return fail("prime out of range (odd, 3 <= p < 2^31): " + std::to_string(p), -2);
+  }
+  return 0;
+}
+
+int upload_primes(const uint32_t* primes, int K, Prime** d_out) {
+  Prime* hp;
+  void* hv;
+  int rc = host_buf("primes", sizeof(Prime) * K, &hv);
+  if (rc) return rc;
+  hp = (Prime*)hv;
+  for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
+  Prime* d;
+  if ((rc = dbuf("primes", K, &d))) return rc;
+  CK(cudaMemcpyAsync(d, hp, sizeof(Prime) * K, cudaMemcpyHostToDevice, g.stream));
+  *d_out = d;
+  return 0;
+}
+
+int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
+  for (auto& e : g.crt) {
+    if ((int)e.primes.size() == K && e.LW == LW && !memcmp(e.primes.data(), primes, 4 * (size_t)K)) {
+      e.last_use = ++g.tick;
+      *out = &e;
+      return 0;
+    }
+  }
+  if (g.crt.size() >= 4) {  // evict least recently used
+    size_t v = 0;
+    for (size_t i = 1; i < g.crt.size(); ++i)
+      if (g.crt[i].last_use < g.crt[v].last_use) v = i;
+    CrtEntry& e = g.crt[v];
+    cudaFree(e.d_primes);
+    cudaFree(e.d_Wm);
+    cudaFree(e.d_invm);
+    cudaFree(e.d_Pl);
+    g.crt.erase(g.crt.begin() + v);
+  }
+  CrtEntry e;
+  e.primes.assign(primes, primes + K);
+  e.LW = LW;
+  std::vector<Prime> hp(K);
+  std::vector<uint32_t> Wm((size_t)K * K, 0), invm(K), Pl((size_t)K * LW, 0);
+  for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
+  for (int i = 0; i < K; ++i) {
+    const uint32_t p = primes[i];
+    uint64_t m = 1 % p;
+    for (int j = 0; j < i; ++j) {
+      Wm[(size_t)j * K + i] = h_mont(m, p);
+      m = m * (primes[j] % p) % p;
+    }
+    if (m == 0) return fail("CRT primes are not pairwise distinct", -2);
+    invm[i] = h_mont(h_powmod(m, p - 2, p), p);
+  }
+  // limbs of M_j = prod_{l<j} p_l
+  std::vector<uint32_t> cur(LW + 1, 0);
+  cur[0] = 1;
+  for (int j = 0; j < K; ++j) {
+    memcpy(&Pl[(size_t)j * LW], cur.data(), 4 * (size_t)LW);
+    uint64_t carry = 0;
+    for (int l = 0; l < LW; ++l) {
+      uint64_t t = (uint64_t)cur[l] * primes[j] + carry;
+      cur[l] = (uint32_t)t;
+      carry = t >> 32;
+    }
+    if (carry) return fail("CRT output width too small for the prime product", -2);
+  }
+  CK(cudaMalloc(&e.d_primes, sizeof(Prime) * K));
+  CK(cudaMalloc(&e.d_Wm, 4 * (size_t)K * K));
+  CK(cudaMalloc(&e.d_invm, 4 * (size_t)K));
+  CK(cudaMalloc(&e.d_Pl, 4 * (size_t)K * LW));
+  CK(cudaMemcpy(e.d_primes, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e.d_Wm, Wm.data(), 4 * (size_t)K * K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e.d_invm, invm.data(), 4 * (size_t)K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e.d_Pl, Pl.data(), 4 * (size_t)K * LW, cudaMemcpyHostToDevice));
+  e.last_use = ++g.tick;
+  g.crt.push_back(e);
+  *out = &g.crt.back();
+  return 0;
+}
+
+int ensure_ready() {
+  if (!g.ready) return fail("ckb_init() has not been called", -3);
+  CK(cudaSetDevice(g.device));
+  return 0;
+}
+
+cudaStream_t pick_stream(void* s) { return s ? (cudaStream_t)s : g.stream; }
+
+// plan buffers for K primes x N points
+int plan_bufs(int K, int N, InterpPlan* pl) {
+  int rc = 0;
+  pl->K = K;
+  pl->N = N;
+  const size_t kn = (size_t)K * N, kn1 = (size_t)K * (N + 1);
+  if ((rc = dbuf("pl.xpts", kn, &pl->xpts))) return rc;
+  if ((rc = dbuf("pl.hC", 2 * kn, &pl->hC))) return rc;
+  if ((rc = dbuf("pl.z", kn, &pl->z))) return rc;
+  if ((rc = dbuf("pl.hCinv", kn, &pl->hCinv))) return rc;
+  if ((rc = dbuf("pl.Mt", kn1, &pl->Mt))) return rc;
+  if ((rc = dbuf("pl.Mtc", kn1, &pl->Mtc))) return rc;
+  if ((rc = dbuf("pl.cinv", kn, &pl->cinv))) return rc;
+  if ((rc = dbuf("pl.phi", kn1, &pl->phi))) return rc;
+  if ((rc = dbuf("pl.iphi", kn1, &pl->iphi))) return rc;
+  if ((rc = dbuf("pl.cval", (size_t)K, &pl->cval))) return rc;
+  return 0;
+}
+
+// the modular part of the pipeline on device buffers:
+// limbs -> residues -> plan -> images -> interpolated coefficients [K][N]
+int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
+                  int n, int dfx, int dgx, const Prime* d_primes, const uint32_t* d_gens, int K, int N,
+                  uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st) {
+  if (images_maxd(m, n) < 0) return fail("y-degree above 64 is not supported by the image kernel", -2);
+  uint32_t *d_red, *d_vals, *d_a, *d_ac, *d_S;
+  int rc;
+  if ((rc = dbuf("red", (size_t)K * C, &d_red))) return rc;
+  if ((rc = dbuf("vals", (size_t)K * N, &d_vals))) return rc;
+  if ((rc = dbuf("ia", (size_t)K * N, &d_a))) return rc;
+  if ((rc = dbuf("iac", (size_t)K * N, &d_ac))) return rc;
+  if ((rc = dbuf("iS", (size_t)K * N, &d_S))) return rc;
+  InterpPlan pl;
+  if ((rc = plan_bufs(K, N, &pl))) return rc;
+  launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
+  const int lcf_off = m * (dfx + 1), lcg_off = (m + 1) * (dfx + 1) + n * (dgx + 1);
+  launch_plan(d_primes, d_gens, K, N, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], pl, d_status, st);
+  ImageArgs a;
+  a.red = d_red;
+  a.degs = d_degs;
+  a.xpts = pl.xpts;
+  a.primes = d_primes;
+  a.C = C;
+  a.m = m;
+  a.n = n;
+  a.dfx = dfx;
+  a.dgx = dgx;
+  a.N = N;
+  a.K = K;
+  a.values = d_vals;
+  a.status = d_status;
+  launch_images(a, st);
+  launch_interp(pl, d_primes, d_vals, d_coeffs, d_a, d_ac, d_S, st);
+  g.launches += 6;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ckb_abi_version(void) { return CKB_ABI_VERSION; }
+
+const char* ckb_last_error(void) { return g_err.c_str(); }
+
+int ckb_init(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g.ready) {
+    if (device == g.device) return 0;
+    return fail("ckb_init: already initialised on another device", -3);
+  }
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail("ckb_init: no such CUDA device", -3);
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&g.ev0));
+  CK(cudaEventCreate(&g.ev1));
+  g.device = device;
+  g.ready = true;
+  return 0;
+}
+
+int ckb_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g.ready) return 0;
+  cudaSetDevice(g.device);
+  cudaStreamSynchronize(g.stream);
+  for (auto& kv : g.dev) cudaFree(kv.second.p);
+  for (auto& kv : g.host) cudaFreeHost(kv.second.p);
+  for (auto& e : g.crt) {
+    cudaFree(e.d_primes);
+    cudaFree(e.d_Wm);
+    cudaFree(e.d_invm);
+    cudaFree(e.d_Pl);
+  }
+  g.dev.clear();
+  g.host.clear();
+  g.crt.clear();
+  cudaEventDestroy(g.ev0);
+  cudaEventDestroy(g.ev1);
+  cudaStreamDestroy(g.stream);
+  g = Ctx();
+  return 0;
+}
+
+unsigned long long ckb_launch_count(void) { return g.launches; }
+
+int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
+                      const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, uint32_t* out,
+                      uint32_t* status, float* device_ms) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if (m < 1 || n < 1 || K < 1 || N < 1 || L < 1 || LW < 1) return fail("ckb_biv_resultant: bad sizes", -2);
+  if (C != (m + 1) * (dfx + 1) + (n + 1) * (dgx + 1)) return fail("ckb_biv_resultant: C mismatch", -2);
+  if ((rc = check_primes(primes, K))) return rc;
+  cudaStream_t st = g.stream;
+  // stage inputs in pinned memory, then one async copy each
+  const size_t nl = (size_t)C * L, nd = (size_t)(m + n + 2);
+  void *h_in, *h_out;
+  if ((rc = host_buf("in", 4 * nl + 2 * nd + 4 * (size_t)K + 64, &h_in))) return rc;
+  if ((rc = host_buf("out", 4 * (size_t)N * LW + 64, &h_out))) return rc;
+  uint8_t* hb = (uint8_t*)h_in;
+  memcpy(hb, limbs, 4 * nl);
+  memcpy(hb + 4 * nl, gens, 4 * (size_t)K);
+  memcpy(hb + 4 * nl + 4 * (size_t)K, degs, 2 * nd);
+  uint32_t *d_limbs, *d_gens, *d_coeffs, *d_out, *d_status;
+  int16_t* d_degs;
+  if ((rc = dbuf("limbs", nl, &d_limbs))) return rc;
+  if ((rc = dbuf("gens", (size_t)K, &d_gens))) return rc;
+  if ((rc = dbuf("degs", nd, &d_degs))) return rc;
+  if ((rc = dbuf("coeffs", (size_t)K * N, &d_coeffs))) return rc;
+  if ((rc = dbuf("out", (size_t)N * LW, &d_out))) return rc;
+  if ((rc = dbuf("status", 4, &d_status))) return rc;
+  CrtEntry* ce;
+  if ((rc = get_crt(primes, K, LW, &ce))) return rc;
+  CK(cudaEventRecord(g.ev0, st));
+  CK(cudaMemcpyAsync(d_limbs, hb, 4 * nl, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_gens, hb + 4 * nl, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_degs, hb + 4 * nl + 4 * (size_t)K, 2 * nd, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_status, 0, 4, st));
+  if ((rc = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, d_gens, K, N, d_coeffs,
+                          d_status, st)))
+    return rc;
+  CrtTables t;
+  t.K = K;
+  t.LW = LW;
+  t.primes = ce->d_primes;
+  t.Wm = ce->d_Wm;
+  t.invm = ce->d_invm;
+  t.Pl = ce->d_Pl;
+  launch_crt(t, d_coeffs, N, d_out, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  uint8_t* ho = (uint8_t*)h_out;
+  CK(cudaMemcpyAsync(ho, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ho + 4 * (size_t)N * LW, d_status, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(g.ev1, st));
+  CK(cudaStreamSynchronize(st));
+  memcpy(out, ho, 4 * (size_t)N * LW);
+  uint32_t s;
+  memcpy(&s, ho + 4 * (size_t)N * LW, 4);
+  if (status) *status = s;
+  if (device_ms) CK(cudaEventElapsedTime(device_ms, g.ev0, g.ev1));
+  return s ? CKB_STATUS_REPLAN : 0;
+}
+
+int ckb_reduce(const uint32_t* limbs, int C, int L, const uint32_t* primes, int K, uint32_t* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, K))) return rc;
+  cudaStream_t st = g.stream;
+  uint32_t *d_limbs, *d_out;
+  Prime* d_primes;
+  if ((rc = dbuf("r.limbs", (size_t)C * L, &d_limbs))) return rc;
+  if ((rc = dbuf("r.out", (size_t)K * C, &d_out))) return rc;
+  if ((rc = upload_primes(primes, K, &d_primes))) return rc;
+  CK(cudaMemcpyAsync(d_limbs, limbs, 4 * (size_t)C * L, cudaMemcpyHostToDevice, st));
+  launch_reduce(d_limbs, C, L, d_primes, K, d_out, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)K * C, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ckb_uni_resultant_batch(const uint32_t* fa, const int32_t* da, const uint32_t* gb, const int32_t* db, int W,
+                            const uint32_t* primes, int P, const int32_t* pidx, int B, uint32_t* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, P))) return rc;
+  if (W < 1 || images_maxd(W - 1, 0) < 0) return fail("ckb_uni_resultant_batch: degree above 64", -2);
+  if (B == 0) return 0;
+  cudaStream_t st = g.stream;
+  uint32_t *d_fa, *d_gb, *d_out;
+  int32_t *d_da, *d_db, *d_pi;
+  Prime* d_primes;
+  if ((rc = dbuf("u.fa", (size_t)B * W, &d_fa))) return rc;
+  if ((rc = dbuf("u.gb", (size_t)B * W, &d_gb))) return rc;
+  if ((rc = dbuf("u.da", (size_t)B, &d_da))) return rc;
+  if ((rc = dbuf("u.db", (size_t)B, &d_db))) return rc;
+  if ((rc = dbuf("u.pi", (size_t)B, &d_pi))) return rc;
+  if ((rc = dbuf("u.out", (size_t)B, &d_out))) return rc;
+  if ((rc = upload_primes(primes, P, &d_primes))) return rc;
+  CK(cudaMemcpyAsync(d_fa, fa, 4 * (size_t)B * W, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_gb, gb, 4 * (size_t)B * W, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_da, da, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_db, db, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_pi, pidx, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
+  launch_uni_resultant(d_fa, d_da, d_gb, d_db, W, d_primes, d_pi, B, d_out, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)B, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ckb_crt_lift(const uint32_t* residues, int K, int N, const uint32_t* primes, int LW, uint32_t* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, K))) return rc;
+  cudaStream_t st = g.stream;
+  CrtEntry* ce;
+  if ((rc = get_crt(primes, K, LW, &ce))) return rc;
+  uint32_t *d_res, *d_out;
+  if ((rc = dbuf("c.res", (size_t)K * N, &d_res))) return rc;
+  if ((rc = dbuf("c.out", (size_t)N * LW, &d_out))) return rc;
+  CK(cudaMemcpyAsync(d_res, residues, 4 * (size_t)K * N, cudaMemcpyHostToDevice, st));
+  CrtTables t;
+  t.K = K;
+  t.LW = LW;
+  t.primes = ce->d_primes;
+  t.Wm = ce->d_Wm;
+  t.invm = ce->d_invm;
+  t.Pl = ce->d_Pl;
+  launch_crt(t, d_res, N, d_out, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ckb_interp_plan_points(const uint32_t* primes, const uint32_t* gens, int K, int N, uint32_t* xpts) {
+  // the planned points for constant leading coefficients (c = 1): x_t = q^t
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, K))) return rc;
+  cudaStream_t st = g.stream;
+  Prime* d_primes;
+  uint32_t *d_gens, *d_red, *d_status;
+  if ((rc = upload_primes(primes, K, &d_primes))) return rc;
+  if ((rc = dbuf("p.gens", (size_t)K, &d_gens))) return rc;
+  if ((rc = dbuf("p.red", (size_t)K * 2, &d_red))) return rc;
+  if ((rc = dbuf("p.status", 1, &d_status))) return rc;
+  std::vector<uint32_t> ones((size_t)K * 2, 1u);
+  CK(cudaMemcpyAsync(d_gens, gens, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_red, ones.data(), 4 * (size_t)K * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_status, 0, 4, st));
+  InterpPlan pl;
+  if ((rc = plan_bufs(K, N, &pl))) return rc;
+  launch_plan(d_primes, d_gens, K, N, d_red, 2, 0, 0, 1, 0, pl, d_status, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(xpts, pl.xpts, 4 * (size_t)K * N, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ckb_interp_geometric(const uint32_t* values, const uint32_t* primes, const uint32_t* gens, int K, int N,
+                         uint32_t* coeffs) {
+  // interpolate values given at the planned points x_t = q^t (c = 1)
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, K))) return rc;
+  cudaStream_t st = g.stream;
+  Prime* d_primes;
+  uint32_t *d_gens, *d_red, *d_status, *d_vals, *d_coeffs, *d_a, *d_ac, *d_S;
+  if ((rc = upload_primes(primes, K, &d_primes))) return rc;
+  if ((rc = dbuf("p.gens", (size_t)K, &d_gens))) return rc;
+  if ((rc = dbuf("p.red", (size_t)K * 2, &d_red))) return rc;
+  if ((rc = dbuf("p.status", 1, &d_status))) return rc;
+  if ((rc = dbuf("i.vals", (size_t)K * N, &d_vals))) return rc;
+  if ((rc = dbuf("i.coeffs", (size_t)K * N, &d_coeffs))) return rc;
+  if ((rc = dbuf("ia", (size_t)K * N, &d_a))) return rc;
+  if ((rc = dbuf("iac", (size_t)K * N, &d_ac))) return rc;
+  if ((rc = dbuf("iS", (size_t)K * N, &d_S))) return rc;
+  std::vector<uint32_t> ones((size_t)K * 2, 1u);
+  CK(cudaMemcpyAsync(d_gens, gens, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_red, ones.data(), 4 * (size_t)K * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_vals, values, 4 * (size_t)K * N, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_status, 0, 4, st));
+  InterpPlan pl;
+  if ((rc = plan_bufs(K, N, &pl))) return rc;
+  launch_plan(d_primes, d_gens, K, N, d_red, 2, 0, 0, 1, 0, pl, d_status, st);
+  launch_interp(pl, d_primes, d_vals, d_coeffs, d_a, d_ac, d_S, st);
+  g.launches += 4;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(coeffs, d_coeffs, 4 * (size_t)K * N, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ckb_gcd_mod_batch(const uint32_t* fa, const int32_t* da, int Wf, const uint32_t* gb, const int32_t* db, int Wg,
+                      const uint32_t* primes, int P, const int32_t* pidx, int B, uint32_t* out, int Wo,
+                      int32_t* odeg) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, P))) return rc;
+  if (B == 0) return 0;
+  if ((size_t)2 * (Wf > Wg ? Wf : Wg) * 4 > 200 * 1024) return fail("ckb_gcd_mod_batch: degree too large", -2);
+  cudaStream_t st = g.stream;
+  uint32_t *d_fa, *d_gb, *d_out;
+  int32_t *d_da, *d_db, *d_pi, *d_odeg;
+  Prime* d_primes;
+  if ((rc = dbuf("g.fa", (size_t)B * Wf, &d_fa))) return rc;
+  if ((rc = dbuf("g.gb", (size_t)B * Wg, &d_gb))) return rc;
+  if ((rc = dbuf("g.da", (size_t)B, &d_da))) return rc;
+  if ((rc = dbuf("g.db", (size_t)B, &d_db))) return rc;
+  if ((rc = dbuf("g.pi", (size_t)B, &d_pi))) return rc;
+  if ((rc = dbuf("g.out", (size_t)B * Wo, &d_out))) return rc;
+  if ((rc = dbuf("g.odeg", (size_t)B, &d_odeg))) return rc;
+  if ((rc = upload_primes(primes, P, &d_primes))) return rc;
+  CK(cudaMemcpyAsync(d_fa, fa, 4 * (size_t)B * Wf, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_gb, gb, 4 * (size_t)B * Wg, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_da, da, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_db, db, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_pi, pidx, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
+  launch_gcd_mod(d_fa, d_da, Wf, d_gb, d_db, Wg, d_primes, d_pi, B, d_out, Wo, d_odeg, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)B * Wo, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(odeg, d_odeg, 4 * (size_t)B, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const uint32_t* primes, int P,
+                      const int32_t* pidx, int B, uint32_t* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, P))) return rc;
+  if (B == 0) return 0;
+  if (W > 4096) return fail("ckb_interp_points: at most 4096 points", -2);
+  cudaStream_t st = g.stream;
+  uint32_t *d_xs, *d_vs, *d_out;
+  int32_t *d_ns, *d_pi;
+  Prime* d_primes;
+  if ((rc = dbuf("ip.xs", (size_t)B * W, &d_xs))) return rc;
+  if ((rc = dbuf("ip.vs", (size_t)B * W, &d_vs))) return rc;
+  if ((rc = dbuf("ip.ns", (size_t)B, &d_ns))) return rc;
+  if ((rc = dbuf("ip.pi", (size_t)B, &d_pi))) return rc;
+  if ((rc = dbuf("ip.out", (size_t)B * W, &d_out))) return rc;
+  if ((rc = upload_primes(primes, P, &d_primes))) return rc;
+  CK(cudaMemcpyAsync(d_xs, xs, 4 * (size_t)B * W, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_vs, vs, 4 * (size_t)B * W, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_ns, ns, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_pi, pidx, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
+  launch_interp_points(d_xs, d_vs, d_ns, W, d_primes, d_pi, B, d_out, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)B * W, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// ---- device-pointer entry points for the multi-GPU driver -------------------
+int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
+                           int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* d_gens, int K, int N,
+                           uint32_t* d_coeffs, uint32_t* d_status, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, K))) return rc;
+  cudaStream_t st = pick_stream(stream);
+  Prime* hp;
+  void* hv;
+  if ((rc = host_buf("dprimes", sizeof(Prime) * K, &hv))) return rc;
+  hp = (Prime*)hv;
+  for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
+  Prime* d_primes;
+  if ((rc = dbuf("dprimes", K, &d_primes))) return rc;
+  CK(cudaMemcpyAsync(d_primes, hp, sizeof(Prime) * K, cudaMemcpyHostToDevice, st));
+  rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, d_primes, d_gens, K, N, d_coeffs, d_status, st);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(st));  // the pinned prime staging buffer is reused by the next call
+  return 0;
+}
+
+int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, int LW, uint32_t* d_out,
+                void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, K))) return rc;
+  cudaStream_t st = pick_stream(stream);
+  CrtEntry* ce;
+  if ((rc = get_crt(primes, K, LW, &ce))) return rc;
+  CrtTables t;
+  t.K = K;
+  t.LW = LW;
+  t.primes = ce->d_primes;
+  t.Wm = ce->d_Wm;
+  t.invm = ce->d_invm;
+  t.Pl = ce->d_Pl;
+  launch_crt(t, d_coeffs, N, d_out, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// Word-size modular arithmetic for odd primes 3 <= p < 2^31 on sm_100a.
+//
+// Measured on B200 (tools/imad_peak.cu, profiles/r01_imad_peak.json): IMAD runs
+// at ~71 lanes/clk/SM but IMAD.WIDE.U32 and IMAD.HI.U32 at only ~23-25.  A
+// product therefore costs what its *high-half* multiplies cost, and the kernels
+// use Shoup multiplication by a fixed multiplier w (companion w' = floor(w*2^32/p)):
+//     q = hi(x*w'), r = x*w - q*p  (mod 2^32)   -> r in [0, 2p)
+// one IMAD.HI + two IMAD, valid for every 32-bit x.  General products (both
+// operands varying, rare: bookkeeping, plans) use signed Montgomery REDC.
+#pragma once
+#include <cstdint>
+
+namespace ckb {
+
+struct Prime {
+  uint32_t p;     // odd prime < 2^31
+  uint32_t pinv;  // p^-1 mod 2^32
+  uint32_t r2;    // 2^64 mod p
+};
+
+__host__ __device__ __forceinline__ uint32_t inv32(uint32_t p) {
+  uint32_t x = p;  // Newton: correct to 3 bits for odd p
+  for (int i = 0; i < 5; ++i) x *= 2u - p * x;
+  return x;
+}
+
+// [0, 2p) -> [0, p) without a branch (unsigned wrap makes r - p huge if r < p)
+__device__ __forceinline__ uint32_t red1(uint32_t r, uint32_t p) { return min(r, r - p); }
+
+__device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) {
+  return red1(a + b, p);  // a, b < p < 2^31
+}
+__device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) {
+  uint32_t d = a - b;
+  return min(d, d + p);
+}
+__device__ __forceinline__ uint32_t neg_mod(uint32_t a, uint32_t p) { return a ? p - a : 0u; }
+
+// signed Montgomery reduction: t < p * 2^32  ->  t * 2^-32 mod p in [0, p)
+__device__ __forceinline__ uint32_t redc(uint64_t t, const Prime& P) {
+  uint32_t m = (uint32_t)t * P.pinv;
+  int32_t u = (int32_t)((uint32_t)(t >> 32) - __umulhi(m, P.p));
+  return (uint32_t)(u + ((u >> 31) & (int32_t)P.p));
+}
+
+// general product a*b mod p (a, b < p): two REDCs
+__device__ __forceinline__ uint32_t mul_mod(uint32_t a, uint32_t b, const Prime& P) {
+  uint32_t t = redc((uint64_t)a * b, P);   // a b 2^-32
+  return redc((uint64_t)t * P.r2, P);      // a b
+}
+
+// Shoup companion of w < p: floor(w * 2^32 / p) = (w*2^32 - (w*2^32 mod p)) / p,
+// and exact division by odd p is multiplication by p^-1 mod 2^32.
+__device__ __forceinline__ uint32_t shoup_comp(uint32_t w, const Prime& P) {
+  uint32_t r = redc((uint64_t)w * P.r2, P);  // w * 2^32 mod p
+  return (0u - r) * P.pinv;
+}
+
+// x * w mod p, lazily in [0, 2p); any 32-bit x
+__device__ __forceinline__ uint32_t shoup_lazy(uint32_t x, uint32_t w, uint32_t wc, uint32_t p) {
+  uint32_t q = __umulhi(x, wc);
+  return x * w - q * p;
+}
+__device__ __forceinline__ uint32_t shoup(uint32_t x, uint32_t w, uint32_t wc, uint32_t p) {
+  return red1(shoup_lazy(x, w, wc, p), p);
+}
+
+__device__ __forceinline__ uint32_t pow_mod(uint32_t a, uint64_t e, const Prime& P) {
+  uint32_t r = 1u % P.p, b = a;
+  while (e) {
+    if (e & 1) r = mul_mod(r, b, P);
+    b = mul_mod(b, b, P);
+    e >>= 1;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint32_t inv_mod(uint32_t a, const Prime& P) {
+  return pow_mod(a, P.p - 2, P);  // Fermat; a != 0
+}
+
+// x mod p for an arbitrary 32-bit x (Shoup with w = 1)
+__device__ __forceinline__ uint32_t mod_word(uint32_t x, uint32_t one_comp, uint32_t p) {
+  return shoup(x, 1u, one_comp, p);
+}
+
+__device__ __forceinline__ Prime make_prime(uint32_t p) {
+  Prime P;
+  P.p = p;
+  P.pinv = inv32(p);
+  // 2^64 mod p via (2^32 mod p)^2
+  uint64_t r1 = (uint64_t)(0x100000000ull % p);
+  P.r2 = (uint32_t)((r1 * r1) % p);
+  return P;
+}
+
+}  // namespace ckb

@@ -1,0 +1,532 @@
+"""Drop-in B200 replacement for ``curvekit.modpoly`` (the reference hot path).
+
+Same public names, argument meaning, return types and exceptions as
+pkg/src/curvekit/modpoly.py; every modular computation runs in
+libcurvekit_b200.so (include/curvekit_b200.h) on the GPU.  There is no CPU
+fallback: without the library or a CUDA device these functions raise.
+
+What stays on the host is what the reference itself does outside its modular
+loops: argument checks, the degenerate branches of ``biv_resultant``
+(modpoly.py:363-369), primitive parts and the exact trial division that
+verifies a modular gcd (:337-340), and the conversion of the GPU's output limbs
+into Python ints.  ``prime_table``/``prime_stream`` are the reference's own
+(host constants, :31-73); the GPU pipeline draws its primes from
+``primes30.PRIMES30`` because the result does not depend on the primes.
+"""
+
+from __future__ import annotations
+
+import random
+from dataclasses import dataclass
+from functools import lru_cache
+from math import gcd as int_gcd
+
+import numpy as np
+
+from . import _lib
+from .bivpoly import as_biv
+from .planner import (ints_to_limbs, limbs_to_ints, pack_grid, plan_resultant)
+from .primes30 import PRIMES30
+
+__all__ = [
+    "UnluckyPrime", "prime_table", "prime_stream", "ModPoly", "ResidueSystem",
+    "ModularSubresultantProfile", "zp_resultant_uni", "zp_resultant_batch", "zp_interpolate",
+    "zp_gcd_sylvester", "crt_reconstruct", "int_gcd_uni", "biv_resultant",
+    "modular_subres_profile",
+]
+
+
+class UnluckyPrime(Exception):
+    """Raised when a chosen prime degenerates the leading coefficients."""
+
+
+# ---------------------------------------------------------------------------
+# prime table (host constants; restated from modpoly.py:29-73)
+# ---------------------------------------------------------------------------
+
+_MR_BASES = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)
+
+
+def _is_prime(n: int) -> bool:
+    if n < 2:
+        return False
+    for b in _MR_BASES:
+        if n % b == 0:
+            return n == b
+    d, s = n - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        s += 1
+    for b in _MR_BASES:
+        x = pow(b, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(s - 1):
+            x = x * x % n
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
+
+
+@lru_cache(maxsize=8)
+def prime_table(bits: int = 31, count: int = 4096) -> tuple:
+    """The ``count`` largest primes below 2**bits, descending (modpoly.py:57-66)."""
+    out = []
+    n = (1 << bits) - 1
+    while len(out) < count and n > 2:
+        if _is_prime(n):
+            out.append(n)
+        n -= 2
+    return tuple(out)
+
+
+def prime_stream(seed: int = 0, bits: int = 31):
+    """Deterministic enumeration of the prime table in seeded order (:69-73)."""
+    table = list(prime_table(bits))
+    random.Random(seed).shuffle(table)
+    return iter(table)
+
+
+# ---------------------------------------------------------------------------
+# value types (modpoly.py:80-99, :258-261, :421-425)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class ModPoly:
+    p: int
+    coeffs: tuple  # residues in [0, p), lowest degree first, no trailing zeros
+
+    @staticmethod
+    def make(coeffs, p: int) -> "ModPoly":
+        c = [x % p for x in coeffs]
+        while c and c[-1] == 0:
+            c.pop()
+        return ModPoly(p, tuple(c))
+
+    def degree(self) -> int:
+        return len(self.coeffs) - 1
+
+    def is_zero(self) -> bool:
+        return not self.coeffs
+
+
+@dataclass(frozen=True)
+class ResidueSystem:
+    primes: tuple
+    residues: tuple
+
+
+@dataclass(frozen=True)
+class ModularSubresultantProfile:
+    prime: int
+    chain_degrees: tuple
+    factor_degrees: tuple
+
+
+def _same_type_modpoly(like, p: int, coeffs) -> object:
+    """Return a ModPoly of the caller's class (reference or ours)."""
+    cls = type(like) if hasattr(like, "coeffs") and hasattr(like, "p") else ModPoly
+    c = list(coeffs)
+    while c and c[-1] == 0:
+        c.pop()
+    return cls(p, tuple(int(x) for x in c))
+
+
+def _trim(c: list) -> list:
+    while c and c[-1] == 0:
+        c.pop()
+    return c
+
+
+# ---------------------------------------------------------------------------
+# univariate kernels mod p (batched on the GPU)
+# ---------------------------------------------------------------------------
+
+def _check_prime_word(p: int):
+    if not (3 <= p < 2 ** 31) or p % 2 == 0:
+        raise ValueError("the GPU kernels need an odd prime 3 <= p < 2^31")
+
+
+def _prime_index(ps):
+    uniq = sorted(set(ps))
+    for p in uniq:
+        _check_prime_word(p)
+    pos = {p: i for i, p in enumerate(uniq)}
+    return np.array(uniq, dtype=np.uint32), np.array([pos[p] for p in ps], dtype=np.int32)
+
+
+def zp_resultant_batch(triples) -> list:
+    """res(a, b) mod p for a batch of (a, b, p) low-first residue lists.
+
+    Semantics of ``_zp_resultant`` (modpoly.py:132-153) for each triple,
+    one GPU thread per pair.
+    """
+    triples = list(triples)
+    if not triples:
+        return []
+    lib = _lib.lib()
+    B = len(triples)
+    A = [_trim([x % p for x in a]) for a, _, p in triples]
+    Bb = [_trim([x % p for x in b]) for _, b, p in triples]
+    W = max(1, max(max(len(a), len(b)) for a, b in zip(A, Bb)))
+    if W - 1 > 64:
+        raise NotImplementedError("univariate resultant kernel supports degree <= 64")
+    fa = np.zeros((B, W), dtype=np.uint32)
+    gb = np.zeros((B, W), dtype=np.uint32)
+    for i, (a, b) in enumerate(zip(A, Bb)):
+        fa[i, :len(a)] = a
+        gb[i, :len(b)] = b
+    da = np.array([len(a) - 1 for a in A], dtype=np.int32)
+    db = np.array([len(b) - 1 for b in Bb], dtype=np.int32)
+    primes, pidx = _prime_index([p for _, _, p in triples])
+    out = np.empty(B, dtype=np.uint32)
+    _lib.check(lib.ckb_uni_resultant_batch(_lib.ptr(fa), _lib.ptr(da), _lib.ptr(gb), _lib.ptr(db), W,
+                                           _lib.ptr(primes), len(primes), _lib.ptr(pidx), B, _lib.ptr(out)),
+               "ckb_uni_resultant_batch")
+    return [int(v) for v in out]
+
+
+def zp_resultant_uni(f, g) -> int:
+    """modpoly.py:156-161."""
+    if f.p != g.p:
+        raise ValueError("mismatched primes")
+    if f.is_zero() or g.is_zero():
+        raise ValueError("zero polynomial")
+    return zp_resultant_batch([(list(f.coeffs), list(g.coeffs), f.p)])[0]
+
+
+def zp_interpolate_batch(problems) -> list:
+    """Coefficient lists for a batch of (points, values, p) (modpoly.py:164-185)."""
+    problems = list(problems)
+    if not problems:
+        return []
+    lib = _lib.lib()
+    for pts, vals, p in problems:
+        if len(vals) != len(pts):
+            raise ValueError("points/values length mismatch")
+        if len(set(pts)) != len(pts):
+            raise ValueError("duplicate interpolation points")
+    B = len(problems)
+    W = max(1, max(len(pts) for pts, _, _ in problems))
+    if W > 4096:
+        raise NotImplementedError("at most 4096 points per interpolation problem")
+    xs = np.zeros((B, W), dtype=np.uint32)
+    vs = np.zeros((B, W), dtype=np.uint32)
+    ns = np.zeros(B, dtype=np.int32)
+    for i, (pts, vals, p) in enumerate(problems):
+        xs[i, :len(pts)] = [x % p for x in pts]
+        vs[i, :len(vals)] = [v % p for v in vals]
+        ns[i] = len(pts)
+    primes, pidx = _prime_index([p for _, _, p in problems])
+    out = np.zeros((B, W), dtype=np.uint32)
+    _lib.check(lib.ckb_interp_points(_lib.ptr(xs), _lib.ptr(vs), _lib.ptr(ns), W, _lib.ptr(primes), len(primes),
+                                     _lib.ptr(pidx), B, _lib.ptr(out)), "ckb_interp_points")
+    return [_trim([int(v) for v in out[i, :ns[i]]]) for i in range(B)]
+
+
+def zp_interpolate(points, values, p: int):
+    """modpoly.py:188-189."""
+    points, values = list(points), list(values)
+    if len(values) != len(points):
+        raise ValueError("points/values length mismatch")
+    if len(set(points)) != len(points):
+        raise ValueError("duplicate interpolation points")
+    if not points:
+        return ModPoly(p, ())
+    return ModPoly.make(zp_interpolate_batch([(points, values, p)])[0], p)
+
+
+def zp_gcd_batch(triples) -> list:
+    """Monic gcds mod p of (a, b, p) triples (``_zp_gcd``, modpoly.py:115-122)."""
+    triples = list(triples)
+    if not triples:
+        return []
+    lib = _lib.lib()
+    B = len(triples)
+    A = [_trim([x % p for x in a]) for a, _, p in triples]
+    Bb = [_trim([x % p for x in b]) for _, b, p in triples]
+    Wf = max(1, max(len(a) for a in A))
+    Wg = max(1, max(len(b) for b in Bb))
+    fa = np.zeros((B, Wf), dtype=np.uint32)
+    gb = np.zeros((B, Wg), dtype=np.uint32)
+    for i, (a, b) in enumerate(zip(A, Bb)):
+        fa[i, :len(a)] = a
+        gb[i, :len(b)] = b
+    da = np.array([len(a) - 1 for a in A], dtype=np.int32)
+    db = np.array([len(b) - 1 for b in Bb], dtype=np.int32)
+    primes, pidx = _prime_index([p for _, _, p in triples])
+    Wo = max(Wf, Wg)
+    out = np.zeros((B, Wo), dtype=np.uint32)
+    odeg = np.zeros(B, dtype=np.int32)
+    _lib.check(lib.ckb_gcd_mod_batch(_lib.ptr(fa), _lib.ptr(da), Wf, _lib.ptr(gb), _lib.ptr(db), Wg,
+                                     _lib.ptr(primes), len(primes), _lib.ptr(pidx), B, _lib.ptr(out), Wo,
+                                     _lib.ptr(odeg)), "ckb_gcd_mod_batch")
+    return [[int(v) for v in out[i, :odeg[i] + 1]] for i in range(B)]
+
+
+def _zp_gcd(a: list, b: list, p: int) -> list:
+    """modpoly.py:115-122 (GPU batch of one)."""
+    return zp_gcd_batch([(a, b, p)])[0]
+
+
+def zp_gcd_sylvester(f, g):
+    """Monic gcd mod p (modpoly.py:192-244).
+
+    The reference reads it off the row-echelon Sylvester matrix (Thm.,
+    PAPER.md:1469-1474); the division-free elimination on the Sylvester
+    generators computes the same monic polynomial.
+    """
+    if f.p != g.p:
+        raise ValueError("mismatched primes")
+    p = f.p
+    fa, gb = list(f.coeffs), list(g.coeffs)
+    if not fa or not gb:
+        raise ValueError("zero polynomial")
+    if len(fa) == 1 or len(gb) == 1:
+        return _same_type_modpoly(f, p, [1])
+    gm = _zp_gcd(fa, gb, p)
+    if len(gm) <= 1:
+        gm = [1]
+    return _same_type_modpoly(f, p, gm)
+
+
+# ---------------------------------------------------------------------------
+# Chinese remaindering (modpoly.py:258-300)
+# ---------------------------------------------------------------------------
+
+def crt_lift(residues: np.ndarray, primes) -> list:
+    """Symmetric CRT of K x N residues (rows = primes) -> N Python ints."""
+    lib = _lib.lib()
+    primes = [int(p) for p in primes]
+    K = len(primes)
+    res = np.ascontiguousarray(residues, dtype=np.uint32).reshape(K, -1)
+    N = res.shape[1]
+    mod = 1
+    for p in primes:
+        mod *= p
+    LW = (mod.bit_length() + 31) // 32
+    parr = np.array(primes, dtype=np.uint32)
+    out = np.empty(N * LW, dtype=np.uint32)
+    _lib.check(lib.ckb_crt_lift(_lib.ptr(res), K, N, _lib.ptr(parr), LW, _lib.ptr(out)), "ckb_crt_lift")
+    return limbs_to_ints(out, N, LW)
+
+
+def crt_reconstruct(rs) -> int:
+    """The unique representative in (-M/2, M/2] congruent to every residue."""
+    if len(set(rs.primes)) != len(rs.primes):
+        raise ValueError("primes must be pairwise distinct")
+    if not rs.primes:
+        return 0
+    for p in rs.primes:
+        _check_prime_word(p)
+    res = np.array([[r % p] for p, r in zip(rs.primes, rs.residues)], dtype=np.uint32)
+    return crt_lift(res, rs.primes)[0]
+
+
+# ---------------------------------------------------------------------------
+# integer univariate gcd (modpoly.py:307-341)
+# ---------------------------------------------------------------------------
+
+def _content(p: list) -> int:
+    g = 0
+    for a in p:
+        g = int_gcd(g, a)
+    return g
+
+
+def _primitive(p: list) -> list:
+    """upoly.primitive (upoly.py:88-95)."""
+    if not p:
+        return []
+    c = _content(p)
+    if p[-1] < 0:
+        c = -c
+    return [a // c for a in p]
+
+
+def _divexact(p: list, d: list):
+    """upoly.divexact (upoly.py:98-118): exact quotient over Z or None."""
+    if not d:
+        raise ZeroDivisionError
+    if not p:
+        return []
+    if len(p) < len(d):
+        return None
+    r = list(p)
+    q = [0] * (len(p) - len(d) + 1)
+    lead = d[-1]
+    for k in range(len(q) - 1, -1, -1):
+        c = r[k + len(d) - 1]
+        if c % lead:
+            return None
+        c //= lead
+        q[k] = c
+        if c:
+            for j, b in enumerate(d):
+                r[k + j] -= c * b
+    return _trim(q) if not any(r[: len(d) - 1]) else None
+
+
+def _reduce_many(polys: list, primes: list) -> list:
+    """Residues of each integer polynomial mod each prime: [K] x [poly] lists (K1 on the GPU)."""
+    lib = _lib.lib()
+    flat = [c for poly in polys for c in poly]
+    limbs, L = ints_to_limbs(flat)
+    C = len(flat)
+    parr = np.array(primes, dtype=np.uint32)
+    K = len(primes)
+    out = np.empty((K, C), dtype=np.uint32)
+    _lib.check(lib.ckb_reduce(_lib.ptr(limbs), C, L, _lib.ptr(parr), K, _lib.ptr(out)), "ckb_reduce")
+    return out
+
+
+def int_gcd_uni(f, g, seed: int = 0):
+    """Primitive gcd over Z with positive leading coefficient (modpoly.py:307-341).
+
+    Per-prime Euclid runs on the GPU for a batch of primes at once (the
+    reference's incremental loop, made speculative); the
+    CRT of the surviving images runs on the GPU; the candidate is verified by
+    exact trial division exactly as in the reference.  ``seed`` is accepted
+    for API parity (the result does not depend on it).
+    """
+    f = _trim(list(f))
+    g = _trim(list(g))
+    if not f and not g:
+        raise ValueError("gcd of two zero polynomials")
+    if not f:
+        return _primitive(g)
+    if not g:
+        return _primitive(f)
+    fp, gp = _primitive(f), _primitive(g)
+    if len(fp) == 1 or len(gp) == 1:
+        return [1]
+    gamma = int_gcd(fp[-1], gp[-1])
+    lf, lg = fp[-1], gp[-1]
+    best = None
+    acc_p, acc_r = [], []
+    idx = 0
+    batch = 2
+    while True:
+        primes = []
+        while len(primes) < batch:
+            if idx >= len(PRIMES30):
+                raise ArithmeticError("prime table exhausted in gcd computation")
+            p = PRIMES30[idx][0]
+            idx += 1
+            if lf % p and lg % p:
+                primes.append(p)
+        red = _reduce_many([fp, gp], primes)
+        nf = len(fp)
+        gms = zp_gcd_batch([(red[i, :nf].tolist(), red[i, nf:].tolist(), p) for i, p in enumerate(primes)])
+        for p, gm in zip(primes, gms):
+            d = len(gm) - 1
+            if d == 0:
+                return [1]
+            if best is None or d < best:
+                best = d
+                acc_p, acc_r = [], []
+            elif d > best:
+                continue
+            gmod = (np.array(gm, dtype=np.uint64) * (gamma % p)) % p
+            acc_p.append(p)
+            acc_r.append(gmod.astype(np.uint32))
+        if acc_p:
+            vals = crt_lift(np.stack(acc_r), acc_p)
+            cand = _primitive(_trim(vals))
+            if len(cand) - 1 == best and _divexact(fp, cand) is not None and \
+                    _divexact(gp, cand) is not None:
+                return cand
+        batch = min(2 * batch, 64)
+
+
+# ---------------------------------------------------------------------------
+# bivariate resultants (modpoly.py:348-394)
+# ---------------------------------------------------------------------------
+
+def _mul(p: list, q: list) -> list:
+    if not p or not q:
+        return []
+    out = [0] * (len(p) + len(q) - 1)
+    for i, a in enumerate(p):
+        if a:
+            for j, b in enumerate(q):
+                out[i + j] += a * b
+    return _trim(out)
+
+
+def _pow(p: list, k: int) -> list:
+    out = [1]
+    for _ in range(k):
+        out = _mul(out, p)
+    return out
+
+
+def biv_resultant(f, g, var: str = "y", seed: int = 0) -> list:
+    """Resultant of f and g with respect to ``var``, exactly over Z.
+
+    Equals the determinant of the Sylvester matrix of f and g viewed as
+    polynomials in ``var``; the result is a polynomial in the other variable
+    (lowest degree first), ``[]`` if it vanishes.  Every modular step (K1
+    reduce, plan, fused evaluation + resultant per (prime, point), geometric
+    interpolation, mixed-radix CRT with limbs out) runs in one call of
+    ``ckb_biv_resultant`` on the GPU.
+    """
+    f, g = as_biv(f), as_biv(g)
+    if f.is_zero() or g.is_zero():
+        raise ValueError("resultant of zero polynomial")
+    if var == "x":
+        f, g = f.swap(), g.swap()
+    elif var != "y":
+        raise ValueError("var must be 'x' or 'y'")
+    fc = f.coeffs_wrt_y()
+    gc = g.coeffs_wrt_y()
+    m, n = len(fc) - 1, len(gc) - 1
+    if m == 0 and n == 0:
+        return [1]
+    if m == 0:
+        return _pow(fc[0], n)
+    if n == 0:
+        return _pow(gc[0], m)
+    res, _ = _biv_resultant_gpu(fc, gc, f.total_degree(), g.total_degree())
+    return res
+
+
+def _biv_resultant_gpu(fc, gc, tdf: int, tdg: int):
+    lib = _lib.lib()
+    m, n = len(fc) - 1, len(gc) - 1
+    if max(m, n) > 64:
+        raise NotImplementedError("the image kernel supports y-degrees up to 64")
+    packed = pack_grid(fc, gc)
+    start = 0
+    for _attempt in range(4):
+        plan = plan_resultant(fc, gc, tdf, tdg, packed.dfx, packed.dgx, start)
+        K, N, LW = len(plan.primes), plan.N, plan.LW
+        out = np.empty(N * LW, dtype=np.uint32)
+        status = np.zeros(1, dtype=np.uint32)
+        ms = np.zeros(1, dtype=np.float32)
+        rc = _lib.check(lib.ckb_biv_resultant(
+            _lib.ptr(packed.limbs), packed.C, packed.L, _lib.ptr(packed.degs), m, n, packed.dfx, packed.dgx,
+            _lib.ptr(plan.primes), _lib.ptr(plan.gens), K, N, LW, _lib.ptr(out), _lib.ptr(status),
+            _lib.ptr(ms)), "ckb_biv_resultant")
+        if rc == 0:
+            vals = _trim(limbs_to_ints(out, N, LW))
+            return vals, {"K": K, "N": N, "LW": LW, "device_ms": float(ms[0]),
+                          "bound_bits": plan.bound_bits, "modulus_bits": plan.modulus_bits}
+        start += K  # a prime had no admissible point set: use the next primes
+    raise ArithmeticError("no admissible evaluation points after re-planning")
+
+
+# ---------------------------------------------------------------------------
+# modular subresultant degree profiles (modpoly.py:421-526)
+# ---------------------------------------------------------------------------
+
+def modular_subres_profile(f, g, rstar, p: int):
+    """Degree profile of the subresultant gcd chain of f, g mod p.
+
+    Not yet on the GPU ("next"); raising keeps the
+    no-CPU-fallback contract -- ``install()`` leaves the reference's own
+    function in place for it.
+    """
+    raise NotImplementedError("modular_subres_profile is not on the GPU path yet")

@@ -1,0 +1,208 @@
+"""Host planner for the multi-modular resultant: bounds, primes, points, packing.
+
+Reference behaviour being planned (pkg/src/curvekit/modpoly.py:348-394):
+  * CRT stops once the modulus exceeds 2 * _det_coeff_bound (:370, :374-375,
+    :397-414).  Here the bound is min(reference bound, row Hadamard bound,
+    column Hadamard bound) -- all valid bounds on every coefficient of
+    det Sylvester(f, g) (a coefficient of det S(x) is at most
+    max_{|z|=1} |det S(z)| <= prod_rows ||row||_2 with |S_ij(z)| <= ||S_ij||_1).
+  * The number of points is one more than a degree bound of res.  The
+    reference uses deg_x f * n + deg_x g * m (:371); the Bezout-type bound
+    n * tdeg f + m * tdeg g - m n (sum of row/column degree weights of the
+    Sylvester matrix) is also valid; N = 1 + min of both.
+  * Primes: the device table (primes30.py) in descending order, skipping
+    primes that annihilate a leading y-coefficient polynomial (:378-379).
+The result is the unique integer polynomial determined by these bounds, so it
+is identical to the reference's for every seed.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from math import isqrt
+
+import numpy as np
+
+from .primes30 import PRIMES30
+
+
+@dataclass
+class Packed:
+    limbs: np.ndarray   # uint32 [C * L]
+    degs: np.ndarray    # int16 [m + n + 2]
+    C: int
+    L: int
+    m: int
+    n: int
+    dfx: int
+    dgx: int
+
+
+@dataclass
+class Plan:
+    primes: np.ndarray  # uint32 [K]
+    gens: np.ndarray    # uint32 [K]
+    N: int
+    LW: int
+    bound_bits: int
+    modulus_bits: int
+
+
+def _trimmed_deg(c) -> int:
+    d = len(c) - 1
+    while d >= 0 and c[d] == 0:
+        d -= 1
+    return d
+
+
+def _norm1(c) -> int:
+    return sum(abs(a) for a in c)
+
+
+def det_coeff_bound_ref(fc, gc) -> int:
+    """The reference's bound (modpoly.py:397-414), restated verbatim."""
+    m, n = len(fc) - 1, len(gc) - 1
+    norm_f = [_norm1(c) for c in fc]
+    norm_g = [_norm1(c) for c in gc]
+    bound = 1
+    for j in range(m + n):
+        s = 0
+        for r in range(n):
+            k = m - j + r
+            if 0 <= k <= m:
+                s += norm_f[k]
+        for r in range(m):
+            k = n - j + r
+            if 0 <= k <= n:
+                s += norm_g[k]
+        bound *= max(1, s)
+    return bound
+
+
+def det_coeff_bound(fc, gc) -> int:
+    """min(reference bound, row Hadamard, column Hadamard) -- all valid."""
+    m, n = len(fc) - 1, len(gc) - 1
+    nf = [_norm1(c) for c in fc]
+    ng = [_norm1(c) for c in gc]
+    ref = det_coeff_bound_ref(fc, gc)
+    # rows: n rows carrying f's coefficients, m rows carrying g's
+    row2 = sum(a * a for a in nf) ** n * sum(a * a for a in ng) ** m
+    col2 = 1
+    for j in range(m + n):
+        s = 0
+        for r in range(n):
+            k = m - j + r
+            if 0 <= k <= m:
+                s += nf[k] * nf[k]
+        for r in range(m):
+            k = n - j + r
+            if 0 <= k <= n:
+                s += ng[k] * ng[k]
+        col2 *= max(1, s)
+    had = isqrt(min(row2, col2)) + 1
+    return min(ref, had)
+
+
+def point_count(fc, gc, dfx: int, dgx: int, tdf: int, tdg: int) -> int:
+    m, n = len(fc) - 1, len(gc) - 1
+    ref = dfx * n + dgx * m
+    bez = n * tdf + m * tdg - m * n
+    return min(ref, bez) + 1
+
+
+def _lc_vanishes(lc, p: int) -> bool:
+    return all(c % p == 0 for c in lc)
+
+
+def choose_primes(need_bits_bound: int, lcf, lcg, start: int = 0, table=PRIMES30):
+    """Primes (descending, from ``start``) until prod > 2 * bound."""
+    target = 2 * need_bits_bound
+    primes, gens = [], []
+    mod = 1
+    i = start
+    const = len(lcf) == 1 and len(lcg) == 1
+    a, b = (lcf[0], lcg[0]) if const else (None, None)
+    while mod <= target:
+        if i >= len(table):
+            raise ArithmeticError("prime table exhausted in resultant computation")
+        p, g = table[i]
+        i += 1
+        if const:
+            if a % p == 0 or b % p == 0:
+                continue
+        elif _lc_vanishes(lcf, p) or _lc_vanishes(lcg, p):
+            continue
+        primes.append(p)
+        gens.append(g)
+        mod *= p
+    return primes, gens, mod
+
+
+def pack_grid(fc, gc) -> Packed:
+    """Dense two's-complement limb grid of f's then g's y-coefficients."""
+    m, n = len(fc) - 1, len(gc) - 1
+    degf = [_trimmed_deg(c) for c in fc]
+    degg = [_trimmed_deg(c) for c in gc]
+    dfx = max(0, max(degf))
+    dgx = max(0, max(degg))
+    C = (m + 1) * (dfx + 1) + (n + 1) * (dgx + 1)
+    maxbits = 0
+    for cs in (fc, gc):
+        for c in cs:
+            for a in c:
+                if a:
+                    b = a.bit_length() if a > 0 else (-a).bit_length()
+                    if b > maxbits:
+                        maxbits = b
+    L = max(1, (maxbits + 1 + 31) // 32)
+    if L <= 2:
+        grid = np.zeros(C, dtype=np.int64)
+        base = 0
+        for cs, dx in ((fc, dfx), (gc, dgx)):
+            for j, c in enumerate(cs):
+                if c:
+                    grid[base + j * (dx + 1): base + j * (dx + 1) + len(c)] = c
+            base += len(cs) * (dx + 1)
+        limbs = grid.view(np.uint32)
+        if L == 1:
+            limbs = np.ascontiguousarray(limbs.reshape(C, 2)[:, 0])
+        L = 1 if L == 1 else 2
+    else:
+        nb = 4 * L
+        zero = bytes(nb)
+        parts = []
+        for cs, dx in ((fc, dfx), (gc, dgx)):
+            for c in cs:
+                row = [a.to_bytes(nb, "little", signed=True) if a else zero for a in c]
+                row += [zero] * (dx + 1 - len(c))
+                parts.extend(row)
+        limbs = np.frombuffer(b"".join(parts), dtype=np.uint32)
+    degs = np.array(degf + degg, dtype=np.int16)
+    return Packed(np.ascontiguousarray(limbs), degs, C, L, m, n, dfx, dgx)
+
+
+def plan_resultant(fc, gc, tdf: int, tdg: int, dfx: int, dgx: int, start: int = 0) -> Plan:
+    bound = det_coeff_bound(fc, gc)
+    N = point_count(fc, gc, dfx, dgx, tdf, tdg)
+    primes, gens, mod = choose_primes(bound, fc[-1], gc[-1], start)
+    LW = (mod.bit_length() + 31) // 32
+    return Plan(np.array(primes, dtype=np.uint32), np.array(gens, dtype=np.uint32), N, LW,
+                bound.bit_length(), mod.bit_length())
+
+
+def limbs_to_ints(buf: np.ndarray, N: int, LW: int) -> list:
+    """[N][LW] two's-complement u32 limbs -> list of Python ints."""
+    raw = buf.tobytes()
+    w = 4 * LW
+    fb = int.from_bytes
+    return [fb(raw[i * w:(i + 1) * w], "little", signed=True) for i in range(N)]
+
+
+def ints_to_limbs(vals, L: int | None = None) -> tuple:
+    """list of ints -> ([len][L] two's-complement u32 limbs, L)."""
+    if L is None:
+        mb = max((abs(v).bit_length() for v in vals), default=0)
+        L = max(1, (mb + 1 + 31) // 32)
+    nb = 4 * L
+    raw = b"".join(int(v).to_bytes(nb, "little", signed=True) for v in vals)
+    return np.frombuffer(raw, dtype=np.uint32).copy(), L

@@ -1,0 +1,251 @@
+"""GPU parity: every entry point against the reference's golden vectors and the oracle.
+
+Bit-exact for everything (integer arithmetic).  Full-size configurations are
+checked against committed golden outputs of the unmodified reference (cfg2,
+cfg3) and, at cfg4 size, through the specialisation property
+res_y(f, g)(a) = res(f(a, y), g(a, y)) modulo independent primes.
+"""
+
+import hashlib
+import random
+
+import numpy as np
+import pytest
+
+from conftest import ints_in, load_golden, terms_in
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mp():
+    from paper_1201_1548_b200 import modpoly
+    return modpoly
+
+
+# ---------------------------------------------------------------------------
+# bivariate resultant (modpoly.py:348-394)
+# ---------------------------------------------------------------------------
+
+def test_known_answers(mp):
+    # test_modpoly.py:29-38
+    circle = {(2, 0): 1, (0, 2): 1, (0, 0): -1}
+    assert mp.biv_resultant(circle, {(0, 1): 2}, "y") == [-4, 0, 4]
+    assert mp.biv_resultant({(0, 2): 1, (3, 0): -1}, {(0, 1): 2}, "y") == [0, 0, 0, -4]
+    assert mp.biv_resultant(circle, {(0, 1): 1, (1, 0): -1}, "y") == [-1, 0, 2]
+
+
+def test_golden_resultant_cases(mp, small):
+    for case in small["resultant_cases"]:
+        got = mp.biv_resultant(terms_in(case["f"]), terms_in(case["g"]), case["var"])
+        assert got == ints_in(case["res"]), case
+
+
+def test_golden_random50_both_directions(mp, small):
+    for case in small["random50"]:
+        f, g = terms_in(case["f"]), terms_in(case["g"])
+        assert mp.biv_resultant(f, g, "y") == ints_in(case["res_y"])
+        assert mp.biv_resultant(f, g, "x") == ints_in(case["res_x"])
+
+
+def test_errors(mp):
+    with pytest.raises(ValueError):
+        mp.biv_resultant({}, {(0, 1): 1})
+    with pytest.raises(ValueError):
+        mp.biv_resultant({(0, 1): 1}, {(0, 1): 1}, "z")
+
+
+def test_random_vs_oracle(mp, oracle_mod):
+    rng = random.Random(77)
+    for _ in range(40):
+        d1, d2 = rng.randint(1, 9), rng.randint(1, 9)
+        bits = rng.choice([3, 20, 70, 140])
+        f = {(i, j): rng.randint(-2 ** bits, 2 ** bits) for i in range(d1 + 1) for j in range(d1 + 1 - i)
+             if rng.random() < 0.7}
+        g = {(i, j): rng.randint(-2 ** bits, 2 ** bits) for i in range(d2 + 1) for j in range(d2 + 1 - i)
+             if rng.random() < 0.7}
+        f = {k: v for k, v in f.items() if v} or {(0, 1): 1}
+        g = {k: v for k, v in g.items() if v} or {(1, 1): 1}
+        for var in ("y", "x"):
+            assert mp.biv_resultant(f, g, var) == oracle_mod.biv_resultant(f, g, var)
+
+
+def test_cfg2_golden(mp):
+    from paper_1201_1548_b200.synth import make_pair
+    gold = load_golden("cfg2_seed0.json.gz")
+    f, g = make_pair("cfg2", 0)
+    got = mp.biv_resultant(f, g, "y")
+    assert hashlib.sha256(repr(got).encode()).hexdigest()[:16] == gold["sha16_repr"]
+    assert got == [int(c, 16) for c in gold["res"]]
+
+
+def test_cfg3_golden(mp):
+    from paper_1201_1548_b200.synth import make_pair
+    gold = load_golden("cfg3_seed0.json.gz")
+    f, g = make_pair("cfg3", 0)
+    got = mp.biv_resultant(f, g, "y")
+    assert hashlib.sha256(repr(got).encode()).hexdigest()[:16] == gold["sha16_repr"] == "2273dd0debe66770"
+    assert got == [int(c, 16) for c in gold["res"]]
+    # the reference's square-free structure: R is square-free, gcd(R, R') = 1
+    assert mp.int_gcd_uni(got, [i * c for i, c in enumerate(got)][1:]) == ints_in(gold["gcd_r_dr"])
+
+
+def _specialisation_check(mp, oracle_mod, f, g, res, rng, trials=6):
+    fc, gc = oracle_mod.coeffs_wrt_y(f), oracle_mod.coeffs_wrt_y(g)
+    for _ in range(trials):
+        q = rng.choice(oracle_mod.prime_table()[100:400])
+        a = rng.randrange(q)
+        fu = [sum(c * pow(a, i, q) for i, c in enumerate(col)) % q for col in fc]
+        gu = [sum(c * pow(a, i, q) for i, c in enumerate(col)) % q for col in gc]
+        if fu[-1] == 0 or gu[-1] == 0:
+            continue
+        want = oracle_mod.zp_resultant(fu, gu, q)
+        got = sum(c * pow(a, i, q) for i, c in enumerate(res)) % q
+        assert got == want
+
+
+def test_cfg4_specialisation(mp, oracle_mod):
+    from paper_1201_1548_b200.synth import make_pair
+    f, g = make_pair("cfg4", 0)
+    res = mp.biv_resultant(f, g, "y")
+    assert len(res) == 1601
+    _specialisation_check(mp, oracle_mod, f, g, res, random.Random(4))
+
+
+def test_cfg4_one_prime_of_the_reference_loop(mp, oracle_mod):
+    """Residues of the GPU result mod the reference's first cfg4 prime equal
+    the reference loop body's interpolated polynomial at that prime."""
+    from paper_1201_1548_b200.synth import make_pair
+    gold = load_golden("cfg4_prime0.json.gz")
+    f, g = make_pair("cfg4", 0)
+    res = mp.biv_resultant(f, g, "y")
+    p = gold["p"]
+    assert [c % p for c in res] == gold["poly"] + [0] * (len(res) - len(gold["poly"]))
+
+
+# ---------------------------------------------------------------------------
+# per-prime entry points
+# ---------------------------------------------------------------------------
+
+def test_zp_resultant_golden(mp, small):
+    batch = [(c["f"], c["g"], c["p"]) for c in small["zp_resultant"]]
+    assert mp.zp_resultant_batch(batch) == [c["res"] for c in small["zp_resultant"]]
+    p = 7
+    f = mp.ModPoly.make([-1, 0, 1], p)
+    assert mp.zp_resultant_uni(f, mp.ModPoly.make([-2, 1], p)) == 3
+    assert mp.zp_resultant_uni(f, mp.ModPoly.make([5], p)) == pow(5, 2, p)
+    assert mp.zp_resultant_uni(f, f) == 0
+    with pytest.raises(ValueError):
+        mp.zp_resultant_uni(f, mp.ModPoly.make([1], 5))
+
+
+def test_zp_resultant_random_degrees_vs_oracle(mp, oracle_mod):
+    rng = random.Random(8)
+    ps = [1073692673, 536952833, 2147483647, 2147483629, 101, 7]
+    batch = []
+    for _ in range(400):
+        p = rng.choice(ps)
+        la, lb = rng.randint(1, 65), rng.randint(1, 65)
+        a = [rng.randrange(p) if rng.random() < 0.8 else 0 for _ in range(la)]
+        b = [rng.randrange(p) if rng.random() < 0.8 else 0 for _ in range(lb)]
+        batch.append((a, b, p))
+    got = mp.zp_resultant_batch(batch)
+    want = [oracle_mod.zp_resultant(a, b, p) for a, b, p in batch]
+    assert got == want
+
+
+def test_zp_interpolate_golden(mp, small):
+    for c in small["zp_interpolate"]:
+        assert list(mp.zp_interpolate(c["x"], c["v"], c["p"]).coeffs) == c["c"]
+    with pytest.raises(ValueError):
+        mp.zp_interpolate([1, 1], [0, 0], 5)
+
+
+def test_crt_golden(mp, small):
+    for c in small["crt"]:
+        assert mp.crt_reconstruct(mp.ResidueSystem(tuple(c["primes"]), tuple(c["res"]))) == int(c["x"])
+
+
+def test_crt_lift_roundtrip_large(mp):
+    from paper_1201_1548_b200.primes30 import PRIMES30
+    rng = random.Random(12)
+    primes = [p for p, _ in PRIMES30[:200]]
+    M = 1
+    for p in primes:
+        M *= p
+    vals = [rng.randint(-(M // 2) + 1, M // 2) for _ in range(300)] + [0, 1, -1, M // 2, -(M // 2) + 1]
+    res = np.array([[v % p for v in vals] for p in primes], dtype=np.uint32)
+    assert mp.crt_lift(res, primes) == vals
+
+
+def test_int_gcd_golden(mp, small):
+    for c in small["int_gcd"]:
+        assert mp.int_gcd_uni(ints_in(c["f"]), ints_in(c["g"])) == ints_in(c["gcd"]), c
+
+
+def test_zp_gcd_sylvester_golden(mp, small):
+    cases = small["zp_gcd_sylvester"]
+    for c in cases[:3]:
+        got = mp.zp_gcd_sylvester(mp.ModPoly.make(c["f"], c["p"]), mp.ModPoly.make(c["g"], c["p"]))
+        assert list(got.coeffs) == c["gcd"]
+    got = mp.zp_gcd_batch([(c["f"], c["g"], c["p"]) for c in cases[3:]])
+    for c, gm in zip(cases[3:], got):
+        want = c["euclid"] or [1]
+        assert (gm if len(gm) > 1 else [1]) == (want if len(want) > 1 else [1])
+        assert list(mp.zp_gcd_sylvester(mp.ModPoly.make(c["f"], c["p"]),
+                                        mp.ModPoly.make(c["g"], c["p"])).coeffs) == c["gcd"]
+
+
+def test_reduce_matches_python_mod():
+    from paper_1201_1548_b200 import _lib
+    from paper_1201_1548_b200.planner import ints_to_limbs
+    rng = random.Random(3)
+    vals = [rng.randint(-2 ** 300, 2 ** 300) for _ in range(500)] + [0, -1, 2 ** 31, -(2 ** 64)]
+    limbs, L = ints_to_limbs(vals)
+    primes = np.array([1073692673, 2147483647, 7, 536952833], dtype=np.uint32)
+    out = np.empty((4, len(vals)), dtype=np.uint32)
+    lib = _lib.lib()
+    _lib.check(lib.ckb_reduce(_lib.ptr(limbs), len(vals), L, _lib.ptr(primes), 4, _lib.ptr(out)), "reduce")
+    for k, p in enumerate(primes.tolist()):
+        assert out[k].tolist() == [v % p for v in vals]
+
+
+def test_geometric_interpolation_roundtrip():
+    """values at the planned points x_t = q^t interpolate back to the polynomial."""
+    from paper_1201_1548_b200 import _lib
+    from paper_1201_1548_b200.primes30 import PRIMES30
+    rng = random.Random(5)
+    lib = _lib.lib()
+    for N in (1, 2, 3, 17, 300, 1601):
+        K = 3
+        primes = np.array([p for p, _ in PRIMES30[10:10 + K]], dtype=np.uint32)
+        gens = np.array([g for _, g in PRIMES30[10:10 + K]], dtype=np.uint32)
+        pts = np.empty((K, N), dtype=np.uint32)
+        _lib.check(lib.ckb_interp_plan_points(_lib.ptr(primes), _lib.ptr(gens), K, N, _lib.ptr(pts)), "plan")
+        polys = [[rng.randrange(int(p)) for _ in range(N)] for p in primes.tolist()]
+        vals = np.empty((K, N), dtype=np.uint32)
+        for k, p in enumerate(primes.tolist()):
+            assert pts[k, 0] == 1 and len(set(pts[k].tolist())) == N
+            for t in range(N):
+                x = int(pts[k, t])
+                acc = 0
+                for c in reversed(polys[k]):
+                    acc = (acc * x + c) % p
+                vals[k, t] = acc
+        out = np.empty((K, N), dtype=np.uint32)
+        _lib.check(lib.ckb_interp_geometric(_lib.ptr(vals), _lib.ptr(primes), _lib.ptr(gens), K, N,
+                                            _lib.ptr(out)), "interp")
+        for k in range(K):
+            assert out[k].tolist() == polys[k], N
+
+
+# ---------------------------------------------------------------------------
+# square-free decomposition through the gcd plug-in point (upoly.py:253)
+# ---------------------------------------------------------------------------
+
+def test_squarefree_golden(small):
+    from paper_1201_1548_b200.upoly import squarefree_decompose
+    for c in small["squarefree"]:
+        dec = squarefree_decompose(ints_in(c["p"]))
+        assert dec.content == int(c["content"])
+        assert [(list(f), m) for f, m in dec.factors] == [(ints_in(f), m) for f, m in c["factors"]]
