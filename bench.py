@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 multi-modular resultant (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+Workload: cfg4 of BASELINE.json -- res_y(f, g) for random dense degree-40
+bivariates with 64-bit coefficients (synthetic, seed 0; SURVEY.md §8(d)
+generator).  A step is one complete res_y (reduce -> plan -> fused
+evaluation + resultant per (prime, point) -> interpolation -> CRT to limbs).
+  value  res_y per second with inputs resident in HBM (device time, CUDA
+         events on the launching stream, L2 flushed between steps, max over
+         ranks); at N > 1 the primes are sharded and the residues all-gathered
+         over NCCL before the CRT on rank 0 (strong scaling).
+  e2e    the same metric through the C-ABI call with HOST buffers
+         (ckb_biv_resultant: H2D of the limbs, D2H of the result limbs), plus
+         the Python-level time of modpoly.biv_resultant (packing, planning and
+         int conversion) reported beside it.
+  --impl reference: the CPU reference path (the oracle port of
+         modpoly.py's loop, all host threads) on a bounded sample of the same
+         workload, extrapolated to one res_y.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+from paper_1201_1548_b200.bivpoly import BivPoly  # noqa: E402
+from paper_1201_1548_b200.synth import CONFIGS, make_pair  # noqa: E402
+
+METRIC = "res_y(f,g) wall time & modular images/sec at 1/2/4/8 B200 vs CPU ref"
+UNIT = "res_y/s"
+
+
+def workload(config):
+    d, bits, kind = CONFIGS[config]
+    f, g = make_pair(config, 0)
+    F, G = BivPoly(f), BivPoly(g)
+    return F, G, {"workload": f"{config}: res_y(f,{'f_y' if kind == 'fy' else 'g'}) dense total degree {d}, "
+                              f"{bits}-bit coefficients, seed 0", "degree": d, "coeff_bits": bits}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of modpoly.py's loop) on a bounded sample
+# ---------------------------------------------------------------------------
+
+def cpu_reference(F, G, target_s: float = 12.0, threads=None):
+    """Time the reference's per-prime loop body (modpoly.py:376-391, ported to C,
+    all host threads) on a sample of its own primes; extrapolate to one res_y."""
+    from oracle import oracle
+    threads = threads or os.cpu_count() or 1
+    fc, gc = F.coeffs_wrt_y(), G.coeffs_wrt_y()
+    m, n = len(fc) - 1, len(gc) - 1
+    npts = F.deg_x() * n + G.deg_x() * m + 1          # the reference's point count (:371)
+    bound = oracle.det_coeff_bound(fc, gc)
+    stream = oracle._stream(0)
+    k_ref, mod = 0, 1
+    while mod <= 2 * bound:
+        mod *= stream[k_ref]
+        k_ref += 1
+    # calibrate: one prime on one thread
+    t0 = time.perf_counter()
+    oracle.prime_images(fc, gc, [stream[0]], npts, threads=1)
+    t1 = time.perf_counter() - t0
+    per_round = t1  # one prime per thread per round
+    rounds = max(1, min(8, int(target_s / max(per_round, 1e-3))))
+    sample = min(k_ref, threads * rounds)
+    t0 = time.perf_counter()
+    oracle.prime_images(fc, gc, list(stream[:sample]), npts, threads=threads)
+    ts = time.perf_counter() - t0
+    t_res = ts * k_ref / sample
+    return {"value": 1.0 / t_res, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample} of {k_ref} primes of the reference loop body (modpoly.py:376-391, "
+                      f"{npts} points/prime, C port, {threads} threads) in {ts:.2f} s; res_y time "
+                      f"extrapolated x{k_ref}/{sample} = {t_res:.1f} s",
+            "seconds_per_res_y": t_res, "images_per_s": sample * npts / ts,
+            "one_prime_one_thread_s": t1}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    F, G, cfg = workload(args.config)
+    vals = []
+    budget = min(args.ref_seconds, 150.0 / max(1, args.steps))  # whole run within a few minutes
+    for _ in range(args.steps):
+        vals.append(cpu_reference(F, G, target_s=budget))
+    v = statistics.median(r["value"] for r in vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32 (mod p < 2^31), exact integers", "data": "synthetic",
+            "config": cfg, "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1201_1548_b200 import _lib, modpoly, workmodel
+    from paper_1201_1548_b200.distributed import CudaBackend, plan_sharded, sharded_resultant_step
+    from paper_1201_1548_b200.planner import limbs_to_ints, pack_grid, plan_resultant
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ["CKB_DEVICE"] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    lib = _lib.lib()
+    F, G, cfg = workload(args.config)
+    fc, gc = F.coeffs_wrt_y(), G.coeffs_wrt_y()
+    tdf, tdg = F.total_degree(), G.total_degree()
+    plan = plan_sharded(fc, gc, tdf, tdg, world)
+    K, N, LW = len(plan.primes), plan.N, plan.LW
+    backend = CudaBackend(fc, gc, dev)
+    pk = backend.packed
+    stream = torch.cuda.Stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def step():
+        with torch.cuda.stream(stream):
+            return sharded_resultant_step(backend, plan, rank, world, None, stream.cuda_stream)
+
+    # correctness of the timed path against the single-call API (rank 0)
+    out = step()
+    torch.cuda.synchronize()
+    if rank == 0:
+        got = modpoly._trim(limbs_to_ints(out.cpu().numpy().view(np.uint32).reshape(-1), N, LW))
+        ref, _ = modpoly._biv_resultant_gpu(fc, gc, tdf, tdg)
+        assert got == ref, "sharded result differs from the single-GPU result"
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    n0 = lib.ckb_launch_count()
+    times = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                step()
+                e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    launches = int(lib.ckb_launch_count() - n0)
+    barrier()
+    torch.cuda.synchronize()
+    tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tot.item()) / args.steps
+    clocks = clk.summary()
+
+    # stage breakdown of the single-GPU pipeline (CUDA events between launches)
+    stages = None
+    peak = np.zeros(4, dtype=np.float32)
+    if rank == 0:
+        _lib.check(lib.ckb_measure_peak(_lib.ptr(peak)), "ckb_measure_peak")
+        lib.ckb_set_timing(1)
+        acc = np.zeros(5)
+        reps = max(3, args.steps)
+        d_out = torch.empty((N, LW), dtype=torch.int32, device=dev)
+        hp = np.array(plan.primes, dtype=np.uint32)
+        d_gens = torch.from_numpy(np.array(plan.gens, dtype=np.uint32).view(np.int32)).to(dev)
+        for _ in range(reps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            _lib.check(lib.ckb_dev_biv_resultant(
+                backend.d_limbs.data_ptr(), pk.C, pk.L, backend.d_degs.data_ptr(), _lib.ptr(backend.h_degs),
+                pk.m, pk.n, pk.dfx, pk.dgx, _lib.ptr(hp), d_gens.data_ptr(), K, N, LW, d_out.data_ptr(),
+                backend.d_status.data_ptr(), stream.cuda_stream), "ckb_dev_biv_resultant")
+            st = np.zeros(8, dtype=np.float32)
+            cnt = lib.ckb_stage_times(_lib.ptr(st), 8)
+            acc += st[:5] if cnt >= 5 else 0
+        lib.ckb_set_timing(0)
+        stages = dict(zip(["reduce", "plan", "images", "interp", "crt"], (acc / reps).tolist()))
+
+    # e2e: through the C-ABI with host buffers (rank 0, single GPU), and the Python API
+    e2e = None
+    if rank == 0:
+        p1 = plan_resultant(fc, gc, tdf, tdg, pk.dfx, pk.dgx)
+        hout = np.empty(p1.N * p1.LW, dtype=np.uint32)
+        status = np.zeros(1, dtype=np.uint32)
+        args_c = (_lib.ptr(pk.limbs), pk.C, pk.L, _lib.ptr(pk.degs), pk.m, pk.n, pk.dfx, pk.dgx,
+                  _lib.ptr(p1.primes), _lib.ptr(p1.gens), len(p1.primes), p1.N, p1.LW, _lib.ptr(hout),
+                  _lib.ptr(status), None)
+        for _ in range(args.warmup):
+            lib.ckb_biv_resultant(*args_c)
+        et = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            stream.synchronize()
+            t0 = time.perf_counter()
+            _lib.check(lib.ckb_biv_resultant(*args_c), "ckb_biv_resultant")
+            et.append(time.perf_counter() - t0)
+        pt = []
+        for _ in range(max(3, args.steps // 2)):
+            t0 = time.perf_counter()
+            modpoly.biv_resultant(F, G, "y")
+            pt.append(time.perf_counter() - t0)
+        e_ms = 1e3 * statistics.median(et)
+        e2e = {"value": 1e3 / e_ms, "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(pk.limbs.nbytes + pk.degs.nbytes + 4 * len(p1.gens)),
+               "d2h_bytes_per_step": int(hout.nbytes + 4),
+               "path": "ckb_biv_resultant (C-ABI, host buffers, pinned staging, copies in the timed region)",
+               "python_api_ms": 1e3 * statistics.median(pt),
+               "python_api_note": "modpoly.biv_resultant incl. packing, planning, int conversion"}
+
+    if rank == 0:
+        dfs = [len(c) - 1 for c in fc]
+        dgs = [len(c) - 1 for c in gc]
+        img_prod = workmodel.images_products(pk.m, pk.n, dfs, dgs, K, N)
+        t_img = stages["images"] * 1e-3
+        achieved = img_prod / t_img / 1e12
+        contract = workmodel.contract_imad(pk.m, pk.n, dfs, dgs, K, N, pk.C, pk.L)
+        images = K * N
+        cpu = cpu_reference(F, G, target_s=args.ref_seconds) if (world == 1 and not args.no_cpu) else None
+        line = {
+            "metric": METRIC, "value": 1e3 / ms_per_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32 (mod p < 2^30), exact integers", "data": "synthetic",
+            "config": dict(cfg, primes=K, points_per_prime=N, images_per_res_y=images, out_words=LW,
+                           l2="flushed (256 MB write) before every timed step", parallelism=f"primes/{world}"),
+            "images_per_s": images * 1e3 / ms_per_step,
+            "stages_ms": stages,
+            "roofline": {"bound": "imad", "kernel": "k_images (fused eval + elimination)",
+                         "achieved": achieved, "peak": float(peak[3]), "unit": "T modular products/s",
+                         "frac": achieved / float(peak[3]),
+                         "peak_source": "measured live: Shoup-pair product microbenchmark (csrc/ckb_peak.cu)",
+                         "algorithmic_products_per_launch": img_prod, "traffic": None,
+                         "imad_peaks_tops": {"imad": float(peak[0]), "imad_hi": float(peak[1]),
+                                             "imad_wide": float(peak[2])},
+                         "contract": {"survey_W_imad_per_res_y": contract,
+                                      "achieved_tops": contract / (ms_per_step * 1e-3) / 1e12,
+                                      "frac_of_measured_imad": contract / (ms_per_step * 1e-3) / 1e12 / float(peak[0])}},
+            "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -95,6 +95,23 @@ int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t*
 int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, int LW, uint32_t* d_out,
                 void* stream);
 
+/* Whole pipeline on device buffers (inputs already resident in HBM):
+ * same arguments as ckb_biv_resultant with d_ pointers; d_out [N][LW]. */
+int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
+                          int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* d_gens, int K, int N, int LW,
+                          uint32_t* d_out, uint32_t* d_status, void* stream);
+
+/* Instrumentation: record CUDA events between the stages of the next pipeline
+ * calls; ckb_stage_times returns the durations (ms) of reduce, plan, images,
+ * interpolation, CRT for the last call (count returned). */
+int ckb_set_timing(int on);
+int ckb_stage_times(float* ms, int max);
+
+/* Roofline denominators measured on the current device: out4 = [IMAD,
+ * IMAD.HI, IMAD.WIDE rates in T ops/s, Shoup-pair modular products in
+ * T products/s] (csrc/ckb_peak.cu). */
+int ckb_measure_peak(float* out4);
+
 #ifdef __cplusplus
 }
 #endif

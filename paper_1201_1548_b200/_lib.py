@@ -20,7 +20,8 @@ EXPORTS = (
     "ckb_abi_version", "ckb_last_error", "ckb_init", "ckb_shutdown", "ckb_launch_count",
     "ckb_biv_resultant", "ckb_reduce", "ckb_uni_resultant_batch", "ckb_interp_plan_points",
     "ckb_interp_geometric", "ckb_crt_lift", "ckb_dev_modular_images", "ckb_dev_crt",
-    "ckb_interp_points", "ckb_gcd_mod_batch",
+    "ckb_interp_points", "ckb_gcd_mod_batch", "ckb_dev_biv_resultant", "ckb_set_timing",
+    "ckb_stage_times", "ckb_measure_peak",
 )
 
 _P = ctypes.c_void_p

@@ -61,6 +61,9 @@ struct Ctx {
   std::vector<CrtEntry> crt;
   uint64_t tick = 0;
   uint64_t launches = 0;
+  bool timing = false;
+  cudaEvent_t sev[8] = {};
+  int nsev = 0;
 };
 
 Ctx g;
@@ -212,6 +215,37 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
   return 0;
 }
 
+void stage_mark(cudaStream_t st) {
+  if (g.timing && g.nsev < 8) cudaEventRecord(g.sev[g.nsev++], st);
+}
+
+struct PrimeEntry {
+  std::vector<uint32_t> primes;
+  Prime* d = nullptr;
+};
+std::vector<PrimeEntry> g_pcache;
+
+int get_primes_dev(const uint32_t* primes, int K, Prime** out) {
+  for (auto& e : g_pcache)
+    if ((int)e.primes.size() == K && !memcmp(e.primes.data(), primes, 4 * (size_t)K)) {
+      *out = e.d;
+      return 0;
+    }
+  if (g_pcache.size() >= 16) {
+    cudaFree(g_pcache.front().d);
+    g_pcache.erase(g_pcache.begin());
+  }
+  PrimeEntry e;
+  e.primes.assign(primes, primes + K);
+  std::vector<Prime> hp(K);
+  for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
+  CK(cudaMalloc(&e.d, sizeof(Prime) * K));
+  CK(cudaMemcpy(e.d, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice));
+  g_pcache.push_back(e);
+  *out = g_pcache.back().d;
+  return 0;
+}
+
 int ensure_ready() {
   if (!g.ready) return fail("ckb_init() has not been called", -3);
   CK(cudaSetDevice(g.device));
@@ -254,9 +288,12 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   if ((rc = dbuf("iS", (size_t)K * N, &d_S))) return rc;
   InterpPlan pl;
   if ((rc = plan_bufs(K, N, &pl))) return rc;
+  stage_mark(st);
   launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
+  stage_mark(st);
   const int lcf_off = m * (dfx + 1), lcg_off = (m + 1) * (dfx + 1) + n * (dgx + 1);
   launch_plan(d_primes, d_gens, K, N, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], pl, d_status, st);
+  stage_mark(st);
   ImageArgs a;
   a.red = d_red;
   a.degs = d_degs;
@@ -272,7 +309,9 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   a.values = d_vals;
   a.status = d_status;
   launch_images(a, st);
+  stage_mark(st);
   launch_interp(pl, d_primes, d_vals, d_coeffs, d_a, d_ac, d_S, st);
+  stage_mark(st);
   g.launches += 6;
   CK(cudaGetLastError());
   return 0;
@@ -299,6 +338,7 @@ int ckb_init(int device) {
   CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&g.ev0));
   CK(cudaEventCreate(&g.ev1));
+  for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&g.sev[i]));
   g.device = device;
   g.ready = true;
   return 0;
@@ -317,11 +357,14 @@ int ckb_shutdown(void) {
     cudaFree(e.d_invm);
     cudaFree(e.d_Pl);
   }
+  for (auto& e : g_pcache) cudaFree(e.d);
+  g_pcache.clear();
   g.dev.clear();
   g.host.clear();
   g.crt.clear();
   cudaEventDestroy(g.ev0);
   cudaEventDestroy(g.ev1);
+  for (int i = 0; i < 8; ++i) cudaEventDestroy(g.sev[i]);
   cudaStreamDestroy(g.stream);
   g = Ctx();
   return 0;
@@ -363,6 +406,7 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   CK(cudaMemcpyAsync(d_gens, hb + 4 * nl, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_degs, hb + 4 * nl + 4 * (size_t)K, 2 * nd, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(d_status, 0, 4, st));
+  g.nsev = 0;
   if ((rc = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, d_gens, K, N, d_coeffs,
                           d_status, st)))
     return rc;
@@ -374,6 +418,7 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   t.invm = ce->d_invm;
   t.Pl = ce->d_Pl;
   launch_crt(t, d_coeffs, N, d_out, st);
+  stage_mark(st);
   g.launches += 1;
   CK(cudaGetLastError());
   uint8_t* ho = (uint8_t*)h_out;
@@ -604,18 +649,11 @@ int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t*
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, K))) return rc;
   cudaStream_t st = pick_stream(stream);
-  Prime* hp;
-  void* hv;
-  if ((rc = host_buf("dprimes", sizeof(Prime) * K, &hv))) return rc;
-  hp = (Prime*)hv;
-  for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
   Prime* d_primes;
-  if ((rc = dbuf("dprimes", K, &d_primes))) return rc;
-  CK(cudaMemcpyAsync(d_primes, hp, sizeof(Prime) * K, cudaMemcpyHostToDevice, st));
-  rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, d_primes, d_gens, K, N, d_coeffs, d_status, st);
-  if (rc) return rc;
-  CK(cudaStreamSynchronize(st));  // the pinned prime staging buffer is reused by the next call
-  return 0;
+  if ((rc = get_primes_dev(primes, K, &d_primes))) return rc;
+  g.nsev = 0;
+  return modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, d_primes, d_gens, K, N, d_coeffs, d_status,
+                       st);
 }
 
 int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, int LW, uint32_t* d_out,
@@ -638,6 +676,57 @@ int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, 
   g.launches += 1;
   CK(cudaGetLastError());
   return 0;
+}
+
+int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
+                          int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* d_gens, int K, int N, int LW,
+                          uint32_t* d_out, uint32_t* d_status, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if (m < 1 || n < 1 || K < 1 || N < 1 || L < 1 || LW < 1) return fail("ckb_dev_biv_resultant: bad sizes", -2);
+  if ((rc = check_primes(primes, K))) return rc;
+  cudaStream_t st = pick_stream(stream);
+  CrtEntry* ce;
+  if ((rc = get_crt(primes, K, LW, &ce))) return rc;
+  uint32_t* d_coeffs;
+  if ((rc = dbuf("coeffs", (size_t)K * N, &d_coeffs))) return rc;
+  g.nsev = 0;
+  if ((rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, d_gens, K, N, d_coeffs,
+                          d_status, st)))
+    return rc;
+  CrtTables t;
+  t.K = K;
+  t.LW = LW;
+  t.primes = ce->d_primes;
+  t.Wm = ce->d_Wm;
+  t.invm = ce->d_invm;
+  t.Pl = ce->d_Pl;
+  launch_crt(t, d_coeffs, N, d_out, st);
+  stage_mark(st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int ckb_set_timing(int on) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g.timing = on != 0;
+  g.nsev = 0;
+  return 0;
+}
+
+int ckb_stage_times(float* ms, int max) {
+  // durations between consecutive stage marks of the last pipeline call:
+  // reduce, plan, images, interpolation, crt
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if (g.nsev < 2) return 0;
+  CK(cudaEventSynchronize(g.sev[g.nsev - 1]));
+  int n = 0;
+  for (int i = 1; i < g.nsev && n < max; ++i, ++n) CK(cudaEventElapsedTime(&ms[n], g.sev[i - 1], g.sev[i]));
+  return n;
 }
 
 }  // extern "C"

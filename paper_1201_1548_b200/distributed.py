@@ -1,0 +1,150 @@
+"""Primes sharded over GPUs, one process per GPU (torch.distributed over NCCL).
+
+The path partitions naturally: every
+prime's images and interpolation are independent; the only exchange is the
+residue gather before the CRT (option A).  Rank r takes a
+contiguous block of K/W primes (K rounded up to a multiple of W -- extra
+primes only enlarge the CRT modulus, which leaves the symmetric lift
+unchanged), runs reduce -> plan -> images -> interpolation on its GPU, the
+[K/W][N] coefficient residues are all-gathered over NCCL into prime order,
+and rank 0 runs the mixed-radix CRT and returns the integers.
+
+The device stages are behind a small backend object so the sharding,
+padding, collective and assembly logic is testable on CPU with gloo
+(tests/test_distributed.py) while the GPU backend is the C-ABI library.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .planner import (choose_primes, det_coeff_bound, limbs_to_ints, pack_grid, point_count)
+from .primes30 import PRIMES30
+
+
+@dataclass
+class ShardPlan:
+    primes: list        # all K primes (K % world == 0), CRT order
+    gens: list
+    N: int
+    LW: int
+    per_rank: int
+
+    def shard(self, rank: int):
+        a = rank * self.per_rank
+        return self.primes[a:a + self.per_rank], self.gens[a:a + self.per_rank]
+
+
+def plan_sharded(fc, gc, tdf: int, tdg: int, world: int, table=PRIMES30) -> ShardPlan:
+    m, n = len(fc) - 1, len(gc) - 1
+    dfx = max(0, max(len(c) - 1 for c in fc))
+    dgx = max(0, max(len(c) - 1 for c in gc))
+    bound = det_coeff_bound(fc, gc)
+    N = point_count(fc, gc, dfx, dgx, tdf, tdg)
+    primes, gens, mod = choose_primes(bound, fc[-1], gc[-1], 0, table)
+    start = table.index((primes[-1], gens[-1])) + 1
+    while len(primes) % world:  # pad with the next admissible primes
+        if start >= len(table):
+            raise ArithmeticError("prime table exhausted in resultant computation")
+        p, g = table[start]
+        start += 1
+        if all(c % p == 0 for c in fc[-1]) or all(c % p == 0 for c in gc[-1]):
+            continue
+        primes.append(p)
+        gens.append(g)
+        mod *= p
+    LW = (mod.bit_length() + 31) // 32
+    return ShardPlan(primes, gens, N, LW, len(primes) // world)
+
+
+class CudaBackend:
+    """Device stages through the C-ABI (device pointers from torch tensors)."""
+
+    def __init__(self, fc, gc, device):
+        import torch
+        from . import _lib
+        self.torch = torch
+        self._lib = _lib
+        self.lib = _lib.lib()
+        self.packed = pack_grid(fc, gc)
+        pk = self.packed
+        self.d_limbs = torch.from_numpy(pk.limbs.view(np.int32).copy()).to(device)
+        self.d_degs = torch.from_numpy(pk.degs.copy()).to(device)
+        self.h_degs = np.ascontiguousarray(pk.degs)
+        self.device = device
+        self.d_status = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def modular_images(self, primes, gens, N, stream):
+        torch = self.torch
+        pk = self.packed
+        K = len(primes)
+        hp = np.array(primes, dtype=np.uint32)
+        d_gens = torch.from_numpy(np.array(gens, dtype=np.uint32).view(np.int32)).to(self.device)
+        out = torch.empty((K, N), dtype=torch.int32, device=self.device)
+        self._lib.check(self.lib.ckb_dev_modular_images(
+            self.d_limbs.data_ptr(), pk.C, pk.L, self.d_degs.data_ptr(), self._lib.ptr(self.h_degs), pk.m, pk.n,
+            pk.dfx, pk.dgx, self._lib.ptr(hp), d_gens.data_ptr(), K, N, out.data_ptr(), self.d_status.data_ptr(),
+            stream), "ckb_dev_modular_images")
+        return out
+
+    def crt(self, coeffs, primes, N, LW, stream):
+        torch = self.torch
+        hp = np.array(primes, dtype=np.uint32)
+        out = torch.empty((N, LW), dtype=torch.int32, device=self.device)
+        self._lib.check(self.lib.ckb_dev_crt(coeffs.data_ptr(), len(primes), N, self._lib.ptr(hp), LW,
+                                             out.data_ptr(), stream), "ckb_dev_crt")
+        return out
+
+
+def sharded_resultant_step(backend, plan: ShardPlan, rank: int, world: int, group=None, stream=None):
+    """One res_y: local primes -> all_gather -> CRT on rank 0 (returns limbs tensor or None)."""
+    import torch.distributed as dist
+    primes, gens = plan.shard(rank)
+    local = backend.modular_images(primes, gens, plan.N, stream)
+    if world > 1:
+        import torch
+        gathered = torch.empty((world * plan.per_rank, plan.N), dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(gathered, local.contiguous(), group=group)
+    else:
+        gathered = local
+    if rank != 0:
+        return None
+    return backend.crt(gathered, plan.primes, plan.N, plan.LW, stream)
+
+
+def biv_resultant_distributed(f, g, var: str = "y", group=None) -> list | None:
+    """res_var(f, g) over all ranks of the default process group (SPMD call).
+
+    Every rank passes the same f, g; rank 0 returns the coefficient list,
+    the others return None.
+    """
+    import torch
+    import torch.distributed as dist
+    from .bivpoly import as_biv
+    from .modpoly import _pow, _trim
+    f, g = as_biv(f), as_biv(g)
+    if f.is_zero() or g.is_zero():
+        raise ValueError("resultant of zero polynomial")
+    if var == "x":
+        f, g = f.swap(), g.swap()
+    elif var != "y":
+        raise ValueError("var must be 'x' or 'y'")
+    fc, gc = f.coeffs_wrt_y(), g.coeffs_wrt_y()
+    m, n = len(fc) - 1, len(gc) - 1
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if m == 0 and n == 0:
+        return [1] if rank == 0 else None
+    if m == 0 or n == 0:
+        return (_pow(fc[0], n) if m == 0 else _pow(gc[0], m)) if rank == 0 else None
+    device = torch.device("cuda", torch.cuda.current_device())
+    plan = plan_sharded(fc, gc, f.total_degree(), g.total_degree(), world)
+    backend = CudaBackend(fc, gc, device)
+    s = torch.cuda.current_stream(device)
+    with torch.cuda.stream(s):
+        out = sharded_resultant_step(backend, plan, rank, world, group, s.cuda_stream)
+    if rank != 0:
+        return None
+    host = out.cpu().numpy().view(np.uint32).reshape(-1)
+    return _trim(limbs_to_ints(host, plan.N, plan.LW))

@@ -1,0 +1,48 @@
+"""Algorithmic work model of the hot path (used for roofline reporting).
+
+Two counts are kept apart:
+  * ``kernel_products`` -- modular products the B200 algorithm performs
+    (Shoup-Horner evaluation + division-free elimination), the work the
+    images kernel must do; achieved = products / kernel time, against the
+    measured Shoup-pair product peak (csrc/ckb_peak.cu).
+  * ``contract_imad`` -- SURVEY.md §8(d)'s fixed per-res_y figure
+    W = 3 IMAD x [k N (E + 4 r (r + 1)) + k N^2 + N k (k - 1)/2 + C L k]
+    (the Schur-algorithm count of PAPER.md's design), reported unchanged so
+    the two can be compared.
+"""
+
+from __future__ import annotations
+
+
+def eval_products(degs_f, degs_g) -> int:
+    """Shoup-Horner steps per image: sum of x-degrees of the y-coefficients."""
+    return sum(max(d, 0) for d in degs_f) + sum(max(d, 0) for d in degs_g)
+
+
+def elim_products(m: int, n: int) -> int:
+    """Products of the generic division-free elimination (ckb_resultant.cuh):
+    each step with nominal degree `nom` forms nom outputs of 2 products."""
+    da, db = max(m, n), min(m, n)
+    total = 0
+    while db >= 1:
+        e = da - db + 1
+        for s in range(e):
+            total += 2 * (da - s)
+        da, db = db, db - 1
+    return total
+
+
+def images_products(m, n, degs_f, degs_g, K, N) -> int:
+    return K * N * (eval_products(degs_f, degs_g) + elim_products(m, n))
+
+
+def interp_products(K: int, N: int) -> int:
+    """Hankel (N^2) + triangular Toeplitz (N(N+1)/2) products per prime."""
+    return K * (N * N + N * (N + 1) // 2)
+
+
+def contract_imad(m, n, degs_f, degs_g, K, N, C, L) -> int:
+    r = m + n
+    E = eval_products(degs_f, degs_g)
+    w = K * N * (E + 4 * r * (r + 1)) + K * N * N + N * K * (K - 1) // 2 + C * L * K
+    return 3 * w
