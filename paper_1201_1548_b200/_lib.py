@@ -28,6 +28,29 @@ _P = ctypes.c_void_p
 _I = ctypes.c_int
 _U32P = ctypes.POINTER(ctypes.c_uint32)
 
+# full C signatures (pointers must never be passed as 32-bit ints)
+_SIGS = {
+    "ckb_abi_version": (_I, []),
+    "ckb_last_error": (ctypes.c_char_p, []),
+    "ckb_init": (_I, [_I]),
+    "ckb_shutdown": (_I, []),
+    "ckb_launch_count": (ctypes.c_ulonglong, []),
+    "ckb_biv_resultant": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P, _P]),
+    "ckb_reduce": (_I, [_P, _I, _I, _P, _I, _P]),
+    "ckb_uni_resultant_batch": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _P]),
+    "ckb_interp_plan_points": (_I, [_P, _P, _I, _I, _P]),
+    "ckb_interp_geometric": (_I, [_P, _P, _P, _I, _I, _P]),
+    "ckb_crt_lift": (_I, [_P, _I, _I, _P, _I, _P]),
+    "ckb_gcd_mod_batch": (_I, [_P, _P, _I, _P, _P, _I, _P, _I, _P, _I, _P, _I, _P]),
+    "ckb_interp_points": (_I, [_P, _P, _P, _I, _P, _I, _P, _I, _P]),
+    "ckb_dev_modular_images": (_I, [_P, _I, _I, _P, _P, _I, _I, _I, _I, _P, _P, _I, _I, _P, _P, _P]),
+    "ckb_dev_crt": (_I, [_P, _I, _I, _P, _I, _P, _P]),
+    "ckb_dev_biv_resultant": (_I, [_P, _I, _I, _P, _P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P, _P]),
+    "ckb_set_timing": (_I, [_I]),
+    "ckb_stage_times": (_I, [_P, _I]),
+    "ckb_measure_peak": (_I, [_P]),
+}
+
 _lock = threading.Lock()
 _lib = None
 _ready = False
@@ -46,11 +69,12 @@ def load(path: str = LIB_PATH):
         raise CkbError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                        "(there is no CPU fallback)")
     lib = ctypes.CDLL(path)
-    lib.ckb_last_error.restype = ctypes.c_char_p
-    lib.ckb_abi_version.restype = _I
-    lib.ckb_launch_count.restype = ctypes.c_ulonglong
     for name in EXPORTS:
         getattr(lib, name)  # raises AttributeError if not exported
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
     _lib = lib
     return lib
 

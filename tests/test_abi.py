@@ -48,3 +48,16 @@ def test_product_package_never_imports_the_oracle():
     for path in glob.glob(os.path.join(REPO, "paper_1201_1548_b200", "**", "*.py"), recursive=True):
         src = open(path).read()
         assert "oracle" not in re.sub(r"#.*", "", src).replace("oracle/", ""), path
+
+
+def test_ctypes_signatures_match_header_arity():
+    """Every export has a ctypes signature whose arity equals the header's."""
+    from paper_1201_1548_b200 import _lib
+    src = ""
+    for h in glob.glob(os.path.join(REPO, "include", "*.h")):
+        src += re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+    assert set(_lib._SIGS) == set(_lib.EXPORTS)
+    for name, (_, args) in _lib._SIGS.items():
+        m = re.search(r"\b" + name + r"\s*\(([^)]*)\)", src)
+        params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
+        assert len(params) == len(args), name
