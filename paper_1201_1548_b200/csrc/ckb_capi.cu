@@ -45,9 +45,8 @@ struct CrtEntry {
   std::vector<uint32_t> primes;
   int LW = 0;
   Prime* d_primes = nullptr;
-  uint32_t* d_Wm = nullptr;
-  uint32_t* d_invm = nullptr;
-  uint32_t* d_Pl = nullptr;
+  void* d_blob = nullptr;  // p, c, cc, pinvd, Mi, Ml, Mh
+  CrtTables t;
   uint64_t last_use = 0;
 };
 
@@ -167,48 +166,80 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
       if (g.crt[i].last_use < g.crt[v].last_use) v = i;
     CrtEntry& e = g.crt[v];
     cudaFree(e.d_primes);
-    cudaFree(e.d_Wm);
-    cudaFree(e.d_invm);
-    cudaFree(e.d_Pl);
+    cudaFree(e.d_blob);
     g.crt.erase(g.crt.begin() + v);
   }
   CrtEntry e;
   e.primes.assign(primes, primes + K);
   e.LW = LW;
   std::vector<Prime> hp(K);
-  std::vector<uint32_t> Wm((size_t)K * K, 0), invm(K), Pl((size_t)K * LW, 0);
   for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
-  for (int i = 0; i < K; ++i) {
-    const uint32_t p = primes[i];
-    uint64_t m = 1 % p;
-    for (int j = 0; j < i; ++j) {
-      Wm[(size_t)j * K + i] = h_mont(m, p);
-      m = m * (primes[j] % p) % p;
-    }
-    if (m == 0) return fail("CRT primes are not pairwise distinct", -2);
-    invm[i] = h_mont(h_powmod(m, p - 2, p), p);
-  }
-  // limbs of M_j = prod_{l<j} p_l
-  std::vector<uint32_t> cur(LW + 1, 0);
-  cur[0] = 1;
+  // M = prod p_i as LW limbs
+  std::vector<uint32_t> M(LW + 1, 0);
+  M[0] = 1;
   for (int j = 0; j < K; ++j) {
-    memcpy(&Pl[(size_t)j * LW], cur.data(), 4 * (size_t)LW);
     uint64_t carry = 0;
-    for (int l = 0; l < LW; ++l) {
-      uint64_t t = (uint64_t)cur[l] * primes[j] + carry;
-      cur[l] = (uint32_t)t;
+    for (int l = 0; l <= LW; ++l) {
+      uint64_t t = (uint64_t)M[l] * primes[j] + carry;
+      M[l] = (uint32_t)t;
       carry = t >> 32;
     }
-    if (carry) return fail("CRT output width too small for the prime product", -2);
   }
+  if (M[LW]) return fail("CRT output width too small for the prime product", -2);
+  std::vector<uint32_t> hc(K), hcc(K), Mi((size_t)K * LW), Mh(LW);
+  std::vector<double> pinvd(K);
+  for (int i = 0; i < K; ++i) {
+    const uint32_t p = primes[i];
+    // M / p_i by long division, and (M/p_i) mod p_i as prod_{l != i} p_l
+    uint64_t rem = 0;
+    for (int l = LW - 1; l >= 0; --l) {
+      const uint64_t cur = (rem << 32) | M[l];
+      Mi[(size_t)i * LW + l] = (uint32_t)(cur / p);
+      rem = cur % p;
+    }
+    uint64_t mod = 1 % p;
+    for (int j = 0; j < K; ++j)
+      if (j != i) mod = mod * (primes[j] % p) % p;
+    if (mod == 0) return fail("CRT primes are not pairwise distinct", -2);
+    hc[i] = h_powmod(mod, p - 2, p);
+    hcc[i] = (uint32_t)(((uint64_t)hc[i] << 32) / p);
+    pinvd[i] = 1.0 / (double)p;
+  }
+  {
+    uint32_t carry = 0;
+    for (int l = LW - 1; l >= 0; --l) {
+      Mh[l] = (M[l] >> 1) | (carry << 31);
+      carry = M[l] & 1u;
+    }
+  }
+  const size_t nb = 4 * (size_t)K * 3 + 8 * (size_t)K + 4 * (size_t)K * LW + 8 * (size_t)LW + 64;
   CK(cudaMalloc(&e.d_primes, sizeof(Prime) * K));
-  CK(cudaMalloc(&e.d_Wm, 4 * (size_t)K * K));
-  CK(cudaMalloc(&e.d_invm, 4 * (size_t)K));
-  CK(cudaMalloc(&e.d_Pl, 4 * (size_t)K * LW));
+  CK(cudaMalloc(&e.d_blob, nb));
+  uint8_t* b = (uint8_t*)e.d_blob;
+  double* d_pinvd = (double*)b;  // 8-byte aligned first
+  uint32_t* d_p = (uint32_t*)(b + 8 * (size_t)K);
+  uint32_t* d_c = d_p + K;
+  uint32_t* d_cc = d_c + K;
+  uint32_t* d_Mi = d_cc + K;
+  uint32_t* d_Ml = d_Mi + (size_t)K * LW;
+  uint32_t* d_Mh = d_Ml + LW;
   CK(cudaMemcpy(e.d_primes, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e.d_Wm, Wm.data(), 4 * (size_t)K * K, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e.d_invm, invm.data(), 4 * (size_t)K, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e.d_Pl, Pl.data(), 4 * (size_t)K * LW, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_pinvd, pinvd.data(), 8 * (size_t)K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_p, primes, 4 * (size_t)K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_c, hc.data(), 4 * (size_t)K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_cc, hcc.data(), 4 * (size_t)K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_Mi, Mi.data(), 4 * (size_t)K * LW, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_Ml, M.data(), 4 * (size_t)LW, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_Mh, Mh.data(), 4 * (size_t)LW, cudaMemcpyHostToDevice));
+  e.t.K = K;
+  e.t.LW = LW;
+  e.t.p = d_p;
+  e.t.c = d_c;
+  e.t.cc = d_cc;
+  e.t.pinvd = d_pinvd;
+  e.t.Mi = d_Mi;
+  e.t.Ml = d_Ml;
+  e.t.Mh = d_Mh;
   e.last_use = ++g.tick;
   g.crt.push_back(e);
   *out = &g.crt.back();
@@ -353,9 +384,7 @@ int ckb_shutdown(void) {
   for (auto& kv : g.host) cudaFreeHost(kv.second.p);
   for (auto& e : g.crt) {
     cudaFree(e.d_primes);
-    cudaFree(e.d_Wm);
-    cudaFree(e.d_invm);
-    cudaFree(e.d_Pl);
+    cudaFree(e.d_blob);
   }
   for (auto& e : g_pcache) cudaFree(e.d);
   g_pcache.clear();
@@ -410,14 +439,9 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   if ((rc = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, d_gens, K, N, d_coeffs,
                           d_status, st)))
     return rc;
-  CrtTables t;
-  t.K = K;
-  t.LW = LW;
-  t.primes = ce->d_primes;
-  t.Wm = ce->d_Wm;
-  t.invm = ce->d_invm;
-  t.Pl = ce->d_Pl;
-  launch_crt(t, d_coeffs, N, d_out, st);
+  uint32_t* d_crtS;
+  if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
+  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
   stage_mark(st);
   g.launches += 1;
   CK(cudaGetLastError());
@@ -498,14 +522,9 @@ int ckb_crt_lift(const uint32_t* residues, int K, int N, const uint32_t* primes,
   if ((rc = dbuf("c.res", (size_t)K * N, &d_res))) return rc;
   if ((rc = dbuf("c.out", (size_t)N * LW, &d_out))) return rc;
   CK(cudaMemcpyAsync(d_res, residues, 4 * (size_t)K * N, cudaMemcpyHostToDevice, st));
-  CrtTables t;
-  t.K = K;
-  t.LW = LW;
-  t.primes = ce->d_primes;
-  t.Wm = ce->d_Wm;
-  t.invm = ce->d_invm;
-  t.Pl = ce->d_Pl;
-  launch_crt(t, d_res, N, d_out, st);
+  uint32_t* d_crtS;
+  if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
+  launch_crt(ce->t, d_res, N, d_out, d_crtS, st);
   g.launches += 1;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
@@ -665,14 +684,9 @@ int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, 
   cudaStream_t st = pick_stream(stream);
   CrtEntry* ce;
   if ((rc = get_crt(primes, K, LW, &ce))) return rc;
-  CrtTables t;
-  t.K = K;
-  t.LW = LW;
-  t.primes = ce->d_primes;
-  t.Wm = ce->d_Wm;
-  t.invm = ce->d_invm;
-  t.Pl = ce->d_Pl;
-  launch_crt(t, d_coeffs, N, d_out, st);
+  uint32_t* d_crtS;
+  if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
+  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
   g.launches += 1;
   CK(cudaGetLastError());
   return 0;
@@ -695,14 +709,9 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
   if ((rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, d_gens, K, N, d_coeffs,
                           d_status, st)))
     return rc;
-  CrtTables t;
-  t.K = K;
-  t.LW = LW;
-  t.primes = ce->d_primes;
-  t.Wm = ce->d_Wm;
-  t.invm = ce->d_invm;
-  t.Pl = ce->d_Pl;
-  launch_crt(t, d_coeffs, N, d_out, st);
+  uint32_t* d_crtS;
+  if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
+  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
   stage_mark(st);
   g.launches += 1;
   CK(cudaGetLastError());

@@ -1,137 +1,161 @@
-// K5: mixed-radix (Garner) CRT of every coefficient and the symmetric lift to
-// two's-complement 32-bit limbs, one warp per coefficient.
+// K5: Chinese remaindering of every coefficient and the symmetric lift to
+// two's-complement 32-bit limbs.
 //
 // Reference: curvekit.modpoly._CrtAccumulator.add / symmetric
 // (pkg/src/curvekit/modpoly.py:278-300) and crt_reconstruct (:264-275):
-//   x_{i+1} = x_i + M_i * ((r_i - x_i) * M_i^-1 mod p_i),  M_i = prod_{l<i} p_l
-//   result  = x - M if 2x > M else x.
-// Here the digits a_i = ((r_i - x_i) M_i^-1 mod p_i) are computed for all i
-// at once (column-updated residues, Montgomery table of M_j mod p_i), the sign
-// is decided on the digits (2x > M  <=>  digits > ((p_i - 1)/2)_i lexicographic
-// from the top, M being odd), and the magnitude sum_i b_i M_i is formed as
-// 32-bit column sums with a ballot carry-lookahead, so only bytes leave the GPU.
+// incremental Garner, then x - M if 2x > M.  The result is the unique
+// representative of the residues in (-M/2, M/2]; this kernel computes the
+// same integer by the *explicit* CRT, which has no sequential recurrence:
+//     y_i = r_i * (M/p_i)^-1 mod p_i                     (one Shoup product)
+//     X   = sum_i y_i * (M/p_i)                           (an N x K x LW integer
+//                                                          product: K2 below)
+//     q   = round(sum_i y_i / p_i)                       (FP64)
+//     x   = X - q M
+// X/M = q + x/M exactly; the planner guarantees M > 4 * bound, so |x/M| < 1/4
+// and the FP64 sum (error < K^2 2^-52) always rounds to the right q.
 #include "ckb_kernels.cuh"
 
 namespace ckb {
 
-constexpr int CRT_WARPS = 4;
+constexpr int TN = 64;   // coefficients per CTA tile
+constexpr int TL = 32;   // limbs per CTA tile
+constexpr int TI = 32;   // primes per k-step
+constexpr int CRT_THREADS = 256;
 
-__global__ void __launch_bounds__(CRT_WARPS * 32) k_crt(CrtTables T, const uint32_t* __restrict__ coeffs, int N,
-                                                       uint32_t* __restrict__ out) {
-  extern __shared__ uint32_t sm[];
+// K2: S[k][l] = sum_i y_i(k) * (M/p_i)[l] as 96-bit (lo64, hi32) column sums.
+// Thread micro-tile: 2 coefficients x 4 limbs.
+__global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uint32_t* __restrict__ r, int N,
+                                                          uint32_t* __restrict__ S) {
+  __shared__ uint32_t sy[TI][TN];
+  __shared__ uint32_t sm[TI][TL];
   const int K = T.K, LW = T.LW;
-  uint32_t* sp = sm;            // [K] primes
-  uint32_t* spinv = sm + K;     // [K] p^-1 mod 2^32
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* dig = sm + 2 * K + warp * K;
-  for (int i = threadIdx.x; i < K; i += blockDim.x) {
-    sp[i] = T.primes[i].p;
-    spinv[i] = T.primes[i].pinv;
-  }
-  __syncthreads();
-  const int k = blockIdx.x * CRT_WARPS + warp;
-  if (k >= N) return;
-  const unsigned FULL = 0xffffffffu;
-
-  for (int i = lane; i < K; i += 32) dig[i] = coeffs[(size_t)i * N + k];
-  __syncwarp();
-  // Garner digits
-  for (int j = 0; j < K; ++j) {
-    uint32_t aj = 0;
-    if (lane == (j & 31)) {
-      Prime Pj;
-      Pj.p = sp[j];
-      Pj.pinv = spinv[j];
-      aj = redc((uint64_t)dig[j] * T.invm[j], Pj);
-      dig[j] = aj;
-    }
-    aj = __shfl_sync(FULL, aj, j & 31);
-    const uint32_t* Wrow = T.Wm + (size_t)j * K;
-    for (int i = j + 1 + lane; i < K; i += 32) {
-      Prime Pi;
-      Pi.p = sp[i];
-      Pi.pinv = spinv[i];
-      const uint32_t tt = redc((uint64_t)aj * Wrow[i], Pi);
-      dig[i] = sub_mod(dig[i], tt, Pi.p);
-    }
-    __syncwarp();
-  }
-  // sign: x > (M-1)/2 ?
-  bool neg = false;
-  for (int s = (K - 1) >> 5; s >= 0; --s) {
-    const int i = (s << 5) + lane;
-    const bool d = (i < K) && (dig[i] != ((sp[i] - 1) >> 1));
-    const unsigned b = __ballot_sync(FULL, d);
-    if (b) {
-      const int il = (s << 5) + (31 - __clz(b));
-      neg = dig[il] > ((sp[il] - 1) >> 1);
-      break;
-    }
-  }
-  if (neg) {  // |x - M| = (M - 1 - x) + 1, digits p_i - 1 - a_i
-    for (int i = lane; i < K; i += 32) dig[i] = sp[i] - 1 - dig[i];
-  }
-  __syncwarp();
-
-  // column sums S_l = sum_j b_j * M_j[l] (+1 at l = 0 if neg), carry-resolved
-  uint32_t prev_a1 = 0, prev_a2_30 = 0, prev_a2_31 = 0, prev_t1 = 0, cin = 0, ncin = 1;
-  uint32_t* orow = out + (size_t)k * LW;
-  for (int l0 = 0; l0 < LW; l0 += 32) {
-    const int l = l0 + lane;
-    uint64_t lo = 0;
-    uint32_t hi = 0;
-    if (l < LW) {
-      for (int j = l0; j < K; ++j) {  // M_j has no limb at index >= j (j >= 1)
-        const uint64_t pr = (uint64_t)dig[j] * T.Pl[(size_t)j * LW + l];
-        lo += pr;
-        hi += (lo < pr);
+  const int k0 = blockIdx.x * TN, l0 = blockIdx.y * TL;
+  const int tid = threadIdx.x;
+  const int tk = (tid % 32) * 2;        // coefficient offset (0..62)
+  const int tl = (tid / 32) * 4;        // limb offset (0..28)
+  uint64_t lo[2][4] = {};
+  uint32_t hi[2][4] = {};
+  for (int i0 = 0; i0 < K; i0 += TI) {
+    // stage y (computed on the fly from the residues) and the M/p_i limbs
+    for (int e = tid; e < TI * TN; e += CRT_THREADS) {
+      const int ii = e / TN, kk = e % TN;
+      const int i = i0 + ii, k = k0 + kk;
+      uint32_t y = 0;
+      if (i < K && k < N) {
+        const uint32_t p = T.p[i];
+        y = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
       }
-      if (l0 == 0 && lane == 0) {  // j = 0 term handled above only if l0 == 0; add the +1
-        if (neg) {
-          lo += 1;
-          hi += (lo == 0);
+      sy[ii][kk] = y;
+    }
+    for (int e = tid; e < TI * TL; e += CRT_THREADS) {
+      const int ii = e / TL, ll = e % TL;
+      const int i = i0 + ii, l = l0 + ll;
+      sm[ii][ll] = (i < K && l < LW) ? T.Mi[(size_t)i * LW + l] : 0u;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int ii = 0; ii < TI; ++ii) {
+      const uint2 yv = *reinterpret_cast<const uint2*>(&sy[ii][tk]);
+      const uint4 mv = *reinterpret_cast<const uint4*>(&sm[ii][tl]);
+      const uint32_t ys[2] = {yv.x, yv.y};
+      const uint32_t ms[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint64_t pr = (uint64_t)ys[a] * ms[b];
+          const uint64_t s = lo[a][b] + pr;
+          hi[a][b] += (s < pr);
+          lo[a][b] = s;
         }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int k = k0 + tk + a, l = l0 + tl + b;
+      if (k < N && l < LW) {
+        uint32_t* o = S + ((size_t)k * LW + l) * 3;
+        o[0] = (uint32_t)lo[a][b];
+        o[1] = (uint32_t)(lo[a][b] >> 32);
+        o[2] = hi[a][b];
       }
     }
-    const uint32_t a0 = (uint32_t)lo, a1 = (uint32_t)(lo >> 32), a2 = hi;
-    uint32_t a1m = __shfl_up_sync(FULL, a1, 1);
-    uint32_t a2m = __shfl_up_sync(FULL, a2, 2);
-    if (lane == 0) a1m = prev_a1;
-    if (lane == 0) a2m = prev_a2_30;
-    if (lane == 1) a2m = prev_a2_31;
-    const uint64_t Tsum = (uint64_t)a0 + a1m + a2m;
-    const uint32_t t0 = (uint32_t)Tsum, t1 = (uint32_t)(Tsum >> 32);
-    uint32_t t1m = __shfl_up_sync(FULL, t1, 1);
-    if (lane == 0) t1m = prev_t1;
-    const uint64_t y = (uint64_t)t0 + t1m;  // <= 2^32 + 1
-    const bool G = y >= 0x100000000ull;
-    const bool Pp = (uint32_t)y == 0xffffffffu && !G;
-    const unsigned X = __ballot_sync(FULL, G || Pp), Y = __ballot_sync(FULL, G);
-    const uint64_t sum = (uint64_t)X + Y + cin;
-    const uint32_t carries = (uint32_t)(sum ^ X ^ Y);
-    uint32_t mag = (uint32_t)y + ((carries >> lane) & 1u);
-    // spill to the next chunk
-    prev_a1 = __shfl_sync(FULL, a1, 31);
-    prev_a2_30 = __shfl_sync(FULL, a2, 30);
-    prev_a2_31 = __shfl_sync(FULL, a2, 31);
-    prev_t1 = __shfl_sync(FULL, t1, 31);
-    cin = (uint32_t)(sum >> 32);
-    if (neg) {  // two's complement: ~mag + 1
-      const uint32_t ym = ~mag;
-      const unsigned Pn = __ballot_sync(FULL, ym == 0xffffffffu);
-      const uint64_t sn = (uint64_t)Pn + ncin;
-      const uint32_t cn = (uint32_t)(sn ^ Pn);
-      mag = ym + ((cn >> lane) & 1u);
-      ncin = (uint32_t)(sn >> 32);
+}
+
+// K3: per coefficient, q = round(sum y_i / p_i), then x = S - q M with a
+// signed carry chain over the limbs -> two's complement out[k][0..LW).
+__global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, const uint32_t* __restrict__ r, int N,
+                                                   const uint32_t* __restrict__ S, uint32_t* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const int K = T.K, LW = T.LW;
+  double s = 0.0;
+  for (int i = 0; i < K; ++i) {
+    const uint32_t p = T.p[i];
+    const uint32_t y = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
+    s = fma((double)y, T.pinvd[i], s);
+  }
+  const uint64_t q = (uint64_t)llrint(s);
+  const uint32_t* Sk = S + (size_t)k * LW * 3;
+  uint32_t* ok = out + (size_t)k * LW;
+  // carry = (c_hi:c_lo) signed 128-bit; value at limb l = S_l - q M_l + carry
+  long long c_hi = 0;
+  unsigned long long c_lo = 0;
+  for (int l = 0; l < LW; ++l) {
+    const unsigned long long s_lo = (unsigned long long)Sk[3 * l] | ((unsigned long long)Sk[3 * l + 1] << 32);
+    const long long s_hi = Sk[3 * l + 2];
+    const unsigned long long qm = q * (unsigned long long)T.Ml[l];  // < 2^44
+    // t = s - qm + carry
+    unsigned long long t_lo = s_lo - qm;
+    long long t_hi = s_hi - (long long)(s_lo < qm);
+    const unsigned long long u = t_lo + c_lo;
+    t_hi += c_hi + (long long)(u < t_lo);
+    t_lo = u;
+    ok[l] = (uint32_t)t_lo;
+    // carry = t >> 32 (arithmetic)
+    c_lo = (t_lo >> 32) | ((unsigned long long)t_hi << 32);
+    c_hi = t_hi >> 32;
+  }
+  // Exactness guard for callers without the 4x margin (crt_reconstruct on
+  // arbitrary residues): if s was near a half-integer, q may be off by one;
+  // fold x into [-floor(M/2), floor(M/2)] exactly.  Never taken when M > 4 bound.
+  const double fr = s - floor(s);
+  if (fabs(fr - 0.5) < 1e-3) {
+    // d = x - H - 1 ; if d >= 0 then x -= M
+    long long br = 0;
+    for (int l = 0; l < LW; ++l) {
+      const long long v = (long long)ok[l] - (long long)T.Mh[l] - (l == 0 ? 1 : 0) + br;
+      br = v >> 32;
     }
-    if (l < LW) orow[l] = mag;
+    const bool x_top_neg = (int32_t)ok[LW - 1] < 0;
+    // the sign of d is the sign of the full-width result: x (signed) - H - 1
+    const bool gt = !x_top_neg && br >= 0;
+    // e = x + H ; if e < 0 then x += M
+    long long cr = 0;
+    for (int l = 0; l < LW; ++l) {
+      const long long v = (long long)ok[l] + (long long)T.Mh[l] + cr;
+      cr = v >> 32;
+    }
+    const bool lt = x_top_neg && cr == 0;  // x + H did not carry out of a negative x: still negative
+    if (gt || lt) {
+      long long c = 0;
+      for (int l = 0; l < LW; ++l) {
+        const long long v = (long long)ok[l] + (gt ? -(long long)T.Ml[l] : (long long)T.Ml[l]) + c;
+        ok[l] = (uint32_t)v;
+        c = v >> 32;
+      }
+    }
   }
 }
 
-void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, cudaStream_t st) {
-  const size_t smem = (size_t)(2 + CRT_WARPS) * t.K * 4;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_crt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_crt<<<(N + CRT_WARPS - 1) / CRT_WARPS, CRT_WARPS * 32, smem, st>>>(t, coeffs, N, out);
+void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
+                cudaStream_t st) {
+  dim3 g1((N + TN - 1) / TN, (t.LW + TL - 1) / TL);
+  k_crt_gemm<<<g1, CRT_THREADS, 0, st>>>(t, coeffs, N, scratch);
+  k_crt_carry<<<(N + 127) / 128, 128, 0, st>>>(t, coeffs, N, scratch, out);
 }
 
 }  // namespace ckb

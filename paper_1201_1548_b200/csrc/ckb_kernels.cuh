@@ -55,16 +55,20 @@ void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t*
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, uint32_t* coeffs,
                    uint32_t* a, uint32_t* ac, uint32_t* S, cudaStream_t st);
 
-// ---- K5: mixed-radix CRT + symmetric lift to two's-complement limbs ----------
+// ---- K5: explicit CRT + symmetric lift to two's-complement limbs -----------
 struct CrtTables {
   int K, LW;
-  const Prime* primes;   // [K]
-  const uint32_t* Wm;    // [K][K]  Montgomery(prod_{l<j} p_l mod p_i) at [j][i]
-  const uint32_t* invm;  // [K]     Montgomery((prod_{l<i} p_l)^-1 mod p_i)
-  const uint32_t* Pl;    // [K][LW] limbs of prod_{l<j} p_l
+  const uint32_t* p;      // [K] primes
+  const uint32_t* c;      // [K] (M/p_i)^-1 mod p_i
+  const uint32_t* cc;     // [K] Shoup companions of c
+  const double* pinvd;    // [K] 1/p_i
+  const uint32_t* Mi;     // [K][LW] limbs of M/p_i
+  const uint32_t* Ml;     // [LW] limbs of M
+  const uint32_t* Mh;     // [LW] limbs of floor(M/2)
 };
-// coeffs [K][N] -> out [N][LW]
-void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, cudaStream_t st);
+// coeffs [K][N] -> out [N][LW]; scratch >= 3 N LW words
+void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
+                cudaStream_t st);
 
 // ---- K6: batched gcd mod p (modpoly.py:115-122), interpolation at arbitrary points
 void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_t* gb, const int32_t* db, int Wg,

@@ -114,9 +114,13 @@ def _lc_vanishes(lc, p: int) -> bool:
     return all(c % p == 0 for c in lc)
 
 
-def choose_primes(need_bits_bound: int, lcf, lcg, start: int = 0, table=PRIMES30):
-    """Primes (descending, from ``start``) until prod > 2 * bound."""
-    target = 2 * need_bits_bound
+def choose_primes(bound: int, lcf, lcg, start: int = 0, table=PRIMES30):
+    """Primes (descending, from ``start``) until prod > 4 * bound.
+
+    The reference stops at prod > 2 * bound (modpoly.py:374-375); one more bit
+    of margin keeps |x / M| < 1/4 so the explicit CRT's FP64 rounding of
+    sum_i y_i / p_i is always exact (csrc/ckb_crt.cu)."""
+    target = 4 * bound
     primes, gens = [], []
     mod = 1
     i = start
