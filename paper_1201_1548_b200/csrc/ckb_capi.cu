@@ -339,11 +339,14 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   a.K = K;
   a.values = d_vals;
   a.status = d_status;
+  if ((rc = dbuf("fail", (size_t)K * N + 1, &a.fail_list))) return rc;
+  a.fail_count = a.fail_list + (size_t)K * N;
+  CK(cudaMemsetAsync(a.fail_count, 0, 4, st));
   launch_images(a, st);
   stage_mark(st);
   launch_interp(pl, d_primes, d_vals, d_coeffs, d_a, d_ac, d_S, st);
   stage_mark(st);
-  g.launches += 6;
+  g.launches += 7;
   CK(cudaGetLastError());
   return 0;
 }

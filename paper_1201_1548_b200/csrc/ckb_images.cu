@@ -4,9 +4,11 @@
 // then _zp_resultant of the two univariate images) with:
 //   * the prime's residue coefficients staged once per CTA in shared memory
 //     (all threads of a CTA share the prime; reads are warp broadcasts),
-//   * Shoup-Horner evaluation straight into top-aligned registers,
-//   * the division-free elimination of ckb_resultant.cuh (no inverse in the
-//     loop; one Fermat inverse per image).
+//   * lazy Shoup-Horner evaluation straight into top-aligned registers,
+//   * the fused division-free elimination of ckb_resultant.cuh (no inverse in
+//     the loop; one Fermat inverse per image),
+//   * images whose remainder sequence is not generic appended to a list that
+//     the general warp kernel (ckb_general.cu) recomputes exactly.
 #include "ckb_kernels.cuh"
 #include "ckb_resultant.cuh"
 
@@ -31,7 +33,7 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
   const Prime P = a.primes[pi];
   const uint32_t p = P.p;
   const uint32_t x = a.xpts[(size_t)pi * a.N + t];
-  const uint32_t xc = shoup_comp(x, P);
+  const uint32_t xc = comp_from_mont(to_mont(x, P), P);
 
   const bool sw = a.m < a.n;  // reference swaps so that deg a >= deg b
   const int da = sw ? a.n : a.m, db = sw ? a.m : a.n;
@@ -42,19 +44,59 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
   const int* Adeg = sdeg + (sw ? a.m + 1 : 0);
   const int* Bdeg = sdeg + (sw ? 0 : a.m + 1);
 
+  // Horner of all y-coefficients in lock-step: one dynamic loop over the x
+  // power, every register an independent chain (ILP = m + n + 2).  Rows are
+  // zero-padded to their common length, so a chain that has not started yet
+  // stays 0; the per-chunk max-degree guards only skip work.
+  constexpr int NCH = (MAXD + 4) / 4;
+  int cmA[NCH], cmB[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    int ma = -1, mb = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = 4 * c + k;
+      if (i <= da) ma = max(ma, Adeg[da - i]);
+      if (i <= db) mb = max(mb, Bdeg[db - i]);
+    }
+    cmA[c] = ma;
+    cmB[c] = mb;
+  }
   uint32_t A[MAXD + 1], B[MAXD + 1];
 #pragma unroll
-  for (int i = 0; i <= MAXD; ++i) {
-    A[i] = (i <= da) ? horner(Ares + (da - i) * Astr, Adeg[da - i], x, xc, p) : 0u;
-    B[i] = (i <= db) ? horner(Bres + (db - i) * Bstr, Bdeg[db - i], x, xc, p) : 0u;
+  for (int i = 0; i <= MAXD; ++i) A[i] = B[i] = 0u;
+  const int dmax = max(sw ? a.dgx : a.dfx, sw ? a.dfx : a.dgx);
+  for (int e = dmax; e >= 0; --e) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      if (cmA[c] >= e) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = 4 * c + k;
+          if (i <= MAXD && i <= da) A[i] = shoup_lazy(A[i], x, xc, p) + Ares[(da - i) * Astr + e];
+        }
+      }
+      if (cmB[c] >= e) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = 4 * c + k;
+          if (i <= MAXD && i <= db) B[i] = shoup_lazy(B[i], x, xc, p) + Bres[(db - i) * Bstr + e];
+        }
+      }
+    }
   }
   uint32_t v;
-  if (A[0] == 0u || B[0] == 0u) {
+  if (red4(A[0], p) == 0u || red4(B[0], p) == 0u) {
     atomicOr(a.status, 2u);  // the plan guarantees this never happens
     v = 0u;
   } else {
     const bool neg = sw && ((a.m * a.n) & 1);
-    v = resultant_topaligned<MAXD>(A, da, B, db, neg, P);
+    v = resultant_generic<MAXD>(A, da, B, db, neg, P);
+    if (v == CKB_FAIL) {
+      const uint32_t slot = atomicAdd(a.fail_count, 1u);
+      a.fail_list[slot] = (uint32_t)((size_t)pi * a.N + t);
+      v = 0u;
+    }
   }
   a.values[(size_t)pi * a.N + t] = v;
 }
@@ -74,73 +116,15 @@ void launch_images(const ImageArgs& a, cudaStream_t st) {
   const int maxd = images_maxd(a.m, a.n);
   dim3 grid((a.N + IMG_THREADS - 1) / IMG_THREADS, a.K);
   const size_t smem = (size_t)(a.C + a.m + a.n + 2) * 4;
-#define LAUNCH(D)                                                                          \
-  if (maxd == D) {                                                                         \
-    if (smem > 48 * 1024)                                                                  \
-      cudaFuncSetAttribute(k_images<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_images<D><<<grid, IMG_THREADS, smem, st>>>(a);                                       \
-    return;                                                                                \
+#define LAUNCH(D)                                                                                    \
+  if (maxd == D) {                                                                                   \
+    if (smem > 48 * 1024)                                                                            \
+      cudaFuncSetAttribute(k_images<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    k_images<D><<<grid, IMG_THREADS, smem, st>>>(a);                                                 \
   }
   CKB_MAXD_LIST(LAUNCH)
 #undef LAUNCH
-}
-
-// ---------------------------------------------------------------------------
-// batch of independent univariate resultants (zp_resultant_uni, modpoly.py:156)
-// ---------------------------------------------------------------------------
-template <int MAXD>
-__global__ void __launch_bounds__(IMG_THREADS) k_uni_resultant(const uint32_t* __restrict__ fa,
-                                                              const int32_t* __restrict__ da_,
-                                                              const uint32_t* __restrict__ gb,
-                                                              const int32_t* __restrict__ db_, int W,
-                                                              const Prime* __restrict__ primes,
-                                                              const int32_t* __restrict__ pidx, int Bn,
-                                                              uint32_t* __restrict__ out) {
-  const int b = blockIdx.x * IMG_THREADS + threadIdx.x;
-  if (b >= Bn) return;
-  const Prime P = primes[pidx[b]];
-  int da = da_[b], db = db_[b];
-  if (da < 0 || db < 0) {  // a zero polynomial (modpoly.py:135-136)
-    out[b] = 0u;
-    return;
-  }
-  const uint32_t* fp = fa + (size_t)b * W;
-  const uint32_t* gp = gb + (size_t)b * W;
-  bool neg = false;
-  if (da < db) {  // modpoly.py:138-141
-    neg = (da * db) & 1;
-    const uint32_t* tp = fp; fp = gp; gp = tp;
-    int td = da; da = db; db = td;
-  }
-  uint32_t A[MAXD + 1], B[MAXD + 1];
-#pragma unroll
-  for (int i = 0; i <= MAXD; ++i) {
-    A[i] = (i <= da) ? fp[da - i] : 0u;
-    B[i] = (i <= db) ? gp[db - i] : 0u;
-  }
-  uint32_t v;
-  if (db == 0) {  // modpoly.py:145-146: res * b0^da
-    const uint32_t one = redc(P.r2, P);
-    v = redc(mpow(to_mont(B[0], P), da, one, P), P);
-    if (neg) v = neg_mod(v, P.p);
-  } else {
-    v = resultant_topaligned<MAXD>(A, da, B, db, neg, P);
-  }
-  out[b] = v;
-}
-
-void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t* gb, const int32_t* db, int W,
-                          const Prime* primes, const int32_t* pidx, int B, uint32_t* out, cudaStream_t st) {
-  const int maxd = W - 1;
-  const int bucket = images_maxd(maxd, 0);
-  const int grid = (B + IMG_THREADS - 1) / IMG_THREADS;
-#define LAUNCH(D)                                                                                 \
-  if (bucket == D) {                                                                              \
-    k_uni_resultant<D><<<grid, IMG_THREADS, 0, st>>>(fa, da, gb, db, W, primes, pidx, B, out);    \
-    return;                                                                                       \
-  }
-  CKB_MAXD_LIST(LAUNCH)
-#undef LAUNCH
+  launch_images_fallback(a, st);
 }
 
 }  // namespace ckb

@@ -41,9 +41,13 @@ struct ImageArgs {
   int C, m, n, dfx, dgx, N, K;
   uint32_t* values;        // [K][N]
   uint32_t* status;        // bit 1: an image hit a vanishing leading coefficient
+  uint32_t* fail_list;     // [K*N] flat indices of non-generic images
+  uint32_t* fail_count;    // zeroed before the launch
 };
 int images_maxd(int m, int n);  // template bucket or -1
+// fast generic kernel followed by the general warp kernel on its fail list
 void launch_images(const ImageArgs& a, cudaStream_t st);
+void launch_images_fallback(const ImageArgs& a, cudaStream_t st);
 
 // batch of independent univariate resultants (modpoly.py:156-161)
 // fa/gb: [B][W] padded low-first coefficients; degrees da/db; per-pair prime index

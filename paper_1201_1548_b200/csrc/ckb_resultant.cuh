@@ -2,25 +2,37 @@
 //
 // Behavioural reference: curvekit.modpoly._zp_resultant (pkg/src/curvekit/
 // modpoly.py:132-153), the Euclidean remainder sequence
-//     res = prod_i (-1)^(d_{i-1} d_i) lc(R_i)^(d_{i-1} - d_{i+1}) * lc(R_K)^(d_{K-1}).
-// Here the sequence is computed division-free.  Both operands are kept
-// TOP-ALIGNED in registers (X[i] = coefficient of degree deg X - i), so one
-// elimination step is the same static-index register update for every
-// degree difference:
-//     A[i] <- lc(B) * A[i+1] - A[0] * B[i+1]
-// (this is one step of the Schur algorithm on the rank-2 displacement
-// generators of the Sylvester matrix, with the generators
-// shrinking as the degrees fall and the zero-pivot case handled by look-ahead
-// = a degree drop larger than one).  With P_i = c_i R_i the pseudo-remainders,
-//     P_{i+1} = lc(P_i)^{e_i} c_{i-1} R_{i+1},  e_i = d_{i-1} - d_i + 1,
-// so the reference product is rebuilt from lc(P_i) and c_i with a handful of
-// Montgomery products per remainder and ONE inverse per image.
+//     res(P_{i-1}, P_i) = (-1)^(d_{i-1} d_i) lc(P_i)^(d_{i-1} - d_{i+1}) res(P_i, r_i).
+// This header computes the same value division-free on TOP-ALIGNED registers
+// (X[i] = coefficient of degree deg X - i), so every elimination is a
+// static-index register update.  (One elimination is one step of the Schur
+// algorithm on the rank-2 displacement generators of the Sylvester matrix,
+// PAPER.md:1384-1443, with generators that shrink as the degrees fall.)
+//
+// Division-free remainders P_{i+1} = prem(P_{i-1}, P_i) = L_i^{e_i} r_i, with
+// L_i = lc(P_i) and e_i = d_{i-1} - d_i + 1, turn the reference's product into
+//     res = sgn * prod_i L_i^{(d_{i-1} - d_{i+1}) - e_i d_i} * lc(P_K)^{d_{K-1}}
+// (res(B, c R) = c^deg B res(B, R)); no scale factors need tracking.  On the
+// GENERIC sequence (every remainder drops the degree by exactly one) the
+// exponents are 2 - 2 d_i, so with running products T = prod L_i and
+// Q = prod_j T_j (which equals prod L_i^{d_i}) the whole bookkeeping is two
+// Montgomery products per remainder and one inverse per image.  The two
+// elimination steps of a generic remainder are fused into one sweep:
+//     D''[i] = L^2 D[i+2] - L lc(D) V[i+2] - lc(D') V[i+1]      (3 products)
+// Arithmetic is lazy: for p < 2^30 every register holds a value in [0, 4p)
+// and a Shoup product accepts any 32-bit input, so no reduction is needed
+// per output.  A non-generic image (a leading coefficient vanishing mid-way)
+// returns CKB_FAIL and is recomputed by the general warp kernel.
 #pragma once
 #include "ckb_modarith.cuh"
 
 namespace ckb {
 
-// Montgomery-domain helpers for the bookkeeping scalars
+constexpr uint32_t CKB_FAIL = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t red4(uint32_t x, uint32_t p) {  // [0, 4p) -> [0, p)
+  return red1(red1(x, 2u * p), p);
+}
 __device__ __forceinline__ uint32_t to_mont(uint32_t a, const Prime& P) { return redc((uint64_t)a * P.r2, P); }
 __device__ __forceinline__ uint32_t mmul(uint32_t a, uint32_t b, const Prime& P) { return redc((uint64_t)a * b, P); }
 __device__ __forceinline__ uint32_t mpow(uint32_t a, int e, uint32_t one, const Prime& P) {
@@ -32,125 +44,135 @@ __device__ __forceinline__ uint32_t mpow(uint32_t a, int e, uint32_t one, const 
   }
   return r;
 }
+// Shoup companion from a Montgomery form wm = w R mod p
+__device__ __forceinline__ uint32_t comp_from_mont(uint32_t wm, const Prime& P) { return (0u - wm) * P.pinv; }
 
-// one division-free elimination step on top-aligned registers; `nom` is the
-// nominal degree of A before the step (entries beyond it are zero)
+// single division-free step D <- lb D - lc(D) V (aligned tops); nom = nominal deg D
 template <int MAXD>
-__device__ __forceinline__ void elim_step(uint32_t (&A)[MAXD + 1], const uint32_t (&B)[MAXD + 1], int nom,
-                                          uint32_t L, uint32_t Lc, const Prime& P) {
+__device__ __forceinline__ void step1(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int nom, uint32_t lb,
+                                      uint32_t lbc, const Prime& P) {
   const uint32_t p = P.p;
-  const uint32_t nla = neg_mod(A[0], p);
-  const uint32_t nlac = shoup_comp(nla, P);
+  const uint32_t la = red4(D[0], p);
+  const uint32_t nla = la ? p - la : 0u;
+  const uint32_t nlac = comp_from_mont(to_mont(nla, P), P);
 #pragma unroll
   for (int c = 0; c < (MAXD + 3) / 4; ++c) {
     if (4 * c <= nom) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int i = 4 * c + k;
-        if (i < MAXD) {
-          uint32_t u = red1(shoup_lazy(A[i + 1], L, Lc, p), p);
-          uint32_t v = red1(shoup_lazy(B[i + 1], nla, nlac, p), p);
-          A[i] = red1(u + v, p);
+        if (i < MAXD) D[i] = shoup_lazy(D[i + 1], lb, lbc, p) + shoup_lazy(V[i + 1], nla, nlac, p);
+      }
+    }
+  }
+  D[MAXD] = 0u;
+}
+
+// fused generic remainder: D (nominal deg k+1) <- prem(D, V) (deg k-1), V of deg k.
+// Returns the Montgomery form of lc(V).
+template <int MAXD>
+__device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int k,
+                                          const Prime& P) {
+  const uint32_t p = P.p;
+  const uint32_t lb = red4(V[0], p), la = red4(D[0], p);
+  const uint32_t nla = la ? p - la : 0u;
+  const uint32_t lbm = to_mont(lb, P), nlam = to_mont(nla, P);
+  // lc of the intermediate remainder: la' = lb D[1] - la V[1]
+  const uint32_t d1 = red4(D[1], p), v1 = red4(V[1], p);
+  const uint32_t lap = redc((uint64_t)lbm * d1 + (uint64_t)nlam * v1, P);
+  const uint32_t w1 = redc((uint64_t)lbm * lb, P);                     // lb^2
+  const uint32_t w1c = comp_from_mont(redc((uint64_t)lbm * lbm, P), P);
+  const uint32_t w2 = redc((uint64_t)lbm * nla, P);                    // -lb la
+  const uint32_t w2c = comp_from_mont(redc((uint64_t)lbm * nlam, P), P);
+  const uint32_t w3 = lap ? p - lap : 0u;                               // -la'
+  const uint32_t w3c = comp_from_mont(to_mont(w3, P), P);
+#pragma unroll
+  for (int c = 0; c < (MAXD + 3) / 4; ++c) {
+    if (4 * c <= k + 1) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = 4 * c + j;
+        if (i < MAXD - 1) {
+          const uint32_t t1 = red1(shoup_lazy(D[i + 2], w1, w1c, p), p);
+          const uint32_t t2 = red1(shoup_lazy(V[i + 2], w2, w2c, p), p);
+          D[i] = t1 + t2 + shoup_lazy(V[i + 1], w3, w3c, p);
         }
       }
     }
   }
-  A[MAXD] = 0u;
+  D[MAXD - 1] = 0u;
+  D[MAXD] = 0u;
+  return lbm;
 }
 
-// shift A up until its top entry is nonzero; returns the true degree (-1: zero)
+// res(A, B) for top-aligned A (deg da) and B (deg db), da >= db >= 1 with
+// nonzero leading coefficients; `neg` carries the sign of an initial swap.
+// Returns CKB_FAIL on a non-generic remainder sequence.
 template <int MAXD>
-__device__ __forceinline__ int normalize(uint32_t (&A)[MAXD + 1], int d) {
-  while (d >= 0 && A[0] == 0u) {
-#pragma unroll
-    for (int i = 0; i < MAXD; ++i) A[i] = A[i + 1];
-    A[MAXD] = 0u;
-    --d;
-  }
-  return d;
-}
-
-// Pseudo-remainder of (A, da) by (B, db) in place in A; bookkeeping of the
-// reference product.  Returns the degree of the remainder (-1 if zero).
-template <int MAXD>
-__device__ __forceinline__ int prem_and_account(uint32_t (&A)[MAXD + 1], int da, uint32_t cA,
-                                                const uint32_t (&B)[MAXD + 1], int db, uint32_t cB,
-                                                uint32_t& num, uint32_t& den, uint32_t& cR, bool& neg,
-                                                uint32_t one, const Prime& P) {
-  const uint32_t L = B[0];
-  const uint32_t Lc = shoup_comp(L, P);
-  const int e = da - db + 1;
-  int nom = da;
-  for (int s = 0; s < e; ++s) {
-    elim_step<MAXD>(A, B, nom, L, Lc, P);
-    --nom;
-  }
-  const int dr = normalize<MAXD>(A, db - 1);
-  if (dr < 0) return -1;
+__device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], int da, uint32_t (&B)[MAXD + 1], int db,
+                                                      bool neg, const Prime& P) {
+  const uint32_t p = P.p;
+  const uint32_t one = redc(P.r2, P);  // R mod p
+  // first remainder: e0 single steps (e0 = 1 for m = n)
+  const uint32_t lb = red4(B[0], p);
+  const uint32_t lbm = to_mont(lb, P);
+  const uint32_t lbc = comp_from_mont(lbm, P);
+  const int e0 = da - db + 1;
+  for (int s = 0; s < e0; ++s) step1<MAXD>(A, B, da - s, lb, lbc, P);
+  uint32_t a0 = red4(A[0], p);
+  if (!a0) return CKB_FAIL;
   neg ^= (bool)(da & db & 1);
-  const int x = da - dr;
-  const uint32_t Lm = to_mont(L, P);
-  if (x == 2 && e == 2) {  // the generic step
-    const uint32_t L2 = mmul(Lm, Lm, P);
-    num = mmul(num, L2, P);
-    den = mmul(den, mmul(cB, cB, P), P);
-    cR = mmul(L2, cA, P);
+  const uint32_t l1e = mpow(lbm, e0, one, P);
+  uint32_t num = l1e, den = mpow(l1e, db, one, P);
+  uint32_t T = one, Q = one;
+  int k = db - 1;
+  if (k == 0) {
+    num = mmul(num, to_mont(a0, P), P);  // lc(P_K)^(d_{K-1}), d_{K-1} = db = 1
   } else {
-    num = mmul(num, mpow(Lm, x, one, P), P);
-    den = mmul(den, mpow(cB, x, one, P), P);
-    cR = mmul(mpow(Lm, e, one, P), cA, P);
-  }
-  return dr;
-}
-
-// res(A, B) for top-aligned A (deg da) and B (deg db), da >= db >= 1, both
-// leading coefficients nonzero; `neg` carries the sign of an initial swap.
-template <int MAXD>
-__device__ __forceinline__ uint32_t resultant_topaligned(uint32_t (&A)[MAXD + 1], int da, uint32_t (&B)[MAXD + 1],
-                                                         int db, bool neg, const Prime& P) {
-  const uint32_t one = redc(P.r2, P);  // R mod p = Montgomery 1
-  uint32_t num = one, den = one, cA = one, cB = one, cR = one, resm;
-  for (;;) {
-    // (A, da, cA) dividend, (B, db, cB) divisor, db >= 1
-    int dr = prem_and_account<MAXD>(A, da, cA, B, db, cB, num, den, cR, neg, one, P);
-    if (dr < 0) return 0u;
-    if (dr == 0) {
-      num = mmul(num, mpow(to_mont(A[0], P), db, one, P), P);
-      den = mmul(den, mpow(cR, db, one, P), P);
-      break;
+    for (;;) {
+      // dividend B (deg k+1), divisor A (deg k)
+      uint32_t lm = step2<MAXD>(B, A, k, P);
+      T = mmul(T, lm, P);
+      Q = mmul(Q, T, P);
+      --k;
+      const uint32_t b0 = red4(B[0], p);
+      if (!b0) return CKB_FAIL;
+      if (k == 0) {
+        num = mmul(num, to_mont(b0, P), P);
+        break;
+      }
+      // dividend A (deg k+1), divisor B (deg k)
+      lm = step2<MAXD>(A, B, k, P);
+      T = mmul(T, lm, P);
+      Q = mmul(Q, T, P);
+      --k;
+      a0 = red4(A[0], p);
+      if (!a0) return CKB_FAIL;
+      if (k == 0) {
+        num = mmul(num, to_mont(a0, P), P);
+        break;
+      }
     }
-    // roles swap: (B, db, cB) dividend, (A, dr, cR) divisor
-    uint32_t cR2 = one;
-    int dr2 = prem_and_account<MAXD>(B, db, cB, A, dr, cR, num, den, cR2, neg, one, P);
-    if (dr2 < 0) return 0u;
-    if (dr2 == 0) {
-      num = mmul(num, mpow(to_mont(B[0], P), dr, one, P), P);
-      den = mmul(den, mpow(cR2, dr, one, P), P);
-      break;
-    }
-    da = dr;
-    db = dr2;
-    cA = cR;
-    cB = cR2;
+    num = mmul(num, mmul(T, T, P), P);
+    den = mmul(den, mmul(Q, Q, P), P);
   }
-  // num / den, leave the Montgomery domain; Fermat inverse den^(p-2)
+  // num / den (Fermat inverse in the Montgomery domain), leave the domain
   uint32_t inv = one, b = den;
-  uint32_t ex = P.p - 2;
+  uint32_t ex = p - 2;
   while (ex) {
     if (ex & 1) inv = mmul(inv, b, P);
     ex >>= 1;
     if (ex) b = mmul(b, b, P);
   }
-  resm = mmul(num, inv, P);
-  uint32_t r = redc((uint64_t)resm, P);
-  return neg ? neg_mod(r, P.p) : r;
+  const uint32_t r = redc((uint64_t)mmul(num, inv, P), P);
+  return neg ? neg_mod(r, p) : r;
 }
 
-// Shoup-Horner evaluation of a residue polynomial c[0..deg] at x
-__device__ __forceinline__ uint32_t horner(const uint32_t* c, int deg, uint32_t x, uint32_t xc, uint32_t p) {
+// Lazy Shoup-Horner evaluation of a residue polynomial c[0..deg] at x: [0, 3p)
+__device__ __forceinline__ uint32_t horner_lazy(const uint32_t* c, int deg, uint32_t x, uint32_t xc, uint32_t p) {
   if (deg < 0) return 0u;
   uint32_t acc = c[deg];
-  for (int i = deg - 1; i >= 0; --i) acc = red1(red1(shoup_lazy(acc, x, xc, p), p) + c[i], p);
+  for (int i = deg - 1; i >= 0; --i) acc = shoup_lazy(acc, x, xc, p) + c[i];
   return acc;
 }
 
