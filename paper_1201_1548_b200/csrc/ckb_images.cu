@@ -16,16 +16,48 @@ namespace ckb {
 
 constexpr int IMG_THREADS = 128;
 
+// shared-memory row width of the transposed, top-aligned residue tables
+template <int MAXD>
+struct ImgLayout {
+  static constexpr int NCH = (MAXD + 4) / 4;  // chunks of 4 registers
+  static constexpr int SW = NCH * 4;          // words per x-power row
+};
+
 template <int MAXD>
 __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
-  extern __shared__ uint32_t sm[];
+  using LY = ImgLayout<MAXD>;
+  constexpr int NCH = LY::NCH, SW = LY::SW;
+  extern __shared__ __align__(16) uint32_t sm[];
   const int pi = blockIdx.y;
-  uint32_t* sres = sm;                                  // C residues
-  int* sdeg = reinterpret_cast<int*>(sm + a.C);          // (m+1)+(n+1) degrees
+  const bool sw = a.m < a.n;  // reference swaps so that deg a >= deg b
+  const int da = sw ? a.n : a.m, db = sw ? a.m : a.n;
+  const int offF = 0, offG = (a.m + 1) * (a.dfx + 1);
+  const int offA = sw ? offG : offF, offB = sw ? offF : offG;
+  const int Astr = sw ? a.dgx + 1 : a.dfx + 1, Bstr = sw ? a.dfx + 1 : a.dgx + 1;
+  const int16_t* Adeg = a.degs + (sw ? a.m + 1 : 0);
+  const int16_t* Bdeg = a.degs + (sw ? 0 : a.m + 1);
+  const int dmax = max(a.dfx, a.dgx);
+  // TA[e][i] = coefficient of x^e in the y-coefficient of degree da - i (top-aligned),
+  // zero beyond each row; maskA[e] = chunks of registers with a term at x^e
+  uint32_t* TA = sm;
+  uint32_t* TB = sm + (dmax + 1) * SW;
+  uint32_t* maskA = sm + 2 * (dmax + 1) * SW;
+  uint32_t* maskB = maskA + (dmax + 1);
   const uint32_t* gres = a.red + (size_t)pi * a.C;
-  for (int i = threadIdx.x; i < a.C; i += IMG_THREADS) sres[i] = gres[i];
-  const int nd = a.m + a.n + 2;
-  for (int i = threadIdx.x; i < nd; i += IMG_THREADS) sdeg[i] = a.degs[i];
+  for (int idx = threadIdx.x; idx < (dmax + 1) * SW; idx += IMG_THREADS) {
+    const int e = idx / SW, i = idx % SW;
+    TA[idx] = (i <= da && e < Astr) ? gres[offA + (da - i) * Astr + e] : 0u;
+    TB[idx] = (i <= db && e < Bstr) ? gres[offB + (db - i) * Bstr + e] : 0u;
+  }
+  for (int e = threadIdx.x; e <= dmax; e += IMG_THREADS) {
+    uint32_t ma = 0, mb = 0;
+    for (int i = 0; i <= MAXD; ++i) {
+      if (i <= da && Adeg[da - i] >= e) ma |= 1u << (i >> 2);
+      if (i <= db && Bdeg[db - i] >= e) mb |= 1u << (i >> 2);
+    }
+    maskA[e] = ma;
+    maskB[e] = mb;
+  }
   __syncthreads();
 
   const int t = blockIdx.x * IMG_THREADS + threadIdx.x;
@@ -35,53 +67,32 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
   const uint32_t x = a.xpts[(size_t)pi * a.N + t];
   const uint32_t xc = comp_from_mont(to_mont(x, P), P);
 
-  const bool sw = a.m < a.n;  // reference swaps so that deg a >= deg b
-  const int da = sw ? a.n : a.m, db = sw ? a.m : a.n;
-  const int offF = 0, offG = (a.m + 1) * (a.dfx + 1);
-  const uint32_t* Ares = sres + (sw ? offG : offF);
-  const uint32_t* Bres = sres + (sw ? offF : offG);
-  const int Astr = sw ? a.dgx + 1 : a.dfx + 1, Bstr = sw ? a.dfx + 1 : a.dgx + 1;
-  const int* Adeg = sdeg + (sw ? a.m + 1 : 0);
-  const int* Bdeg = sdeg + (sw ? 0 : a.m + 1);
-
   // Horner of all y-coefficients in lock-step: one dynamic loop over the x
-  // power, every register an independent chain (ILP = m + n + 2).  Rows are
-  // zero-padded to their common length, so a chain that has not started yet
-  // stays 0; the per-chunk max-degree guards only skip work.
-  constexpr int NCH = (MAXD + 4) / 4;
-  int cmA[NCH], cmB[NCH];
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    int ma = -1, mb = -1;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = 4 * c + k;
-      if (i <= da) ma = max(ma, Adeg[da - i]);
-      if (i <= db) mb = max(mb, Bdeg[db - i]);
-    }
-    cmA[c] = ma;
-    cmB[c] = mb;
-  }
+  // power, every register an independent chain (ILP = m + n + 2); each chunk
+  // of 4 coefficients is one 16-byte broadcast load.  A chain that has not
+  // started yet multiplies 0, so the masks only skip work.
   uint32_t A[MAXD + 1], B[MAXD + 1];
 #pragma unroll
   for (int i = 0; i <= MAXD; ++i) A[i] = B[i] = 0u;
-  const int dmax = max(sw ? a.dgx : a.dfx, sw ? a.dfx : a.dgx);
   for (int e = dmax; e >= 0; --e) {
+    const uint4* ta = reinterpret_cast<const uint4*>(TA + e * SW);
+    const uint4* tb = reinterpret_cast<const uint4*>(TB + e * SW);
+    const uint32_t mA = maskA[e], mB = maskB[e];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
-      if (cmA[c] >= e) {
+      if (mA & (1u << c)) {
+        const uint4 v = ta[c];
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int i = 4 * c + k;
-          if (i <= MAXD && i <= da) A[i] = shoup_lazy(A[i], x, xc, p) + Ares[(da - i) * Astr + e];
-        }
+        for (int k = 0; k < 4; ++k)
+          if (4 * c + k <= MAXD) A[4 * c + k] = shoup_lazy(A[4 * c + k], x, xc, p) + vv[k];
       }
-      if (cmB[c] >= e) {
+      if (mB & (1u << c)) {
+        const uint4 v = tb[c];
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int i = 4 * c + k;
-          if (i <= MAXD && i <= db) B[i] = shoup_lazy(B[i], x, xc, p) + Bres[(db - i) * Bstr + e];
-        }
+        for (int k = 0; k < 4; ++k)
+          if (4 * c + k <= MAXD) B[4 * c + k] = shoup_lazy(B[4 * c + k], x, xc, p) + vv[k];
       }
     }
   }
@@ -115,9 +126,10 @@ int images_maxd(int m, int n) {
 void launch_images(const ImageArgs& a, cudaStream_t st) {
   const int maxd = images_maxd(a.m, a.n);
   dim3 grid((a.N + IMG_THREADS - 1) / IMG_THREADS, a.K);
-  const size_t smem = (size_t)(a.C + a.m + a.n + 2) * 4;
+  const int dmax = a.dfx > a.dgx ? a.dfx : a.dgx;
 #define LAUNCH(D)                                                                                    \
   if (maxd == D) {                                                                                   \
+    const size_t smem = (size_t)(2 * (dmax + 1) * ImgLayout<D>::SW + 2 * (dmax + 1)) * 4;          \
     if (smem > 48 * 1024)                                                                            \
       cudaFuncSetAttribute(k_images<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
     k_images<D><<<grid, IMG_THREADS, smem, st>>>(a);                                                 \
