@@ -71,16 +71,17 @@ __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uin
     }
     __syncthreads();
   }
+  // limb-major layout S[l][0..2][k]: the carry pass reads it coalesced
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int k = k0 + tk + a, l = l0 + tl + b;
       if (k < N && l < LW) {
-        uint32_t* o = S + ((size_t)k * LW + l) * 3;
+        uint32_t* o = S + (size_t)l * 3 * N + k;
         o[0] = (uint32_t)lo[a][b];
-        o[1] = (uint32_t)(lo[a][b] >> 32);
-        o[2] = hi[a][b];
+        o[N] = (uint32_t)(lo[a][b] >> 32);
+        o[2 * N] = hi[a][b];
       }
     }
 }
@@ -90,35 +91,52 @@ __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uin
 __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, const uint32_t* __restrict__ r, int N,
                                                    const uint32_t* __restrict__ S, uint32_t* __restrict__ out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= N) return;
+  __shared__ uint32_t stage[128][33];
+  const int tid = threadIdx.x, k0 = blockIdx.x * blockDim.x;
+  const bool act = k < N;
   const int K = T.K, LW = T.LW;
   double s = 0.0;
-  for (int i = 0; i < K; ++i) {
-    const uint32_t p = T.p[i];
-    const uint32_t y = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
-    s = fma((double)y, T.pinvd[i], s);
+  if (act) {
+#pragma unroll 8
+    for (int i = 0; i < K; ++i) {
+      const uint32_t p = T.p[i];
+      const uint32_t y = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
+      s = fma((double)y, T.pinvd[i], s);
+    }
   }
   const uint64_t q = (uint64_t)llrint(s);
-  const uint32_t* Sk = S + (size_t)k * LW * 3;
-  uint32_t* ok = out + (size_t)k * LW;
   // carry = (c_hi:c_lo) signed 128-bit; value at limb l = S_l - q M_l + carry
   long long c_hi = 0;
   unsigned long long c_lo = 0;
-  for (int l = 0; l < LW; ++l) {
-    const unsigned long long s_lo = (unsigned long long)Sk[3 * l] | ((unsigned long long)Sk[3 * l + 1] << 32);
-    const long long s_hi = Sk[3 * l + 2];
-    const unsigned long long qm = q * (unsigned long long)T.Ml[l];  // < 2^44
-    // t = s - qm + carry
-    unsigned long long t_lo = s_lo - qm;
-    long long t_hi = s_hi - (long long)(s_lo < qm);
-    const unsigned long long u = t_lo + c_lo;
-    t_hi += c_hi + (long long)(u < t_lo);
-    t_lo = u;
-    ok[l] = (uint32_t)t_lo;
-    // carry = t >> 32 (arithmetic)
-    c_lo = (t_lo >> 32) | ((unsigned long long)t_hi << 32);
-    c_hi = t_hi >> 32;
+  for (int l0 = 0; l0 < LW; l0 += 32) {
+    if (act) {
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const int l = l0 + j;
+        if (l >= LW) break;
+        const uint32_t* Sl = S + (size_t)l * 3 * N + k;
+        const unsigned long long s_lo = (unsigned long long)Sl[0] | ((unsigned long long)Sl[N] << 32);
+        const long long s_hi = Sl[2 * N];
+        const unsigned long long qm = q * (unsigned long long)T.Ml[l];  // < 2^44
+        unsigned long long t_lo = s_lo - qm;  // t = s - qm + carry
+        long long t_hi = s_hi - (long long)(s_lo < qm);
+        const unsigned long long u = t_lo + c_lo;
+        t_hi += c_hi + (long long)(u < t_lo);
+        t_lo = u;
+        stage[tid][j] = (uint32_t)t_lo;
+        c_lo = (t_lo >> 32) | ((unsigned long long)t_hi << 32);  // carry = t >> 32
+        c_hi = t_hi >> 32;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < 128 * 32; e += blockDim.x) {  // coalesced rows
+      const int rr = e >> 5, j = e & 31;
+      if (k0 + rr < N && l0 + j < LW) out[(size_t)(k0 + rr) * LW + l0 + j] = stage[rr][j];
+    }
+    __syncthreads();
   }
+  if (!act) return;
+  uint32_t* ok = out + (size_t)k * LW;
   // Exactness guard for callers without the 4x margin (crt_reconstruct on
   // arbitrary residues): if s was near a half-integer, q may be off by one;
   // fold x into [-floor(M/2), floor(M/2)] exactly.  Never taken when M > 4 bound.
