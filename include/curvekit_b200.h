@@ -85,12 +85,13 @@ int ckb_gcd_mod_batch(const uint32_t* fa, const int32_t* da, int Wf, const uint3
 int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const uint32_t* primes, int P,
                       const int32_t* pidx, int B, uint32_t* out);
 
-/* Device-pointer stages for the multi-GPU driver (one process per GPU).
+/* Device-pointer stages for the multi-GPU driver (one process per GPU); primes
+ * and gens are HOST arrays (they key the cached interpolation plan).
  * stream: a cudaStream_t or NULL for the context stream.
  * modular_images: limbs/degs on device (h_degs: host copy) -> d_coeffs [K][N]
  * residues of res's coefficients for this rank's primes. */
 int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
-                           int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* d_gens, int K, int N,
+                           int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* gens, int K, int N,
                            uint32_t* d_coeffs, uint32_t* d_status, void* stream);
 int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, int LW, uint32_t* d_out,
                 void* stream);
@@ -98,7 +99,7 @@ int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, 
 /* Whole pipeline on device buffers (inputs already resident in HBM):
  * same arguments as ckb_biv_resultant with d_ pointers; d_out [N][LW]. */
 int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
-                          int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* d_gens, int K, int N, int LW,
+                          int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* gens, int K, int N, int LW,
                           uint32_t* d_out, uint32_t* d_status, void* stream);
 
 /* Instrumentation: record CUDA events between the stages of the next pipeline

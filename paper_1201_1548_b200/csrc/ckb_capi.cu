@@ -285,50 +285,112 @@ int ensure_ready() {
 
 cudaStream_t pick_stream(void* s) { return s ? (cudaStream_t)s : g.stream; }
 
-// plan buffers for K primes x N points
-int plan_bufs(int K, int N, InterpPlan* pl) {
-  int rc = 0;
-  pl->K = K;
-  pl->N = N;
-  const size_t kn = (size_t)K * N, kn1 = (size_t)K * (N + 1);
-  if ((rc = dbuf("pl.xpts", kn, &pl->xpts))) return rc;
-  if ((rc = dbuf("pl.hC", 2 * kn, &pl->hC))) return rc;
-  if ((rc = dbuf("pl.z", kn, &pl->z))) return rc;
-  if ((rc = dbuf("pl.hCinv", kn, &pl->hCinv))) return rc;
-  if ((rc = dbuf("pl.Mt", kn1, &pl->Mt))) return rc;
-  if ((rc = dbuf("pl.Mtc", kn1, &pl->Mtc))) return rc;
-  if ((rc = dbuf("pl.cinv", kn, &pl->cinv))) return rc;
-  if ((rc = dbuf("pl.phi", kn1, &pl->phi))) return rc;
-  if ((rc = dbuf("pl.iphi", kn1, &pl->iphi))) return rc;
-  if ((rc = dbuf("pl.cval", (size_t)K, &pl->cval))) return rc;
+// ---- interpolation plans, cached per (primes, generators, N) -----------------
+struct PlanEntry {
+  std::vector<uint32_t> primes, gens;
+  int N = 0;
+  InterpPlan pl;
+  void* blob = nullptr;
+  uint64_t last_use = 0;
+};
+std::vector<PlanEntry> g_plans;
+
+int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int N, InterpPlan* out) {
+  for (auto& e : g_plans)
+    if (e.N == N && (int)e.primes.size() == K && !memcmp(e.primes.data(), primes, 4 * (size_t)K) &&
+        !memcmp(e.gens.data(), gens, 4 * (size_t)K)) {
+      e.last_use = ++g.tick;
+      *out = e.pl;
+      return 0;
+    }
+  int logL = 0;
+  while ((1 << logL) < 2 * N - 1) ++logL;
+  if (logL > 14) return fail("interpolation supports N <= 8192 points (NTT length <= 2^14)", -2);
+  const uint32_t L = 1u << logL;
+  for (int i = 0; i < K; ++i)
+    if ((primes[i] - 1) % L) return fail("pipeline primes must be 1 mod the NTT length (use PRIMES30)", -2);
+  if (g_plans.size() >= 4) {
+    size_t v = 0;
+    for (size_t i = 1; i < g_plans.size(); ++i)
+      if (g_plans[i].last_use < g_plans[v].last_use) v = i;
+    cudaFree(g_plans[v].blob);
+    g_plans.erase(g_plans.begin() + v);
+  }
+  PlanEntry e;
+  e.primes.assign(primes, primes + K);
+  e.gens.assign(gens, gens + K);
+  e.N = N;
+  InterpPlan& pl = e.pl;
+  pl.N = N;
+  pl.K = K;
+  pl.L = (int)L;
+  pl.logL = logL;
+  const size_t kn = (size_t)K * N, kn1 = (size_t)K * (N + 1), kl = (size_t)K * L, kh = kl / 2;
+  const size_t words = kn * 8 + kn1 * 3 + kh * 4 + kl * 4 + K + K * 3 + 64;
+  CK(cudaMalloc(&e.blob, 4 * words));
+  uint32_t* b = (uint32_t*)e.blob;
+  auto take = [&](size_t n) { uint32_t* r = b; b += n; return r; };
+  pl.xq = take(kn);
+  pl.hC = take(2 * kn);
+  pl.hCinv = take(kn);
+  pl.z = take(kn);
+  pl.zc = take(kn);
+  pl.sS = take(kn);
+  pl.sSc = take(kn);
+  pl.Mt = take(kn1);
+  pl.phi = take(kn1);
+  pl.iphi = take(kn1);
+  pl.W = take(kh);
+  pl.Wc = take(kh);
+  pl.Wi = take(kh);
+  pl.Wic = take(kh);
+  pl.Hf = take(kl);
+  pl.Hfc = take(kl);
+  pl.Mf = take(kl);
+  pl.Mfc = take(kl);
+  pl.Linv = take(K);
+  uint32_t* d_gens = take(K);
+  Prime* d_primes = reinterpret_cast<Prime*>(take((size_t)K * 3));
+  std::vector<Prime> hp(K);
+  for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
+  CK(cudaMemcpy(d_gens, gens, 4 * (size_t)K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_primes, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice));
+  launch_plan_base(d_primes, d_gens, pl, g.stream);
+  launch_plan_ntt(d_primes, d_gens, pl, g.stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(g.stream));
+  e.last_use = ++g.tick;
+  g_plans.push_back(e);
+  *out = pl;
   return 0;
 }
 
 // the modular part of the pipeline on device buffers:
-// limbs -> residues -> plan -> images -> interpolated coefficients [K][N]
+// limbs -> residues -> choose c -> images -> interpolated coefficients [K][N]
 int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
-                  int n, int dfx, int dgx, const Prime* d_primes, const uint32_t* d_gens, int K, int N,
-                  uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st) {
+                  int n, int dfx, int dgx, const Prime* d_primes, const uint32_t* h_primes, const uint32_t* h_gens,
+                  int K, int N, uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st) {
   if (images_maxd(m, n) < 0) return fail("y-degree above 64 is not supported by the image kernel", -2);
-  uint32_t *d_red, *d_vals, *d_a, *d_ac, *d_S;
+  for (int i = 0; i < K; ++i)
+    if (h_primes[i] >= (1u << 30)) return fail("pipeline primes must be below 2^30", -2);
+  uint32_t *d_red, *d_vals, *d_cval;
   int rc;
+  InterpPlan pl;
+  if ((rc = get_plan(h_primes, h_gens, K, N, &pl))) return rc;
   if ((rc = dbuf("red", (size_t)K * C, &d_red))) return rc;
   if ((rc = dbuf("vals", (size_t)K * N, &d_vals))) return rc;
-  if ((rc = dbuf("ia", (size_t)K * N, &d_a))) return rc;
-  if ((rc = dbuf("iac", (size_t)K * N, &d_ac))) return rc;
-  if ((rc = dbuf("iS", (size_t)K * N, &d_S))) return rc;
-  InterpPlan pl;
-  if ((rc = plan_bufs(K, N, &pl))) return rc;
+  if ((rc = dbuf("cval", (size_t)K, &d_cval))) return rc;
   stage_mark(st);
   launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
   stage_mark(st);
   const int lcf_off = m * (dfx + 1), lcg_off = (m + 1) * (dfx + 1) + n * (dgx + 1);
-  launch_plan(d_primes, d_gens, K, N, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], pl, d_status, st);
+  launch_choose_c(d_primes, pl, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], d_cval, d_status, st);
   stage_mark(st);
   ImageArgs a;
   a.red = d_red;
   a.degs = d_degs;
-  a.xpts = pl.xpts;
+  a.xq = pl.xq;
+  a.cval = d_cval;
   a.primes = d_primes;
   a.C = C;
   a.m = m;
@@ -344,9 +406,9 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   CK(cudaMemsetAsync(a.fail_count, 0, 4, st));
   launch_images(a, st);
   stage_mark(st);
-  launch_interp(pl, d_primes, d_vals, d_coeffs, d_a, d_ac, d_S, st);
+  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st);
   stage_mark(st);
-  g.launches += 7;
+  g.launches += 5;
   CK(cudaGetLastError());
   return 0;
 }
@@ -391,6 +453,8 @@ int ckb_shutdown(void) {
   }
   for (auto& e : g_pcache) cudaFree(e.d);
   g_pcache.clear();
+  for (auto& e : g_plans) cudaFree(e.blob);
+  g_plans.clear();
   g.dev.clear();
   g.host.clear();
   g.crt.clear();
@@ -423,10 +487,9 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   memcpy(hb, limbs, 4 * nl);
   memcpy(hb + 4 * nl, gens, 4 * (size_t)K);
   memcpy(hb + 4 * nl + 4 * (size_t)K, degs, 2 * nd);
-  uint32_t *d_limbs, *d_gens, *d_coeffs, *d_out, *d_status;
+  uint32_t *d_limbs, *d_coeffs, *d_out, *d_status;
   int16_t* d_degs;
   if ((rc = dbuf("limbs", nl, &d_limbs))) return rc;
-  if ((rc = dbuf("gens", (size_t)K, &d_gens))) return rc;
   if ((rc = dbuf("degs", nd, &d_degs))) return rc;
   if ((rc = dbuf("coeffs", (size_t)K * N, &d_coeffs))) return rc;
   if ((rc = dbuf("out", (size_t)N * LW, &d_out))) return rc;
@@ -435,18 +498,17 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   if ((rc = get_crt(primes, K, LW, &ce))) return rc;
   CK(cudaEventRecord(g.ev0, st));
   CK(cudaMemcpyAsync(d_limbs, hb, 4 * nl, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_gens, hb + 4 * nl, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_degs, hb + 4 * nl + 4 * (size_t)K, 2 * nd, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(d_status, 0, 4, st));
   g.nsev = 0;
-  if ((rc = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, d_gens, K, N, d_coeffs,
+  if ((rc = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
                           d_status, st)))
     return rc;
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
   launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
   stage_mark(st);
-  g.launches += 1;
+  g.launches += 2;
   CK(cudaGetLastError());
   uint8_t* ho = (uint8_t*)h_out;
   CK(cudaMemcpyAsync(ho, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
@@ -528,7 +590,7 @@ int ckb_crt_lift(const uint32_t* residues, int K, int N, const uint32_t* primes,
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
   launch_crt(ce->t, d_res, N, d_out, d_crtS, st);
-  g.launches += 1;
+  g.launches += 2;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -536,29 +598,14 @@ int ckb_crt_lift(const uint32_t* residues, int K, int N, const uint32_t* primes,
 }
 
 int ckb_interp_plan_points(const uint32_t* primes, const uint32_t* gens, int K, int N, uint32_t* xpts) {
-  // the planned points for constant leading coefficients (c = 1): x_t = q^t
+  // the planned evaluation points for constant leading coefficients (c = 1): x_t = q^t
   std::lock_guard<std::mutex> lk(g_mu);
   int rc;
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, K))) return rc;
-  cudaStream_t st = g.stream;
-  Prime* d_primes;
-  uint32_t *d_gens, *d_red, *d_status;
-  if ((rc = upload_primes(primes, K, &d_primes))) return rc;
-  if ((rc = dbuf("p.gens", (size_t)K, &d_gens))) return rc;
-  if ((rc = dbuf("p.red", (size_t)K * 2, &d_red))) return rc;
-  if ((rc = dbuf("p.status", 1, &d_status))) return rc;
-  std::vector<uint32_t> ones((size_t)K * 2, 1u);
-  CK(cudaMemcpyAsync(d_gens, gens, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_red, ones.data(), 4 * (size_t)K * 2, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(d_status, 0, 4, st));
   InterpPlan pl;
-  if ((rc = plan_bufs(K, N, &pl))) return rc;
-  launch_plan(d_primes, d_gens, K, N, d_red, 2, 0, 0, 1, 0, pl, d_status, st);
-  g.launches += 1;
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(xpts, pl.xpts, 4 * (size_t)K * N, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if ((rc = get_plan(primes, gens, K, N, &pl))) return rc;
+  CK(cudaMemcpy(xpts, pl.xq, 4 * (size_t)K * N, cudaMemcpyDeviceToHost));
   return 0;
 }
 
@@ -570,27 +617,19 @@ int ckb_interp_geometric(const uint32_t* values, const uint32_t* primes, const u
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, K))) return rc;
   cudaStream_t st = g.stream;
+  InterpPlan pl;
+  if ((rc = get_plan(primes, gens, K, N, &pl))) return rc;
   Prime* d_primes;
-  uint32_t *d_gens, *d_red, *d_status, *d_vals, *d_coeffs, *d_a, *d_ac, *d_S;
-  if ((rc = upload_primes(primes, K, &d_primes))) return rc;
-  if ((rc = dbuf("p.gens", (size_t)K, &d_gens))) return rc;
-  if ((rc = dbuf("p.red", (size_t)K * 2, &d_red))) return rc;
-  if ((rc = dbuf("p.status", 1, &d_status))) return rc;
+  uint32_t *d_vals, *d_coeffs, *d_cval;
+  if ((rc = get_primes_dev(primes, K, &d_primes))) return rc;
   if ((rc = dbuf("i.vals", (size_t)K * N, &d_vals))) return rc;
   if ((rc = dbuf("i.coeffs", (size_t)K * N, &d_coeffs))) return rc;
-  if ((rc = dbuf("ia", (size_t)K * N, &d_a))) return rc;
-  if ((rc = dbuf("iac", (size_t)K * N, &d_ac))) return rc;
-  if ((rc = dbuf("iS", (size_t)K * N, &d_S))) return rc;
-  std::vector<uint32_t> ones((size_t)K * 2, 1u);
-  CK(cudaMemcpyAsync(d_gens, gens, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_red, ones.data(), 4 * (size_t)K * 2, cudaMemcpyHostToDevice, st));
+  if ((rc = dbuf("i.cval", (size_t)K, &d_cval))) return rc;
+  std::vector<uint32_t> ones((size_t)K, 1u);
+  CK(cudaMemcpyAsync(d_cval, ones.data(), 4 * (size_t)K, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_vals, values, 4 * (size_t)K * N, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(d_status, 0, 4, st));
-  InterpPlan pl;
-  if ((rc = plan_bufs(K, N, &pl))) return rc;
-  launch_plan(d_primes, d_gens, K, N, d_red, 2, 0, 0, 1, 0, pl, d_status, st);
-  launch_interp(pl, d_primes, d_vals, d_coeffs, d_a, d_ac, d_S, st);
-  g.launches += 4;
+  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st);
+  g.launches += 1;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(coeffs, d_coeffs, 4 * (size_t)K * N, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -664,7 +703,7 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
 
 // ---- device-pointer entry points for the multi-GPU driver -------------------
 int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
-                           int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* d_gens, int K, int N,
+                           int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* gens, int K, int N,
                            uint32_t* d_coeffs, uint32_t* d_status, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   int rc;
@@ -674,7 +713,7 @@ int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t*
   Prime* d_primes;
   if ((rc = get_primes_dev(primes, K, &d_primes))) return rc;
   g.nsev = 0;
-  return modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, d_primes, d_gens, K, N, d_coeffs, d_status,
+  return modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, d_primes, primes, gens, K, N, d_coeffs, d_status,
                        st);
 }
 
@@ -690,13 +729,13 @@ int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, 
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
   launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
-  g.launches += 1;
+  g.launches += 2;
   CK(cudaGetLastError());
   return 0;
 }
 
 int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
-                          int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* d_gens, int K, int N, int LW,
+                          int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* gens, int K, int N, int LW,
                           uint32_t* d_out, uint32_t* d_status, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   int rc;
@@ -709,14 +748,14 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
   uint32_t* d_coeffs;
   if ((rc = dbuf("coeffs", (size_t)K * N, &d_coeffs))) return rc;
   g.nsev = 0;
-  if ((rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, d_gens, K, N, d_coeffs,
+  if ((rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
                           d_status, st)))
     return rc;
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
   launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
   stage_mark(st);
-  g.launches += 1;
+  g.launches += 2;
   CK(cudaGetLastError());
   return 0;
 }

@@ -110,14 +110,23 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, const uint32_t* 
   unsigned long long c_lo = 0;
   for (int l0 = 0; l0 < LW; l0 += 32) {
     if (act) {
-#pragma unroll 4
+      // issue every load of the chunk before the (sequential) carry chain
+      uint32_t v0[32], v1[32], v2[32], ml[32];
+#pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int l = l0 + j;
-        if (l >= LW) break;
-        const uint32_t* Sl = S + (size_t)l * 3 * N + k;
-        const unsigned long long s_lo = (unsigned long long)Sl[0] | ((unsigned long long)Sl[N] << 32);
-        const long long s_hi = Sl[2 * N];
-        const unsigned long long qm = q * (unsigned long long)T.Ml[l];  // < 2^44
+        const bool in = l < LW;
+        const uint32_t* Sl = S + (size_t)(in ? l : 0) * 3 * N + k;
+        v0[j] = in ? Sl[0] : 0u;
+        v1[j] = in ? Sl[N] : 0u;
+        v2[j] = in ? Sl[2 * N] : 0u;
+        ml[j] = in ? T.Ml[l] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const unsigned long long s_lo = (unsigned long long)v0[j] | ((unsigned long long)v1[j] << 32);
+        const long long s_hi = v2[j];
+        const unsigned long long qm = q * (unsigned long long)ml[j];  // < 2^44
         unsigned long long t_lo = s_lo - qm;  // t = s - qm + carry
         long long t_hi = s_hi - (long long)(s_lo < qm);
         const unsigned long long u = t_lo + c_lo;

@@ -77,7 +77,9 @@ __global__ void k_images_fallback(ImageArgs a, int W) {
     const int pi = (int)(flat / (uint32_t)a.N);
     const Prime P = a.primes[pi];
     const uint32_t p = P.p;
-    const uint32_t x = a.xpts[flat];
+    const uint32_t c = a.cval[pi];
+    uint32_t x = a.xq[flat];
+    if (c != 1u) x = shoup(x, c, shoup_comp(c, P), p);
     const uint32_t xc = shoup_comp(x, P);
     const uint32_t* res = a.red + (size_t)pi * a.C;
     const int offG = (a.m + 1) * (a.dfx + 1);

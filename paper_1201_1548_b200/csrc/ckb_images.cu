@@ -64,7 +64,9 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
   if (t >= a.N) return;
   const Prime P = a.primes[pi];
   const uint32_t p = P.p;
-  const uint32_t x = a.xpts[(size_t)pi * a.N + t];
+  const uint32_t c = a.cval[pi];
+  uint32_t x = a.xq[(size_t)pi * a.N + t];
+  if (c != 1u) x = shoup(x, c, shoup_comp(c, P), p);  // x_t = c q^t
   const uint32_t xc = comp_from_mont(to_mont(x, P), P);
 
   // Horner of all y-coefficients in lock-step: one dynamic loop over the x

@@ -3,101 +3,157 @@
 // with a Fermat inverse inside the O(N^2) loop (pkg/src/curvekit/
 // modpoly.py:164-185) by the Lagrange form with closed-form weights:
 //   P~(y) = sum_t u_t M~(y)/(y - q^t),  M~(y) = prod_t (y - q^t),  u_t = v_t / M~'(q^t)
-//   P~_k  = sum_{l>k} M~_l S_{l-k-1},   S_e = sum_t u_t q^(t e)
-//   q^(t e) = q^C(t+e,2) q^-C(t,2) q^-C(e,2)   (chirp identity)
-// so both O(N^2) stages are structured (Hankel, then triangular Toeplitz)
-// products against per-prime plan tables, fully parallel over the output
-// index, with no inverse anywhere.  P_k = P~_k c^-k undoes the scaling.
+//   P~_k  = sum_{j} S_j M~_{k+1+j},     S_e = sum_t u_t q^(t e)
+//   q^(t e) = q^C(t+e,2) q^-C(t,2) q^-C(e,2)             (chirp identity)
+// Both sums are correlations with per-(prime, N) constant sequences, done as
+// cyclic convolutions of length L = 2^ceil(log2(2N-1)) with NTTs (our primes
+// are 1 mod 2^14): 4 transforms of length L per prime instead of 1.5 N^2
+// products.  The transforms of the constant operands live in the cached plan.
+// P_k = P~_k c^-k undoes the point scale.
 #include "ckb_kernels.cuh"
+#include "ckb_ntt.cuh"
 
 namespace ckb {
 
-constexpr int INT_THREADS = 128;
+constexpr int NTT_THREADS = 512;
+constexpr int MAX_PER_THREAD = 16;  // N <= 16 * 512
 
-// acc < p * 2^32  ->  acc mod p
-__device__ __forceinline__ uint32_t mod64(uint64_t acc, const Prime& P) {
-  return redc((uint64_t)redc(acc, P) * P.r2, P);
-}
-
-// a_t = v_t * z_t, with its Shoup companion
-__global__ void k_interp_prologue(InterpPlan plan, const Prime* __restrict__ primes,
-                                  const uint32_t* __restrict__ values, uint32_t* __restrict__ a,
-                                  uint32_t* __restrict__ ac) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x, pi = blockIdx.y, N = plan.N;
-  if (t >= N) return;
-  const Prime P = primes[pi];
-  const size_t o = (size_t)pi * N + t;
-  const uint32_t v = mul_mod(values[o], plan.z[o], P);
-  a[o] = v;
-  ac[o] = shoup_comp(v, P);
-}
-
-// S_e = q^-C(e,2) * sum_t a_t q^C(t+e,2)
-__global__ void __launch_bounds__(INT_THREADS) k_interp_hankel(InterpPlan plan, const Prime* __restrict__ primes,
-                                                               const uint32_t* __restrict__ a,
-                                                               const uint32_t* __restrict__ ac,
-                                                               uint32_t* __restrict__ S) {
-  extern __shared__ uint32_t sm[];
-  const int N = plan.N, pi = blockIdx.y, e0 = blockIdx.x * INT_THREADS;
-  uint32_t* sa = sm;
-  uint32_t* sac = sm + N;
-  uint32_t* sh = sm + 2 * N;  // hC[e0 .. e0 + INT_THREADS + N - 1)
-  const size_t oN = (size_t)pi * N, o2N = (size_t)pi * 2 * N;
-  for (int i = threadIdx.x; i < N; i += INT_THREADS) {
-    sa[i] = a[oN + i];
-    sac[i] = ac[oN + i];
-  }
-  const int hn = min(INT_THREADS + N, 2 * N - e0);
-  for (int i = threadIdx.x; i < hn; i += INT_THREADS) sh[i] = plan.hC[o2N + e0 + i];
-  __syncthreads();
-  const int e = e0 + threadIdx.x;
-  if (e >= N) return;
+// plan, part 1: twiddles, 1/L, and the Shoup companions of the pointwise tables
+__global__ void __launch_bounds__(NTT_THREADS) k_plan_twiddles(const Prime* __restrict__ primes,
+                                                               const uint32_t* __restrict__ gens, InterpPlan plan) {
+  const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pi];
   const uint32_t p = P.p;
-  uint64_t acc = 0;
-  const uint32_t* hh = sh + threadIdx.x;
-#pragma unroll 4
-  for (int t = 0; t < N; ++t) acc += shoup_lazy(hh[t], sa[t], sac[t], p);
-  S[oN + e] = mul_mod(mod64(acc, P), plan.hCinv[oN + e], P);
+  const int N = plan.N, L = plan.L, half = L >> 1;
+  const uint32_t w = pow_mod(gens[pi] % p, (uint64_t)(p - 1) >> plan.logL, P);  // primitive L-th root
+  const uint32_t wi = inv_mod(w, P);
+  const uint32_t wc = shoup_comp(w, P), wic = shoup_comp(wi, P);
+  const size_t oH = (size_t)pi * half, oN = (size_t)pi * N;
+  const int seg = (half + T - 1) / T;
+  const int s0 = min(half, tid * seg), s1 = min(half, s0 + seg);
+  if (s0 < s1) {
+    uint32_t a = pow_mod(w, s0, P), b = pow_mod(wi, s0, P);
+    for (int j = s0; j < s1; ++j) {
+      plan.W[oH + j] = a;
+      plan.Wc[oH + j] = shoup_comp(a, P);
+      plan.Wi[oH + j] = b;
+      plan.Wic[oH + j] = shoup_comp(b, P);
+      a = shoup(a, w, wc, p);
+      b = shoup(b, wi, wic, p);
+    }
+  }
+  const uint32_t linv = inv_mod((uint32_t)L % p, P);
+  if (tid == 0) plan.Linv[pi] = linv;
+  for (int e = tid; e < N; e += T) {
+    const uint32_t s = mul_mod(plan.hCinv[oN + e], linv, P);
+    plan.sS[oN + e] = s;
+    plan.sSc[oN + e] = shoup_comp(s, P);
+    plan.zc[oN + e] = shoup_comp(plan.z[oN + e], P);
+  }
 }
 
-// P_k = c^-k * sum_{l=k+1..N} M~_l S_{l-k-1}
-__global__ void __launch_bounds__(INT_THREADS) k_interp_toeplitz(InterpPlan plan, const Prime* __restrict__ primes,
-                                                                 const uint32_t* __restrict__ S,
-                                                                 uint32_t* __restrict__ coeffs) {
-  extern __shared__ uint32_t sm[];
-  const int N = plan.N, pi = blockIdx.y;
-  uint32_t* sS = sm;
-  uint32_t* sM = sm + N;
-  uint32_t* sMc = sm + 2 * N + 1;
-  const size_t oN = (size_t)pi * N, oN1 = (size_t)pi * (N + 1);
-  for (int i = threadIdx.x; i < N; i += INT_THREADS) sS[i] = S[oN + i];
-  for (int i = threadIdx.x; i <= N; i += INT_THREADS) {
-    sM[i] = plan.Mt[oN1 + i];
-    sMc[i] = plan.Mtc[oN1 + i];
-  }
-  __syncthreads();
-  const int k = blockIdx.x * INT_THREADS + threadIdx.x;
-  if (k >= N) return;
+// plan, part 2: DIF transforms of the chirp q^C(m,2) (m < 2N-1) and of M~_{u+1} (u < N)
+__global__ void __launch_bounds__(NTT_THREADS) k_plan_transforms(const Prime* __restrict__ primes, InterpPlan plan) {
+  extern __shared__ uint32_t buf[];
+  const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pi];
   const uint32_t p = P.p;
-  uint64_t acc = 0;
-#pragma unroll 4
-  for (int l = k + 1; l <= N; ++l) acc += shoup_lazy(sS[l - k - 1], sM[l], sMc[l], p);
-  coeffs[oN + k] = mul_mod(mod64(acc, P), plan.cinv[oN + k], P);
+  const int N = plan.N, L = plan.L;
+  const size_t oL = (size_t)pi * L, oH = (size_t)pi * (L >> 1);
+  const size_t o2N = (size_t)pi * 2 * N, oN1 = (size_t)pi * (N + 1);
+  const uint32_t* W = plan.W + oH;
+  const uint32_t* Wc = plan.Wc + oH;
+  for (int m = tid; m < L; m += T) buf[m] = (m < 2 * N - 1) ? plan.hC[o2N + m] : 0u;
+  __syncthreads();
+  ntt_dif(buf, plan.logL, W, Wc, p);
+  for (int u = tid; u < L; u += T) {
+    const uint32_t v = red1(buf[u], p);
+    plan.Hf[oL + u] = v;
+    plan.Hfc[oL + u] = shoup_comp(v, P);
+  }
+  __syncthreads();
+  for (int u = tid; u < L; u += T) buf[u] = (u < N) ? plan.Mt[oN1 + u + 1] : 0u;
+  __syncthreads();
+  ntt_dif(buf, plan.logL, W, Wc, p);
+  for (int u = tid; u < L; u += T) {
+    const uint32_t v = red1(buf[u], p);
+    plan.Mf[oL + u] = v;
+    plan.Mfc[oL + u] = shoup_comp(v, P);
+  }
 }
 
-void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, uint32_t* coeffs,
-                   uint32_t* a, uint32_t* ac, uint32_t* S, cudaStream_t st) {
-  const int N = plan.N, K = plan.K;
-  k_interp_prologue<<<dim3((N + 255) / 256, K), 256, 0, st>>>(plan, primes, values, a, ac);
-  const dim3 grid((N + INT_THREADS - 1) / INT_THREADS, K);
-  const size_t sm1 = (size_t)(3 * N + INT_THREADS) * 4;
-  const size_t sm2 = (size_t)(3 * N + 2) * 4;
-  if (sm1 > 48 * 1024) cudaFuncSetAttribute(k_interp_hankel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-  if (sm2 > 48 * 1024) cudaFuncSetAttribute(k_interp_toeplitz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-  k_interp_hankel<<<grid, INT_THREADS, sm1, st>>>(plan, primes, a, ac, S);
-  k_interp_toeplitz<<<grid, INT_THREADS, sm2, st>>>(plan, primes, S, coeffs);
+void launch_plan_ntt(const Prime* primes, const uint32_t* gens, const InterpPlan& plan, cudaStream_t st) {
+  k_plan_twiddles<<<plan.K, NTT_THREADS, 0, st>>>(primes, gens, plan);
+  const size_t smem = (size_t)plan.L * 4;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_plan_transforms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_plan_transforms<<<plan.K, NTT_THREADS, smem, st>>>(primes, plan);
+}
+
+// per call: values -> coefficients, one CTA per prime, everything in shared memory
+__global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const Prime* __restrict__ primes,
+                                                        const uint32_t* __restrict__ values,
+                                                        const uint32_t* __restrict__ cval,
+                                                        uint32_t* __restrict__ coeffs) {
+  extern __shared__ uint32_t buf[];
+  const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
+  const Prime P = primes[pi];
+  const uint32_t p = P.p;
+  const int N = plan.N, L = plan.L, logL = plan.logL;
+  const size_t oN = (size_t)pi * N, oL = (size_t)pi * L, oH = (size_t)pi * (L >> 1);
+  const uint32_t *W = plan.W + oH, *Wc = plan.Wc + oH, *Wi = plan.Wi + oH, *Wic = plan.Wic + oH;
+  const uint32_t *Hf = plan.Hf + oL, *Hfc = plan.Hfc + oL, *Mf = plan.Mf + oL, *Mfc = plan.Mfc + oL;
+  const uint32_t* v = values + oN;
+  // a'_s = u_{N-1-s} q^-C(N-1-s,2) = v_t z_t with t = N-1-s
+  for (int s = tid; s < L; s += T) {
+    uint32_t a = 0u;
+    if (s < N) {
+      const int t = N - 1 - s;
+      a = shoup_lazy(v[t], plan.z[oN + t], plan.zc[oN + t], p);
+    }
+    buf[s] = a;
+  }
+  __syncthreads();
+  ntt_dif(buf, logL, W, Wc, p);
+  for (int u = tid; u < L; u += T) buf[u] = shoup_lazy(buf[u], Hf[u], Hfc[u], p);
+  __syncthreads();
+  ntt_dit(buf, logL, Wi, Wic, p);
+  // S_e = conv[N-1+e] q^-C(e,2) / L, then s'_u = S_{N-1-u}
+  uint32_t sv[MAX_PER_THREAD];
+#pragma unroll
+  for (int r = 0; r < MAX_PER_THREAD; ++r) {
+    const int e = tid + r * T;
+    sv[r] = (e < N) ? shoup_lazy(buf[N - 1 + e], plan.sS[oN + e], plan.sSc[oN + e], p) : 0u;
+  }
+  __syncthreads();
+  for (int u = tid; u < L; u += T) buf[u] = 0u;
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < MAX_PER_THREAD; ++r) {
+    const int e = tid + r * T;
+    if (e < N) buf[N - 1 - e] = sv[r];
+  }
+  __syncthreads();
+  ntt_dif(buf, logL, W, Wc, p);
+  for (int u = tid; u < L; u += T) buf[u] = shoup_lazy(buf[u], Mf[u], Mfc[u], p);
+  __syncthreads();
+  ntt_dit(buf, logL, Wi, Wic, p);
+  // P_k = conv[N-1+k] / L * c^-k
+  const uint32_t linv = plan.Linv[pi];
+  const uint32_t linvc = shoup_comp(linv, P);
+  const uint32_t c = cval[pi];
+  const uint32_t cinv = (c == 1u) ? 1u : inv_mod(c, P);
+  for (int k = tid; k < N; k += T) {
+    uint32_t r = shoup(buf[N - 1 + k], linv, linvc, p);
+    if (c != 1u) r = mul_mod(r, pow_mod(cinv, (uint64_t)k, P), P);
+    coeffs[oN + k] = r;
+  }
+}
+
+void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
+                   uint32_t* coeffs, cudaStream_t st) {
+  const size_t smem = (size_t)plan.L * 4;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_interp<<<plan.K, NTT_THREADS, smem, st>>>(plan, primes, values, cval, coeffs);
 }
 
 }  // namespace ckb

@@ -12,31 +12,49 @@ void launch_reduce(const uint32_t* limbs, int C, int L, const Prime* primes, int
                    cudaStream_t st);
 
 // ---- plan: evaluation points + interpolation tables per prime ---------------
+// Depends only on (primes, generators, N): built once and cached, like an FFT
+// plan.  Points are x_t = c q^t; every table is for c = 1 (the interpolation
+// runs in y = x / c and the per-call scale c only enters through c^-k).
 struct InterpPlan {
   int N;              // points per prime
   int K;              // primes
-  uint32_t* xpts;     // [K][N]    x_t = c * q^t
-  uint32_t* hC;       // [K][2N]   q^C(m,2)
-  uint32_t* z;        // [K][N]    w_t * q^-C(t,2), w_t = 1/M'(q^t)
-  uint32_t* hCinv;    // [K][N]    q^-C(e,2)
-  uint32_t* Mt;       // [K][N+1]  coefficients of prod_t (y - q^t)
-  uint32_t* Mtc;      // [K][N+1]  Shoup companions of Mt
-  uint32_t* cinv;     // [K][N]    c^-k
-  uint32_t* phi;      // [K][N+1]  scratch: prod_{i<=j} (q^i - 1)
-  uint32_t* iphi;     // [K][N+1]  scratch: inverses of phi
-  uint32_t* cval;     // [K]       chosen scale c
+  int L, logL;        // NTT length: power of two >= 2N - 1
+  uint32_t* xq;       // [K][N]    q^t
+  uint32_t* hC;       // [K][2N]   q^C(m,2)              (construction scratch)
+  uint32_t* hCinv;    // [K][N]    q^-C(e,2)             (construction scratch)
+  uint32_t* Mt;       // [K][N+1]  coefficients of M~(y) = prod_t (y - q^t)   (scratch)
+  uint32_t* phi;      // [K][N+1]  prod_{i<=j} (q^i - 1)  (scratch)
+  uint32_t* iphi;     // [K][N+1]  inverses of phi       (scratch)
+  uint32_t* z;        // [K][N]    1/M~'(q^t) * q^-C(t,2)   and companions zc
+  uint32_t* zc;
+  uint32_t* sS;       // [K][N]    q^-C(e,2) / L           and companions sSc
+  uint32_t* sSc;
+  uint32_t* W;        // [K][L/2]  w^j, w a primitive L-th root; Wc companions
+  uint32_t* Wc;
+  uint32_t* Wi;       // [K][L/2]  w^-j; Wic companions
+  uint32_t* Wic;
+  uint32_t* Hf;       // [K][L]    DIF-NTT of q^C(m,2) (m < 2N-1); Hfc companions
+  uint32_t* Hfc;
+  uint32_t* Mf;       // [K][L]    DIF-NTT of M~_{u+1} (u < N); Mfc companions
+  uint32_t* Mfc;
+  uint32_t* Linv;     // [K]       1/L mod p
 };
-// lc polynomials of f and g (residues) are read from the reduced buffer:
-// lcf = red + lcf_off (deg lcf_deg), lcg = red + lcg_off (deg lcg_deg), row stride C.
-void launch_plan(const Prime* primes, const uint32_t* gens, int K, int N, const uint32_t* red, int C,
-                 int lcf_off, int lcf_deg, int lcg_off, int lcg_deg, const InterpPlan& plan,
-                 uint32_t* status, cudaStream_t st);
+// build every table of the plan: base tables (ckb_plan.cu), then twiddles and
+// the transforms of the two constant convolution operands (ckb_interp.cu)
+void launch_plan_base(const Prime* primes, const uint32_t* gens, const InterpPlan& plan, cudaStream_t st);
+void launch_plan_ntt(const Prime* primes, const uint32_t* gens, const InterpPlan& plan, cudaStream_t st);
+// per call: choose c per prime so that no leading coefficient vanishes at
+// x_t = c q^t (t < N).  lc polynomials of f and g (residues) are read from the
+// reduced buffer: lcf = red + lcf_off (deg lcf_deg), lcg likewise, row stride C.
+void launch_choose_c(const Prime* primes, const InterpPlan& plan, const uint32_t* red, int C, int lcf_off,
+                     int lcf_deg, int lcg_off, int lcg_deg, uint32_t* cval, uint32_t* status, cudaStream_t st);
 
 // ---- K2+K3: fused evaluation + univariate resultant (modpoly.py:382-390) ----
 struct ImageArgs {
   const uint32_t* red;     // [K][C]
   const int16_t* degs;     // [(m+1) + (n+1)] x-degree of each y-coefficient (-1 = zero)
-  const uint32_t* xpts;    // [K][N]
+  const uint32_t* xq;      // [K][N] q^t (plan)
+  const uint32_t* cval;    // [K] point scale c: x_t = c q^t
   const Prime* primes;
   int C, m, n, dfx, dgx, N, K;
   uint32_t* values;        // [K][N]
@@ -55,9 +73,9 @@ void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t*
                           const Prime* primes, const int32_t* pidx, int B, uint32_t* out, cudaStream_t st);
 
 // ---- K4: interpolation at the planned points (modpoly.py:164-185) -----------
-// values [K][N] -> coeffs [K][N] (canonical residues), scratch a/ac/S [K][N]
-void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, uint32_t* coeffs,
-                   uint32_t* a, uint32_t* ac, uint32_t* S, cudaStream_t st);
+// values [K][N] at x_t = c q^t -> coeffs [K][N] (canonical residues)
+void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
+                   uint32_t* coeffs, cudaStream_t st);
 
 // ---- K5: explicit CRT + symmetric lift to two's-complement limbs -----------
 struct CrtTables {

@@ -77,11 +77,9 @@ __device__ void block_scan_mul(uint32_t* buf, int n, bool reverse, const Prime& 
 
 __device__ __forceinline__ uint64_t binom2(uint64_t m) { return m * (m - 1) / 2; }
 
+// base tables of the plan for c = 1 (one CTA per prime)
 __global__ void __launch_bounds__(PLAN_THREADS) k_plan(const Prime* __restrict__ primes,
-                                                       const uint32_t* __restrict__ gens, int N,
-                                                       const uint32_t* __restrict__ red, int C, int lcf_off,
-                                                       int lcf_deg, int lcg_off, int lcg_deg, InterpPlan plan,
-                                                       uint32_t* status) {
+                                                       const uint32_t* __restrict__ gens, int N, InterpPlan plan) {
   __shared__ uint32_t sh[PLAN_THREADS];
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pi];
@@ -154,63 +152,24 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(const Prime* __restrict__
   __syncthreads();
   block_scan_mul(iphi, N + 1, true, P, sh);
 
-  // choose c: no leading coefficient may vanish at x_t = c q^t, t < N
-  uint32_t c = 1u % p;
-  const uint32_t* lcf = red + (size_t)pi * C + lcf_off;
-  const uint32_t* lcg = red + (size_t)pi * C + lcg_off;
-  bool found = false;
-  for (int attempt = 0; attempt < 64; ++attempt) {
-    c = (uint32_t)(attempt + 1) % p;
-    if (c == 0) continue;
-    int bad = 0;
-    if (lcf_deg > 0 || lcg_deg > 0) {
-      const uint32_t cc = shoup_comp(c, P);
-      for (int t = tid; t < N; t += T) {
-        uint32_t x = shoup(pow_mod(q, t, P), c, cc, p);
-        uint32_t xc = shoup_comp(x, P);
-        uint32_t vf = 0, vg = 0;
-        for (int i = lcf_deg; i >= 0; --i) vf = add_mod(shoup(vf, x, xc, p), lcf[i], p);
-        for (int i = lcg_deg; i >= 0; --i) vg = add_mod(shoup(vg, x, xc, p), lcg[i], p);
-        if (vf == 0u || vg == 0u) bad = 1;
-      }
-    } else {
-      bad = (lcf[0] == 0u || lcg[0] == 0u) ? 2 : 0;
-    }
-    bad = __syncthreads_or(bad);
-    if (!bad) {
-      found = true;
-      break;
-    }
-    if (lcf_deg <= 0 && lcg_deg <= 0) break;  // constant lc vanishes: no c helps
-  }
-  if (tid == 0) {
-    plan.cval[pi] = c;
-    if (!found) atomicOr(status, 1u);
-  }
-  const uint32_t cinv = inv_mod(c, P);
-  const uint32_t cc = shoup_comp(c, P), cic = shoup_comp(cinv, P);
   const uint32_t r = pow_mod(qinv, (uint64_t)(N >= 2 ? N - 2 : 0) % pm1, P);  // q^-(N-2)
   const uint32_t rc = shoup_comp(r, P);
   const uint32_t phiN = phi[N];
   __syncthreads();
-  // per-point tables: x_t, z_t, c^-k
+  // per-point tables: x_t = q^t and z_t = (-1)^(N-1-t) q^-t(N-2) iphi_t iphi_{N-1-t}
   {
     const int n = N, seg = (n + T - 1) / T;
     const int s0 = min(n, tid * seg), s1 = min(n, s0 + seg);
     if (s0 < s1) {
       uint32_t qt = pow_mod(q, s0, P);
       uint32_t rt = (N >= 2) ? pow_mod(r, s0, P) : 1u;
-      uint32_t ck = pow_mod(cinv, s0, P);
       for (int t = s0; t < s1; ++t) {
-        plan.xpts[oN + t] = shoup(qt, c, cc, p);
-        // z_t = (-1)^(N-1-t) q^-t(N-2) iphi_t iphi_{N-1-t}
+        plan.xq[oN + t] = qt;
         uint32_t z = mul_mod(mul_mod(rt, iphi[t], P), iphi[N - 1 - t], P);
         if ((N - 1 - t) & 1) z = neg_mod(z, p);
         plan.z[oN + t] = z;
-        plan.cinv[oN + t] = ck;
         qt = shoup(qt, q, qc, p);
         rt = shoup(rt, r, rc, p);
-        ck = shoup(ck, cinv, cic, p);
       }
     }
   }
@@ -219,14 +178,61 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(const Prime* __restrict__
     uint32_t v = mul_mod(mul_mod(plan.hC[o2N + k], phiN, P), mul_mod(iphi[k], iphi[N - k], P), P);
     if (k & 1) v = neg_mod(v, p);
     plan.Mt[oN1 + (N - k)] = v;
-    plan.Mtc[oN1 + (N - k)] = shoup_comp(v, P);
   }
 }
 
-void launch_plan(const Prime* primes, const uint32_t* gens, int K, int N, const uint32_t* red, int C,
-                 int lcf_off, int lcf_deg, int lcg_off, int lcg_deg, const InterpPlan& plan,
-                 uint32_t* status, cudaStream_t st) {
-  k_plan<<<K, PLAN_THREADS, 0, st>>>(primes, gens, N, red, C, lcf_off, lcf_deg, lcg_off, lcg_deg, plan, status);
+// per call: the point scale c of every prime (modpoly.py:380-390 skips the
+// points where a leading coefficient vanishes; here the whole progression is
+// shifted by c instead, keeping the cached plan valid)
+__global__ void __launch_bounds__(PLAN_THREADS) k_choose_c(const Prime* __restrict__ primes, InterpPlan plan,
+                                                           const uint32_t* __restrict__ red, int C, int lcf_off,
+                                                           int lcf_deg, int lcg_off, int lcg_deg,
+                                                           uint32_t* __restrict__ cval, uint32_t* status) {
+  const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, N = plan.N;
+  const Prime P = primes[pi];
+  const uint32_t p = P.p;
+  const uint32_t* lcf = red + (size_t)pi * C + lcf_off;
+  const uint32_t* lcg = red + (size_t)pi * C + lcg_off;
+  if (lcf_deg <= 0 && lcg_deg <= 0) {  // constant leading coefficients
+    if (tid == 0) {
+      cval[pi] = 1u;
+      if (lcf[0] == 0u || lcg[0] == 0u) atomicOr(status, 1u);
+    }
+    return;
+  }
+  const uint32_t* xq = plan.xq + (size_t)pi * N;
+  for (int attempt = 0; attempt < 64; ++attempt) {
+    const uint32_t c = (uint32_t)(attempt + 1) % p;
+    const uint32_t cc = shoup_comp(c, P);
+    int bad = 0;
+    for (int t = tid; t < N; t += T) {
+      const uint32_t x = shoup(xq[t], c, cc, p);
+      const uint32_t xc = shoup_comp(x, P);
+      uint32_t vf = 0, vg = 0;
+      for (int i = lcf_deg; i >= 0; --i) vf = add_mod(shoup(vf, x, xc, p), lcf[i], p);
+      for (int i = lcg_deg; i >= 0; --i) vg = add_mod(shoup(vg, x, xc, p), lcg[i], p);
+      if (vf == 0u || vg == 0u) bad = 1;
+    }
+    bad = __syncthreads_or(bad);
+    if (!bad) {
+      if (tid == 0) cval[pi] = c;
+      return;
+    }
+  }
+  if (tid == 0) {
+    cval[pi] = 1u;
+    atomicOr(status, 1u);
+  }
+}
+
+void launch_choose_c(const Prime* primes, const InterpPlan& plan, const uint32_t* red, int C, int lcf_off,
+                     int lcf_deg, int lcg_off, int lcg_deg, uint32_t* cval, uint32_t* status, cudaStream_t st) {
+  k_choose_c<<<plan.K, PLAN_THREADS, 0, st>>>(primes, plan, red, C, lcf_off, lcf_deg, lcg_off, lcg_deg, cval,
+                                               status);
+}
+
+void launch_plan_base(const Prime* primes, const uint32_t* gens, const InterpPlan& plan, cudaStream_t st) {
+  k_plan<<<plan.K, PLAN_THREADS, 0, st>>>(primes, gens, plan.N, plan);
 }
 
 }  // namespace ckb

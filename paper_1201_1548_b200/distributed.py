@@ -81,11 +81,11 @@ class CudaBackend:
         pk = self.packed
         K = len(primes)
         hp = np.array(primes, dtype=np.uint32)
-        d_gens = torch.from_numpy(np.array(gens, dtype=np.uint32).view(np.int32)).to(self.device)
+        hg = np.array(gens, dtype=np.uint32)
         out = torch.empty((K, N), dtype=torch.int32, device=self.device)
         self._lib.check(self.lib.ckb_dev_modular_images(
             self.d_limbs.data_ptr(), pk.C, pk.L, self.d_degs.data_ptr(), self._lib.ptr(self.h_degs), pk.m, pk.n,
-            pk.dfx, pk.dgx, self._lib.ptr(hp), d_gens.data_ptr(), K, N, out.data_ptr(), self.d_status.data_ptr(),
+            pk.dfx, pk.dgx, self._lib.ptr(hp), self._lib.ptr(hg), K, N, out.data_ptr(), self.d_status.data_ptr(),
             stream), "ckb_dev_modular_images")
         return out
 
