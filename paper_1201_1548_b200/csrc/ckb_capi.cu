@@ -326,7 +326,7 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int N, InterpP
   pl.L = (int)L;
   pl.logL = logL;
   const size_t kn = (size_t)K * N, kn1 = (size_t)K * (N + 1), kl = (size_t)K * L, kh = kl / 2;
-  const size_t words = kn * 8 + kn1 * 3 + kh * 4 + kl * 4 + K + K * 3 + 64;
+  const size_t words = kn * 8 + kn1 * 3 + kh * 4 + kl * 4 + (size_t)K * 5 + 64;  // see take() below
   CK(cudaMalloc(&e.blob, 4 * words));
   uint32_t* b = (uint32_t*)e.blob;
   auto take = [&](size_t n) { uint32_t* r = b; b += n; return r; };
