@@ -76,6 +76,11 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
   uint32_t A[MAXD + 1], B[MAXD + 1];
 #pragma unroll
   for (int i = 0; i <= MAXD; ++i) A[i] = B[i] = 0u;
+  uint32_t negp = 0u - p;
+  uint32_t xcp = xc;
+  // opaque to the optimiser: keeps both in registers instead of letting
+  // ptxas rematerialise the companion (7 instructions) in every chunk
+  asm volatile("" : "+r"(negp), "+r"(xcp));
   for (int e = dmax; e >= 0; --e) {
     const uint4* ta = reinterpret_cast<const uint4*>(TA + e * SW);
     const uint4* tb = reinterpret_cast<const uint4*>(TB + e * SW);
@@ -87,14 +92,14 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
         const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (4 * c + k <= MAXD) A[4 * c + k] = shoup_lazy(A[4 * c + k], x, xc, p) + vv[k];
+          if (4 * c + k <= MAXD) A[4 * c + k] = shoup_lazy_add(A[4 * c + k], x, xcp, negp, vv[k]);
       }
       if (mB & (1u << c)) {
         const uint4 v = tb[c];
         const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (4 * c + k <= MAXD) B[4 * c + k] = shoup_lazy(B[4 * c + k], x, xc, p) + vv[k];
+          if (4 * c + k <= MAXD) B[4 * c + k] = shoup_lazy_add(B[4 * c + k], x, xcp, negp, vv[k]);
       }
     }
   }

@@ -56,10 +56,16 @@ __device__ __forceinline__ uint32_t shoup_comp(uint32_t w, const Prime& P) {
   return (0u - r) * P.pinv;
 }
 
-// x * w mod p, lazily in [0, 2p); any 32-bit x
+// x * w mod p, lazily in [0, 2p); any 32-bit x.  Written as x w + q (-p) so
+// that it compiles to IMAD.HI + IMAD + IMAD with no negation of q.
 __device__ __forceinline__ uint32_t shoup_lazy(uint32_t x, uint32_t w, uint32_t wc, uint32_t p) {
-  uint32_t q = __umulhi(x, wc);
-  return x * w - q * p;
+  const uint32_t q = __umulhi(x, wc);
+  return x * w + q * (0u - p);
+}
+// x * w + c mod p, lazily in [0, 2p) + c (the add folds into the first IMAD)
+__device__ __forceinline__ uint32_t shoup_lazy_add(uint32_t x, uint32_t w, uint32_t wc, uint32_t negp, uint32_t c) {
+  const uint32_t q = __umulhi(x, wc);
+  return (x * w + c) + q * negp;
 }
 __device__ __forceinline__ uint32_t shoup(uint32_t x, uint32_t w, uint32_t wc, uint32_t p) {
   return red1(shoup_lazy(x, w, wc, p), p);
