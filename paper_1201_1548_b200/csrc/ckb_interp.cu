@@ -94,13 +94,19 @@ __global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const P
                                                         const uint32_t* __restrict__ values,
                                                         const uint32_t* __restrict__ cval,
                                                         uint32_t* __restrict__ coeffs) {
-  extern __shared__ uint32_t buf[];
+  extern __shared__ uint32_t buf[];  // [L] data, then 4 x [L/2] twiddle tables
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pi];
   const uint32_t p = P.p;
-  const int N = plan.N, L = plan.L, logL = plan.logL;
-  const size_t oN = (size_t)pi * N, oL = (size_t)pi * L, oH = (size_t)pi * (L >> 1);
-  const uint32_t *W = plan.W + oH, *Wc = plan.Wc + oH, *Wi = plan.Wi + oH, *Wic = plan.Wic + oH;
+  const int N = plan.N, L = plan.L, logL = plan.logL, half = L >> 1;
+  const size_t oN = (size_t)pi * N, oL = (size_t)pi * L, oH = (size_t)pi * half;
+  uint32_t *W = buf + L, *Wc = W + half, *Wi = Wc + half, *Wic = Wi + half;
+  for (int j = tid; j < half; j += T) {  // stage the twiddles once (no global loads in the stages)
+    W[j] = plan.W[oH + j];
+    Wc[j] = plan.Wc[oH + j];
+    Wi[j] = plan.Wi[oH + j];
+    Wic[j] = plan.Wic[oH + j];
+  }
   const uint32_t *Hf = plan.Hf + oL, *Hfc = plan.Hfc + oL, *Mf = plan.Mf + oL, *Mfc = plan.Mfc + oL;
   const uint32_t* v = values + oN;
   // a'_s = u_{N-1-s} q^-C(N-1-s,2) = v_t z_t with t = N-1-s
@@ -113,10 +119,10 @@ __global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const P
     buf[s] = a;
   }
   __syncthreads();
-  ntt_dif(buf, logL, W, Wc, p);
+  ntt_dif8<NTT_THREADS>(buf, logL, W, Wc, p);
   for (int u = tid; u < L; u += T) buf[u] = shoup_lazy(buf[u], Hf[u], Hfc[u], p);
   __syncthreads();
-  ntt_dit(buf, logL, Wi, Wic, p);
+  ntt_dit8<NTT_THREADS>(buf, logL, Wi, Wic, p);
   // S_e = conv[N-1+e] q^-C(e,2) / L, then s'_u = S_{N-1-u}
   uint32_t sv[MAX_PER_THREAD];
 #pragma unroll
@@ -133,10 +139,10 @@ __global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const P
     if (e < N) buf[N - 1 - e] = sv[r];
   }
   __syncthreads();
-  ntt_dif(buf, logL, W, Wc, p);
+  ntt_dif8<NTT_THREADS>(buf, logL, W, Wc, p);
   for (int u = tid; u < L; u += T) buf[u] = shoup_lazy(buf[u], Mf[u], Mfc[u], p);
   __syncthreads();
-  ntt_dit(buf, logL, Wi, Wic, p);
+  ntt_dit8<NTT_THREADS>(buf, logL, Wi, Wic, p);
   // P_k = conv[N-1+k] / L * c^-k
   const uint32_t linv = plan.Linv[pi];
   const uint32_t linvc = shoup_comp(linv, P);
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const P
 
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
                    uint32_t* coeffs, cudaStream_t st) {
-  const size_t smem = (size_t)plan.L * 4;
+  const size_t smem = (size_t)plan.L * 4 * 3;  // data + 4 twiddle tables of L/2
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_interp<<<plan.K, NTT_THREADS, smem, st>>>(plan, primes, values, cval, coeffs);
 }
