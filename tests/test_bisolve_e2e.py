@@ -1,0 +1,110 @@
+"""End-to-end parity through the reference's own consumer.
+
+The unmodified reference package (installed offline into baseline/_ref, see
+DESIGN.md) runs Bisolve (pkg/src/curvekit/bisolve.py:541-556) with its
+resultants, gcds and square-free decompositions served by the B200 engine
+(paper_1201_1548_b200.install(), rebinding modpoly.py's names and the names
+bisolve.py:26 bound at import).  The isolating boxes must equal the ones the
+reference produced on its own (tests/golden/cfg1_bisolve.json).
+"""
+
+import os
+import sys
+
+import pytest
+
+from conftest import REPO, load_golden, terms_in
+
+REF = os.path.join(REPO, "baseline", "_ref")
+
+
+@pytest.fixture(scope="module")
+def curvekit_mod():
+    if not os.path.isdir(os.path.join(REF, "curvekit")):
+        pytest.skip("reference install baseline/_ref is absent")
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    pytest.importorskip("mpmath")
+    import curvekit.bisolve  # noqa: F401
+    import curvekit.modpoly  # noqa: F401
+    return sys.modules["curvekit"]
+
+
+def test_install_rebinds_and_restores(curvekit_mod):
+    import curvekit.bisolve as B
+    import curvekit.modpoly as M
+
+    import paper_1201_1548_b200 as pkg
+    from paper_1201_1548_b200 import modpoly as ours
+    orig = (M.biv_resultant, M.int_gcd_uni, B.biv_resultant, B.int_gcd_uni)
+    saved = pkg.install()
+    try:
+        assert M.biv_resultant is ours.biv_resultant and B.biv_resultant is ours.biv_resultant
+        assert M.int_gcd_uni is ours.int_gcd_uni and B.int_gcd_uni is ours.int_gcd_uni
+        assert M.zp_gcd_sylvester is ours.zp_gcd_sylvester
+    finally:
+        pkg.uninstall(saved)
+    assert (M.biv_resultant, M.int_gcd_uni, B.biv_resultant, B.int_gcd_uni) == orig
+
+
+def _boxes(sols):
+    out = []
+    for s in sols:
+        xi, yi = s.x.interval, s.y.interval
+        out.append([[str(xi.lo.man), xi.lo.exp], [str(xi.hi.man), xi.hi.exp],
+                    [str(yi.lo.man), yi.lo.exp], [str(yi.hi.man), yi.hi.exp]])
+    return out
+
+
+@pytest.mark.gpu
+def test_bisolve_cfg1_boxes_match_reference(curvekit_mod):
+    from curvekit.bisolve import solve
+    from curvekit.bivpoly import BivPoly
+
+    import paper_1201_1548_b200 as pkg
+    gold = load_golden("cfg1_bisolve.json")
+    saved = pkg.install()
+    try:
+        for sysd in gold["systems"]:
+            f, g = BivPoly(terms_in(sysd["f"])), BivPoly(terms_in(sysd["g"]))
+            sols = solve(f, g, filters=frozenset({"combinatorial"}), seed=0)
+            assert _boxes(sols) == sysd["boxes"], sysd["seed"]
+    finally:
+        pkg.uninstall(saved)
+
+
+@pytest.mark.gpu
+def test_bisolve_known_x_suite_matches_reference(curvekit_mod):
+    # test_bisolve.py:142-195's 30 systems under the combinatorial filter
+    from curvekit.bisolve import solve
+    from curvekit.bivpoly import BivPoly
+
+    import paper_1201_1548_b200 as pkg
+    gold = load_golden("cfg1_bisolve.json")
+    saved = pkg.install()
+    try:
+        for case in gold["known_x"]:
+            f, g = BivPoly(terms_in(case["f"])), BivPoly(terms_in(case["g"]))
+            sols = solve(f, g, filters=frozenset({"combinatorial"}))
+            assert _boxes(sols) == case["boxes"]
+    finally:
+        pkg.uninstall(saved)
+
+
+@pytest.mark.gpu
+def test_reference_squarefree_uses_gpu_gcd(curvekit_mod):
+    from curvekit import upoly
+
+    import paper_1201_1548_b200 as pkg
+    from paper_1201_1548_b200 import _lib
+    small = load_golden("small.json")
+    saved = pkg.install()
+    try:
+        n0 = _lib.launch_count()
+        for c in small["squarefree"]:
+            dec = upoly.squarefree_decompose([int(v) for v in c["p"]])
+            assert str(dec.content) == c["content"]
+            assert [[list(map(str, f)), m] for f, m in dec.factors] == c["factors"]
+        assert _lib.launch_count() > n0, "the reference's Yun must reach the GPU gcd"
+    finally:
+        pkg.uninstall(saved)

@@ -112,6 +112,23 @@ def test_cfg4_specialisation(mp, oracle_mod):
     _specialisation_check(mp, oracle_mod, f, g, res, random.Random(4))
 
 
+def test_cfg5_specialisation(mp, oracle_mod):
+    """cfg5 (d = 64, 256-bit): ~1,150 primes x 4,097 points, NTT length 2^14."""
+    from paper_1201_1548_b200.synth import make_pair
+    f, g = make_pair("cfg5", 0)
+    res = mp.biv_resultant(f, g, "y")
+    assert len(res) == 64 * 64 + 1
+    _specialisation_check(mp, oracle_mod, f, g, res, random.Random(5), trials=4)
+
+
+def test_cfg3_f_fy_and_x_direction_specialisation(mp, oracle_mod):
+    from paper_1201_1548_b200.synth import make_pair
+    f, g = make_pair("cfg3", 1)
+    swap = lambda t: {(j, i): c for (i, j), c in t.items()}
+    res = mp.biv_resultant(f, g, "x")
+    _specialisation_check(mp, oracle_mod, swap(f), swap(g), res, random.Random(6), trials=4)
+
+
 def test_cfg4_one_prime_of_the_reference_loop(mp, oracle_mod):
     """Residues of the GPU result mod the reference's first cfg4 prime equal
     the reference loop body's interpolated polynomial at that prime."""

@@ -1,0 +1,114 @@
+"""Host planner (CPU): bounds, point counts, prime choice, limb packing."""
+
+import random
+
+import numpy as np
+
+from conftest import ints_in, load_golden, terms_in
+from paper_1201_1548_b200 import planner, workmodel
+from paper_1201_1548_b200.bivpoly import BivPoly
+from paper_1201_1548_b200.primes30 import NTT_LOG2, PRIMES30
+
+
+def _cases(small):
+    for case in small["random50"]:
+        f, g = BivPoly(terms_in(case["f"])), BivPoly(terms_in(case["g"]))
+        yield f, g, ints_in(case["res_y"])
+        yield f.swap(), g.swap(), ints_in(case["res_x"])
+
+
+def test_bounds_and_point_counts_are_valid(small):
+    n = 0
+    for f, g, res in _cases(small):
+        fc, gc = f.coeffs_wrt_y(), g.coeffs_wrt_y()
+        if len(fc) < 2 or len(gc) < 2:
+            continue
+        b = planner.det_coeff_bound(fc, gc)
+        assert b <= planner.det_coeff_bound_ref(fc, gc)
+        assert all(abs(c) <= b for c in res)
+        N = planner.point_count(fc, gc, f.deg_x(), g.deg_x(), f.total_degree(), g.total_degree())
+        assert len(res) <= N
+        n += 1
+    assert n > 50
+
+
+def test_bezout_point_count_is_tight_for_dense_inputs():
+    from paper_1201_1548_b200.synth import make_pair
+    f, g = (BivPoly(t) for t in make_pair("cfg4", 0))
+    fc, gc = f.coeffs_wrt_y(), g.coeffs_wrt_y()
+    assert planner.point_count(fc, gc, f.deg_x(), g.deg_x(), 40, 40) == 40 * 40 + 1  # reference: 3201
+
+
+def test_golden_big_results_within_bounds():
+    from paper_1201_1548_b200.synth import make_pair
+    for cfg, name in (("cfg2", "cfg2_seed0.json.gz"), ("cfg3", "cfg3_seed0.json.gz")):
+        gold = load_golden(name)
+        res = [int(c, 16) for c in gold["res"]]
+        f, g = (BivPoly(t) for t in make_pair(cfg, 0))
+        fc, gc = f.coeffs_wrt_y(), g.coeffs_wrt_y()
+        b = planner.det_coeff_bound(fc, gc)
+        assert max(abs(c) for c in res) <= b
+        plan = planner.plan_resultant(fc, gc, f.total_degree(), g.total_degree(), f.deg_x(), g.deg_x())
+        mod = 1
+        for p in plan.primes.tolist():
+            mod *= p
+        assert mod > 4 * b and plan.N >= len(res)
+        assert (mod.bit_length() + 31) // 32 == plan.LW
+
+
+def test_prime_table_properties():
+    assert len(PRIMES30) > 3000
+    seen = set()
+    for p, g in PRIMES30[:400]:
+        assert (1 << 29) < p < (1 << 30) and (p - 1) % (1 << NTT_LOG2) == 0
+        assert pow(g, (p - 1) // 2, p) == p - 1  # a generator is a non-residue
+        assert p not in seen
+        seen.add(p)
+
+
+def test_choose_primes_skips_vanishing_leading_coefficients():
+    p0, p1 = PRIMES30[0][0], PRIMES30[1][0]
+    primes, gens, mod = planner.choose_primes(10 ** 30, [p0 * 7, p0], [1], 0)
+    assert p0 not in primes and p1 == primes[0]
+    assert mod > 4 * 10 ** 30
+
+
+def test_pack_grid_roundtrip():
+    rng = random.Random(4)
+    for bits in (5, 40, 62, 63, 64, 200):
+        fc = [[rng.randint(-2 ** bits, 2 ** bits) for _ in range(rng.randint(0, 6))] for _ in range(4)]
+        gc = [[rng.randint(-2 ** bits, 2 ** bits) for _ in range(rng.randint(0, 6))] for _ in range(3)]
+        fc = [[c for c in col] for col in fc]
+        for col in fc + gc:
+            while col and col[-1] == 0:
+                col.pop()
+        fc[-1] = fc[-1] or [1]
+        gc[-1] = gc[-1] or [1]
+        pk = planner.pack_grid(fc, gc)
+        vals = planner.limbs_to_ints(pk.limbs, pk.C, pk.L)
+        pos = 0
+        for cs, dx in ((fc, pk.dfx), (gc, pk.dgx)):
+            for col in cs:
+                row = vals[pos:pos + dx + 1]
+                assert row[:len(col)] == col and not any(row[len(col):])
+                pos += dx + 1
+        assert list(pk.degs) == [len(c) - 1 for c in fc] + [len(c) - 1 for c in gc]
+
+
+def test_limb_roundtrip():
+    rng = random.Random(5)
+    vals = [rng.randint(-2 ** 500, 2 ** 500) for _ in range(100)] + [0, -1, 1, 2 ** 31, -2 ** 31]
+    limbs, L = planner.ints_to_limbs(vals)
+    assert planner.limbs_to_ints(limbs, len(vals), L) == vals
+    assert limbs.dtype == np.uint32
+
+
+def test_work_model():
+    # generic division-free elimination: first step 2m outputs... (m = n = 2):
+    # step nom=2 -> 4 products; then (2,1): noms 2,1 -> 6 products
+    assert workmodel.elim_products(2, 2) == 4 + 6
+    assert workmodel.elim_products(1, 1) == 2
+    assert workmodel.eval_products([0, 1, 2], [3, -1]) == 6
+    d = 40
+    degs = [d - j for j in range(d + 1)]
+    assert workmodel.eval_products(degs, degs) == d * (d + 1)
