@@ -20,15 +20,15 @@ def eval_products(degs_f, degs_g) -> int:
 
 
 def elim_products(m: int, n: int) -> int:
-    """Products of the generic division-free elimination (ckb_resultant.cuh):
-    each step with nominal degree `nom` forms nom outputs of 2 products."""
+    """Vector products of the generic division-free elimination (ckb_resultant.cuh):
+    the first remainder is e0 = da - db + 1 single steps (a step with nominal
+    degree `nom` forms nom outputs of 2 products); every later remainder with
+    divisor degree k is one fused sweep of k outputs of 3 products."""
     da, db = max(m, n), min(m, n)
-    total = 0
-    while db >= 1:
-        e = da - db + 1
-        for s in range(e):
-            total += 2 * (da - s)
-        da, db = db, db - 1
+    if db < 1:
+        return 0
+    total = sum(2 * (da - s) for s in range(da - db + 1))
+    total += sum(3 * k for k in range(1, db))
     return total
 
 

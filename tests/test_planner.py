@@ -104,10 +104,12 @@ def test_limb_roundtrip():
 
 
 def test_work_model():
-    # generic division-free elimination: first step 2m outputs... (m = n = 2):
-    # step nom=2 -> 4 products; then (2,1): noms 2,1 -> 6 products
-    assert workmodel.elim_products(2, 2) == 4 + 6
+    # m = n = 2: first remainder one step of nominal degree 2 (4 products),
+    # then one fused remainder with divisor degree 1 (3 products)
+    assert workmodel.elim_products(2, 2) == 4 + 3
     assert workmodel.elim_products(1, 1) == 2
+    assert workmodel.elim_products(40, 40) == 80 + 3 * 780
+    assert workmodel.elim_products(24, 23) == 2 * 24 + 2 * 23 + 3 * (22 * 23 // 2)
     assert workmodel.eval_products([0, 1, 2], [3, -1]) == 6
     d = 40
     degs = [d - j for j in range(d + 1)]
