@@ -20,7 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .planner import (choose_primes, det_coeff_bound, limbs_to_ints, pack_grid, point_count)
+from .planner import (choose_primes_log2, limbs_to_ints, log2_coeff_bound, pack_grid, point_count)
 from .primes30 import PRIMES30
 
 
@@ -41,9 +41,11 @@ def plan_sharded(fc, gc, tdf: int, tdg: int, world: int, table=PRIMES30) -> Shar
     m, n = len(fc) - 1, len(gc) - 1
     dfx = max(0, max(len(c) - 1 for c in fc))
     dgx = max(0, max(len(c) - 1 for c in gc))
-    bound = det_coeff_bound(fc, gc)
     N = point_count(fc, gc, dfx, dgx, tdf, tdg)
-    primes, gens, mod = choose_primes(bound, fc[-1], gc[-1], 0, table)
+    primes, gens = choose_primes_log2(log2_coeff_bound(fc, gc), fc[-1], gc[-1], 0, table)
+    mod = 1
+    for p in primes:
+        mod *= p
     start = table.index((primes[-1], gens[-1])) + 1
     while len(primes) % world:  # pad with the next admissible primes
         if start >= len(table):

@@ -103,6 +103,69 @@ def det_coeff_bound(fc, gc) -> int:
     return min(ref, had)
 
 
+def log2_coeff_bound(fc, gc) -> float:
+    """log2 of det_coeff_bound(fc, gc), evaluated in floating point.
+
+    Only the number of primes depends on the bound, so the planner works in
+    log2 space (no big-integer products): every term is a log2 of an exact
+    integer (relative error ~1e-16), the sums have ~(m + n) terms, and the
+    planner adds a full bit of margin on top -- far above the rounding error.
+    """
+    from math import log2
+    m, n = len(fc) - 1, len(gc) - 1
+    nf = [_norm1(c) for c in fc]
+    ng = [_norm1(c) for c in gc]
+    # column j of the Sylvester matrix holds f's coefficients k in
+    # [max(0, m-j), min(m, m-j+n-1)] and g's in [max(0, n-j), min(n, n-j+m-1)]:
+    # contiguous ranges, so prefix sums give every column sum exactly
+    pf, pf2, pg, pg2 = [0], [0], [0], [0]
+    for a in nf:
+        pf.append(pf[-1] + a)
+        pf2.append(pf2[-1] + a * a)
+    for a in ng:
+        pg.append(pg[-1] + a)
+        pg2.append(pg2[-1] + a * a)
+    ref = 0.0
+    col = 0.0
+    for j in range(m + n):
+        lo, hi = max(0, m - j), min(m, m - j + n - 1)
+        s = pf[hi + 1] - pf[lo] if lo <= hi else 0
+        s2 = pf2[hi + 1] - pf2[lo] if lo <= hi else 0
+        lo, hi = max(0, n - j), min(n, n - j + m - 1)
+        if lo <= hi:
+            s += pg[hi + 1] - pg[lo]
+            s2 += pg2[hi + 1] - pg2[lo]
+        ref += log2(max(1, s))
+        col += 0.5 * log2(max(1, s2))
+    row = 0.5 * (n * log2(max(1, sum(a * a for a in nf))) + m * log2(max(1, sum(a * a for a in ng))))
+    return min(ref, row, col)
+
+
+def choose_primes_log2(bound_log2: float, lcf, lcg, start: int = 0, table=PRIMES30):
+    """Primes (descending, from ``start``) until log2(prod) > log2(4 B) + 1."""
+    from math import log2
+    target = bound_log2 + 3.0
+    primes, gens = [], []
+    acc = 0.0
+    i = start
+    const = len(lcf) == 1 and len(lcg) == 1
+    a, b = (lcf[0], lcg[0]) if const else (None, None)
+    while acc <= target:
+        if i >= len(table):
+            raise ArithmeticError("prime table exhausted in resultant computation")
+        p, g = table[i]
+        i += 1
+        if const:
+            if a % p == 0 or b % p == 0:
+                continue
+        elif _lc_vanishes(lcf, p) or _lc_vanishes(lcg, p):
+            continue
+        primes.append(p)
+        gens.append(g)
+        acc += log2(p)
+    return primes, gens
+
+
 def point_count(fc, gc, dfx: int, dgx: int, tdf: int, tdg: int) -> int:
     m, n = len(fc) - 1, len(gc) - 1
     ref = dfx * n + dgx * m
@@ -160,13 +223,12 @@ def pack_grid(fc, gc) -> Packed:
                         maxbits = b
     L = max(1, (maxbits + 1 + 31) // 32)
     if L <= 2:
-        grid = np.zeros(C, dtype=np.int64)
-        base = 0
+        flat = []
         for cs, dx in ((fc, dfx), (gc, dgx)):
-            for j, c in enumerate(cs):
-                if c:
-                    grid[base + j * (dx + 1): base + j * (dx + 1) + len(c)] = c
-            base += len(cs) * (dx + 1)
+            for c in cs:
+                flat.extend(c)
+                flat.extend([0] * (dx + 1 - len(c)))
+        grid = np.array(flat, dtype=np.int64)
         limbs = grid.view(np.uint32)
         if L == 1:
             limbs = np.ascontiguousarray(limbs.reshape(C, 2)[:, 0])
@@ -186,17 +248,21 @@ def pack_grid(fc, gc) -> Packed:
 
 
 def plan_resultant(fc, gc, tdf: int, tdg: int, dfx: int, dgx: int, start: int = 0) -> Plan:
-    bound = det_coeff_bound(fc, gc)
+    from math import log2
+    blog = log2_coeff_bound(fc, gc)
     N = point_count(fc, gc, dfx, dgx, tdf, tdg)
-    primes, gens, mod = choose_primes(bound, fc[-1], gc[-1], start)
-    LW = (mod.bit_length() + 31) // 32
+    primes, gens = choose_primes_log2(blog, fc[-1], gc[-1], start)
+    # bit length of the modulus (LW words must hold M): the float sum is within
+    # ~1e-12 of log2 M; rounding it up by 1e-6 can only add a spare word
+    mbits = int(sum(log2(p) for p in primes) + 1e-6) + 1
+    LW = (mbits + 31) // 32
     return Plan(np.array(primes, dtype=np.uint32), np.array(gens, dtype=np.uint32), N, LW,
-                bound.bit_length(), mod.bit_length())
+                int(blog) + 1, mbits)
 
 
 def limbs_to_ints(buf: np.ndarray, N: int, LW: int) -> list:
     """[N][LW] two's-complement u32 limbs -> list of Python ints."""
-    raw = buf.tobytes()
+    raw = np.ascontiguousarray(buf).tobytes()  # bytes slices beat memoryview slices here
     w = 4 * LW
     fb = int.from_bytes
     return [fb(raw[i * w:(i + 1) * w], "little", signed=True) for i in range(N)]

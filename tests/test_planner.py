@@ -114,3 +114,22 @@ def test_work_model():
     d = 40
     degs = [d - j for j in range(d + 1)]
     assert workmodel.eval_products(degs, degs) == d * (d + 1)
+
+
+def test_log2_bound_matches_exact_bound():
+    import math
+    rng = random.Random(3)
+    for _ in range(300):
+        m, n = rng.randint(1, 9), rng.randint(1, 9)
+        fc = [[rng.randint(-2 ** rng.randint(1, 80), 2 ** 80) for _ in range(rng.randint(1, 5))] for _ in range(m + 1)]
+        gc = [[rng.randint(-2 ** rng.randint(1, 80), 2 ** 80) for _ in range(rng.randint(1, 5))] for _ in range(n + 1)]
+        fc[-1] = fc[-1] or [1]
+        gc[-1] = gc[-1] or [1]
+        exact = math.log2(planner.det_coeff_bound(fc, gc))
+        fast = planner.log2_coeff_bound(fc, gc)
+        assert exact - 1e-6 <= fast <= exact + 1e-6
+        primes, _ = planner.choose_primes_log2(fast, fc[-1], gc[-1])
+        mod = 1
+        for p in primes:
+            mod *= p
+        assert mod > 4 * planner.det_coeff_bound(fc, gc)
