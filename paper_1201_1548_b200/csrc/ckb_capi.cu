@@ -505,7 +505,7 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
                           d_status, st)))
     return rc;
   uint32_t* d_crtS;
-  if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
+  if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
   launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
   stage_mark(st);
   g.launches += 2;
@@ -588,7 +588,7 @@ int ckb_crt_lift(const uint32_t* residues, int K, int N, const uint32_t* primes,
   if ((rc = dbuf("c.out", (size_t)N * LW, &d_out))) return rc;
   CK(cudaMemcpyAsync(d_res, residues, 4 * (size_t)K * N, cudaMemcpyHostToDevice, st));
   uint32_t* d_crtS;
-  if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
+  if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
   launch_crt(ce->t, d_res, N, d_out, d_crtS, st);
   g.launches += 2;
   CK(cudaGetLastError());
@@ -727,7 +727,7 @@ int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, 
   CrtEntry* ce;
   if ((rc = get_crt(primes, K, LW, &ce))) return rc;
   uint32_t* d_crtS;
-  if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
+  if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
   launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
   g.launches += 2;
   CK(cudaGetLastError());
@@ -752,7 +752,7 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
                           d_status, st)))
     return rc;
   uint32_t* d_crtS;
-  if ((rc = dbuf("crtS", (size_t)3 * N * LW, &d_crtS))) return rc;
+  if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
   launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
   stage_mark(st);
   g.launches += 2;

@@ -4,15 +4,17 @@
 // Reference: curvekit.modpoly._CrtAccumulator.add / symmetric
 // (pkg/src/curvekit/modpoly.py:278-300) and crt_reconstruct (:264-275):
 // incremental Garner, then x - M if 2x > M.  The result is the unique
-// representative of the residues in (-M/2, M/2]; this kernel computes the
-// same integer by the *explicit* CRT, which has no sequential recurrence:
-//     y_i = r_i * (M/p_i)^-1 mod p_i                     (one Shoup product)
-//     X   = sum_i y_i * (M/p_i)                           (an N x K x LW integer
-//                                                          product: K2 below)
-//     q   = round(sum_i y_i / p_i)                       (FP64)
-//     x   = X - q M
+// representative of the residues in (-M/2, M/2]; this computes the same
+// integer by the *explicit* CRT, which has no sequential recurrence:
+//     y_i = r_i * (M/p_i)^-1 mod p_i                     (k_crt_prep)
+//     q   = round(sum_i y_i / p_i)                       (k_crt_prep, FP64)
+//     X   = sum_i y_i * (M/p_i)                           (k_crt_gemm: an N x K x LW
+//                                                          integer product, 96-bit sums)
+//     x   = X - q M                                      (k_crt_carry: signed carries)
 // X/M = q + x/M exactly; the planner guarantees M > 4 * bound, so |x/M| < 1/4
-// and the FP64 sum (error < K^2 2^-52) always rounds to the right q.
+// and the FP64 sum (error < K^2 2^-52) always rounds to the right q.  Callers
+// without that margin (crt_reconstruct on arbitrary residues) get an exact
+// fold when the sum lands near a half-integer.
 #include "ckb_kernels.cuh"
 
 namespace ckb {
@@ -22,12 +24,45 @@ constexpr int TL = 32;   // limbs per CTA tile
 constexpr int TI = 32;   // primes per k-step
 constexpr int CRT_THREADS = 256;
 
-// K2: S[k][l] = sum_i y_i(k) * (M/p_i)[l] as 96-bit (lo64, hi32) column sums.
-// Thread micro-tile: 2 coefficients x 4 limbs.
-__global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uint32_t* __restrict__ r, int N,
+// ---------------------------------------------------------------------------
+// prep: y[i][k] and q[k]; 32 coefficients x 8 prime slices per CTA
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_crt_prep(CrtTables T, const uint32_t* __restrict__ r, int N,
+                                                  uint32_t* __restrict__ y, int64_t* __restrict__ qk,
+                                                  uint32_t* __restrict__ amb) {
+  __shared__ double part[8][33];
+  const int kk = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + kk;
+  const int K = T.K;
+  double s = 0.0;
+  if (k < N) {
+    for (int i = sl; i < K; i += 8) {
+      const uint32_t p = T.p[i];
+      const uint32_t v = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
+      y[(size_t)i * N + k] = v;
+      s = fma((double)v, T.pinvd[i], s);
+    }
+  }
+  part[sl][kk] = s;
+  __syncthreads();
+  if (sl == 0 && k < N) {
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += part[j][kk];
+    qk[k] = llrint(t);
+    amb[k] = fabs((t - floor(t)) - 0.5) < 1e-3;  // near a half-integer: exact fold needed
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gemm: S[k][l] = sum_i y_i(k) * (M/p_i)[l] as 96-bit (lo64, hi32) column sums,
+// coefficient-major S[k][l][3].  Thread micro-tile: 2 coefficients x 4 limbs;
+// products of 30-bit y and 32-bit limbs accumulate 4 at a time in 64 bits.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uint32_t* __restrict__ y, int N,
                                                           uint32_t* __restrict__ S) {
-  __shared__ uint32_t sy[TI][TN];
-  __shared__ uint32_t sm[TI][TL];
+  __shared__ uint32_t sy[2][TI][TN];
+  __shared__ uint32_t sm[2][TI][TL];
   const int K = T.K, LW = T.LW;
   const int k0 = blockIdx.x * TN, l0 = blockIdx.y * TL;
   const int tid = threadIdx.x;
@@ -35,144 +70,189 @@ __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uin
   const int tl = (tid / 32) * 4;        // limb offset (0..28)
   uint64_t lo[2][4] = {};
   uint32_t hi[2][4] = {};
-  for (int i0 = 0; i0 < K; i0 += TI) {
-    // stage y (computed on the fly from the residues) and the M/p_i limbs
+  auto stage = [&](int buf, int i0) {
     for (int e = tid; e < TI * TN; e += CRT_THREADS) {
       const int ii = e / TN, kk = e % TN;
       const int i = i0 + ii, k = k0 + kk;
-      uint32_t y = 0;
-      if (i < K && k < N) {
-        const uint32_t p = T.p[i];
-        y = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
-      }
-      sy[ii][kk] = y;
+      sy[buf][ii][kk] = (i < K && k < N) ? y[(size_t)i * N + k] : 0u;
     }
     for (int e = tid; e < TI * TL; e += CRT_THREADS) {
       const int ii = e / TL, ll = e % TL;
       const int i = i0 + ii, l = l0 + ll;
-      sm[ii][ll] = (i < K && l < LW) ? T.Mi[(size_t)i * LW + l] : 0u;
+      sm[buf][ii][ll] = (i < K && l < LW) ? T.Mi[(size_t)i * LW + l] : 0u;
     }
-    __syncthreads();
-#pragma unroll 4
-    for (int ii = 0; ii < TI; ++ii) {
-      const uint2 yv = *reinterpret_cast<const uint2*>(&sy[ii][tk]);
-      const uint4 mv = *reinterpret_cast<const uint4*>(&sm[ii][tl]);
-      const uint32_t ys[2] = {yv.x, yv.y};
-      const uint32_t ms[4] = {mv.x, mv.y, mv.z, mv.w};
+  };
+  stage(0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int i0 = 0; i0 < K; i0 += TI) {
+    if (i0 + TI < K) stage(buf ^ 1, i0 + TI);  // prefetch the next tile while computing this one
+#pragma unroll
+    for (int i4 = 0; i4 < TI; i4 += 4) {
+      uint64_t acc[2][4] = {};
+#pragma unroll
+      for (int ii = i4; ii < i4 + 4; ++ii) {
+        const uint2 yv = *reinterpret_cast<const uint2*>(&sy[buf][ii][tk]);
+        const uint4 mv = *reinterpret_cast<const uint4*>(&sm[buf][ii][tl]);
+        const uint32_t ys[2] = {yv.x, yv.y};
+        const uint32_t ms[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] += (uint64_t)ys[a] * ms[b];  // 4 products < 2^64
+      }
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const uint64_t pr = (uint64_t)ys[a] * ms[b];
-          const uint64_t s = lo[a][b] + pr;
-          hi[a][b] += (s < pr);
+          const uint64_t s = lo[a][b] + acc[a][b];
+          hi[a][b] += (s < acc[a][b]);
           lo[a][b] = s;
         }
     }
     __syncthreads();
+    buf ^= 1;
   }
-  // limb-major layout S[l][0..2][k]: the carry pass reads it coalesced
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 2; ++a) {
+    const int k = k0 + tk + a;
+    if (k >= N) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int k = k0 + tk + a, l = l0 + tl + b;
-      if (k < N && l < LW) {
-        uint32_t* o = S + (size_t)l * 3 * N + k;
+      const int l = l0 + tl + b;
+      if (l < LW) {
+        uint32_t* o = S + ((size_t)k * LW + l) * 3;
         o[0] = (uint32_t)lo[a][b];
-        o[N] = (uint32_t)(lo[a][b] >> 32);
-        o[2 * N] = hi[a][b];
+        o[1] = (uint32_t)(lo[a][b] >> 32);
+        o[2] = hi[a][b];
       }
     }
+  }
 }
 
-// K3: per coefficient, q = round(sum y_i / p_i), then x = S - q M with a
-// signed carry chain over the limbs -> two's complement out[k][0..LW).
-__global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, const uint32_t* __restrict__ r, int N,
-                                                   const uint32_t* __restrict__ S, uint32_t* __restrict__ out) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  __shared__ uint32_t stage[128][33];
-  const int tid = threadIdx.x, k0 = blockIdx.x * blockDim.x;
-  const bool act = k < N;
-  const int K = T.K, LW = T.LW;
-  double s = 0.0;
-  if (act) {
-#pragma unroll 8
-    for (int i = 0; i < K; ++i) {
-      const uint32_t p = T.p[i];
-      const uint32_t y = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
-      s = fma((double)y, T.pinvd[i], s);
-    }
-  }
-  const uint64_t q = (uint64_t)llrint(s);
-  // carry = (c_hi:c_lo) signed 128-bit; value at limb l = S_l - q M_l + carry
-  long long c_hi = 0;
-  unsigned long long c_lo = 0;
-  for (int l0 = 0; l0 < LW; l0 += 32) {
-    if (act) {
-      // issue every load of the chunk before the (sequential) carry chain
-      uint32_t v0[32], v1[32], v2[32], ml[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int l = l0 + j;
-        const bool in = l < LW;
-        const uint32_t* Sl = S + (size_t)(in ? l : 0) * 3 * N + k;
-        v0[j] = in ? Sl[0] : 0u;
-        v1[j] = in ? Sl[N] : 0u;
-        v2[j] = in ? Sl[2 * N] : 0u;
-        ml[j] = in ? T.Ml[l] : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const unsigned long long s_lo = (unsigned long long)v0[j] | ((unsigned long long)v1[j] << 32);
-        const long long s_hi = v2[j];
-        const unsigned long long qm = q * (unsigned long long)ml[j];  // < 2^44
-        unsigned long long t_lo = s_lo - qm;  // t = s - qm + carry
-        long long t_hi = s_hi - (long long)(s_lo < qm);
-        const unsigned long long u = t_lo + c_lo;
-        t_hi += c_hi + (long long)(u < t_lo);
-        t_lo = u;
-        stage[tid][j] = (uint32_t)t_lo;
-        c_lo = (t_lo >> 32) | ((unsigned long long)t_hi << 32);  // carry = t >> 32
-        c_hi = t_hi >> 32;
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < 128 * 32; e += blockDim.x) {  // coalesced rows
-      const int rr = e >> 5, j = e & 31;
-      if (k0 + rr < N && l0 + j < LW) out[(size_t)(k0 + rr) * LW + l0 + j] = stage[rr][j];
-    }
-    __syncthreads();
-  }
-  if (!act) return;
+// ---------------------------------------------------------------------------
+// carry: one warp per coefficient, 8 limbs per lane per 256-limb chunk.
+// Each lane carries through its 8 limbs with carry-in 0, then the true
+// carry-ins run along the lanes (32 cheap sequential steps: adding a carry-in
+// below 2^63 to a segment changes its carry-out by -1, 0 or +1, decided by the
+// segment's low 64 bits and whether its upper limbs are all ones / all zeros),
+// then each lane applies its carry-in.
+// ---------------------------------------------------------------------------
+struct I128 {
+  long long hi;
+  unsigned long long lo;
+};
+__device__ __forceinline__ I128 add128(I128 a, long long bhi, unsigned long long blo) {
+  I128 r;
+  r.lo = a.lo + blo;
+  r.hi = a.hi + bhi + (long long)(r.lo < a.lo);
+  return r;
+}
+
+__global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uint32_t* __restrict__ S,
+                                                   const int64_t* __restrict__ qk, const uint32_t* __restrict__ amb,
+                                                   uint32_t* __restrict__ out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 4 + warp;
+  if (k >= N) return;
+  const unsigned FULL = 0xffffffffu;
+  const int LW = T.LW;
+  const unsigned long long q = (unsigned long long)qk[k];
+  const uint32_t* Sk = S + (size_t)k * LW * 3;
   uint32_t* ok = out + (size_t)k * LW;
-  // Exactness guard for callers without the 4x margin (crt_reconstruct on
-  // arbitrary residues): if s was near a half-integer, q may be off by one;
-  // fold x into [-floor(M/2), floor(M/2)] exactly.  Never taken when M > 4 bound.
-  const double fr = s - floor(s);
-  if (fabs(fr - 0.5) < 1e-3) {
-    // d = x - H - 1 ; if d >= 0 then x -= M
-    long long br = 0;
-    for (int l = 0; l < LW; ++l) {
-      const long long v = (long long)ok[l] - (long long)T.Mh[l] - (l == 0 ? 1 : 0) + br;
-      br = v >> 32;
+  long long cin_hi = 0;            // carry into the chunk (signed 128-bit, fits in hi:lo)
+  unsigned long long cin_lo = 0;
+  for (int c0 = 0; c0 < LW; c0 += 256) {
+    const int l0 = c0 + lane * 8;
+    uint32_t o[8];
+    I128 c = {0, 0};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int l = l0 + j;
+      unsigned long long s_lo = 0, qm = 0;
+      long long s_hi = 0;
+      if (l < LW) {
+        s_lo = (unsigned long long)Sk[3 * l] | ((unsigned long long)Sk[3 * l + 1] << 32);
+        s_hi = Sk[3 * l + 2];
+        qm = q * (unsigned long long)T.Ml[l];
+      }
+      I128 t;
+      t.lo = s_lo - qm;
+      t.hi = s_hi - (long long)(s_lo < qm);
+      t = add128(t, c.hi, c.lo);
+      o[j] = (uint32_t)t.lo;
+      c.lo = (t.lo >> 32) | ((unsigned long long)t.hi << 32);  // t >> 32
+      c.hi = t.hi >> 32;
     }
-    const bool x_top_neg = (int32_t)ok[LW - 1] < 0;
-    // the sign of d is the sign of the full-width result: x (signed) - H - 1
-    const bool gt = !x_top_neg && br >= 0;
-    // e = x + H ; if e < 0 then x += M
-    long long cr = 0;
-    for (int l = 0; l < LW; ++l) {
-      const long long v = (long long)ok[l] + (long long)T.Mh[l] + cr;
-      cr = v >> 32;
+    // segment summary for the carry-in transfer
+    const unsigned long long seg_lo = (unsigned long long)o[0] | ((unsigned long long)o[1] << 32);
+    bool ones = true, zeros = true;
+#pragma unroll
+    for (int j = 2; j < 8; ++j) {
+      ones &= (o[j] == 0xffffffffu);
+      zeros &= (o[j] == 0u);
     }
-    const bool lt = x_top_neg && cr == 0;  // x + H did not carry out of a negative x: still negative
-    if (gt || lt) {
-      long long c = 0;
+    // sequential carry-ins along the lanes (c is small: |c| < 2^63)
+    long long my_cin = 0;  // carry into this lane's segment (fits in 64 bits)
+    long long run = (long long)cin_lo;  // carry entering lane 0 (|.| < 2^63)
+    (void)cin_hi;
+    for (int s = 0; s < 32; ++s) {
+      if (lane == s) {
+        my_cin = run;
+        // value added to limbs 0..1: seg_lo + run (signed); carry kappa into limb 2
+        const unsigned long long u = seg_lo + (unsigned long long)run;
+        long long kappa = (run >= 0) ? (long long)(u < seg_lo) : -(long long)(u > seg_lo);
+        long long delta = 0;
+        if (kappa == 1 && ones) delta = 1;
+        if (kappa == -1 && zeros) delta = -1;
+        run = (long long)c.lo + delta;  // this lane's carry-out
+      }
+      run = __shfl_sync(FULL, run, s);
+    }
+    // apply the carry-in
+    {
+      const unsigned long long u = seg_lo + (unsigned long long)my_cin;
+      long long kappa = (my_cin >= 0) ? (long long)(u < seg_lo) : -(long long)(u > seg_lo);
+      o[0] = (uint32_t)u;
+      o[1] = (uint32_t)(u >> 32);
+#pragma unroll
+      for (int j = 2; j < 8; ++j) {
+        const long long v = (long long)o[j] + kappa;
+        o[j] = (uint32_t)v;
+        kappa = v >> 32;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (l0 + j < LW) ok[l0 + j] = o[j];
+    cin_lo = (unsigned long long)run;  // carry out of lane 31 = into the next chunk
+  }
+  // Exactness guard (never taken when M > 4 bound): fold x into
+  // [-floor(M/2), floor(M/2)] if q came from a sum near a half-integer.
+  if (amb[k]) {
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) {
+      long long br = 0;  // d = x - H - 1 >= 0  <=>  x > H
       for (int l = 0; l < LW; ++l) {
-        const long long v = (long long)ok[l] + (gt ? -(long long)T.Ml[l] : (long long)T.Ml[l]) + c;
-        ok[l] = (uint32_t)v;
-        c = v >> 32;
+        const long long v = (long long)ok[l] - (long long)T.Mh[l] - (l == 0 ? 1 : 0) + br;
+        br = v >> 32;
+      }
+      const bool x_top_neg = (int32_t)ok[LW - 1] < 0;
+      const bool gt = !x_top_neg && br >= 0;
+      long long cr = 0;  // e = x + H < 0  <=>  x < -H
+      for (int l = 0; l < LW; ++l) {
+        const long long v = (long long)ok[l] + (long long)T.Mh[l] + cr;
+        cr = v >> 32;
+      }
+      const bool lt = x_top_neg && cr == 0;
+      if (gt || lt) {
+        long long cc = 0;
+        for (int l = 0; l < LW; ++l) {
+          const long long v = (long long)ok[l] + (gt ? -(long long)T.Ml[l] : (long long)T.Ml[l]) + cc;
+          ok[l] = (uint32_t)v;
+          cc = v >> 32;
+        }
       }
     }
   }
@@ -180,9 +260,19 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, const uint32_t* 
 
 void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
                 cudaStream_t st) {
+  // scratch: S [N][LW][3] | y [K][N] | q [N] (int64) | amb [N]
+  uint32_t* S = scratch;
+  uint32_t* y = S + (size_t)3 * N * t.LW;
+  int64_t* qk = reinterpret_cast<int64_t*>(y + (((size_t)t.K * N + 1) & ~(size_t)1));
+  uint32_t* amb = reinterpret_cast<uint32_t*>(qk + N);
+  k_crt_prep<<<(N + 31) / 32, 256, 0, st>>>(t, coeffs, N, y, qk, amb);
   dim3 g1((N + TN - 1) / TN, (t.LW + TL - 1) / TL);
-  k_crt_gemm<<<g1, CRT_THREADS, 0, st>>>(t, coeffs, N, scratch);
-  k_crt_carry<<<(N + 127) / 128, 128, 0, st>>>(t, coeffs, N, scratch, out);
+  k_crt_gemm<<<g1, CRT_THREADS, 0, st>>>(t, y, N, S);
+  k_crt_carry<<<(N + 3) / 4, 128, 0, st>>>(t, N, S, qk, amb, out);
+}
+
+size_t crt_scratch_words(int K, int N, int LW) {
+  return (size_t)3 * N * LW + (size_t)K * N + 2 + (size_t)2 * N + N + 16;
 }
 
 }  // namespace ckb

@@ -91,6 +91,7 @@ struct CrtTables {
 // coeffs [K][N] -> out [N][LW]; scratch >= 3 N LW words
 void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
                 cudaStream_t st);
+size_t crt_scratch_words(int K, int N, int LW);  // scratch size for launch_crt
 
 // ---- K6: batched gcd mod p (modpoly.py:115-122), interpolation at arbitrary points
 void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_t* gb, const int32_t* db, int Wg,
