@@ -260,11 +260,11 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uin
 
 void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
                 cudaStream_t st) {
-  // scratch: S [N][LW][3] | y [K][N] | q [N] (int64) | amb [N]
-  uint32_t* S = scratch;
-  uint32_t* y = S + (size_t)3 * N * t.LW;
-  int64_t* qk = reinterpret_cast<int64_t*>(y + (((size_t)t.K * N + 1) & ~(size_t)1));
+  // scratch (cudaMalloc-aligned): q [N] (int64) | amb [N] | S [N][LW][3] | y [K][N]
+  int64_t* qk = reinterpret_cast<int64_t*>(scratch);
   uint32_t* amb = reinterpret_cast<uint32_t*>(qk + N);
+  uint32_t* S = amb + N;
+  uint32_t* y = S + (size_t)3 * N * t.LW;
   k_crt_prep<<<(N + 31) / 32, 256, 0, st>>>(t, coeffs, N, y, qk, amb);
   dim3 g1((N + TN - 1) / TN, (t.LW + TL - 1) / TL);
   k_crt_gemm<<<g1, CRT_THREADS, 0, st>>>(t, y, N, S);
