@@ -88,10 +88,10 @@ __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uin
   for (int i0 = 0; i0 < K; i0 += TI) {
     if (i0 + TI < K) stage(buf ^ 1, i0 + TI);  // prefetch the next tile while computing this one
 #pragma unroll
-    for (int i4 = 0; i4 < TI; i4 += 4) {
-      uint64_t acc[2][4] = {};
+    for (int i4 = 0; i4 < TI; i4 += 2) {
+      uint64_t acc[2][4] = {};  // 2 products of y < 2^31 and a 32-bit limb stay below 2^64
 #pragma unroll
-      for (int ii = i4; ii < i4 + 4; ++ii) {
+      for (int ii = i4; ii < i4 + 2; ++ii) {
         const uint2 yv = *reinterpret_cast<const uint2*>(&sy[buf][ii][tk]);
         const uint4 mv = *reinterpret_cast<const uint4*>(&sm[buf][ii][tl]);
         const uint32_t ys[2] = {yv.x, yv.y};
