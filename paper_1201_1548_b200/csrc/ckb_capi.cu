@@ -288,21 +288,24 @@ cudaStream_t pick_stream(void* s) { return s ? (cudaStream_t)s : g.stream; }
 // ---- interpolation plans, cached per (primes, generators, N) -----------------
 struct PlanEntry {
   std::vector<uint32_t> primes, gens;
-  int N = 0;
+  int N = 0, S = 1;
   InterpPlan pl;
   void* blob = nullptr;
   uint64_t last_use = 0;
 };
 std::vector<PlanEntry> g_plans;
 
-int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int N, InterpPlan* out) {
+// Nfull points per prime, polyphase factor S (1 or 8): the interpolation plan
+// has M = ceil(Nfull / S) points with ratio g^S
+int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int S, InterpPlan* out) {
   for (auto& e : g_plans)
-    if (e.N == N && (int)e.primes.size() == K && !memcmp(e.primes.data(), primes, 4 * (size_t)K) &&
+    if (e.N == Nfull && e.S == S && (int)e.primes.size() == K && !memcmp(e.primes.data(), primes, 4 * (size_t)K) &&
         !memcmp(e.gens.data(), gens, 4 * (size_t)K)) {
       e.last_use = ++g.tick;
       *out = e.pl;
       return 0;
     }
+  const int N = (Nfull + S - 1) / S;
   int logL = 0;
   while ((1 << logL) < 2 * N - 1) ++logL;
   if (logL > 14) return fail("interpolation supports N <= 8192 points (NTT length <= 2^14)", -2);
@@ -319,17 +322,23 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int N, InterpP
   PlanEntry e;
   e.primes.assign(primes, primes + K);
   e.gens.assign(gens, gens + K);
-  e.N = N;
+  e.N = Nfull;
+  e.S = S;
   InterpPlan& pl = e.pl;
   pl.N = N;
   pl.K = K;
+  pl.S = S;
+  pl.Nfull = Nfull;
   pl.L = (int)L;
   pl.logL = logL;
   const size_t kn = (size_t)K * N, kn1 = (size_t)K * (N + 1), kl = (size_t)K * L, kh = kl / 2;
-  const size_t words = kn * 8 + kn1 * 3 + kh * 4 + kl * 4 + (size_t)K * 5 + 64;  // see take() below
+  const size_t words = kn * 10 + kn1 * 3 + kh * 4 + kl * 4 + (size_t)K * 5 + (size_t)K * 4 * S + 64;  // take()s
   CK(cudaMalloc(&e.blob, 4 * words));
   uint32_t* b = (uint32_t*)e.blob;
   auto take = [&](size_t n) { uint32_t* r = b; b += n; return r; };
+  pl.yq = take(kn);
+  pl.yqi = take(kn);
+  pl.om = take((size_t)K * 4 * S);
   pl.xq = take(kn);
   pl.hC = take(2 * kn);
   pl.hCinv = take(kn);
@@ -376,9 +385,11 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   uint32_t *d_red, *d_vals, *d_cval;
   int rc;
   InterpPlan pl;
-  if ((rc = get_plan(h_primes, h_gens, K, N, &pl))) return rc;
+  constexpr int S = 8;  // polyphase cosets (the images kernel's 8-lane groups)
+  if ((rc = get_plan(h_primes, h_gens, K, N, S, &pl))) return rc;
+  const int NI = S * pl.N;  // images per prime (>= N)
   if ((rc = dbuf("red", (size_t)K * C, &d_red))) return rc;
-  if ((rc = dbuf("vals", (size_t)K * N, &d_vals))) return rc;
+  if ((rc = dbuf("vals", (size_t)K * NI, &d_vals))) return rc;
   if ((rc = dbuf("cval", (size_t)K, &d_cval))) return rc;
   stage_mark(st);
   launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
@@ -389,7 +400,8 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   ImageArgs a;
   a.red = d_red;
   a.degs = d_degs;
-  a.xq = pl.xq;
+  a.yq = pl.yq;
+  a.om = pl.om;
   a.cval = d_cval;
   a.primes = d_primes;
   a.C = C;
@@ -397,12 +409,13 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   a.n = n;
   a.dfx = dfx;
   a.dgx = dgx;
-  a.N = N;
+  a.N = NI;
+  a.M = pl.N;
   a.K = K;
   a.values = d_vals;
   a.status = d_status;
-  if ((rc = dbuf("fail", (size_t)K * N + 1, &a.fail_list))) return rc;
-  a.fail_count = a.fail_list + (size_t)K * N;
+  if ((rc = dbuf("fail", (size_t)K * NI + 1, &a.fail_list))) return rc;
+  a.fail_count = a.fail_list + (size_t)K * NI;
   CK(cudaMemsetAsync(a.fail_count, 0, 4, st));
   launch_images(a, st);
   stage_mark(st);
@@ -604,7 +617,7 @@ int ckb_interp_plan_points(const uint32_t* primes, const uint32_t* gens, int K, 
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, K))) return rc;
   InterpPlan pl;
-  if ((rc = get_plan(primes, gens, K, N, &pl))) return rc;
+  if ((rc = get_plan(primes, gens, K, N, 1, &pl))) return rc;
   CK(cudaMemcpy(xpts, pl.xq, 4 * (size_t)K * N, cudaMemcpyDeviceToHost));
   return 0;
 }
@@ -618,7 +631,7 @@ int ckb_interp_geometric(const uint32_t* values, const uint32_t* primes, const u
   if ((rc = check_primes(primes, K))) return rc;
   cudaStream_t st = g.stream;
   InterpPlan pl;
-  if ((rc = get_plan(primes, gens, K, N, &pl))) return rc;
+  if ((rc = get_plan(primes, gens, K, N, 1, &pl))) return rc;
   Prime* d_primes;
   uint32_t *d_vals, *d_coeffs, *d_cval;
   if ((rc = get_primes_dev(primes, K, &d_primes))) return rc;

@@ -78,7 +78,9 @@ __global__ void k_images_fallback(ImageArgs a, int W) {
     const Prime P = a.primes[pi];
     const uint32_t p = P.p;
     const uint32_t c = a.cval[pi];
-    uint32_t x = a.xq[flat];
+    const int loc = (int)(flat - (uint32_t)pi * (uint32_t)a.N), S = a.N / a.M;
+    const uint32_t* om = a.om + (size_t)pi * 4 * S;
+    uint32_t x = shoup(a.yq[(size_t)pi * a.M + loc / S], om[loc % S], om[S + loc % S], p);  // w^j g^u
     if (c != 1u) x = shoup(x, c, shoup_comp(c, P), p);
     const uint32_t xc = shoup_comp(x, P);
     const uint32_t* res = a.red + (size_t)pi * a.C;

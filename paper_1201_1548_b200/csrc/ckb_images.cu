@@ -16,11 +16,15 @@ namespace ckb {
 
 constexpr int IMG_THREADS = 128;
 
-// shared-memory row width of the transposed, top-aligned residue tables
+constexpr int POLY = 8;  // polyphase factor S: one 8-lane group per coset {w^j y_u}
+
+// shared-memory row width of the transposed, top-aligned residue tables.  An
+// odd number of 16-byte chunks per row makes the 8 rows read by one lane
+// group (x-powers r + 8e', r < 8) fall in disjoint banks.
 template <int MAXD>
 struct ImgLayout {
-  static constexpr int NCH = (MAXD + 4) / 4;  // chunks of 4 registers
-  static constexpr int SW = NCH * 4;          // words per x-power row
+  static constexpr int NCH = (MAXD + 4) / 4;                   // chunks of 4 registers
+  static constexpr int SW = ((NCH & 1) ? NCH : NCH + 1) * 4;   // words per x-power row
 };
 
 template <int MAXD>
@@ -37,19 +41,22 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
   const int16_t* Adeg = a.degs + (sw ? a.m + 1 : 0);
   const int16_t* Bdeg = a.degs + (sw ? 0 : a.m + 1);
   const int dmax = max(a.dfx, a.dgx);
+  const int emax = dmax / POLY;               // Horner steps in z = y^8
+  const int rows = POLY * (emax + 1);         // x-power rows, zero-padded
   // TA[e][i] = coefficient of x^e in the y-coefficient of degree da - i (top-aligned),
   // zero beyond each row; maskA[e] = chunks of registers with a term at x^e
   uint32_t* TA = sm;
-  uint32_t* TB = sm + (dmax + 1) * SW;
-  uint32_t* maskA = sm + 2 * (dmax + 1) * SW;
-  uint32_t* maskB = maskA + (dmax + 1);
+  uint32_t* TB = sm + rows * SW;
+  uint32_t* maskA = sm + 2 * rows * SW;
+  uint32_t* maskB = maskA + rows;
+  uint32_t* som = maskB + rows;               // w^k and companions
   const uint32_t* gres = a.red + (size_t)pi * a.C;
-  for (int idx = threadIdx.x; idx < (dmax + 1) * SW; idx += IMG_THREADS) {
+  for (int idx = threadIdx.x; idx < rows * SW; idx += IMG_THREADS) {
     const int e = idx / SW, i = idx % SW;
     TA[idx] = (i <= da && e < Astr) ? gres[offA + (da - i) * Astr + e] : 0u;
     TB[idx] = (i <= db && e < Bstr) ? gres[offB + (db - i) * Bstr + e] : 0u;
   }
-  for (int e = threadIdx.x; e <= dmax; e += IMG_THREADS) {
+  for (int e = threadIdx.x; e < rows; e += IMG_THREADS) {
     uint32_t ma = 0, mb = 0;
     for (int i = 0; i <= MAXD; ++i) {
       if (i <= da && Adeg[da - i] >= e) ma |= 1u << (i >> 2);
@@ -58,30 +65,41 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
     maskA[e] = ma;
     maskB[e] = mb;
   }
+  if (threadIdx.x < 2 * POLY) som[threadIdx.x] = a.om[(size_t)pi * 4 * POLY + threadIdx.x];
   __syncthreads();
 
+  // image (u, j): x = w^j c y_u.  Lane l of an 8-lane group evaluates the
+  // polyphase component G_l = y^l F_l(y^8) of every y-coefficient; a 3-stage
+  // DFT across the group then gives f(w^j y) for all j (j = bitrev(l)).
   const int t = blockIdx.x * IMG_THREADS + threadIdx.x;
-  if (t >= a.N) return;
+  const bool active = t < a.N;  // a.N = 8 M; inactive lanes still join the shuffles
+  const int u = active ? (t >> 3) : 0, l = t & (POLY - 1);
   const Prime P = a.primes[pi];
   const uint32_t p = P.p;
   const uint32_t c = a.cval[pi];
-  uint32_t x = a.xq[(size_t)pi * a.N + t];
-  if (c != 1u) x = shoup(x, c, shoup_comp(c, P), p);  // x_t = c q^t
-  const uint32_t xc = comp_from_mont(to_mont(x, P), P);
+  uint32_t y = a.yq[(size_t)pi * a.M + u];
+  if (c != 1u) y = shoup(y, c, shoup_comp(c, P), p);  // y_u = c g^u
+  const uint32_t y2 = mul_mod(y, y, P), y4 = mul_mod(y2, y2, P);
+  const uint32_t z = mul_mod(y4, y4, P);  // Horner variable y^8
+  uint32_t yl = (l & 1) ? y : 1u;          // y^l, l < 8
+  if (l & 2) yl = mul_mod(yl, y2, P);
+  if (l & 4) yl = mul_mod(yl, y4, P);
+  const uint32_t zc = comp_from_mont(to_mont(z, P), P);
 
-  // Horner of all y-coefficients in lock-step: one dynamic loop over the x
-  // power, every register an independent chain (ILP = m + n + 2); each chunk
-  // of 4 coefficients is one 16-byte broadcast load.  A chain that has not
-  // started yet multiplies 0, so the masks only skip work.
+  // Horner in z of all y-coefficients in lock-step: one dynamic loop, every
+  // register an independent chain (ILP = m + n + 2); each chunk of 4
+  // coefficients is one 16-byte load.  A chain that has not started yet
+  // multiplies 0, so the masks only skip work.
   uint32_t A[MAXD + 1], B[MAXD + 1];
 #pragma unroll
   for (int i = 0; i <= MAXD; ++i) A[i] = B[i] = 0u;
   uint32_t negp = 0u - p;
-  uint32_t xcp = xc;
+  uint32_t zcp = zc;
   // opaque to the optimiser: keeps both in registers instead of letting
   // ptxas rematerialise the companion (7 instructions) in every chunk
-  asm volatile("" : "+r"(negp), "+r"(xcp));
-  for (int e = dmax; e >= 0; --e) {
+  asm volatile("" : "+r"(negp), "+r"(zcp));
+  for (int e2 = emax; e2 >= 0; --e2) {
+    const int e = l + POLY * e2;
     const uint4* ta = reinterpret_cast<const uint4*>(TA + e * SW);
     const uint4* tb = reinterpret_cast<const uint4*>(TB + e * SW);
     const uint32_t mA = maskA[e], mB = maskB[e];
@@ -92,17 +110,47 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
         const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (4 * c + k <= MAXD) A[4 * c + k] = shoup_lazy_add(A[4 * c + k], x, xcp, negp, vv[k]);
+          if (4 * c + k <= MAXD) A[4 * c + k] = shoup_lazy_add(A[4 * c + k], z, zcp, negp, vv[k]);
       }
       if (mB & (1u << c)) {
         const uint4 v = tb[c];
         const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (4 * c + k <= MAXD) B[4 * c + k] = shoup_lazy_add(B[4 * c + k], x, xcp, negp, vv[k]);
+          if (4 * c + k <= MAXD) B[4 * c + k] = shoup_lazy_add(B[4 * c + k], z, zcp, negp, vv[k]);
       }
     }
   }
+  // G_l = y^l F_l, then the radix-2 DIF network across the group
+  {
+    const uint32_t ylc = comp_from_mont(to_mont(yl, P), P);
+#pragma unroll
+    for (int i = 0; i <= MAXD; ++i) {
+      A[i] = shoup_lazy(A[i], yl, ylc, p);
+      B[i] = shoup_lazy(B[i], yl, ylc, p);
+    }
+  }
+  const uint32_t p2 = 2u * p;
+  const unsigned FULL = 0xffffffffu;
+#pragma unroll
+  for (int h = POLY / 2; h >= 1; h >>= 1) {
+    const bool upper = (l & h) != 0;
+    const int widx = (l & (h - 1)) * (POLY / (2 * h));
+    const uint32_t w = upper ? som[widx] : 1u;
+    const uint32_t wc = upper ? som[POLY + widx] : (uint32_t)(0x100000000ull / p);  // companion of 1
+#pragma unroll
+    for (int i = 0; i <= MAXD; ++i) {
+      // upper lane: (lower - own) w in [0, 2p) via min(d, d + 2p) -- an exact
+      // zero stays zero, which the elimination relies on beyond the degree
+      const uint32_t oa = __shfl_xor_sync(FULL, A[i], h), ob = __shfl_xor_sync(FULL, B[i], h);
+      const uint32_t da_ = oa - A[i], db_ = ob - B[i];
+      A[i] = shoup_lazy(upper ? min(da_, da_ + p2) : A[i] + oa, w, wc, p);
+      B[i] = shoup_lazy(upper ? min(db_, db_ + p2) : B[i] + ob, w, wc, p);
+    }
+  }
+  const int j = ((l & 1) << 2) | (l & 2) | ((l >> 2) & 1);  // bitrev3(l)
+  const int idx = u * POLY + j;
+  if (!active) return;  // no shuffles below this point
   uint32_t v;
   if (red4(A[0], p) == 0u || red4(B[0], p) == 0u) {
     atomicOr(a.status, 2u);  // the plan guarantees this never happens
@@ -112,11 +160,11 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
     v = resultant_generic<MAXD>(A, da, B, db, neg, P);
     if (v == CKB_FAIL) {
       const uint32_t slot = atomicAdd(a.fail_count, 1u);
-      a.fail_list[slot] = (uint32_t)((size_t)pi * a.N + t);
+      a.fail_list[slot] = (uint32_t)((size_t)pi * a.N + idx);
       v = 0u;
     }
   }
-  a.values[(size_t)pi * a.N + t] = v;
+  a.values[(size_t)pi * a.N + idx] = v;
 }
 
 #define CKB_MAXD_LIST(X) X(4) X(8) X(12) X(16) X(24) X(32) X(40) X(48) X(56) X(64)
@@ -134,9 +182,10 @@ void launch_images(const ImageArgs& a, cudaStream_t st) {
   const int maxd = images_maxd(a.m, a.n);
   dim3 grid((a.N + IMG_THREADS - 1) / IMG_THREADS, a.K);
   const int dmax = a.dfx > a.dgx ? a.dfx : a.dgx;
+  const int rows = POLY * (dmax / POLY + 1);
 #define LAUNCH(D)                                                                                    \
   if (maxd == D) {                                                                                   \
-    const size_t smem = (size_t)(2 * (dmax + 1) * ImgLayout<D>::SW + 2 * (dmax + 1)) * 4;          \
+    const size_t smem = (size_t)(2 * rows * ImgLayout<D>::SW + 2 * rows + 2 * POLY) * 4;           \
     if (smem > 48 * 1024)                                                                            \
       cudaFuncSetAttribute(k_images<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
     k_images<D><<<grid, IMG_THREADS, smem, st>>>(a);                                                 \

@@ -155,11 +155,103 @@ __global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const P
   }
 }
 
+// Polyphase plan (S > 1): images v[u S + j] at x = w^j y_u, y_u = c g^u.  With
+// P(x) = sum_{r<S} x^r P_r(x^S):  P_r(z_u) = (1/S) y_u^-r sum_j w^-jr v[u S + j],
+// z_u = y_u^S = c^S q^u (q = g^S) -- S independent geometric interpolations of
+// size M, one CTA per (prime, r), interleaved into P_{S k + r}.
+constexpr int POLY_THREADS = 256;
+
+__global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, const Prime* __restrict__ primes,
+                                                              const uint32_t* __restrict__ values,
+                                                              const uint32_t* __restrict__ cval,
+                                                              uint32_t* __restrict__ coeffs) {
+  extern __shared__ uint32_t buf[];  // [L] data, then 4 x [L/2] twiddle tables
+  const int S = plan.S;
+  const int pi = blockIdx.x / S, r = blockIdx.x % S, tid = threadIdx.x, T = blockDim.x;
+  const Prime P = primes[pi];
+  const uint32_t p = P.p;
+  const int M = plan.N, L = plan.L, logL = plan.logL, half = L >> 1, Nfull = plan.Nfull;
+  const size_t oM = (size_t)pi * M, oL = (size_t)pi * L, oH = (size_t)pi * half;
+  uint32_t *W = buf + L, *Wc = W + half, *Wi = Wc + half, *Wic = Wi + half;
+  for (int j = tid; j < half; j += T) {
+    W[j] = plan.W[oH + j];
+    Wc[j] = plan.Wc[oH + j];
+    Wi[j] = plan.Wi[oH + j];
+    Wic[j] = plan.Wic[oH + j];
+  }
+  const uint32_t *Hf = plan.Hf + oL, *Hfc = plan.Hfc + oL, *Mf = plan.Mf + oL, *Mfc = plan.Mfc + oL;
+  const uint32_t* om = plan.om + (size_t)pi * 4 * S;
+  const uint32_t c = cval[pi];
+  // scalar (1/S) c^-r
+  uint32_t sc = inv_mod((uint32_t)S % p, P);
+  if (c != 1u) sc = mul_mod(sc, pow_mod(inv_mod(c, P), (uint64_t)r, P), P);
+  const uint32_t* v = values + (size_t)pi * M * S;
+  // a'_s = P_r(z_t) * zweight_t with t = M-1-s
+  for (int s = tid; s < L; s += T) {
+    uint32_t a = 0u;
+    if (s < M) {
+      const int t = M - 1 - s;
+      uint32_t g = 0u;
+#pragma unroll 8
+      for (int j = 0; j < S; ++j) {
+        const int k = (j * r) & (S - 1);
+        g = add_mod(g, shoup(v[(size_t)t * S + j], om[2 * S + k], om[3 * S + k], p), p);
+      }
+      uint32_t yr = mul_mod(sc, pow_mod(plan.yqi[oM + t], (uint64_t)r, P), P);  // (1/S) y_t^-r
+      g = mul_mod(g, yr, P);
+      a = shoup_lazy(g, plan.z[oM + t], plan.zc[oM + t], p);
+    }
+    buf[s] = a;
+  }
+  __syncthreads();
+  ntt_dif8<POLY_THREADS>(buf, logL, W, Wc, p);
+  for (int u = tid; u < L; u += T) buf[u] = shoup_lazy(buf[u], Hf[u], Hfc[u], p);
+  __syncthreads();
+  ntt_dit8<POLY_THREADS>(buf, logL, Wi, Wic, p);
+  uint32_t sv[MAX_PER_THREAD];
+#pragma unroll
+  for (int q = 0; q < MAX_PER_THREAD; ++q) {
+    const int e = tid + q * T;
+    sv[q] = (e < M) ? shoup_lazy(buf[M - 1 + e], plan.sS[oM + e], plan.sSc[oM + e], p) : 0u;
+  }
+  __syncthreads();
+  for (int u = tid; u < L; u += T) buf[u] = 0u;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < MAX_PER_THREAD; ++q) {
+    const int e = tid + q * T;
+    if (e < M) buf[M - 1 - e] = sv[q];
+  }
+  __syncthreads();
+  ntt_dif8<POLY_THREADS>(buf, logL, W, Wc, p);
+  for (int u = tid; u < L; u += T) buf[u] = shoup_lazy(buf[u], Mf[u], Mfc[u], p);
+  __syncthreads();
+  ntt_dit8<POLY_THREADS>(buf, logL, Wi, Wic, p);
+  // P_r[k] = conv[M-1+k] / L * (c^S)^-k  ->  coefficient S k + r
+  const uint32_t linv = plan.Linv[pi];
+  const uint32_t linvc = shoup_comp(linv, P);
+  const uint32_t cS = (c == 1u) ? 1u : pow_mod(inv_mod(c, P), (uint64_t)S, P);
+  uint32_t* out = coeffs + (size_t)pi * Nfull;
+  for (int k = tid; k < M; k += T) {
+    const int idx = S * k + r;
+    if (idx >= Nfull) continue;
+    uint32_t res = shoup(buf[M - 1 + k], linv, linvc, p);
+    if (c != 1u) res = mul_mod(res, pow_mod(cS, (uint64_t)k, P), P);
+    out[idx] = res;
+  }
+}
+
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
                    uint32_t* coeffs, cudaStream_t st) {
   const size_t smem = (size_t)plan.L * 4 * 3;  // data + 4 twiddle tables of L/2
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_interp<<<plan.K, NTT_THREADS, smem, st>>>(plan, primes, values, cval, coeffs);
+  if (plan.S == 1) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_interp<<<plan.K, NTT_THREADS, smem, st>>>(plan, primes, values, cval, coeffs);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_interp_poly, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_interp_poly<<<plan.K * plan.S, POLY_THREADS, smem, st>>>(plan, primes, values, cval, coeffs);
+  }
 }
 
 }  // namespace ckb

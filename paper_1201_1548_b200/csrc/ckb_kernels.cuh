@@ -16,10 +16,15 @@ void launch_reduce(const uint32_t* limbs, int C, int L, const Prime* primes, int
 // plan.  Points are x_t = c q^t; every table is for c = 1 (the interpolation
 // runs in y = x / c and the per-call scale c only enters through c^-k).
 struct InterpPlan {
-  int N;              // points per prime
+  int N;              // interpolation points per prime (per polyphase component: M = ceil(Nfull / S))
   int K;              // primes
+  int S;              // polyphase factor: images at w^j y_u (j < S, u < N), w a primitive S-th root
+  int Nfull;          // requested points (coefficients of the result)
   int L, logL;        // NTT length: power of two >= 2N - 1
-  uint32_t* xq;       // [K][N]    q^t
+  uint32_t* yq;       // [K][N]    g^u   (image base points y_u for c = 1)
+  uint32_t* yqi;      // [K][N]    g^-u
+  uint32_t* om;       // [K][4S]   w^k, companions, w^-k, companions
+  uint32_t* xq;       // [K][N]    q^t with q = g^S (the interpolation points z_t)
   uint32_t* hC;       // [K][2N]   q^C(m,2)              (construction scratch)
   uint32_t* hCinv;    // [K][N]    q^-C(e,2)             (construction scratch)
   uint32_t* Mt;       // [K][N+1]  coefficients of M~(y) = prod_t (y - q^t)   (scratch)
@@ -53,10 +58,12 @@ void launch_choose_c(const Prime* primes, const InterpPlan& plan, const uint32_t
 struct ImageArgs {
   const uint32_t* red;     // [K][C]
   const int16_t* degs;     // [(m+1) + (n+1)] x-degree of each y-coefficient (-1 = zero)
-  const uint32_t* xq;      // [K][N] q^t (plan)
-  const uint32_t* cval;    // [K] point scale c: x_t = c q^t
+  const uint32_t* yq;      // [K][M] g^u (plan)
+  const uint32_t* om;      // [K][4 S] roots of unity (plan)
+  const uint32_t* cval;    // [K] point scale c: image (u, j) at x = w^j c g^u
   const Prime* primes;
-  int C, m, n, dfx, dgx, N, K;
+  int C, m, n, dfx, dgx, N, K;  // N = S * M images per prime, stored at u * S + j
+  int M;
   uint32_t* values;        // [K][N]
   uint32_t* status;        // bit 1: an image hit a vanishing leading coefficient
   uint32_t* fail_list;     // [K*N] flat indices of non-generic images

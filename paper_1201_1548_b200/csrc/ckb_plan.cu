@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(const Prime* __restrict__
   const Prime P = primes[pi];
   const uint32_t p = P.p;
   const uint64_t pm1 = p - 1;
-  const uint32_t q = gens[pi] % p;
+  const uint32_t q = pow_mod(gens[pi] % p, (uint64_t)plan.S, P);  // ratio of the interpolation points
   const uint32_t qinv = inv_mod(q, P);
   const uint32_t qc = shoup_comp(q, P), qinvc = shoup_comp(qinv, P);
   const size_t oN = (size_t)pi * N, o2N = (size_t)pi * 2 * N, oN1 = (size_t)pi * (N + 1);
@@ -200,13 +200,17 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_choose_c(const Prime* __restri
     }
     return;
   }
-  const uint32_t* xq = plan.xq + (size_t)pi * N;
+  // image points x = w^j c y_u, j < S, u < N (polyphase cosets)
+  const int S = plan.S;
+  const uint32_t* yq = plan.yq + (size_t)pi * N;
+  const uint32_t* om = plan.om + (size_t)pi * 4 * S;
   for (int attempt = 0; attempt < 64; ++attempt) {
     const uint32_t c = (uint32_t)(attempt + 1) % p;
     const uint32_t cc = shoup_comp(c, P);
     int bad = 0;
-    for (int t = tid; t < N; t += T) {
-      const uint32_t x = shoup(xq[t], c, cc, p);
+    for (int t = tid; t < N * S; t += T) {
+      const int u = t / S, j = t % S;
+      const uint32_t x = shoup(shoup(yq[u], om[j], om[S + j], p), c, cc, p);
       const uint32_t xc = shoup_comp(x, P);
       uint32_t vf = 0, vg = 0;
       for (int i = lcf_deg; i >= 0; --i) vf = add_mod(shoup(vf, x, xc, p), lcf[i], p);
@@ -231,8 +235,40 @@ void launch_choose_c(const Prime* primes, const InterpPlan& plan, const uint32_t
                                                status);
 }
 
+// polyphase point tables: y_u = g^u, g^-u (u < M) and the S-th roots of unity
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan_poly(const Prime* __restrict__ primes,
+                                                            const uint32_t* __restrict__ gens, InterpPlan plan) {
+  const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, M = plan.N, S = plan.S;
+  const Prime P = primes[pi];
+  const uint32_t p = P.p;
+  const uint32_t g = gens[pi] % p, gi = inv_mod(g, P);
+  const uint32_t gc = shoup_comp(g, P), gic = shoup_comp(gi, P);
+  const size_t oM = (size_t)pi * M;
+  const int seg = (M + T - 1) / T;
+  const int s0 = min(M, tid * seg), s1 = min(M, s0 + seg);
+  if (s0 < s1) {
+    uint32_t a = pow_mod(g, s0, P), b = pow_mod(gi, s0, P);
+    for (int u = s0; u < s1; ++u) {
+      plan.yq[oM + u] = a;
+      plan.yqi[oM + u] = b;
+      a = shoup(a, g, gc, p);
+      b = shoup(b, gi, gic, p);
+    }
+  }
+  if (tid < S) {  // om[pi]: w^k, companions, w^-k, companions (w a primitive S-th root)
+    const uint32_t w = pow_mod(g, (uint64_t)(p - 1) / S, P);
+    const uint32_t wk = pow_mod(w, tid, P), wik = inv_mod(wk, P);
+    uint32_t* om = plan.om + (size_t)pi * 4 * S;
+    om[tid] = wk;
+    om[S + tid] = shoup_comp(wk, P);
+    om[2 * S + tid] = wik;
+    om[3 * S + tid] = shoup_comp(wik, P);
+  }
+}
+
 void launch_plan_base(const Prime* primes, const uint32_t* gens, const InterpPlan& plan, cudaStream_t st) {
   k_plan<<<plan.K, PLAN_THREADS, 0, st>>>(primes, gens, plan.N, plan);
+  k_plan_poly<<<plan.K, PLAN_THREADS, 0, st>>>(primes, gens, plan);
 }
 
 }  // namespace ckb
