@@ -14,9 +14,24 @@ Two counts are kept apart:
 from __future__ import annotations
 
 
+POLY = 8  # images per polyphase coset (csrc/ckb_images.cu)
+
+
 def eval_products(degs_f, degs_g) -> int:
-    """Shoup-Horner steps per image: sum of x-degrees of the y-coefficients."""
+    """Horner steps of a plain per-point evaluation: sum of the x-degrees."""
     return sum(max(d, 0) for d in degs_f) + sum(max(d, 0) for d in degs_g)
+
+
+def eval_products_poly(degs_f, degs_g, S: int = POLY) -> int:
+    """Products per image of the polyphase evaluation: each lane of an S-lane
+    coset runs Horner in y^S over its share of the coefficients (ceil((D+1)/S)
+    terms of a degree-D poly), then one product by y^r and log2(S) DFT stages."""
+    stages = S.bit_length() - 1
+    tot = 0
+    for d in list(degs_f) + list(degs_g):
+        if d >= 0:
+            tot += -(-(d + 1) // S) + 1 + stages
+    return tot
 
 
 def elim_products(m: int, n: int) -> int:
@@ -33,7 +48,9 @@ def elim_products(m: int, n: int) -> int:
 
 
 def images_products(m, n, degs_f, degs_g, K, N) -> int:
-    return K * N * (eval_products(degs_f, degs_g) + elim_products(m, n))
+    """Modular products of one launch of k_images: K primes x S*ceil(N/S) images."""
+    NI = POLY * -(-N // POLY)
+    return K * NI * (eval_products_poly(degs_f, degs_g) + elim_products(m, n))
 
 
 def interp_products(K: int, N: int) -> int:
