@@ -102,7 +102,11 @@ __global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
     const int e = l + POLY * e2;
     const uint4* ta = reinterpret_cast<const uint4*>(TA + e * SW);
     const uint4* tb = reinterpret_cast<const uint4*>(TB + e * SW);
-    const uint32_t mA = maskA[e], mB = maskB[e];
+    // union over the warp's rows: a chunk is skipped only where no lane's
+    // chains have started (a started chain never sees a cleared bit), so the
+    // union is as valid as the lane's own mask and makes the guards uniform
+    const uint32_t mA = __reduce_or_sync(0xffffffffu, maskA[e]);
+    const uint32_t mB = __reduce_or_sync(0xffffffffu, maskB[e]);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
       if (mA & (1u << c)) {

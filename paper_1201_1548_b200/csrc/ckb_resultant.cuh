@@ -117,10 +117,15 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
   const uint32_t lb = red4(B[0], p);
   const uint32_t lbm = to_mont(lb, P);
   const uint32_t lbc = comp_from_mont(lbm, P);
+  // Control flow depends only on (da, db), which are the same for every lane
+  // of the launch: a lane whose sequence turns out non-generic keeps running
+  // the (now meaningless) generic schedule with `bad` set, so every loop
+  // bound and chunk guard stays warp-uniform (no divergence scaffolding).
+  bool bad = false;
   const int e0 = da - db + 1;
   for (int s = 0; s < e0; ++s) step1<MAXD>(A, B, da - s, lb, lbc, P);
   uint32_t a0 = red4(A[0], p);
-  if (!a0) return CKB_FAIL;
+  bad |= (a0 == 0u);
   neg ^= (bool)(da & db & 1);
   const uint32_t l1e = mpow(lbm, e0, one, P);
   uint32_t num = l1e, den = mpow(l1e, db, one, P);
@@ -136,7 +141,7 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
       Q = mmul(Q, T, P);
       --k;
       const uint32_t b0 = red4(B[0], p);
-      if (!b0) return CKB_FAIL;
+      bad |= (b0 == 0u);
       if (k == 0) {
         num = mmul(num, to_mont(b0, P), P);
         break;
@@ -147,7 +152,7 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
       Q = mmul(Q, T, P);
       --k;
       a0 = red4(A[0], p);
-      if (!a0) return CKB_FAIL;
+      bad |= (a0 == 0u);
       if (k == 0) {
         num = mmul(num, to_mont(a0, P), P);
         break;
@@ -156,6 +161,7 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
     num = mmul(num, mmul(T, T, P), P);
     den = mmul(den, mmul(Q, Q, P), P);
   }
+  if (bad) return CKB_FAIL;
   // num / den (Fermat inverse in the Montgomery domain), leave the domain
   uint32_t inv = one, b = den;
   uint32_t ex = p - 2;
