@@ -378,7 +378,9 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
 // limbs -> residues -> choose c -> images -> interpolated coefficients [K][N]
 int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
                   int n, int dfx, int dgx, const Prime* d_primes, const uint32_t* h_primes, const uint32_t* h_gens,
-                  int K, int N, uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st) {
+                  int K, int N, uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st,
+                  const CrtTables* crt = nullptr) {
+  // with crt: the output rows are the explicit CRT's y = coeff (M/p_i)^-1 mod p_i
   if (images_maxd(m, n) < 0) return fail("y-degree above 64 is not supported by the image kernel", -2);
   for (int i = 0; i < K; ++i)
     if (h_primes[i] >= (1u << 30)) return fail("pipeline primes must be below 2^30", -2);
@@ -419,7 +421,7 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   CK(cudaMemsetAsync(a.fail_count, 0, 4, st));
   launch_images(a, st);
   stage_mark(st);
-  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st);
+  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr);
   stage_mark(st);
   g.launches += 5;
   CK(cudaGetLastError());
@@ -515,11 +517,11 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   CK(cudaMemsetAsync(d_status, 0, 4, st));
   g.nsev = 0;
   if ((rc = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
-                          d_status, st)))
+                          d_status, st, &ce->t)))
     return rc;
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
-  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
+  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
   stage_mark(st);
   g.launches += 2;
   CK(cudaGetLastError());
@@ -762,11 +764,11 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
   if ((rc = dbuf("coeffs", (size_t)K * N, &d_coeffs))) return rc;
   g.nsev = 0;
   if ((rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
-                          d_status, st)))
+                          d_status, st, &ce->t)))
     return rc;
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
-  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
+  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
   stage_mark(st);
   g.launches += 2;
   CK(cudaGetLastError());

@@ -25,33 +25,14 @@ constexpr int TI = 32;   // primes per k-step
 constexpr int CRT_THREADS = 256;
 
 // ---------------------------------------------------------------------------
-// prep: y[i][k] and q[k]; 32 coefficients x 8 prime slices per CTA
+// y[i][k] = r[i][k] (M/p_i)^-1 mod p_i (standalone API path; the pipeline's
+// interpolation kernel writes y directly)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_crt_prep(CrtTables T, const uint32_t* __restrict__ r, int N,
-                                                  uint32_t* __restrict__ y, int64_t* __restrict__ qk,
-                                                  uint32_t* __restrict__ amb) {
-  __shared__ double part[8][33];
-  const int kk = threadIdx.x & 31, sl = threadIdx.x >> 5;
-  const int k = blockIdx.x * 32 + kk;
-  const int K = T.K;
-  double s = 0.0;
-  if (k < N) {
-    for (int i = sl; i < K; i += 8) {
-      const uint32_t p = T.p[i];
-      const uint32_t v = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
-      y[(size_t)i * N + k] = v;
-      s = fma((double)v, T.pinvd[i], s);
-    }
-  }
-  part[sl][kk] = s;
-  __syncthreads();
-  if (sl == 0 && k < N) {
-    double t = 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) t += part[j][kk];
-    qk[k] = llrint(t);
-    amb[k] = fabs((t - floor(t)) - 0.5) < 1e-3;  // near a half-integer: exact fold needed
-  }
+__global__ void k_crt_ymul(CrtTables T, const uint32_t* __restrict__ r, int N, uint32_t* __restrict__ y) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  if (k >= N) return;
+  const uint32_t p = T.p[i];
+  y[(size_t)i * N + k] = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
 }
 
 // ---------------------------------------------------------------------------
@@ -60,7 +41,8 @@ __global__ void __launch_bounds__(256) k_crt_prep(CrtTables T, const uint32_t* _
 // products of 30-bit y and 32-bit limbs accumulate 4 at a time in 64 bits.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uint32_t* __restrict__ y, int N,
-                                                          uint32_t* __restrict__ S) {
+                                                          uint32_t* __restrict__ S, int64_t* __restrict__ qk,
+                                                          uint32_t* __restrict__ amb) {
   __shared__ uint32_t sy[2][TI][TN];
   __shared__ uint32_t sm[2][TI][TL];
   const int K = T.K, LW = T.LW;
@@ -85,8 +67,12 @@ __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uin
   stage(0, 0);
   __syncthreads();
   int buf = 0;
+  const bool qrow = blockIdx.y == 0 && tid < TN;  // these threads also form q = round(sum y_i / p_i)
+  double qs = 0.0;
   for (int i0 = 0; i0 < K; i0 += TI) {
     if (i0 + TI < K) stage(buf ^ 1, i0 + TI);  // prefetch the next tile while computing this one
+    if (qrow)
+      for (int ii = 0; ii < TI && i0 + ii < K; ++ii) qs = fma((double)sy[buf][ii][tid], T.pinvd[i0 + ii], qs);
 #pragma unroll
     for (int i4 = 0; i4 < TI; i4 += 2) {
       uint64_t acc[2][4] = {};  // 2 products of y < 2^31 and a 32-bit limb stay below 2^64
@@ -112,6 +98,10 @@ __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uin
     }
     __syncthreads();
     buf ^= 1;
+  }
+  if (qrow && k0 + tid < N) {
+    qk[k0 + tid] = llrint(qs);
+    amb[k0 + tid] = fabs((qs - floor(qs)) - 0.5) < 1e-3;  // near a half-integer: exact fold needed
   }
 #pragma unroll
   for (int a = 0; a < 2; ++a) {
@@ -259,15 +249,19 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uin
 }
 
 void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
-                cudaStream_t st) {
+                cudaStream_t st, bool input_is_y) {
   // scratch (cudaMalloc-aligned): q [N] (int64) | amb [N] | S [N][LW][3] | y [K][N]
   int64_t* qk = reinterpret_cast<int64_t*>(scratch);
   uint32_t* amb = reinterpret_cast<uint32_t*>(qk + N);
   uint32_t* S = amb + N;
-  uint32_t* y = S + (size_t)3 * N * t.LW;
-  k_crt_prep<<<(N + 31) / 32, 256, 0, st>>>(t, coeffs, N, y, qk, amb);
+  const uint32_t* y = coeffs;
+  if (!input_is_y) {
+    uint32_t* yb = S + (size_t)3 * N * t.LW;
+    k_crt_ymul<<<dim3((N + 255) / 256, t.K), 256, 0, st>>>(t, coeffs, N, yb);
+    y = yb;
+  }
   dim3 g1((N + TN - 1) / TN, (t.LW + TL - 1) / TL);
-  k_crt_gemm<<<g1, CRT_THREADS, 0, st>>>(t, y, N, S);
+  k_crt_gemm<<<g1, CRT_THREADS, 0, st>>>(t, y, N, S, qk, amb);
   k_crt_carry<<<(N + 3) / 4, 128, 0, st>>>(t, N, S, qk, amb, out);
 }
 

@@ -164,7 +164,9 @@ constexpr int POLY_THREADS = 256;
 __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, const Prime* __restrict__ primes,
                                                               const uint32_t* __restrict__ values,
                                                               const uint32_t* __restrict__ cval,
-                                                              uint32_t* __restrict__ coeffs) {
+                                                              uint32_t* __restrict__ coeffs,
+                                                              const uint32_t* __restrict__ crt_c,
+                                                              const uint32_t* __restrict__ crt_cc) {
   extern __shared__ uint32_t buf[];  // [L] data, then 4 x [L/2] twiddle tables
   const int S = plan.S;
   const int pi = blockIdx.x / S, r = blockIdx.x % S, tid = threadIdx.x, T = blockDim.x;
@@ -231,18 +233,26 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
   const uint32_t linv = plan.Linv[pi];
   const uint32_t linvc = shoup_comp(linv, P);
   const uint32_t cS = (c == 1u) ? 1u : pow_mod(inv_mod(c, P), (uint64_t)S, P);
+  // optional CRT pre-multiplication y = coeff (M/p)^-1 mod p (ckb_crt.cu), so
+  // the CRT needs no separate pass over the residues
+  uint32_t fin = linv, finc = linvc;
+  if (crt_c) {
+    fin = shoup(crt_c[pi], linv, linvc, p);
+    finc = shoup_comp(fin, P);
+  }
   uint32_t* out = coeffs + (size_t)pi * Nfull;
   for (int k = tid; k < M; k += T) {
     const int idx = S * k + r;
     if (idx >= Nfull) continue;
-    uint32_t res = shoup(buf[M - 1 + k], linv, linvc, p);
+    uint32_t res = shoup(buf[M - 1 + k], fin, finc, p);
     if (c != 1u) res = mul_mod(res, pow_mod(cS, (uint64_t)k, P), P);
     out[idx] = res;
   }
+  (void)crt_cc;
 }
 
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
-                   uint32_t* coeffs, cudaStream_t st) {
+                   uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c, const uint32_t* crt_cc) {
   const size_t smem = (size_t)plan.L * 4 * 3;  // data + 4 twiddle tables of L/2
   if (plan.S == 1) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -250,7 +260,7 @@ void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* 
   } else {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_interp_poly, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_interp_poly<<<plan.K * plan.S, POLY_THREADS, smem, st>>>(plan, primes, values, cval, coeffs);
+    k_interp_poly<<<plan.K * plan.S, POLY_THREADS, smem, st>>>(plan, primes, values, cval, coeffs, crt_c, crt_cc);
   }
 }
 

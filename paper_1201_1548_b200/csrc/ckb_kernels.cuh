@@ -80,9 +80,12 @@ void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t*
                           const Prime* primes, const int32_t* pidx, int B, uint32_t* out, cudaStream_t st);
 
 // ---- K4: interpolation at the planned points (modpoly.py:164-185) -----------
-// values [K][N] at x_t = c q^t -> coeffs [K][N] (canonical residues)
+// values at the planned points -> coeffs [K][Nfull] (canonical residues); with
+// crt_c (polyphase plans only) each prime's row is pre-multiplied by crt_c[i]
+// for the explicit CRT (then launch_crt must be told the input is already y)
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
-                   uint32_t* coeffs, cudaStream_t st);
+                   uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c = nullptr,
+                   const uint32_t* crt_cc = nullptr);
 
 // ---- K5: explicit CRT + symmetric lift to two's-complement limbs -----------
 struct CrtTables {
@@ -97,7 +100,7 @@ struct CrtTables {
 };
 // coeffs [K][N] -> out [N][LW]; scratch >= 3 N LW words
 void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
-                cudaStream_t st);
+                cudaStream_t st, bool input_is_y = false);
 size_t crt_scratch_words(int K, int N, int LW);  // scratch size for launch_crt
 
 // ---- K6: batched gcd mod p (modpoly.py:115-122), interpolation at arbitrary points
