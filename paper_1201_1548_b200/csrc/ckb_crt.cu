@@ -52,19 +52,29 @@ __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uin
   const int tl = (tid / 32) * 4;        // limb offset (0..28)
   uint64_t lo[2][4] = {};
   uint32_t hi[2][4] = {};
+  // asynchronous global -> shared copies (LDGSTS; src-size 0 zero-fills out
+  // of range), so the next tile streams in while this one is multiplied
+  auto cp4 = [](uint32_t* dst, const uint32_t* src, bool ok) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 4 : 0));
+  };
   auto stage = [&](int buf, int i0) {
     for (int e = tid; e < TI * TN; e += CRT_THREADS) {
       const int ii = e / TN, kk = e % TN;
       const int i = i0 + ii, k = k0 + kk;
-      sy[buf][ii][kk] = (i < K && k < N) ? y[(size_t)i * N + k] : 0u;
+      const bool ok = i < K && k < N;
+      cp4(&sy[buf][ii][kk], ok ? y + (size_t)i * N + k : y, ok);
     }
     for (int e = tid; e < TI * TL; e += CRT_THREADS) {
       const int ii = e / TL, ll = e % TL;
       const int i = i0 + ii, l = l0 + ll;
-      sm[buf][ii][ll] = (i < K && l < LW) ? T.Mi[(size_t)i * LW + l] : 0u;
+      const bool ok = i < K && l < LW;
+      cp4(&sm[buf][ii][ll], ok ? T.Mi + (size_t)i * LW + l : T.Mi, ok);
     }
+    asm volatile("cp.async.commit_group;\n" ::);
   };
   stage(0, 0);
+  asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
   int buf = 0;
   const bool qrow = blockIdx.y == 0 && tid < TN;  // these threads also form q = round(sum y_i / p_i)
@@ -96,6 +106,7 @@ __global__ void __launch_bounds__(CRT_THREADS) k_crt_gemm(CrtTables T, const uin
           lo[a][b] = s;
         }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
     buf ^= 1;
   }

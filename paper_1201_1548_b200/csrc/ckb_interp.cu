@@ -159,8 +159,9 @@ __global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const P
 // P(x) = sum_{r<S} x^r P_r(x^S):  P_r(z_u) = (1/S) y_u^-r sum_j w^-jr v[u S + j],
 // z_u = y_u^S = c^S q^u (q = g^S) -- S independent geometric interpolations of
 // size M, one CTA per (prime, r), interleaved into P_{S k + r}.
-constexpr int POLY_THREADS = 256;
+// threads per CTA = the radix-8 passes' L/8 groups, clamped to [32, 256]
 
+template <int POLY_THREADS>
 __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, const Prime* __restrict__ primes,
                                                               const uint32_t* __restrict__ values,
                                                               const uint32_t* __restrict__ cval,
@@ -258,9 +259,16 @@ void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* 
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_interp<<<plan.K, NTT_THREADS, smem, st>>>(plan, primes, values, cval, coeffs);
   } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_interp_poly, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_interp_poly<<<plan.K * plan.S, POLY_THREADS, smem, st>>>(plan, primes, values, cval, coeffs, crt_c, crt_cc);
+    const int want = plan.L / 8;
+#define POLY_LAUNCH(TT)                                                                                       \
+  if ((TT == 32 && want <= 32) || (TT == 64 && want == 64) || (TT == 128 && want == 128) ||                 \
+      (TT == 256 && want >= 256)) {                                                                           \
+    if (smem > 48 * 1024)                                                                                     \
+      cudaFuncSetAttribute(k_interp_poly<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    k_interp_poly<TT><<<plan.K * plan.S, TT, smem, st>>>(plan, primes, values, cval, coeffs, crt_c, crt_cc); \
+  }
+    POLY_LAUNCH(32) POLY_LAUNCH(64) POLY_LAUNCH(128) POLY_LAUNCH(256)
+#undef POLY_LAUNCH
   }
 }
 
