@@ -85,6 +85,15 @@ int ckb_gcd_mod_batch(const uint32_t* fa, const int32_t* da, int Wf, const uint3
 int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const uint32_t* primes, int P,
                       const int32_t* pidx, int B, uint32_t* out);
 
+/* Principal subresultant coefficients psc_i(t) mod p, i = 1..n, at the points
+ * t = 0..ncand-1 — the per-point determinants of modular_subres_profile
+ * (_psc_det / _zp_det, modpoly.py:428-526).  fres [(m+1)][(dfx+1)], gres
+ * [(n+1)][(dgx+1)]: residues of the y-coefficients (m >= n, as the reference
+ * swaps), fdeg/gdeg their x-degrees.  out [n][ncand]; valid [ncand] = 1 where
+ * neither leading coefficient vanishes at t (the reference skips the others). */
+int ckb_psc_values(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
+                   const int16_t* gdeg, int n, int dgx, uint32_t p, int ncand, uint32_t* out, uint8_t* valid);
+
 /* Device-pointer stages for the multi-GPU driver (one process per GPU); primes
  * and gens are HOST arrays (they key the cached interpolation plan).
  * stream: a cudaStream_t or NULL for the context stream.

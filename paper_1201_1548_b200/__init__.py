@@ -11,7 +11,8 @@ def install():
     """Rebind the reference's hot-path names to the B200 implementations.
 
     Rebinds ``curvekit.modpoly.{biv_resultant, int_gcd_uni, zp_resultant_uni,
-    zp_interpolate, zp_gcd_sylvester, crt_reconstruct}`` and the names
+    zp_interpolate, zp_gcd_sylvester, crt_reconstruct, modular_subres_profile}``
+    and the names
     ``curvekit.bisolve`` bound at import (bisolve.py:26).  ``upoly`` and
     ``bivpoly`` import ``int_gcd_uni`` lazily (upoly.py:258,372,538,569;
     bivpoly.py:186,268), so they pick up the GPU gcd through the first rebinding.
@@ -23,7 +24,7 @@ def install():
     ref = importlib.import_module("curvekit.modpoly")
     saved = {}
     for name in ("biv_resultant", "int_gcd_uni", "zp_resultant_uni", "zp_interpolate",
-                 "zp_gcd_sylvester", "crt_reconstruct"):
+                 "zp_gcd_sylvester", "crt_reconstruct", "modular_subres_profile"):
         saved[("curvekit.modpoly", name)] = getattr(ref, name)
         setattr(ref, name, getattr(ours, name))
     try:

@@ -21,7 +21,7 @@ EXPORTS = (
     "ckb_biv_resultant", "ckb_reduce", "ckb_uni_resultant_batch", "ckb_interp_plan_points",
     "ckb_interp_geometric", "ckb_crt_lift", "ckb_dev_modular_images", "ckb_dev_crt",
     "ckb_interp_points", "ckb_gcd_mod_batch", "ckb_dev_biv_resultant", "ckb_set_timing",
-    "ckb_stage_times", "ckb_measure_peak",
+    "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values",
 )
 
 _P = ctypes.c_void_p
@@ -49,6 +49,7 @@ _SIGS = {
     "ckb_set_timing": (_I, [_I]),
     "ckb_stage_times": (_I, [_P, _I]),
     "ckb_measure_peak": (_I, [_P]),
+    "ckb_psc_values": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, ctypes.c_uint32, _I, _P, _P]),
 }
 
 _lock = threading.Lock()

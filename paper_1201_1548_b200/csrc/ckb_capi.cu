@@ -716,6 +716,39 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
   return 0;
 }
 
+int ckb_psc_values(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
+                   const int16_t* gdeg, int n, int dgx, uint32_t p, int ncand, uint32_t* out, uint8_t* valid) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(&p, 1))) return rc;
+  if (m < 0 || n < 0 || ncand < 1) return fail("ckb_psc_values: bad sizes", -2);
+  if ((size_t)(m + n + 2 + (m + n) * (m + n)) * 4 > 200 * 1024) return fail("ckb_psc_values: degree too large", -2);
+  cudaStream_t st = g.stream;
+  const size_t nf = (size_t)(m + 1) * (dfx + 1), ng = (size_t)(n + 1) * (dgx + 1);
+  uint32_t *d_f, *d_g, *d_out;
+  int16_t *d_fd, *d_gd;
+  uint8_t* d_valid;
+  if ((rc = dbuf("s.f", nf, &d_f))) return rc;
+  if ((rc = dbuf("s.g", ng, &d_g))) return rc;
+  if ((rc = dbuf("s.fd", (size_t)m + 1, &d_fd))) return rc;
+  if ((rc = dbuf("s.gd", (size_t)n + 1, &d_gd))) return rc;
+  const int nrow = n > 0 ? n : 1;
+  if ((rc = dbuf("s.out", (size_t)nrow * ncand, &d_out))) return rc;
+  if ((rc = dbuf("s.valid", (size_t)ncand, &d_valid))) return rc;
+  CK(cudaMemcpyAsync(d_f, fres, 4 * nf, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_g, gres, 4 * ng, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_fd, fdeg, 2 * ((size_t)m + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_gd, gdeg, 2 * ((size_t)n + 1), cudaMemcpyHostToDevice, st));
+  launch_psc(d_f, d_fd, m, dfx, d_g, d_gd, n, dgx, h_prime(p), ncand, d_out, d_valid, st);
+  g.launches += 1;
+  CK(cudaGetLastError());
+  if (n > 0) CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)n * ncand, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(valid, d_valid, (size_t)ncand, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
 // ---- device-pointer entry points for the multi-GPU driver -------------------
 int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
                            int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* gens, int K, int N,

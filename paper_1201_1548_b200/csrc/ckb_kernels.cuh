@@ -110,4 +110,10 @@ void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_
 void launch_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const Prime* primes,
                           const int32_t* pidx, int B, uint32_t* out, cudaStream_t st);
 
+// ---- principal subresultant coefficients at points t = 0..ncand-1 (modpoly.py:428-526)
+// out [n][ncand] psc_i(t) for i = 1..n; valid[t] = no leading coefficient vanishes at t
+void launch_psc(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
+                const int16_t* gdeg, int n, int dgx, const Prime& P, int ncand, uint32_t* out, uint8_t* valid,
+                cudaStream_t st);
+
 }  // namespace ckb

@@ -266,3 +266,40 @@ def test_squarefree_golden(small):
         dec = squarefree_decompose(ints_in(c["p"]))
         assert dec.content == int(c["content"])
         assert [(list(f), m) for f, m in dec.factors] == [(ints_in(f), m) for f, m in c["factors"]]
+
+
+# ---------------------------------------------------------------------------
+# modular subresultant degree profiles (modpoly.py:428-474)
+# ---------------------------------------------------------------------------
+
+def test_subres_profile_golden(mp, small):
+    # test_modpoly.py:218-261 cases plus random f, f_y pairs, reference outputs
+    for c in small["subres_profile"]:
+        pr = mp.modular_subres_profile(terms_in(c["f"]), terms_in(c["g"]), ints_in(c["rstar"]), c["p"])
+        assert pr.prime == c["p"]
+        assert list(pr.chain_degrees) == c["chain"], c
+        assert list(pr.factor_degrees) == c["d"], c
+
+
+def test_subres_profile_unlucky(mp):
+    circle = {(2, 0): 1, (0, 2): 1, (0, 0): -1}
+    # leading y-coefficient 3 vanishes mod 3 (modpoly.py:437-439)
+    with pytest.raises(mp.UnluckyPrime):
+        mp.modular_subres_profile({(0, 2): 3, (0, 0): -1, (1, 0): 1}, {(0, 1): 6}, [1, 1], 3)
+    # rstar drops degree mod p (modpoly.py:462-463)
+    with pytest.raises(mp.UnluckyPrime):
+        mp.modular_subres_profile(circle, {(0, 1): 2}, [-1, 0, 7], 7)
+
+
+def test_cfg3_subres_profile_golden(mp):
+    """The reference's 82 s profile of cfg3 (R square-free: chain 552, 0, ...)."""
+    from paper_1201_1548_b200.synth import make_pair
+    gold = load_golden("cfg3_seed0.json.gz")
+    f, g = make_pair("cfg3", 0)
+    res = [int(c, 16) for c in gold["res"]]
+    content = int(gold["sqf_content"])
+    assert all(c % content == 0 for c in res)
+    rstar = [c // content for c in res]
+    pr = mp.modular_subres_profile(f, g, rstar, gold["profile"]["p"])
+    assert list(pr.chain_degrees) == gold["profile"]["chain"]
+    assert list(pr.factor_degrees) == gold["profile"]["d"]
