@@ -1,3 +1,4 @@
+#include <algorithm>
 // C-ABI boundary of the B200 modular symbolic engine (declared in
 // include/curvekit_b200.h).  Plain pointers and sizes only; every host buffer
 // is caller-owned and never retained; device memory is owned by a
@@ -46,6 +47,7 @@ struct CrtEntry {
   int LW = 0;
   Prime* d_primes = nullptr;
   void* d_blob = nullptr;  // p, c, cc, pinvd, Mi, Ml, Mh
+  void* d_bt = nullptr;    // tensor-core byte table
   CrtTables t;
   uint64_t last_use = 0;
 };
@@ -167,6 +169,7 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
     CrtEntry& e = g.crt[v];
     cudaFree(e.d_primes);
     cudaFree(e.d_blob);
+    cudaFree(e.d_bt);
     g.crt.erase(g.crt.begin() + v);
   }
   CrtEntry e;
@@ -240,6 +243,11 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
   e.t.Mi = d_Mi;
   e.t.Ml = d_Ml;
   e.t.Mh = d_Mh;
+  CK(cudaMalloc(&e.d_bt, crt_btable_bytes(K, LW)));
+  launch_crt_btable(K, LW, d_Mi, (uint32_t*)e.d_bt, g.stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(g.stream));
+  e.t.Bt = (const uint8_t*)e.d_bt;
   e.last_use = ++g.tick;
   g.crt.push_back(e);
   *out = &g.crt.back();
@@ -465,6 +473,7 @@ int ckb_shutdown(void) {
   for (auto& e : g.crt) {
     cudaFree(e.d_primes);
     cudaFree(e.d_blob);
+    cudaFree(e.d_bt);
   }
   for (auto& e : g_pcache) cudaFree(e.d);
   g_pcache.clear();
@@ -506,7 +515,7 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   int16_t* d_degs;
   if ((rc = dbuf("limbs", nl, &d_limbs))) return rc;
   if ((rc = dbuf("degs", nd, &d_degs))) return rc;
-  if ((rc = dbuf("coeffs", (size_t)K * N, &d_coeffs))) return rc;
+  if ((rc = dbuf("coeffs", std::max((size_t)K * N, crt_a_words(K, N)), &d_coeffs))) return rc;
   if ((rc = dbuf("out", (size_t)N * LW, &d_out))) return rc;
   if ((rc = dbuf("status", 4, &d_status))) return rc;
   CrtEntry* ce;
@@ -794,7 +803,7 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
   CrtEntry* ce;
   if ((rc = get_crt(primes, K, LW, &ce))) return rc;
   uint32_t* d_coeffs;
-  if ((rc = dbuf("coeffs", (size_t)K * N, &d_coeffs))) return rc;
+  if ((rc = dbuf("coeffs", std::max((size_t)K * N, crt_a_words(K, N)), &d_coeffs))) return rc;
   g.nsev = 0;
   if ((rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
                           d_status, st, &ce->t)))

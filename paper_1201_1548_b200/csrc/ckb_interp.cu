@@ -242,12 +242,16 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
     finc = shoup_comp(fin, P);
   }
   uint32_t* out = coeffs + (size_t)pi * Nfull;
+  const int KC = (plan.K + 31) / 32;
   for (int k = tid; k < M; k += T) {
     const int idx = S * k + r;
     if (idx >= Nfull) continue;
     uint32_t res = shoup(buf[M - 1 + k], fin, finc, p);
     if (c != 1u) res = mul_mod(res, pow_mod(cS, (uint64_t)k, P), P);
-    out[idx] = res;
+    if (crt_c)
+      coeffs[crt_a_word(pi, idx, KC)] = res;  // straight into the CRT GEMM's A layout
+    else
+      out[idx] = res;
   }
   (void)crt_cc;
 }

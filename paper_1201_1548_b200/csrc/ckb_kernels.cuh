@@ -97,8 +97,24 @@ struct CrtTables {
   const uint32_t* Mi;     // [K][LW] limbs of M/p_i
   const uint32_t* Ml;     // [LW] limbs of M
   const uint32_t* Mh;     // [LW] limbs of floor(M/2)
+  const uint8_t* Bt;      // pre-tiled byte table of the M/p_i for the tensor-core product (ckb_crt_mma.cu)
 };
-// coeffs [K][N] -> out [N][LW]; scratch >= 3 N LW words
+// The CRT input y (residues premultiplied by (M/p_i)^-1) is stored directly in
+// the tensor-core A-operand layout: tiles of 128 coefficients x 32 primes
+// (16 KB), each in the canonical no-swizzle K-major arrangement of 8x16-byte
+// core matrices, so the GEMM streams it with bulk copies.  Word index of y_i(n):
+__host__ __device__ __forceinline__ size_t crt_a_word(int i, int n, int KC) {
+  const size_t tile = (size_t)(n >> 7) * KC + (i >> 5);
+  return tile * 4096 + ((n & 127) >> 3) * 256 + ((i & 31) >> 2) * 32 + (n & 7) * 4 + (i & 3);
+}
+inline size_t crt_a_words(int K, int N) { return (size_t)((N + 127) / 128) * ((K + 31) / 32) * 4096; }
+// tensor-core CRT product (ckb_crt_mma.cu): byte table size / builder, and the
+// GEMM y (A layout) -> S [N][32 ceil(LW/32)] u64 limb sums
+size_t crt_btable_bytes(int K, int LW);
+void launch_crt_btable(int K, int LW, const uint32_t* Mi, uint32_t* Bt, cudaStream_t st);
+void launch_crt_mma(const CrtTables& t, const uint32_t* y, int N, unsigned long long* S, cudaStream_t st);
+// coeffs [K][N] residues (or, input_is_y, y in the A layout) -> out [N][LW];
+// scratch >= crt_scratch_words
 void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
                 cudaStream_t st, bool input_is_y = false);
 size_t crt_scratch_words(int K, int N, int LW);  // scratch size for launch_crt

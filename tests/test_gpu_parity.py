@@ -183,14 +183,16 @@ def test_crt_golden(mp, small):
         assert mp.crt_reconstruct(mp.ResidueSystem(tuple(c["primes"]), tuple(c["res"]))) == int(c["x"])
 
 
-def test_crt_lift_roundtrip_large(mp):
+@pytest.mark.parametrize("K,extra", [(1, 0), (33, 1), (200, 0), (700, 130)])
+def test_crt_lift_roundtrip_large(mp, K, extra):
+    """Tensor-core CRT: K primes (chunks of 32, ring of 4 stages), several 128-row tiles."""
     from paper_1201_1548_b200.primes30 import PRIMES30
-    rng = random.Random(12)
-    primes = [p for p, _ in PRIMES30[:200]]
+    rng = random.Random(12 + K)
+    primes = [p for p, _ in PRIMES30[:K]]
     M = 1
     for p in primes:
         M *= p
-    vals = [rng.randint(-(M // 2) + 1, M // 2) for _ in range(300)] + [0, 1, -1, M // 2, -(M // 2) + 1]
+    vals = [rng.randint(-(M // 2) + 1, M // 2) for _ in range(300 + extra)] + [0, 1, -1, M // 2, -(M // 2) + 1]
     res = np.array([[v % p for v in vals] for p in primes], dtype=np.uint32)
     assert mp.crt_lift(res, primes) == vals
 
