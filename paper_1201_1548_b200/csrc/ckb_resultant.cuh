@@ -20,9 +20,11 @@
 // elimination steps of a generic remainder are fused into one sweep:
 //     D''[i] = L^2 D[i+2] - L lc(D) V[i+2] - lc(D') V[i+1]      (3 products)
 // Arithmetic is lazy: for p < 2^30 every register holds a value in [0, 4p)
-// and a Shoup product accepts any 32-bit input, so no reduction is needed
-// per output.  A non-generic image (a leading coefficient vanishing mid-way)
-// returns CKB_FAIL and is recomputed by the general warp kernel.
+// (entries beyond a degree are only congruent to 0), a Shoup product accepts
+// any 32-bit input, and the fused remainder sums its three products in 64 bits
+// before one Montgomery reduction, so no reduction is needed per output.
+// A non-generic image (a leading coefficient vanishing mid-way) returns
+// CKB_FAIL and is recomputed by the general warp kernel.
 #pragma once
 #include "ckb_modarith.cuh"
 
@@ -80,12 +82,12 @@ __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_
   // lc of the intermediate remainder: la' = lb D[1] - la V[1]
   const uint32_t d1 = red4(D[1], p), v1 = red4(V[1], p);
   const uint32_t lap = redc((uint64_t)lbm * d1 + (uint64_t)nlam * v1, P);
-  const uint32_t w1 = redc((uint64_t)lbm * lb, P);                     // lb^2
-  const uint32_t w1c = comp_from_mont(redc((uint64_t)lbm * lbm, P), P);
-  const uint32_t w2 = redc((uint64_t)lbm * nla, P);                    // -lb la
-  const uint32_t w2c = comp_from_mont(redc((uint64_t)lbm * nlam, P), P);
-  const uint32_t w3 = lap ? p - lap : 0u;                               // -la'
-  const uint32_t w3c = comp_from_mont(to_mont(w3, P), P);
+  // Montgomery forms of the three multipliers: the three products of one
+  // coefficient are summed in 64 bits (3 IMAD.WIDE) and reduced once
+  const uint32_t w1m = redc((uint64_t)lbm * lbm, P);                   // lb^2 R
+  const uint32_t w2m = redc((uint64_t)lbm * nlam, P);                  // -lb la R
+  const uint32_t w3m = to_mont(lap ? p - lap : 0u, P);                  // -la' R
+  const uint32_t pinv = P.pinv;
 #pragma unroll
   for (int c = 0; c < (MAXD + 3) / 4; ++c) {
     if (4 * c <= k + 1) {
@@ -93,9 +95,9 @@ __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_
       for (int j = 0; j < 4; ++j) {
         const int i = 4 * c + j;
         if (i < MAXD - 1) {
-          const uint32_t t1 = red1(shoup_lazy(D[i + 2], w1, w1c, p), p);
-          const uint32_t t2 = red1(shoup_lazy(V[i + 2], w2, w2c, p), p);
-          D[i] = t1 + t2 + shoup_lazy(V[i + 1], w3, w3c, p);
+          // inputs < 4p < 2^32, multipliers < p: t < 12 p^2 < 2^64, result in (0, 4p)
+          const uint64_t t = (uint64_t)D[i + 2] * w1m + (uint64_t)V[i + 2] * w2m + (uint64_t)V[i + 1] * w3m;
+          D[i] = (uint32_t)(t >> 32) - __umulhi((uint32_t)t * pinv, p) + p;
         }
       }
     }
