@@ -88,6 +88,9 @@ __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_
   const uint32_t w2m = redc((uint64_t)lbm * nlam, P);                  // -lb la R
   const uint32_t w3m = to_mont(lap ? p - lap : 0u, P);                  // -la' R
   const uint32_t pinv = P.pinv;
+  // outputs i < k are the new coefficients; i = k, k+1 held the old tail and
+  // must become 0 (later sweeps read one entry past a degree), so chunks up to
+  // index k+1 are written, but only entries below k are computed
 #pragma unroll
   for (int c = 0; c < (MAXD + 3) / 4; ++c) {
     if (4 * c <= k + 1) {
@@ -95,9 +98,13 @@ __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_
       for (int j = 0; j < 4; ++j) {
         const int i = 4 * c + j;
         if (i < MAXD - 1) {
-          // inputs < 4p < 2^32, multipliers < p: t < 12 p^2 < 2^64, result in (0, 4p)
-          const uint64_t t = (uint64_t)D[i + 2] * w1m + (uint64_t)V[i + 2] * w2m + (uint64_t)V[i + 1] * w3m;
-          D[i] = (uint32_t)(t >> 32) - __umulhi((uint32_t)t * pinv, p) + p;
+          if (i < k) {
+            // inputs < 4p < 2^32, multipliers < p: t < 12 p^2 < 2^64, result in (0, 4p)
+            const uint64_t t = (uint64_t)D[i + 2] * w1m + (uint64_t)V[i + 2] * w2m + (uint64_t)V[i + 1] * w3m;
+            D[i] = (uint32_t)(t >> 32) - __umulhi((uint32_t)t * pinv, p) + p;
+          } else {
+            D[i] = 0u;
+          }
         }
       }
     }
