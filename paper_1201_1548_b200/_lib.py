@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcurvekit_b200.so")
+LIB_PATH = os.environ.get("CKB_LIB") or os.path.join(HERE, "libcurvekit_b200.so")  # CKB_LIB: tuning variants
 
 # every symbol include/curvekit_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (

@@ -30,30 +30,33 @@ def _newest(paths):
     return max(os.path.getmtime(p) for p in paths)
 
 
-def _compile(src: str, force: bool) -> str:
+def _compile(src: str, force: bool, obj: str = OBJ, extra=()) -> str:
     s = os.path.join(CSRC, src)
-    o = os.path.join(OBJ, src.replace(".cu", ".o"))
+    o = os.path.join(obj, src.replace(".cu", ".o"))
     if not force and os.path.exists(o) and os.path.getmtime(o) >= _newest([s] + HEADERS):
         return o
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", s, "-o", o]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     return o
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=()) -> str:
+    """Build the library; `defines` (tuning experiments only) go to a separate object dir."""
+    extra = [f"-D{d}" for d in defines]
+    obj = OBJ if not extra else os.path.join(REPO, "build", "obj_" + "_".join(d.replace("=", "") for d in defines))
+    os.makedirs(obj, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
-    if force or not os.path.exists(OUT) or os.path.getmtime(OUT) < _newest(objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"]
+        objs = list(ex.map(lambda s: _compile(s, force, obj, extra), SOURCES))
+    if force or not os.path.exists(out) or os.path.getmtime(out) < _newest(objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
     if verbose:
-        print("built", OUT)
-    return OUT
+        print("built", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -14,6 +14,9 @@
 
 namespace ckb {
 
+#ifndef CKB_IMG_MINB
+#define CKB_IMG_MINB 1
+#endif
 constexpr int IMG_THREADS = 128;
 
 constexpr int POLY = 8;  // polyphase factor S: one 8-lane group per coset {w^j y_u}
@@ -28,7 +31,7 @@ struct ImgLayout {
 };
 
 template <int MAXD>
-__global__ void __launch_bounds__(IMG_THREADS) k_images(ImageArgs a) {
+__global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs a) {
   using LY = ImgLayout<MAXD>;
   constexpr int NCH = LY::NCH, SW = LY::SW;
   extern __shared__ __align__(16) uint32_t sm[];
