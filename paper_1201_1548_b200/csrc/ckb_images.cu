@@ -147,12 +147,15 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
     const uint32_t wc = upper ? som[POLY + widx] : (uint32_t)(0x100000000ull / p);  // companion of 1
 #pragma unroll
     for (int i = 0; i <= MAXD; ++i) {
-      // upper lane: (lower - own) w in [0, 2p) via min(d, d + 2p) -- an exact
-      // zero stays zero, which the elimination relies on beyond the degree
+      // upper lane: (lower - own) w in [0, 2p) via min(d, d + 2p); the last
+      // stage's twiddle is 1 and the elimination accepts [0, 4p), so it skips
+      // the product
       const uint32_t oa = __shfl_xor_sync(FULL, A[i], h), ob = __shfl_xor_sync(FULL, B[i], h);
       const uint32_t da_ = oa - A[i], db_ = ob - B[i];
-      A[i] = shoup_lazy(upper ? min(da_, da_ + p2) : A[i] + oa, w, wc, p);
-      B[i] = shoup_lazy(upper ? min(db_, db_ + p2) : B[i] + ob, w, wc, p);
+      const uint32_t xa = upper ? min(da_, da_ + p2) : A[i] + oa;
+      const uint32_t xb = upper ? min(db_, db_ + p2) : B[i] + ob;
+      A[i] = (h == 1) ? xa : shoup_lazy(xa, w, wc, p);
+      B[i] = (h == 1) ? xb : shoup_lazy(xb, w, wc, p);
     }
   }
   const int j = ((l & 1) << 2) | (l & 2) | ((l >> 2) & 1);  // bitrev3(l)

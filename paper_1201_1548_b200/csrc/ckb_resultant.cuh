@@ -70,7 +70,10 @@ __device__ __forceinline__ void step1(uint32_t (&D)[MAXD + 1], const uint32_t (&
   D[MAXD] = 0u;
 }
 
-// fused generic remainder: D (nominal deg k+1) <- prem(D, V) (deg k-1), V of deg k.
+// fused generic remainder: D (nominal deg k+1) <- R^-2 prem(D, V) (deg k-1), V
+// of deg k.  The three multipliers are formed with one REDC each, so they
+// carry a factor R^-1 and the single reduction of the update another; the
+// caller compensates the R^-2 with R^{2k} (res(V, c X) = c^{deg V} res(V, X)).
 // Returns the Montgomery form of lc(V).
 template <int MAXD>
 __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int k,
@@ -78,15 +81,13 @@ __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_
   const uint32_t p = P.p;
   const uint32_t lb = red4(V[0], p), la = red4(D[0], p);
   const uint32_t nla = la ? p - la : 0u;
-  const uint32_t lbm = to_mont(lb, P), nlam = to_mont(nla, P);
-  // lc of the intermediate remainder: la' = lb D[1] - la V[1]
+  const uint32_t lbm = to_mont(lb, P);
+  // R^-1 (lb^2, -lb la, -la') with la' = lb D[1] - la V[1] the lc of the intermediate remainder
   const uint32_t d1 = red4(D[1], p), v1 = red4(V[1], p);
-  const uint32_t lap = redc((uint64_t)lbm * d1 + (uint64_t)nlam * v1, P);
-  // Montgomery forms of the three multipliers: the three products of one
-  // coefficient are summed in 64 bits (3 IMAD.WIDE) and reduced once
-  const uint32_t w1m = redc((uint64_t)lbm * lbm, P);                   // lb^2 R
-  const uint32_t w2m = redc((uint64_t)lbm * nlam, P);                  // -lb la R
-  const uint32_t w3m = to_mont(lap ? p - lap : 0u, P);                  // -la' R
+  const uint32_t w1m = redc((uint64_t)lb * lb, P);
+  const uint32_t w2m = redc((uint64_t)lb * nla, P);
+  const uint32_t l3 = redc((uint64_t)lb * d1 + (uint64_t)nla * v1, P);
+  const uint32_t w3m = l3 ? p - l3 : 0u;
   const uint32_t pinv = P.pinv;
   // outputs i < k are the new coefficients; i = k, k+1 held the old tail and
   // must become 0 (later sweeps read one entry past a degree), so chunks up to
@@ -171,6 +172,9 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
     den = mmul(den, mmul(Q, Q, P), P);
   }
   if (bad) return CKB_FAIL;
+  // each fused remainder with divisor degree k was stored as R^-2 prem: undo
+  // with R^{2 sum k} = R^{db (db - 1)} (in Montgomery form: mpow of R^2 mod p)
+  const uint32_t corr = mpow(P.r2, db * (db - 1), one, P);
   // num / den (Fermat inverse in the Montgomery domain), leave the domain
   uint32_t inv = one, b = den;
   uint32_t ex = p - 2;
@@ -179,7 +183,7 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
     ex >>= 1;
     if (ex) b = mmul(b, b, P);
   }
-  const uint32_t r = redc((uint64_t)mmul(num, inv, P), P);
+  const uint32_t r = redc((uint64_t)mmul(mmul(num, inv, P), corr, P), P);
   return neg ? neg_mod(r, p) : r;
 }
 
