@@ -399,16 +399,19 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   if ((rc = get_plan(h_primes, h_gens, K, N, S, &pl))) return rc;
   const int NI = S * pl.N;  // images per prime (>= N)
   if ((rc = dbuf("red", (size_t)K * C, &d_red))) return rc;
+  uint32_t* d_tab;
+  if ((rc = dbuf("tab", (size_t)K * images_tab_words(m, n, dfx, dgx), &d_tab))) return rc;
   if ((rc = dbuf("vals", (size_t)K * NI, &d_vals))) return rc;
   if ((rc = dbuf("cval", (size_t)K, &d_cval))) return rc;
   stage_mark(st);
-  launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
+  launch_reduce_tab(d_limbs, C, L, d_primes, K, m, n, dfx, dgx, d_red, d_tab, st);
   stage_mark(st);
   const int lcf_off = m * (dfx + 1), lcg_off = (m + 1) * (dfx + 1) + n * (dgx + 1);
   launch_choose_c(d_primes, pl, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], d_cval, d_status, st);
   stage_mark(st);
   ImageArgs a;
   a.red = d_red;
+  a.tab = d_tab;
   a.degs = d_degs;
   a.yq = pl.yq;
   a.om = pl.om;

@@ -38,9 +38,6 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
   const int pi = blockIdx.y;
   const bool sw = a.m < a.n;  // reference swaps so that deg a >= deg b
   const int da = sw ? a.n : a.m, db = sw ? a.m : a.n;
-  const int offF = 0, offG = (a.m + 1) * (a.dfx + 1);
-  const int offA = sw ? offG : offF, offB = sw ? offF : offG;
-  const int Astr = sw ? a.dgx + 1 : a.dfx + 1, Bstr = sw ? a.dfx + 1 : a.dgx + 1;
   const int16_t* Adeg = a.degs + (sw ? a.m + 1 : 0);
   const int16_t* Bdeg = a.degs + (sw ? 0 : a.m + 1);
   const int dmax = max(a.dfx, a.dgx);
@@ -53,11 +50,11 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
   uint32_t* maskA = sm + 2 * rows * SW;
   uint32_t* maskB = maskA + rows;
   uint32_t* som = maskB + rows;               // w^k and companions
-  const uint32_t* gres = a.red + (size_t)pi * a.C;
-  for (int idx = threadIdx.x; idx < rows * SW; idx += IMG_THREADS) {
-    const int e = idx / SW, i = idx % SW;
-    TA[idx] = (i <= da && e < Astr) ? gres[offA + (da - i) * Astr + e] : 0u;
-    TB[idx] = (i <= db && e < Bstr) ? gres[offB + (db - i) * Bstr + e] : 0u;
+  {
+    // K1 wrote this prime's tables in exactly this layout: one coalesced copy
+    const uint4* src = reinterpret_cast<const uint4*>(a.tab + (size_t)pi * 2 * rows * SW);
+    uint4* dst = reinterpret_cast<uint4*>(TA);
+    for (int idx = threadIdx.x; idx < 2 * rows * SW / 4; idx += IMG_THREADS) dst[idx] = src[idx];
   }
   for (int e = threadIdx.x; e < rows; e += IMG_THREADS) {
     uint32_t ma = 0, mb = 0;
@@ -178,6 +175,54 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
 }
 
 #define CKB_MAXD_LIST(X) X(4) X(8) X(12) X(16) X(24) X(32) X(40) X(48) X(56) X(64)
+
+static int images_sw(int maxd) {
+#define SWOF(D) \
+  if (maxd == D) return ImgLayout<D>::SW;
+  CKB_MAXD_LIST(SWOF)
+#undef SWOF
+  return 0;
+}
+
+size_t images_tab_words(int m, int n, int dfx, int dgx) {
+  const int maxd = images_maxd(m, n);
+  const int dmax = dfx > dgx ? dfx : dgx;
+  const int rows = POLY * (dmax / POLY + 1);
+  return (size_t)2 * rows * images_sw(maxd);
+}
+
+// one thread per table entry: TA[e][i] / TB[e][i] = coefficient of x^e in the
+// y-coefficient of degree d - i of A / B (A the higher y-degree input), 0 in
+// the padding; each real coefficient also lands in red[pi][c]
+__global__ void k_reduce_tab(const uint32_t* __restrict__ limbs, int C, int L, const Prime* __restrict__ primes,
+                             int m, int n, int dfx, int dgx, int rows, int SW, uint32_t* __restrict__ red,
+                             uint32_t* __restrict__ tab) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x, pi = blockIdx.y;
+  const int TW = 2 * rows * SW;
+  if (idx >= TW) return;
+  const bool sw = m < n;
+  const int sel = idx / (rows * SW), rem = idx % (rows * SW), e = rem / SW, i = rem % SW;
+  const bool isA = sel == 0;
+  const bool useg = isA == sw;  // A = g when swapped
+  const int d = useg ? n : m, str = useg ? dgx + 1 : dfx + 1, off = useg ? (m + 1) * (dfx + 1) : 0;
+  uint32_t r = 0u;
+  if (i <= d && e < str) {
+    const int c = off + (d - i) * str + e;
+    r = limbs_mod(limbs + (size_t)c * L, L, primes[pi]);
+    red[(size_t)pi * C + c] = r;
+  }
+  tab[(size_t)pi * TW + idx] = r;
+}
+
+void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes, int K, int m, int n, int dfx,
+                       int dgx, uint32_t* red, uint32_t* tab, cudaStream_t st) {
+  const int maxd = images_maxd(m, n);
+  const int dmax = dfx > dgx ? dfx : dgx;
+  const int rows = POLY * (dmax / POLY + 1);
+  const int SW = images_sw(maxd);
+  const int TW = 2 * rows * SW;
+  k_reduce_tab<<<dim3((TW + 127) / 128, K), 128, 0, st>>>(limbs, C, L, primes, m, n, dfx, dgx, rows, SW, red, tab);
+}
 
 int images_maxd(int m, int n) {
   const int d = m > n ? m : n;

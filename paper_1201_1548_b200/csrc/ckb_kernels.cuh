@@ -57,6 +57,7 @@ void launch_choose_c(const Prime* primes, const InterpPlan& plan, const uint32_t
 // ---- K2+K3: fused evaluation + univariate resultant (modpoly.py:382-390) ----
 struct ImageArgs {
   const uint32_t* red;     // [K][C]
+  const uint32_t* tab;     // [K][images_tab_words] residues in the kernel's shared-memory layout
   const int16_t* degs;     // [(m+1) + (n+1)] x-degree of each y-coefficient (-1 = zero)
   const uint32_t* yq;      // [K][M] g^u (plan)
   const uint32_t* om;      // [K][4 S] roots of unity (plan)
@@ -70,6 +71,11 @@ struct ImageArgs {
   uint32_t* fail_count;    // zeroed before the launch
 };
 int images_maxd(int m, int n);  // template bucket or -1
+// K1 for the pipeline: residues straight into the images kernel's transposed,
+// top-aligned, zero-padded table layout (and the plain [K][C] layout)
+size_t images_tab_words(int m, int n, int dfx, int dgx);
+void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes, int K, int m, int n, int dfx,
+                       int dgx, uint32_t* red, uint32_t* tab, cudaStream_t st);
 // fast generic kernel followed by the general warp kernel on its fail list
 void launch_images(const ImageArgs& a, cudaStream_t st);
 void launch_images_fallback(const ImageArgs& a, cudaStream_t st);

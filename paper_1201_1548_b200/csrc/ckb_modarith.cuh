@@ -90,6 +90,24 @@ __device__ __forceinline__ uint32_t mod_word(uint32_t x, uint32_t one_comp, uint
   return shoup(x, 1u, one_comp, p);
 }
 
+// residue mod p of a two's-complement integer of L little-endian 32-bit limbs
+__device__ __forceinline__ uint32_t limbs_mod(const uint32_t* w, int L, const Prime& P) {
+  const uint32_t p = P.p;
+  const uint32_t R1 = redc(P.r2, P);            // 2^32 mod p
+  const uint32_t R1c = shoup_comp(R1, P);
+  const uint32_t onec = shoup_comp(1u % p, P);
+  uint32_t r = 0;
+  for (int l = L - 1; l >= 0; --l) {
+    r = add_mod(shoup(r, R1, R1c, p), mod_word(w[l], onec, p), p);
+  }
+  if (w[L - 1] >> 31) {  // negative: subtract 2^(32L) mod p
+    uint32_t big = 1u % p;
+    for (int l = 0; l < L; ++l) big = shoup(big, R1, R1c, p);
+    r = sub_mod(r, big, p);
+  }
+  return r;
+}
+
 __device__ __forceinline__ Prime make_prime(uint32_t p) {
   Prime P;
   P.p = p;

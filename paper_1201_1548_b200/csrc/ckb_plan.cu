@@ -19,22 +19,7 @@ __global__ void k_reduce(const uint32_t* __restrict__ limbs, int C, int L, const
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int pi = blockIdx.y;
   if (c >= C) return;
-  const Prime P = primes[pi];
-  const uint32_t p = P.p;
-  const uint32_t R1 = redc(P.r2, P);            // 2^32 mod p
-  const uint32_t R1c = shoup_comp(R1, P);
-  const uint32_t onec = shoup_comp(1u % p, P);
-  const uint32_t* w = limbs + (size_t)c * L;
-  uint32_t r = 0;
-  for (int l = L - 1; l >= 0; --l) {
-    r = add_mod(shoup(r, R1, R1c, p), mod_word(w[l], onec, p), p);
-  }
-  if (w[L - 1] >> 31) {  // negative: subtract 2^(32L) mod p
-    uint32_t big = 1u % p;
-    for (int l = 0; l < L; ++l) big = shoup(big, R1, R1c, p);
-    r = sub_mod(r, big, p);
-  }
-  out[(size_t)pi * C + c] = r;
+  out[(size_t)pi * C + c] = limbs_mod(limbs + (size_t)c * L, L, primes[pi]);
 }
 
 void launch_reduce(const uint32_t* limbs, int C, int L, const Prime* primes, int K, uint32_t* out,
