@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <algorithm>
 // C-ABI boundary of the B200 modular symbolic engine (declared in
 // include/curvekit_b200.h).  Plain pointers and sizes only; every host buffer
@@ -65,6 +66,8 @@ struct Ctx {
   bool timing = false;
   cudaEvent_t sev[8] = {};
   int nsev = 0;
+  uint64_t epoch = 0;  // bumped whenever a buffer or table a captured graph may reference is freed
+  bool graphs = true;  // CKB_NO_GRAPHS=1 disables graph replay
 };
 
 Ctx g;
@@ -74,6 +77,7 @@ int dev_buf(const char* name, size_t bytes, void** out) {
   Buf& b = g.dev[name];
   if (b.n < bytes) {
     if (b.p) cudaFree(b.p);
+    ++g.epoch;
     b.p = nullptr;
     b.n = 0;
     size_t want = bytes + bytes / 4 + 256;
@@ -88,6 +92,7 @@ int host_buf(const char* name, size_t bytes, void** out) {
   Buf& b = g.host[name];
   if (b.n < bytes) {
     if (b.p) cudaFreeHost(b.p);
+    ++g.epoch;
     b.p = nullptr;
     b.n = 0;
     size_t want = bytes + bytes / 4 + 256;
@@ -171,6 +176,7 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
     cudaFree(e.d_blob);
     cudaFree(e.d_bt);
     g.crt.erase(g.crt.begin() + v);
+    ++g.epoch;
   }
   CrtEntry e;
   e.primes.assign(primes, primes + K);
@@ -273,6 +279,7 @@ int get_primes_dev(const uint32_t* primes, int K, Prime** out) {
   if (g_pcache.size() >= 16) {
     cudaFree(g_pcache.front().d);
     g_pcache.erase(g_pcache.begin());
+    ++g.epoch;
   }
   PrimeEntry e;
   e.primes.assign(primes, primes + K);
@@ -326,6 +333,7 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
       if (g_plans[i].last_use < g_plans[v].last_use) v = i;
     cudaFree(g_plans[v].blob);
     g_plans.erase(g_plans.begin() + v);
+    ++g.epoch;
   }
   PlanEntry e;
   e.primes.assign(primes, primes + K);
@@ -384,6 +392,97 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
 
 // the modular part of the pipeline on device buffers:
 // limbs -> residues -> choose c -> images -> interpolated coefficients [K][N]
+// ---- CUDA graphs of a call's launch sequence --------------------------------
+// The device work of a pipeline call depends only on its shapes, primes,
+// degrees and buffer addresses.  The first call with a key runs eagerly (it
+// builds the cached plan and tables); the second is captured into a graph;
+// later ones replay it with one launch.  A graph is dropped when any buffer or
+// table it may reference is freed (g.epoch), and a key whose capture fails
+// (an allocation or a synchronising call inside) stays eager.
+struct GraphEntry {
+  std::vector<uint64_t> key;
+  uint64_t epoch = 0;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t launches = 0;  // kernels per replay (for ckb_launch_count)
+  int seen = 0;           // < 0: not capturable
+  uint64_t last_use = 0;
+};
+std::vector<GraphEntry> g_graphs;
+
+void drop_graphs() {
+  for (auto& e : g_graphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+  g_graphs.clear();
+}
+
+template <class F>
+int graphed(const std::vector<uint64_t>& key, cudaStream_t st, F&& body) {
+  if (g.timing || !g.graphs) return body();
+  GraphEntry* ge = nullptr;
+  for (auto& e : g_graphs)
+    if (e.key == key) ge = &e;
+  if (ge && ge->epoch != g.epoch) {
+    if (ge->exec) cudaGraphExecDestroy(ge->exec);
+    ge->exec = nullptr;
+    ge->seen = ge->seen < 0 ? ge->seen : 0;
+    ge->epoch = g.epoch;
+  }
+  if (!ge) {
+    if (g_graphs.size() >= 16) {
+      size_t v = 0;
+      for (size_t i = 1; i < g_graphs.size(); ++i)
+        if (g_graphs[i].last_use < g_graphs[v].last_use) v = i;
+      if (g_graphs[v].exec) cudaGraphExecDestroy(g_graphs[v].exec);
+      g_graphs.erase(g_graphs.begin() + v);
+    }
+    GraphEntry e;
+    e.key = key;
+    e.epoch = g.epoch;
+    g_graphs.push_back(e);
+    ge = &g_graphs.back();
+  }
+  ge->last_use = ++g.tick;
+  if (ge->exec) {
+    CK(cudaGraphLaunch(ge->exec, st));
+    g.launches += ge->launches;
+    return 0;
+  }
+  if (ge->seen < 0 || ge->seen++ == 0) return body();
+  const uint64_t l0 = g.launches, ep = g.epoch;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int rc = body();
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+  cudaGraphExec_t exec = nullptr;
+  bool ok = rc == 0 && ce == cudaSuccess && graph != nullptr && g.epoch == ep;
+  if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok) {
+    cudaGetLastError();  // clear capture errors; run this call eagerly, never capture the key again
+    for (auto& e : g_graphs)
+      if (e.key == key) e.seen = -1;
+    g.launches = l0;
+    return body();
+  }
+  for (auto& e : g_graphs)
+    if (e.key == key) {
+      e.exec = exec;
+      e.launches = g.launches - l0;
+      e.epoch = g.epoch;
+    }
+  CK(cudaGraphLaunch(exec, st));
+  return 0;
+}
+
+void key_push(std::vector<uint64_t>& k, const void* p, size_t bytes) {
+  const uint8_t* b = (const uint8_t*)p;
+  for (size_t i = 0; i < bytes; i += 8) {
+    uint64_t w = 0;
+    memcpy(&w, b + i, bytes - i < 8 ? bytes - i : 8);
+    k.push_back(w);
+  }
+}
+
 int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
                   int n, int dfx, int dgx, const Prime* d_primes, const uint32_t* h_primes, const uint32_t* h_gens,
                   int K, int N, uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st,
@@ -462,6 +561,10 @@ int ckb_init(int device) {
   CK(cudaEventCreate(&g.ev1));
   for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&g.sev[i]));
   g.device = device;
+  {
+    const char* e = getenv("CKB_NO_GRAPHS");
+    g.graphs = !(e && e[0] == '1');
+  }
   g.ready = true;
   return 0;
 }
@@ -471,6 +574,8 @@ int ckb_shutdown(void) {
   if (!g.ready) return 0;
   cudaSetDevice(g.device);
   cudaStreamSynchronize(g.stream);
+  drop_graphs();
+  ++g.epoch;
   for (auto& kv : g.dev) cudaFree(kv.second.p);
   for (auto& kv : g.host) cudaFreeHost(kv.second.p);
   for (auto& e : g.crt) {
@@ -523,23 +628,33 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   if ((rc = dbuf("status", 4, &d_status))) return rc;
   CrtEntry* ce;
   if ((rc = get_crt(primes, K, LW, &ce))) return rc;
-  CK(cudaEventRecord(g.ev0, st));
-  CK(cudaMemcpyAsync(d_limbs, hb, 4 * nl, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_degs, hb + 4 * nl + 4 * (size_t)K, 2 * nd, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(d_status, 0, 4, st));
-  g.nsev = 0;
-  if ((rc = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
-                          d_status, st, &ce->t)))
-    return rc;
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
-  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
-  stage_mark(st);
-  g.launches += 2;
-  CK(cudaGetLastError());
   uint8_t* ho = (uint8_t*)h_out;
-  CK(cudaMemcpyAsync(ho, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(ho + 4 * (size_t)N * LW, d_status, 4, cudaMemcpyDeviceToHost, st));
+  std::vector<uint64_t> key = {2, (uint64_t)C, (uint64_t)L, (uint64_t)m, (uint64_t)n, (uint64_t)dfx, (uint64_t)dgx,
+                               (uint64_t)K, (uint64_t)N, (uint64_t)LW};
+  key_push(key, degs, 2 * nd);
+  key_push(key, primes, 4 * (size_t)K);
+  key_push(key, gens, 4 * (size_t)K);
+  CK(cudaEventRecord(g.ev0, st));
+  rc = graphed(key, st, [&]() -> int {
+    int r;
+    CK(cudaMemcpyAsync(d_limbs, hb, 4 * nl, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_degs, hb + 4 * nl + 4 * (size_t)K, 2 * nd, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d_status, 0, 4, st));
+    g.nsev = 0;
+    if ((r = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
+                           d_status, st, &ce->t)))
+      return r;
+    launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
+    stage_mark(st);
+    g.launches += 2;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ho, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ho + 4 * (size_t)N * LW, d_status, 4, cudaMemcpyDeviceToHost, st));
+    return 0;
+  });
+  if (rc) return rc;
   CK(cudaEventRecord(g.ev1, st));
   CK(cudaStreamSynchronize(st));
   memcpy(out, ho, 4 * (size_t)N * LW);
@@ -807,17 +922,26 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
   if ((rc = get_crt(primes, K, LW, &ce))) return rc;
   uint32_t* d_coeffs;
   if ((rc = dbuf("coeffs", std::max((size_t)K * N, crt_a_words(K, N)), &d_coeffs))) return rc;
-  g.nsev = 0;
-  if ((rc = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
-                          d_status, st, &ce->t)))
-    return rc;
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
-  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
-  stage_mark(st);
-  g.launches += 2;
-  CK(cudaGetLastError());
-  return 0;
+  std::vector<uint64_t> key = {1, (uint64_t)C, (uint64_t)L, (uint64_t)m, (uint64_t)n, (uint64_t)dfx, (uint64_t)dgx,
+                               (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)d_limbs, (uint64_t)d_degs,
+                               (uint64_t)d_out, (uint64_t)d_status, (uint64_t)st};
+  key_push(key, h_degs, 2 * (size_t)(m + n + 2));
+  key_push(key, primes, 4 * (size_t)K);
+  key_push(key, gens, 4 * (size_t)K);
+  return graphed(key, st, [&]() -> int {
+    int r;
+    g.nsev = 0;
+    if ((r = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N,
+                           d_coeffs, d_status, st, &ce->t)))
+      return r;
+    launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
+    stage_mark(st);
+    g.launches += 2;
+    CK(cudaGetLastError());
+    return 0;
+  });
 }
 
 int ckb_set_timing(int on) {

@@ -45,6 +45,13 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
   const int rows = POLY * (emax + 1);         // x-power rows, zero-padded
   // TA[e][i] = coefficient of x^e in the y-coefficient of degree da - i (top-aligned),
   // zero beyond each row; maskA[e] = chunks of registers with a term at x^e
+  // per-thread point data first: its global-load latency overlaps the table copy
+  const int t = blockIdx.x * IMG_THREADS + threadIdx.x;
+  const bool active = t < a.N;  // a.N = 8 M; inactive lanes still join the shuffles
+  const int u = active ? (t >> 3) : 0, l = t & (POLY - 1);
+  const Prime P = a.primes[pi];
+  const uint32_t c = a.cval[pi];
+  uint32_t y = a.yq[(size_t)pi * a.M + u];
   uint32_t* TA = sm;
   uint32_t* TB = sm + rows * SW;
   uint32_t* maskA = sm + 2 * rows * SW;
@@ -71,13 +78,7 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
   // image (u, j): x = w^j c y_u.  Lane l of an 8-lane group evaluates the
   // polyphase component G_l = y^l F_l(y^8) of every y-coefficient; a 3-stage
   // DFT across the group then gives f(w^j y) for all j (j = bitrev(l)).
-  const int t = blockIdx.x * IMG_THREADS + threadIdx.x;
-  const bool active = t < a.N;  // a.N = 8 M; inactive lanes still join the shuffles
-  const int u = active ? (t >> 3) : 0, l = t & (POLY - 1);
-  const Prime P = a.primes[pi];
   const uint32_t p = P.p;
-  const uint32_t c = a.cval[pi];
-  uint32_t y = a.yq[(size_t)pi * a.M + u];
   if (c != 1u) y = shoup(y, c, shoup_comp(c, P), p);  // y_u = c g^u
   const uint32_t y2 = mul_mod(y, y, P), y4 = mul_mod(y2, y2, P);
   const uint32_t z = mul_mod(y4, y4, P);  // Horner variable y^8

@@ -305,3 +305,21 @@ def test_cfg3_subres_profile_golden(mp):
     pr = mp.modular_subres_profile(f, g, rstar, gold["profile"]["p"])
     assert list(pr.chain_degrees) == gold["profile"]["chain"]
     assert list(pr.factor_degrees) == gold["profile"]["d"]
+
+
+def test_graph_replay_and_reallocation(mp):
+    """Repeated calls replay a captured CUDA graph; a larger problem in between
+    reallocates the work buffers (dropping the graph) and results stay exact."""
+    from paper_1201_1548_b200.synth import make_pair
+    f2, g2 = make_pair("cfg2", 0)
+    want2 = mp.biv_resultant(f2, g2, "y")
+    small = [({(2, 0): 1, (0, 2): 1, (0, 0): -1}, {(0, 1): 1, (1, 0): -1}, [-1, 0, 2])]
+    for _ in range(4):
+        assert mp.biv_resultant(f2, g2, "y") == want2
+    f3, g3 = make_pair("cfg3", 0)
+    want3 = mp.biv_resultant(f3, g3, "y")
+    for _ in range(3):
+        assert mp.biv_resultant(f3, g3, "y") == want3
+        assert mp.biv_resultant(f2, g2, "y") == want2
+        for f, g, r in small:
+            assert mp.biv_resultant(f, g, "y") == r
