@@ -278,9 +278,12 @@ def run_ours(args):
     e2e = None
     if rank == 0:
         p1 = plan_resultant(fc, gc, tdf, tdg, pk.dfx, pk.dgx)
-        hout = np.empty(p1.N * p1.LW, dtype=np.uint32)
+        # page-locked host buffers, as the e2e contract states (inputs copied from pinned memory)
+        hlimbs = _lib.pinned.get("bench_in", pk.limbs.size)
+        hlimbs[:] = pk.limbs.reshape(-1)
+        hout = _lib.pinned.get("bench_out", p1.N * p1.LW)
         status = np.zeros(1, dtype=np.uint32)
-        args_c = (_lib.ptr(pk.limbs), pk.C, pk.L, _lib.ptr(pk.degs), pk.m, pk.n, pk.dfx, pk.dgx,
+        args_c = (_lib.ptr(hlimbs), pk.C, pk.L, _lib.ptr(pk.degs), pk.m, pk.n, pk.dfx, pk.dgx,
                   _lib.ptr(p1.primes), _lib.ptr(p1.gens), len(p1.primes), p1.N, p1.LW, _lib.ptr(hout),
                   _lib.ptr(status), None)
         for _ in range(args.warmup):
@@ -302,7 +305,7 @@ def run_ours(args):
         e2e = {"value": 1e3 / e_ms, "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(pk.limbs.nbytes + pk.degs.nbytes + 4 * len(p1.gens)),
                "d2h_bytes_per_step": int(hout.nbytes + 4),
-               "path": "ckb_biv_resultant (C-ABI, host buffers, pinned staging, copies in the timed region)",
+               "path": "ckb_biv_resultant (C-ABI, page-locked host buffers, copies in the timed region)",
                "python_api_ms": 1e3 * statistics.median(pt),
                "python_api_note": "modpoly.biv_resultant incl. packing, planning, int conversion"}
 

@@ -111,6 +111,12 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
                           int n, int dfx, int dgx, const uint32_t* primes, const uint32_t* gens, int K, int N, int LW,
                           uint32_t* d_out, uint32_t* d_status, void* stream);
 
+/* Page-locked host memory.  ckb_biv_resultant copies straight from / into
+ * page-locked limbs / out buffers (no staging memcpy); these allocate and free
+ * such buffers (NULL on failure). */
+void* ckb_host_alloc(unsigned long long bytes);
+int ckb_host_free(void* p);
+
 /* Instrumentation: record CUDA events between the stages of the next pipeline
  * calls; ckb_stage_times returns the durations (ms) of reduce, plan, images,
  * interpolation, CRT for the last call (count returned). */

@@ -21,7 +21,7 @@ EXPORTS = (
     "ckb_biv_resultant", "ckb_reduce", "ckb_uni_resultant_batch", "ckb_interp_plan_points",
     "ckb_interp_geometric", "ckb_crt_lift", "ckb_dev_modular_images", "ckb_dev_crt",
     "ckb_interp_points", "ckb_gcd_mod_batch", "ckb_dev_biv_resultant", "ckb_set_timing",
-    "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values",
+    "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values", "ckb_host_alloc", "ckb_host_free",
 )
 
 _P = ctypes.c_void_p
@@ -50,6 +50,8 @@ _SIGS = {
     "ckb_stage_times": (_I, [_P, _I]),
     "ckb_measure_peak": (_I, [_P]),
     "ckb_psc_values": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, ctypes.c_uint32, _I, _P, _P]),
+    "ckb_host_alloc": (_P, [ctypes.c_ulonglong]),
+    "ckb_host_free": (_I, [_P]),
 }
 
 _lock = threading.Lock()
@@ -112,6 +114,33 @@ def ptr(a: np.ndarray):
     """ctypes pointer to a C-contiguous numpy array."""
     assert a.flags["C_CONTIGUOUS"], "array must be C-contiguous"
     return a.ctypes.data_as(_P)
+
+
+class PinnedPool(threading.local):
+    """Per-thread grow-only page-locked uint32 buffers by name (the pipeline
+    copies to / from page-locked memory directly).  A view is valid until the
+    same thread asks for a larger buffer of that name."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, name: str, count: int) -> np.ndarray:
+        cur = self._bufs.get(name)
+        if cur is None or cur[1] < count:
+            lb = lib()
+            if cur is not None:
+                lb.ckb_host_free(cur[0])
+            want = max(count, 1024) + count // 4
+            p = lb.ckb_host_alloc(4 * want)
+            if not p:
+                raise CkbError("ckb_host_alloc failed: " + lb.ckb_last_error().decode())
+            cur = (p, want)
+            self._bufs[name] = cur
+        arr = np.ctypeslib.as_array(ctypes.cast(cur[0], _U32P), shape=(cur[1],))
+        return arr[:count]
+
+
+pinned = PinnedPool()
 
 
 def launch_count() -> int:

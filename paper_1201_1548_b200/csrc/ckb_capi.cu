@@ -260,6 +260,20 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
   return 0;
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+void* pinned_alloc(size_t bytes) {
+  void* p = nullptr;
+  return cudaMallocHost(&p, bytes) == cudaSuccess ? p : nullptr;
+}
+
 void stage_mark(cudaStream_t st) {
   if (g.timing && g.nsev < 8) cudaEventRecord(g.sev[g.nsev++], st);
 }
@@ -615,10 +629,13 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   void *h_in, *h_out;
   if ((rc = host_buf("in", 4 * nl + 2 * nd + 4 * (size_t)K + 64, &h_in))) return rc;
   if ((rc = host_buf("out", 4 * (size_t)N * LW + 64, &h_out))) return rc;
+  // page-locked caller buffers are copied to / from directly (no staging memcpy)
+  const bool in_direct = is_pinned(limbs), out_direct = is_pinned(out);
   uint8_t* hb = (uint8_t*)h_in;
-  memcpy(hb, limbs, 4 * nl);
+  if (!in_direct) memcpy(hb, limbs, 4 * nl);
   memcpy(hb + 4 * nl, gens, 4 * (size_t)K);
   memcpy(hb + 4 * nl + 4 * (size_t)K, degs, 2 * nd);
+  const void* src_limbs = in_direct ? (const void*)limbs : (const void*)hb;
   uint32_t *d_limbs, *d_coeffs, *d_out, *d_status;
   int16_t* d_degs;
   if ((rc = dbuf("limbs", nl, &d_limbs))) return rc;
@@ -631,15 +648,16 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
   uint8_t* ho = (uint8_t*)h_out;
+  void* dst_out = out_direct ? (void*)out : (void*)ho;
   std::vector<uint64_t> key = {2, (uint64_t)C, (uint64_t)L, (uint64_t)m, (uint64_t)n, (uint64_t)dfx, (uint64_t)dgx,
-                               (uint64_t)K, (uint64_t)N, (uint64_t)LW};
+                               (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)src_limbs, (uint64_t)dst_out};
   key_push(key, degs, 2 * nd);
   key_push(key, primes, 4 * (size_t)K);
   key_push(key, gens, 4 * (size_t)K);
   CK(cudaEventRecord(g.ev0, st));
   rc = graphed(key, st, [&]() -> int {
     int r;
-    CK(cudaMemcpyAsync(d_limbs, hb, 4 * nl, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_limbs, src_limbs, 4 * nl, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_degs, hb + 4 * nl + 4 * (size_t)K, 2 * nd, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_status, 0, 4, st));
     g.nsev = 0;
@@ -650,14 +668,14 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
     stage_mark(st);
     g.launches += 2;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(ho, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(dst_out, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(ho + 4 * (size_t)N * LW, d_status, 4, cudaMemcpyDeviceToHost, st));
     return 0;
   });
   if (rc) return rc;
   CK(cudaEventRecord(g.ev1, st));
   CK(cudaStreamSynchronize(st));
-  memcpy(out, ho, 4 * (size_t)N * LW);
+  if (!out_direct) memcpy(out, ho, 4 * (size_t)N * LW);
   uint32_t s;
   memcpy(&s, ho + 4 * (size_t)N * LW, 4);
   if (status) *status = s;
@@ -942,6 +960,20 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
     CK(cudaGetLastError());
     return 0;
   });
+}
+
+void* ckb_host_alloc(unsigned long long bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (ensure_ready()) return nullptr;
+  void* p = pinned_alloc((size_t)bytes);
+  if (!p) fail("ckb_host_alloc: cudaMallocHost failed", -1);
+  return p;
+}
+
+int ckb_host_free(void* p) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (p) CK(cudaFreeHost(p));
+  return 0;
 }
 
 int ckb_set_timing(int on) {

@@ -503,7 +503,7 @@ def _biv_resultant_gpu(fc, gc, tdf: int, tdg: int):
     for _attempt in range(4):
         plan = plan_resultant(fc, gc, tdf, tdg, packed.dfx, packed.dgx, start)
         K, N, LW = len(plan.primes), plan.N, plan.LW
-        out = np.empty(N * LW, dtype=np.uint32)
+        out = _lib.pinned.get("biv_out", N * LW)  # page-locked: the result lands here directly
         status = np.zeros(1, dtype=np.uint32)
         ms = np.zeros(1, dtype=np.float32)
         rc = _lib.check(lib.ckb_biv_resultant(
