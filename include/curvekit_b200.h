@@ -123,10 +123,10 @@ int ckb_host_free(void* p);
 int ckb_set_timing(int on);
 int ckb_stage_times(float* ms, int max);
 
-/* Roofline denominators measured on the current device: out4 = [IMAD,
- * IMAD.HI, IMAD.WIDE rates in T ops/s, Shoup-pair modular products in
- * T products/s] (csrc/ckb_peak.cu). */
-int ckb_measure_peak(float* out4);
+/* Roofline denominators measured on the current device (csrc/ckb_peak.cu):
+ * out[0..n) = IMAD, IMAD.HI, IMAD.WIDE rates in T ops/s, then Shoup-pair and
+ * three-product-Montgomery modular products in T products/s (n <= 5 used). */
+int ckb_measure_peak(float* out, int n);
 
 #ifdef __cplusplus
 }

@@ -48,7 +48,7 @@ _SIGS = {
     "ckb_dev_biv_resultant": (_I, [_P, _I, _I, _P, _P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P, _P]),
     "ckb_set_timing": (_I, [_I]),
     "ckb_stage_times": (_I, [_P, _I]),
-    "ckb_measure_peak": (_I, [_P]),
+    "ckb_measure_peak": (_I, [_P, _I]),
     "ckb_psc_values": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, ctypes.c_uint32, _I, _P, _P]),
     "ckb_host_alloc": (_P, [ctypes.c_ulonglong]),
     "ckb_host_free": (_I, [_P]),

@@ -35,7 +35,6 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
   using LY = ImgLayout<MAXD>;
   constexpr int NCH = LY::NCH, SW = LY::SW;
   extern __shared__ __align__(16) uint32_t sm[];
-  const int pi = blockIdx.y;
   const bool sw = a.m < a.n;  // reference swaps so that deg a >= deg b
   const int da = sw ? a.n : a.m, db = sw ? a.m : a.n;
   const int16_t* Adeg = a.degs + (sw ? a.m + 1 : 0);
@@ -43,25 +42,39 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
   const int dmax = max(a.dfx, a.dgx);
   const int emax = dmax / POLY;               // Horner steps in z = y^8
   const int rows = POLY * (emax + 1);         // x-power rows, zero-padded
-  // TA[e][i] = coefficient of x^e in the y-coefficient of degree da - i (top-aligned),
-  // zero beyond each row; maskA[e] = chunks of registers with a term at x^e
+  const int TW = 2 * rows * SW;               // one prime's tables
+  // The images of all primes form one flat range (prime-major, N per prime,
+  // N a multiple of 8 so a coset never straddles primes); a CTA takes 128
+  // consecutive images, so the grid has no per-prime padding and ends in an
+  // (almost) full wave.  The tables of every prime the CTA spans are staged
+  // (two at most once N >= 128; the launch sizes shared memory for the worst case).
+  const int g0 = blockIdx.x * IMG_THREADS;
+  const int total = a.K * a.N;
+  const int pi0 = g0 / a.N, pi1 = min(a.K - 1, (g0 + IMG_THREADS - 1) / a.N);
   // per-thread point data first: its global-load latency overlaps the table copy
-  const int t = blockIdx.x * IMG_THREADS + threadIdx.x;
-  const bool active = t < a.N;  // a.N = 8 M; inactive lanes still join the shuffles
-  const int u = active ? (t >> 3) : 0, l = t & (POLY - 1);
+  const int t = g0 + threadIdx.x;
+  const bool active = t < total;  // inactive lanes still join the shuffles
+  const int pi = active ? t / a.N : pi1;
+  const int tin = active ? t - pi * a.N : 0;  // image index within the prime
+  const int u = tin >> 3, l = t & (POLY - 1);
+  const int tslot = pi - pi0;  // which staged table
   const Prime P = a.primes[pi];
   const uint32_t c = a.cval[pi];
   uint32_t y = a.yq[(size_t)pi * a.M + u];
-  uint32_t* TA = sm;
-  uint32_t* TB = sm + rows * SW;
-  uint32_t* maskA = sm + 2 * rows * SW;
+  // TA[e][i] = coefficient of x^e in the y-coefficient of degree da - i (top-aligned),
+  // zero beyond each row; maskA[e] = chunks of registers with a term at x^e
+  uint32_t* TA = sm + tslot * TW;
+  uint32_t* TB = TA + rows * SW;
+  const int nspan = pi1 - pi0 + 1;
+  uint32_t* maskA = sm + a.span * TW;
   uint32_t* maskB = maskA + rows;
-  uint32_t* som = maskB + rows;               // w^k and companions
+  uint32_t* som = maskB + rows + tslot * 2 * POLY;  // w^k and companions
   {
-    // K1 wrote this prime's tables in exactly this layout: one coalesced copy
-    const uint4* src = reinterpret_cast<const uint4*>(a.tab + (size_t)pi * 2 * rows * SW);
-    uint4* dst = reinterpret_cast<uint4*>(TA);
-    for (int idx = threadIdx.x; idx < 2 * rows * SW / 4; idx += IMG_THREADS) dst[idx] = src[idx];
+    // K1 wrote the tables in exactly this layout: coalesced 16-byte copies
+    const int nt = nspan * TW / 4;
+    const uint4* src = reinterpret_cast<const uint4*>(a.tab + (size_t)pi0 * TW);
+    uint4* dst = reinterpret_cast<uint4*>(sm);
+    for (int idx = threadIdx.x; idx < nt; idx += IMG_THREADS) dst[idx] = src[idx];
   }
   for (int e = threadIdx.x; e < rows; e += IMG_THREADS) {
     uint32_t ma = 0, mb = 0;
@@ -72,7 +85,8 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
     maskA[e] = ma;
     maskB[e] = mb;
   }
-  if (threadIdx.x < 2 * POLY) som[threadIdx.x] = a.om[(size_t)pi * 4 * POLY + threadIdx.x];
+  for (int q = threadIdx.x; q < nspan * 2 * POLY; q += IMG_THREADS)
+    maskB[rows + q] = a.om[(size_t)(pi0 + q / (2 * POLY)) * 4 * POLY + q % (2 * POLY)];
   __syncthreads();
 
   // image (u, j): x = w^j c y_u.  Lane l of an 8-lane group evaluates the
@@ -157,7 +171,7 @@ __global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs 
     }
   }
   const int j = ((l & 1) << 2) | (l & 2) | ((l >> 2) & 1);  // bitrev3(l)
-  const int idx = u * POLY + j;
+  const int idx = u * POLY + j;  // = tin - l + j
   if (!active) return;  // no shuffles below this point
   uint32_t v;
   if (red4(A[0], p) == 0u || red4(B[0], p) == 0u) {
@@ -236,15 +250,18 @@ int images_maxd(int m, int n) {
 
 void launch_images(const ImageArgs& a, cudaStream_t st) {
   const int maxd = images_maxd(a.m, a.n);
-  dim3 grid((a.N + IMG_THREADS - 1) / IMG_THREADS, a.K);
+  dim3 grid((unsigned)(((size_t)a.K * a.N + IMG_THREADS - 1) / IMG_THREADS));
+  ImageArgs b = a;
+  b.span = (IMG_THREADS - 1 + a.N - 1) / a.N + 1;  // primes a window of IMG_THREADS images can touch
+  if (b.span > a.K) b.span = a.K;
   const int dmax = a.dfx > a.dgx ? a.dfx : a.dgx;
   const int rows = POLY * (dmax / POLY + 1);
 #define LAUNCH(D)                                                                                    \
   if (maxd == D) {                                                                                   \
-    const size_t smem = (size_t)(2 * rows * ImgLayout<D>::SW + 2 * rows + 2 * POLY) * 4;           \
+    const size_t smem = (size_t)(b.span * (2 * rows * ImgLayout<D>::SW + 2 * POLY) + 2 * rows) * 4; \
     if (smem > 48 * 1024)                                                                            \
       cudaFuncSetAttribute(k_images<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    k_images<D><<<grid, IMG_THREADS, smem, st>>>(a);                                                 \
+    k_images<D><<<grid, IMG_THREADS, smem, st>>>(b);                                                 \
   }
   CKB_MAXD_LIST(LAUNCH)
 #undef LAUNCH

@@ -69,6 +69,7 @@ struct ImageArgs {
   uint32_t* status;        // bit 1: an image hit a vanishing leading coefficient
   uint32_t* fail_list;     // [K*N] flat indices of non-generic images
   uint32_t* fail_count;    // zeroed before the launch
+  int span;                // set by launch_images: max primes one CTA's images touch
 };
 int images_maxd(int m, int n);  // template bucket or -1
 // K1 for the pipeline: residues straight into the images kernel's transposed,

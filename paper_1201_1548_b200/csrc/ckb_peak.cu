@@ -5,8 +5,9 @@
 // B200, tools/imad_peak.cu).  Their unit of work is one modular product; the
 // densest form in the kernels is the Shoup pair of the elimination step
 //     red(red(x*w - hi(x*w')p) + red(y*v - hi(y*v')p))      (2 products)
-// so the peak is that op in 8 independent chains per thread on every SM.
-// Also reports raw IMAD / IMAD.HI / IMAD.WIDE rates for reference.
+// so the peak is that op in 8 independent chains per thread on every SM; the
+// fused remainders use a three-product Montgomery update, measured the same
+// way.  Also reports raw IMAD / IMAD.HI / IMAD.WIDE rates for reference.
 #include <cuda_runtime.h>
 
 #include "../../include/curvekit_b200.h"
@@ -77,10 +78,29 @@ __global__ void k_pk_shoup2(uint32_t* out, uint32_t p, uint32_t w, uint32_t wc, 
   if (r == 0x9e3779b9u) out[threadIdx.x] = r;
 }
 
+// the fused remainder's update: three products summed in 64 bits, one
+// signed Montgomery reduction (ckb_resultant.cuh mont3)
+__global__ void k_pk_mont3(uint32_t* out, uint32_t p, uint32_t pinv, uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t x[CH];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) x[k] = (threadIdx.x * 7 + k) % p;
+  for (int i = 0; i < IT; ++i)
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const uint64_t t = (uint64_t)x[k] * a + (uint64_t)x[(k + 1) % CH] * b + (uint64_t)x[(k + 2) % CH] * c;
+      x[k] = (uint32_t)(t >> 32) - __umulhi((uint32_t)t * pinv, p) + p;
+    }
+  uint32_t r = 0;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) r ^= x[k];
+  if (r == 0x9e3779b9u) out[threadIdx.x] = r;
+}
+
 }  // namespace
 
-extern "C" int ckb_measure_peak(float* out4) {
-  // out4: [IMAD, IMAD.HI, IMAD.WIDE (T ops/s), Shoup-pair modular products (T products/s)]
+extern "C" int ckb_measure_peak(float* out, int n) {
+  // out[0..n): IMAD, IMAD.HI, IMAD.WIDE (T ops/s), Shoup-pair modular products,
+  // three-product Montgomery modular products (T products/s)
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   cudaDeviceProp prop;
@@ -95,14 +115,17 @@ extern "C" int ckb_measure_peak(float* out4) {
   const uint32_t p = 1073692673u;  // PRIMES30[0]
   const uint64_t w = 123456789u % p, v = 987654321u % p;
   const uint32_t wc = (uint32_t)((w << 32) / p), vc = (uint32_t)((v << 32) / p);
-  float ms[4] = {0, 0, 0, 0};
-  for (int k = 0; k < 4; ++k) {
+  uint32_t pinv = p;
+  for (int i = 0; i < 5; ++i) pinv *= 2u - p * pinv;
+  float ms[5] = {0, 0, 0, 0, 0};
+  for (int k = 0; k < 5; ++k) {
     for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
       cudaEventRecord(a);
       if (k == 0) k_pk_imad<<<blocks, threads>>>(buf, 3);
       if (k == 1) k_pk_hi<<<blocks, threads>>>(buf, 3);
       if (k == 2) k_pk_wide<<<blocks, threads>>>(buf, 3);
       if (k == 3) k_pk_shoup2<<<blocks, threads>>>(buf, p, (uint32_t)w, wc, (uint32_t)v, vc);
+      if (k == 4) k_pk_mont3<<<blocks, threads>>>(buf, p, pinv, (uint32_t)w, (uint32_t)v, 55555555u % p);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms[k], a, b);
@@ -113,7 +136,10 @@ extern "C" int ckb_measure_peak(float* out4) {
   cudaEventDestroy(b);
   cudaFree(buf);
   if (e != cudaSuccess) return -1;
-  for (int k = 0; k < 3; ++k) out4[k] = (float)(per / (ms[k] * 1e-3) / 1e12);
-  out4[3] = (float)(2.0 * per / (ms[3] * 1e-3) / 1e12);
+  float v5[5];
+  for (int k = 0; k < 3; ++k) v5[k] = (float)(per / (ms[k] * 1e-3) / 1e12);
+  v5[3] = (float)(2.0 * per / (ms[3] * 1e-3) / 1e12);
+  v5[4] = (float)(3.0 * per / (ms[4] * 1e-3) / 1e12);
+  for (int k = 0; k < n && k < 5; ++k) out[k] = v5[k];
   return 0;
 }

@@ -1,10 +1,12 @@
 """Algorithmic work model of the hot path (used for roofline reporting).
 
 Two counts are kept apart:
-  * ``kernel_products`` -- modular products the B200 algorithm performs
+  * ``images_products`` -- modular products the B200 algorithm performs
     (Shoup-Horner evaluation + division-free elimination), the work the
-    images kernel must do; achieved = products / kernel time, against the
-    measured Shoup-pair product peak (csrc/ckb_peak.cu).
+    images kernel must do; achieved = products / kernel time.  The peak is
+    mix-weighted: Shoup-form products (evaluation, first remainder) at the
+    measured Shoup-pair rate, fused-remainder products at the measured
+    three-product Montgomery rate (csrc/ckb_peak.cu).
   * ``contract_imad`` -- SURVEY.md §8(d)'s fixed per-res_y figure
     W = 3 IMAD x [k N (E + 4 r (r + 1)) + k N^2 + N k (k - 1)/2 + C L k]
     (the Schur-algorithm count of PAPER.md's design), reported unchanged so
@@ -25,8 +27,9 @@ def eval_products(degs_f, degs_g) -> int:
 def eval_products_poly(degs_f, degs_g, S: int = POLY) -> int:
     """Products per image of the polyphase evaluation: each lane of an S-lane
     coset runs Horner in y^S over its share of the coefficients (ceil((D+1)/S)
-    terms of a degree-D poly), then one product by y^r and log2(S) DFT stages."""
-    stages = S.bit_length() - 1
+    terms of a degree-D poly), then one product by y^r and log2(S) - 1 DFT
+    stages with products (the last stage's twiddle is 1)."""
+    stages = S.bit_length() - 2
     tot = 0
     for d in list(degs_f) + list(degs_g):
         if d >= 0:
@@ -45,6 +48,22 @@ def elim_products(m: int, n: int) -> int:
     total = sum(2 * (da - s) for s in range(da - db + 1))
     total += sum(3 * k for k in range(1, db))
     return total
+
+
+def elim_split(m: int, n: int):
+    """(Shoup products of the first remainder, Montgomery-fold products of the fused remainders)."""
+    da, db = max(m, n), min(m, n)
+    if db < 1:
+        return 0, 0
+    return sum(2 * (da - s) for s in range(da - db + 1)), sum(3 * k for k in range(1, db))
+
+
+def images_products_split(m, n, degs_f, degs_g, K, N):
+    """(Shoup-form, Montgomery-fold) products of one k_images launch: the
+    roofline weights each class by its own measured peak."""
+    NI = POLY * -(-N // POLY)
+    s1, m3 = elim_split(m, n)
+    return K * NI * (eval_products_poly(degs_f, degs_g) + s1), K * NI * m3
 
 
 def images_products(m, n, degs_f, degs_g, K, N) -> int:
