@@ -17,6 +17,11 @@ namespace ckb {
 #ifndef CKB_IMG_MINB
 #define CKB_IMG_MINB 1
 #endif
+#ifndef CKB_IMG_MINB_BIG
+#define CKB_IMG_MINB_BIG CKB_IMG_MINB
+#endif
+// CTAs per SM the register allocation must allow (MAXD >= 56: the big buckets)
+constexpr int img_minb(int maxd) { return maxd >= 56 ? CKB_IMG_MINB_BIG : CKB_IMG_MINB; }
 constexpr int IMG_THREADS = 128;
 
 constexpr int POLY = 8;  // polyphase factor S: one 8-lane group per coset {w^j y_u}
@@ -31,7 +36,7 @@ struct ImgLayout {
 };
 
 template <int MAXD>
-__global__ void __launch_bounds__(IMG_THREADS, CKB_IMG_MINB) k_images(ImageArgs a) {
+__global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArgs a) {
   using LY = ImgLayout<MAXD>;
   constexpr int NCH = LY::NCH, SW = LY::SW;
   extern __shared__ __align__(16) uint32_t sm[];
