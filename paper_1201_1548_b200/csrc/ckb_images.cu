@@ -22,7 +22,10 @@ namespace ckb {
 #endif
 // CTAs per SM the register allocation must allow (MAXD >= 56: the big buckets)
 constexpr int img_minb(int maxd) { return maxd >= 56 ? CKB_IMG_MINB_BIG : CKB_IMG_MINB; }
-constexpr int IMG_THREADS = 128;
+#ifndef CKB_IMG_THREADS
+#define CKB_IMG_THREADS 128
+#endif
+constexpr int IMG_THREADS = CKB_IMG_THREADS;
 
 constexpr int POLY = 8;  // polyphase factor S: one 8-lane group per coset {w^j y_u}
 
