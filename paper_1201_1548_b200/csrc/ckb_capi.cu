@@ -362,7 +362,8 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
   pl.L = (int)L;
   pl.logL = logL;
   const size_t kn = (size_t)K * N, kn1 = (size_t)K * (N + 1), kl = (size_t)K * L, kh = kl / 2;
-  const size_t words = kn * 10 + kn1 * 3 + kh * 4 + kl * 4 + (size_t)K * 5 + (size_t)K * 4 * S + 64;  // take()s
+  const size_t words =
+      kn * 10 + kn1 * 3 + kh * 4 + kl * 4 + (size_t)K * 5 + (size_t)K * 4 * S + (S > 1 ? 2 * (size_t)S * kn : 0) + 64;
   CK(cudaMalloc(&e.blob, 4 * words));
   uint32_t* b = (uint32_t*)e.blob;
   auto take = [&](size_t n) { uint32_t* r = b; b += n; return r; };
@@ -388,6 +389,8 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
   pl.Mf = take(kl);
   pl.Mfc = take(kl);
   pl.Linv = take(K);
+  pl.zr = S > 1 ? take((size_t)S * kn) : nullptr;
+  pl.zrc = S > 1 ? take((size_t)S * kn) : nullptr;
   uint32_t* d_gens = take(K);
   Prime* d_primes = reinterpret_cast<Prime*>(take((size_t)K * 3));
   std::vector<Prime> hp(K);

@@ -82,7 +82,23 @@ __global__ void __launch_bounds__(NTT_THREADS) k_plan_transforms(const Prime* __
   }
 }
 
+// polyphase input weights zr[pi][r][t] = (1/S) y_t^-r z_t: the per-element
+// factor of the phase-r interpolation, tabled once per plan
+__global__ void k_plan_zr(const Prime* __restrict__ primes, InterpPlan plan) {
+  const int pi = blockIdx.y, r = blockIdx.z, S = plan.S, M = plan.N;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= M) return;
+  const Prime P = primes[pi];
+  const uint32_t invS = inv_mod((uint32_t)S % P.p, P);
+  const size_t o = (size_t)pi * M + t;
+  const uint32_t w = mul_mod(mul_mod(invS, pow_mod(plan.yqi[o], (uint64_t)r, P), P), plan.z[o], P);
+  const size_t q = ((size_t)pi * S + r) * M + t;
+  plan.zr[q] = w;
+  plan.zrc[q] = shoup_comp(w, P);
+}
+
 void launch_plan_ntt(const Prime* primes, const uint32_t* gens, const InterpPlan& plan, cudaStream_t st) {
+  if (plan.S > 1) k_plan_zr<<<dim3((plan.N + 127) / 128, plan.K, plan.S), 128, 0, st>>>(primes, plan);
   k_plan_twiddles<<<plan.K, NTT_THREADS, 0, st>>>(primes, gens, plan);
   const size_t smem = (size_t)plan.L * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_plan_transforms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -185,9 +201,11 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
   const uint32_t *Hf = plan.Hf + oL, *Hfc = plan.Hfc + oL, *Mf = plan.Mf + oL, *Mfc = plan.Mfc + oL;
   const uint32_t* om = plan.om + (size_t)pi * 4 * S;
   const uint32_t c = cval[pi];
-  // scalar (1/S) c^-r
-  uint32_t sc = inv_mod((uint32_t)S % p, P);
-  if (c != 1u) sc = mul_mod(sc, pow_mod(inv_mod(c, P), (uint64_t)r, P), P);
+  // c^-r (the shifted point set; 1 almost always)
+  const uint32_t cr = (c == 1u) ? 1u : pow_mod(inv_mod(c, P), (uint64_t)r, P);
+  const uint32_t crc = shoup_comp(cr, P);
+  const uint32_t* zr = plan.zr + ((size_t)pi * S + r) * M;
+  const uint32_t* zrc = plan.zrc + ((size_t)pi * S + r) * M;
   const uint32_t* v = values + (size_t)pi * M * S;
   // a'_s = P_r(z_t) * zweight_t with t = M-1-s
   for (int s = tid; s < L; s += T) {
@@ -200,9 +218,8 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
         const int k = (j * r) & (S - 1);
         g = add_mod(g, shoup(v[(size_t)t * S + j], om[2 * S + k], om[3 * S + k], p), p);
       }
-      uint32_t yr = mul_mod(sc, pow_mod(plan.yqi[oM + t], (uint64_t)r, P), P);  // (1/S) y_t^-r
-      g = mul_mod(g, yr, P);
-      a = shoup_lazy(g, plan.z[oM + t], plan.zc[oM + t], p);
+      if (c != 1u) g = shoup(g, cr, crc, p);
+      a = shoup_lazy(g, zr[t], zrc[t], p);  // (1/S) y_t^-r z_t
     }
     buf[s] = a;
   }

@@ -43,6 +43,8 @@ struct InterpPlan {
   uint32_t* Mf;       // [K][L]    DIF-NTT of M~_{u+1} (u < N); Mfc companions
   uint32_t* Mfc;
   uint32_t* Linv;     // [K]       1/L mod p
+  uint32_t* zr;       // [K][S][N] (1/S) y_t^-r z_t (polyphase plans), companions zrc
+  uint32_t* zrc;
 };
 // build every table of the plan: base tables (ckb_plan.cu), then twiddles and
 // the transforms of the two constant convolution operands (ckb_interp.cu)
