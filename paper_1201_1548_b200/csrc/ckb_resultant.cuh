@@ -111,12 +111,16 @@ __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_
   // outputs i < k are the new coefficients; i = k, k+1 held the old tail and
   // must become 0 (later sweeps read one entry past a degree), so chunks up to
   // index k+1 are written, but only entries below k are computed
+#ifndef CKB_SWEEP_CHUNK
+#define CKB_SWEEP_CHUNK 4
+#endif
+  constexpr int CW = CKB_SWEEP_CHUNK;  // entries per uniform guard
 #pragma unroll
-  for (int c = 0; c < (MAXD + 3) / 4; ++c) {
-    if (4 * c <= k + 1) {
+  for (int c = 0; c < (MAXD + CW - 1) / CW; ++c) {
+    if (CW * c <= k + 1) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = 4 * c + j;
+      for (int j = 0; j < CW; ++j) {
+        const int i = CW * c + j;
         if (i < MAXD - 1) {
           if (i < k) {
             // inputs < 4p < 2^32, multipliers < p: t < 12 p^2 < 2^64, result in (0, 4p)
