@@ -914,9 +914,17 @@ int ckb_dev_modular_images(const uint32_t* d_limbs, int C, int L, const int16_t*
   cudaStream_t st = pick_stream(stream);
   Prime* d_primes;
   if ((rc = get_primes_dev(primes, K, &d_primes))) return rc;
-  g.nsev = 0;
-  return modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, d_primes, primes, gens, K, N, d_coeffs, d_status,
-                       st);
+  std::vector<uint64_t> key = {3, (uint64_t)C, (uint64_t)L, (uint64_t)m, (uint64_t)n, (uint64_t)dfx, (uint64_t)dgx,
+                               (uint64_t)K, (uint64_t)N, (uint64_t)d_limbs, (uint64_t)d_degs, (uint64_t)d_coeffs,
+                               (uint64_t)d_status, (uint64_t)st, (uint64_t)d_primes};
+  key_push(key, h_degs, 2 * (size_t)(m + n + 2));
+  key_push(key, primes, 4 * (size_t)K);
+  key_push(key, gens, 4 * (size_t)K);
+  return graphed(key, st, [&]() -> int {
+    g.nsev = 0;
+    return modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, d_primes, primes, gens, K, N, d_coeffs,
+                         d_status, st);
+  });
 }
 
 int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, int LW, uint32_t* d_out,
@@ -930,10 +938,15 @@ int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, 
   if ((rc = get_crt(primes, K, LW, &ce))) return rc;
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
-  launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
-  g.launches += 2;
-  CK(cudaGetLastError());
-  return 0;
+  std::vector<uint64_t> key = {4, (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)d_coeffs, (uint64_t)d_out,
+                               (uint64_t)st};
+  key_push(key, primes, 4 * (size_t)K);
+  return graphed(key, st, [&]() -> int {
+    launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
+    g.launches += 3;
+    CK(cudaGetLastError());
+    return 0;
+  });
 }
 
 int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,

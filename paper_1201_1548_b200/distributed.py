@@ -78,13 +78,22 @@ class CudaBackend:
         self.device = device
         self.d_status = torch.zeros(1, dtype=torch.int32, device=device)
 
+    def buffer(self, name, shape):
+        """Device buffer reused across calls (stable addresses let the library
+        replay its captured CUDA graph); valid until the next call asks for it."""
+        cache = self.__dict__.setdefault("_bufs", {})
+        buf = cache.get(name)
+        if buf is None or tuple(buf.shape) != tuple(shape):
+            buf = self.torch.empty(shape, dtype=self.torch.int32, device=self.device)
+            cache[name] = buf
+        return buf
+
     def modular_images(self, primes, gens, N, stream):
-        torch = self.torch
         pk = self.packed
         K = len(primes)
         hp = np.array(primes, dtype=np.uint32)
         hg = np.array(gens, dtype=np.uint32)
-        out = torch.empty((K, N), dtype=torch.int32, device=self.device)
+        out = self.buffer("images_out", (K, N))
         self._lib.check(self.lib.ckb_dev_modular_images(
             self.d_limbs.data_ptr(), pk.C, pk.L, self.d_degs.data_ptr(), self._lib.ptr(self.h_degs), pk.m, pk.n,
             pk.dfx, pk.dgx, self._lib.ptr(hp), self._lib.ptr(hg), K, N, out.data_ptr(), self.d_status.data_ptr(),
@@ -92,9 +101,8 @@ class CudaBackend:
         return out
 
     def crt(self, coeffs, primes, N, LW, stream):
-        torch = self.torch
         hp = np.array(primes, dtype=np.uint32)
-        out = torch.empty((N, LW), dtype=torch.int32, device=self.device)
+        out = self.buffer("crt_out", (N, LW))
         self._lib.check(self.lib.ckb_dev_crt(coeffs.data_ptr(), len(primes), N, self._lib.ptr(hp), LW,
                                              out.data_ptr(), stream), "ckb_dev_crt")
         return out
@@ -107,7 +115,9 @@ def sharded_resultant_step(backend, plan: ShardPlan, rank: int, world: int, grou
     local = backend.modular_images(primes, gens, plan.N, stream)
     if world > 1:
         import torch
-        gathered = torch.empty((world * plan.per_rank, plan.N), dtype=local.dtype, device=local.device)
+        shape = (world * plan.per_rank, plan.N)
+        reuse = getattr(backend, "buffer", None)
+        gathered = reuse("gathered", shape) if reuse else torch.empty(shape, dtype=local.dtype, device=local.device)
         dist.all_gather_into_tensor(gathered, local.contiguous(), group=group)
     else:
         gathered = local
