@@ -323,3 +323,36 @@ def test_graph_replay_and_reallocation(mp):
         assert mp.biv_resultant(f2, g2, "y") == want2
         for f, g, r in small:
             assert mp.biv_resultant(f, g, "y") == r
+
+
+def test_sparse_structured_vs_oracle(mp, oracle_mod):
+    """Sparse inputs whose remainder sequences skip degrees at every point: all
+    images take the general (warp, _zp_resultant restatement) kernel."""
+    rng = random.Random(31)
+    cases = [
+        ({(0, 6): 1, (1, 3): 1, (2, 0): 1, (0, 0): 1}, {(0, 4): 1, (3, 1): 1, (0, 0): 2}),
+        ({(0, 8): 3, (2, 4): -5, (4, 0): 7}, {(0, 6): 1, (1, 2): 2, (5, 0): -1}),
+        ({(0, 5): 1, (3, 0): -1}, {(0, 3): 2, (1, 0): 1}),
+        ({(0, 10): 1, (1, 5): 1, (0, 0): -1}, {(0, 10): 2, (3, 0): 1}),
+    ]
+    for _ in range(6):  # random sparse: few terms, large gaps
+        f = {(rng.randint(0, 6), rng.randint(0, 9)): rng.randint(-2 ** 40, 2 ** 40) for _ in range(4)}
+        g = {(rng.randint(0, 6), rng.randint(0, 9)): rng.randint(-2 ** 40, 2 ** 40) for _ in range(4)}
+        f[(0, 9)] = 1
+        g[(0, 7)] = -3
+        cases.append(({k: v for k, v in f.items() if v}, {k: v for k, v in g.items() if v}))
+    for f, g in cases:
+        for var in ("y", "x"):
+            assert mp.biv_resultant(f, g, var) == oracle_mod.biv_resultant(f, g, var), (f, g, var)
+
+
+def test_degenerate_branches(mp):
+    # m = 0 or n = 0 (modpoly.py:363-369) and a zero resultant (common factor)
+    assert mp.biv_resultant({(2, 0): 3}, {(1, 0): 2}, "y") == [1]
+    assert mp.biv_resultant({(2, 0): 3, (0, 0): 1}, {(0, 2): 1, (1, 0): 1}, "y") == [1, 0, 6, 0, 9]
+    assert mp.biv_resultant({(0, 2): 1, (1, 0): 1}, {(1, 0): 2}, "y") == [0, 0, 4]
+    common = {(0, 1): 1, (1, 0): -1}
+    f = {(0, 2): 1, (1, 1): -1}            # y (y - x)
+    g = {(0, 1): 1, (1, 0): -1}  # y - x
+    assert mp.biv_resultant(f, g, "y") == []
+    assert mp.biv_resultant(common, common, "x") == []
