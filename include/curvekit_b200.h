@@ -39,6 +39,8 @@ unsigned long long ckb_launch_count(void);
  *   degs   [m+n+2] trimmed x-degree of each y-coefficient (-1 = zero)
  *   primes/gens [K] primes and a generator of large order for each
  *   N      evaluation points per prime (N > deg_x res)
+ *   any degrees: y-degrees up to 64 run the register kernel, larger ones (or
+ *          tables beyond its shared memory) the general warp kernel
  *   out    [N][LW] coefficients of res (low degree first), two's complement;
  *          requires prod(primes) > 2 * (coefficient bound) and 2^(32 LW) > prod
  *   status bit 0: some prime had no admissible point set (CKB_STATUS_REPLAN)
@@ -55,7 +57,7 @@ int ckb_reduce(const uint32_t* limbs, int C, int L, const uint32_t* primes, int 
 /* Batch of univariate resultants mod p — replaces _zp_resultant / zp_resultant_uni
  * (modpoly.py:132-161).  fa, gb [B][W] low-first residues (< p), da/db their
  * trimmed degrees (-1 = zero polynomial -> result 0), pidx [B] index into
- * primes [P].  W - 1 <= 64. */
+ * primes [P].  W <= 4096 (one warp per pair, operands in shared memory). */
 int ckb_uni_resultant_batch(const uint32_t* fa, const int32_t* da, const uint32_t* gb, const int32_t* db, int W,
                             const uint32_t* primes, int P, const int32_t* pidx, int B, uint32_t* out);
 

@@ -505,7 +505,6 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
                   int K, int N, uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st,
                   const CrtTables* crt = nullptr) {
   // with crt: the output rows are the explicit CRT's y = coeff (M/p_i)^-1 mod p_i
-  if (images_maxd(m, n) < 0) return fail("y-degree above 64 is not supported by the image kernel", -2);
   for (int i = 0; i < K; ++i)
     if (h_primes[i] >= (1u << 30)) return fail("pipeline primes must be below 2^30", -2);
   uint32_t *d_red, *d_vals, *d_cval;
@@ -514,13 +513,19 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   constexpr int S = 8;  // polyphase cosets (the images kernel's 8-lane groups)
   if ((rc = get_plan(h_primes, h_gens, K, N, S, &pl))) return rc;
   const int NI = S * pl.N;  // images per prime (>= N)
+  // y-degrees above the register kernel's buckets, or tables too large for its
+  // shared memory: every image goes through the general warp kernel
+  const bool general = !images_fast_ok(m, n, dfx, dgx, NI, K);
   if ((rc = dbuf("red", (size_t)K * C, &d_red))) return rc;
-  uint32_t* d_tab;
-  if ((rc = dbuf("tab", (size_t)K * images_tab_words(m, n, dfx, dgx), &d_tab))) return rc;
+  uint32_t* d_tab = nullptr;
+  if (!general && (rc = dbuf("tab", (size_t)K * images_tab_words(m, n, dfx, dgx), &d_tab))) return rc;
   if ((rc = dbuf("vals", (size_t)K * NI, &d_vals))) return rc;
   if ((rc = dbuf("cval", (size_t)K, &d_cval))) return rc;
   stage_mark(st);
-  launch_reduce_tab(d_limbs, C, L, d_primes, K, m, n, dfx, dgx, d_red, d_tab, st);
+  if (general)
+    launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
+  else
+    launch_reduce_tab(d_limbs, C, L, d_primes, K, m, n, dfx, dgx, d_red, d_tab, st);
   stage_mark(st);
   const int lcf_off = m * (dfx + 1), lcg_off = (m + 1) * (dfx + 1) + n * (dgx + 1);
   launch_choose_c(d_primes, pl, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], d_cval, d_status, st);
@@ -545,8 +550,12 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   a.status = d_status;
   if ((rc = dbuf("fail", (size_t)K * NI + 1, &a.fail_list))) return rc;
   a.fail_count = a.fail_list + (size_t)K * NI;
-  CK(cudaMemsetAsync(a.fail_count, 0, 4, st));
-  launch_images(a, st);
+  if (general) {
+    launch_images_general(a, st);
+  } else {
+    CK(cudaMemsetAsync(a.fail_count, 0, 4, st));
+    launch_images(a, st);
+  }
   stage_mark(st);
   launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr);
   stage_mark(st);
@@ -718,7 +727,7 @@ int ckb_uni_resultant_batch(const uint32_t* fa, const int32_t* da, const uint32_
   int rc;
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, P))) return rc;
-  if (W < 1 || images_maxd(W - 1, 0) < 0) return fail("ckb_uni_resultant_batch: degree above 64", -2);
+  if (W < 1 || W > 4096) return fail("ckb_uni_resultant_batch: need 1 <= W <= 4096", -2);
   if (B == 0) return 0;
   cudaStream_t st = g.stream;
   uint32_t *d_fa, *d_gb, *d_out;

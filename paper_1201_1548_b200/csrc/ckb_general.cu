@@ -106,6 +106,20 @@ void launch_images_fallback(const ImageArgs& a, cudaStream_t st) {
   k_images_fallback<<<4 * 148, 32, (size_t)3 * W * 4, st>>>(a, W);
 }
 
+__global__ void k_iota(uint32_t* list, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) list[i] = i;
+  if (i == 0) list[n] = n;  // the count slot follows the list
+}
+
+// shapes beyond the register kernel: the general kernel over every image
+void launch_images_general(const ImageArgs& a, cudaStream_t st) {
+  const uint32_t n = (uint32_t)a.K * (uint32_t)a.N;
+  k_iota<<<(n + 255) / 256, 256, 0, st>>>(a.fail_list, n);
+  const int W = (a.m > a.n ? a.m : a.n) + 2;
+  k_images_fallback<<<32 * 148, 32, (size_t)3 * W * 4, st>>>(a, W);
+}
+
 // batched zp_resultant_uni: one warp per pair
 __global__ void k_uni_resultant(const uint32_t* __restrict__ fa, const int32_t* __restrict__ da,
                                 const uint32_t* __restrict__ gb, const int32_t* __restrict__ db, int W,

@@ -256,6 +256,19 @@ int images_maxd(int m, int n) {
   return -1;
 }
 
+static size_t images_smem_bytes(int maxd, int dfx, int dgx, int NI, int K) {
+  const int dmax = dfx > dgx ? dfx : dgx;
+  const int rows = POLY * (dmax / POLY + 1);
+  int span = (IMG_THREADS - 1 + NI - 1) / NI + 1;
+  if (span > K) span = K;
+  return (size_t)(span * (2 * rows * images_sw(maxd) + 2 * POLY) + 2 * rows) * 4;
+}
+
+bool images_fast_ok(int m, int n, int dfx, int dgx, int NI, int K) {
+  const int maxd = images_maxd(m, n);
+  return maxd > 0 && images_smem_bytes(maxd, dfx, dgx, NI, K) <= 200 * 1024;
+}
+
 void launch_images(const ImageArgs& a, cudaStream_t st) {
   const int maxd = images_maxd(a.m, a.n);
   dim3 grid((unsigned)(((size_t)a.K * a.N + IMG_THREADS - 1) / IMG_THREADS));

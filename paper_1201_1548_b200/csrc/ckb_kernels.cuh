@@ -74,6 +74,10 @@ struct ImageArgs {
   int span;                // set by launch_images: max primes one CTA's images touch
 };
 int images_maxd(int m, int n);  // template bucket or -1
+// whether the register kernel handles this shape (bucket exists, tables fit in shared memory)
+bool images_fast_ok(int m, int n, int dfx, int dgx, int NI, int K);
+// every image through the general warp kernel (any degree)
+void launch_images_general(const ImageArgs& a, cudaStream_t st);
 // K1 for the pipeline: residues straight into the images kernel's transposed,
 // top-aligned, zero-padded table layout (and the plain [K][C] layout)
 size_t images_tab_words(int m, int n, int dfx, int dgx);

@@ -171,8 +171,8 @@ def zp_resultant_batch(triples) -> list:
     A = [_trim([x % p for x in a]) for a, _, p in triples]
     Bb = [_trim([x % p for x in b]) for _, b, p in triples]
     W = max(1, max(max(len(a), len(b)) for a, b in zip(A, Bb)))
-    if W - 1 > 64:
-        raise NotImplementedError("univariate resultant kernel supports degree <= 64")
+    if W > 4096:
+        raise NotImplementedError("univariate resultant kernel supports degree < 4096")
     fa = np.zeros((B, W), dtype=np.uint32)
     gb = np.zeros((B, W), dtype=np.uint32)
     for i, (a, b) in enumerate(zip(A, Bb)):
@@ -496,8 +496,6 @@ def biv_resultant(f, g, var: str = "y", seed: int = 0) -> list:
 def _biv_resultant_gpu(fc, gc, tdf: int, tdg: int):
     lib = _lib.lib()
     m, n = len(fc) - 1, len(gc) - 1
-    if max(m, n) > 64:
-        raise NotImplementedError("the image kernel supports y-degrees up to 64")
     packed = pack_grid(fc, gc)
     start = 0
     for _attempt in range(4):

@@ -356,3 +356,22 @@ def test_degenerate_branches(mp):
     g = {(0, 1): 1, (1, 0): -1}  # y - x
     assert mp.biv_resultant(f, g, "y") == []
     assert mp.biv_resultant(common, common, "x") == []
+
+
+def test_high_y_degree_general_path(mp, oracle_mod):
+    """y-degrees beyond the register kernel's buckets (> 64) run every image
+    through the general warp kernel; large univariate resultants likewise."""
+    rng = random.Random(41)
+    f = {(0, 70): 1, (1, 35): rng.randint(-99, 99), (3, 0): rng.randint(1, 99), (0, 12): -5}
+    g = {(0, 66): 3, (2, 1): rng.randint(-99, 99), (0, 0): 7}
+    assert mp.biv_resultant(f, g, "y") == oracle_mod.biv_resultant(f, g, "y")
+    # x-degree 80 as the resultant variable's partner: res_x swaps the roles
+    h = {(80, 0): 1, (0, 2): 1, (7, 1): -2}
+    k = {(75, 0): 2, (0, 1): 1, (1, 0): 1}
+    assert mp.biv_resultant(h, k, "x") == oracle_mod.biv_resultant(h, k, "x")
+    p = oracle_mod.prime_table()[0]
+    a = [rng.randrange(p) for _ in range(150)]
+    b = [rng.randrange(p) for _ in range(121)]
+    a[-1] = a[-1] or 1
+    b[-1] = b[-1] or 1
+    assert mp.zp_resultant_uni(mp.ModPoly.make(a, p), mp.ModPoly.make(b, p)) == oracle_mod.zp_resultant(a, b, p)
