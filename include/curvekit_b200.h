@@ -83,7 +83,7 @@ int ckb_gcd_mod_batch(const uint32_t* fa, const int32_t* da, int Wf, const uint3
 
 /* Interpolation at arbitrary distinct points — replaces _zp_interp /
  * zp_interpolate (modpoly.py:164-189).  xs, vs [B][W] (points reduced mod p),
- * ns [B] point counts (<= W <= 4096) -> out [B][W] coefficients (low first). */
+ * ns [B] point counts (<= W <= 12288) -> out [B][W] coefficients (low first). */
 int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const uint32_t* primes, int P,
                       const int32_t* pidx, int B, uint32_t* out);
 

@@ -856,7 +856,7 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, P))) return rc;
   if (B == 0) return 0;
-  if (W > 4096) return fail("ckb_interp_points: at most 4096 points", -2);
+  if (W > 12288) return fail("ckb_interp_points: at most 12288 points", -2);
   cudaStream_t st = g.stream;
   uint32_t *d_xs, *d_vs, *d_out;
   int32_t *d_ns, *d_pi;

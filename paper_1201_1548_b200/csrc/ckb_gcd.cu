@@ -114,17 +114,30 @@ __global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* _
     c[i] = vs[(size_t)b * W + i];
   }
   __syncthreads();
-  // for j in 1..n-1: for i = n-1 .. j: c[i] = (c[i] - c[i-1]) / (x[i] - x[i-j])
+  // for j in 1..n-1: for i = n-1 .. j: c[i] = (c[i] - c[i-1]) / (x[i] - x[i-j]).
+  // The reference takes one Fermat inverse per entry (modpoly.py:172-178); here
+  // each thread inverts the denominators of its strided entries of a row at
+  // once (Montgomery's trick: running products in o2, one inverse, a backward
+  // pass), so a row costs T inverses instead of n - j.
   for (int j = 1; j < n; ++j) {
-    uint32_t nv[16];
-    int cnt = 0;
-    for (int i = j + tid; i < n && cnt < 16; i += T, ++cnt) {
-      const uint32_t d = sub_mod(x[i], x[i - j], p);
-      nv[cnt] = mul_mod(sub_mod(c[i], c[i - 1], p), inv_mod(d, P), P);
+    int last = -1;
+    uint32_t run = 1u;
+    for (int i = j + tid; i < n; i += T) {
+      run = mul_mod(run, sub_mod(x[i], x[i - j], p), P);
+      o2[i] = run;  // prefix product of this thread's denominators
+      last = i;
+    }
+    if (last >= 0) {
+      uint32_t inv = inv_mod(run, P);
+      for (int i = last; i >= j; i -= T) {
+        const uint32_t d = sub_mod(x[i], x[i - j], p);
+        const uint32_t invd = (i - T >= j) ? mul_mod(inv, o2[i - T], P) : inv;  // 1/d_i
+        inv = mul_mod(inv, d, P);
+        o2[i] = mul_mod(sub_mod(c[i], c[i - 1], p), invd, P);
+      }
     }
     __syncthreads();
-    cnt = 0;
-    for (int i = j + tid; i < n && cnt < 16; i += T, ++cnt) c[i] = nv[cnt];
+    for (int i = j + tid; i < n; i += T) c[i] = o2[i];
     __syncthreads();
   }
   // out = 0; for i = n-1 .. 0: out = out * (x - x_i) + c_i

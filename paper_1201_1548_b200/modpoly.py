@@ -210,8 +210,8 @@ def zp_interpolate_batch(problems) -> list:
             raise ValueError("duplicate interpolation points")
     B = len(problems)
     W = max(1, max(len(pts) for pts, _, _ in problems))
-    if W > 4096:
-        raise NotImplementedError("at most 4096 points per interpolation problem")
+    if W > 12288:
+        raise NotImplementedError("at most 12288 points per interpolation problem")
     xs = np.zeros((B, W), dtype=np.uint32)
     vs = np.zeros((B, W), dtype=np.uint32)
     ns = np.zeros(B, dtype=np.int32)

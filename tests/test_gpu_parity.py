@@ -375,3 +375,23 @@ def test_high_y_degree_general_path(mp, oracle_mod):
     a[-1] = a[-1] or 1
     b[-1] = b[-1] or 1
     assert mp.zp_resultant_uni(mp.ModPoly.make(a, p), mp.ModPoly.make(b, p)) == oracle_mod.zp_resultant(a, b, p)
+
+
+def test_interpolate_large_batch(mp):
+    """Newton interpolation with batched inverses: 5,000 points and a batch of
+    mixed sizes, checked by evaluating the result back at the points."""
+    from paper_1201_1548_b200.primes30 import PRIMES30
+    rng = random.Random(8)
+    probs = []
+    for n, p in ((5000, PRIMES30[3][0]), (1, 1000003), (2, 7), (300, 2147483647), (1500, PRIMES30[9][0])):
+        pts = rng.sample(range(p), n)
+        vals = [rng.randrange(p) for _ in range(n)]
+        probs.append((pts, vals, p))
+    outs = mp.zp_interpolate_batch(probs)
+    for (pts, vals, p), co in zip(probs, outs):
+        assert len(co) <= len(pts)
+        for x, v in zip(pts[:200], vals[:200]):
+            acc = 0
+            for c in reversed(co):
+                acc = (acc * x + c) % p
+            assert acc == v
