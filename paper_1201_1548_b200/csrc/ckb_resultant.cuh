@@ -53,19 +53,8 @@ __device__ __forceinline__ uint32_t comp_from_mont(uint32_t wm, const Prime& P) 
 // 64 bits (IMAD.WIDE chain), one signed Montgomery reduction (+p keeps it positive)
 __device__ __forceinline__ uint32_t mont3(uint32_t x, uint32_t a, uint32_t y, uint32_t b, uint32_t z, uint32_t c,
                                           uint32_t pinv, uint32_t p) {
-#ifdef CKB_PTX_MONT3
-  uint32_t r;
-  asm("{\n .reg .u64 t;\n .reg .u32 lo, hi, m, q;\n"
-      " mul.wide.u32 t, %1, %2;\n mad.wide.u32 t, %3, %4, t;\n mad.wide.u32 t, %5, %6, t;\n"
-      " mov.b64 {lo, hi}, t;\n mul.lo.u32 m, lo, %7;\n mul.hi.u32 q, m, %8;\n"
-      " sub.u32 hi, hi, q;\n add.u32 %0, hi, %8;\n}\n"
-      : "=r"(r)
-      : "r"(x), "r"(a), "r"(y), "r"(b), "r"(z), "r"(c), "r"(pinv), "r"(p));
-  return r;
-#else
   const uint64_t t = (uint64_t)x * a + (uint64_t)y * b + (uint64_t)z * c;
   return (uint32_t)(t >> 32) - __umulhi((uint32_t)t * pinv, p) + p;
-#endif
 }
 
 // single division-free step D <- lb D - lc(D) V (aligned tops); nom = nominal deg D
