@@ -160,6 +160,8 @@ int upload_primes(const uint32_t* primes, int K, Prime** d_out) {
 }
 
 int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
+  // the u8 tensor-core product accumulates 4K * 255^2 per s32 entry
+  if (K > 8192) return fail("CRT over more than 8192 primes is not supported (s32 accumulation bound)", -2);
   for (auto& e : g.crt) {
     if ((int)e.primes.size() == K && e.LW == LW && !memcmp(e.primes.data(), primes, 4 * (size_t)K)) {
       e.last_use = ++g.tick;
