@@ -96,6 +96,20 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
 int ckb_psc_values(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
                    const int16_t* gdeg, int n, int dgx, uint32_t p, int ncand, uint32_t* out, uint8_t* valid);
 
+/* Descartes test of real-root isolation — replaces upoly._variations_on
+ * (pkg/src/curvekit/upoly.py:338-346; compose_linear :202-212, taylor_shift
+ * :193-199, sign_variations :215-224), the inner loop of descartes_isolate
+ * (:358-408).  prepare: the polynomial's limbs [n+1][L] (low degree first) and
+ * K primes (< 2^30, 1 mod the NTT length 2^ceil(log2(2n+1)), e.g. PRIMES30) with
+ * generators; returns a handle >= 0.  variations: aw = [a limbs][w limbs] (AL
+ * words each, unsigned) of the numerators a = a_num, w = b_num - a_num, ld = the
+ * common log2 denominator; uses the first K primes of the handle (their product
+ * must exceed 4x the coefficient bound of the shifted polynomial) and writes the
+ * exact sign-variation count of taylor_shift(reversed(compose_linear(p, a, w, ld)), 1). */
+int ckb_descartes_prepare(const uint32_t* limbs, int n, int L, const uint32_t* primes, const uint32_t* gens, int K);
+int ckb_descartes_variations(int handle, const uint32_t* aw, int AL, int ld, int K, int LW, int32_t* variations);
+int ckb_descartes_release(int handle);
+
 /* Device-pointer stages for the multi-GPU driver (one process per GPU); primes
  * and gens are HOST arrays (they key the cached interpolation plan).
  * stream: a cudaStream_t or NULL for the context stream.

@@ -16,6 +16,8 @@ def install():
     ``curvekit.bisolve`` bound at import (bisolve.py:26).  ``upoly`` and
     ``bivpoly`` import ``int_gcd_uni`` lazily (upoly.py:258,372,538,569;
     bivpoly.py:186,268), so they pick up the GPU gcd through the first rebinding.
+    Also rebinds ``curvekit.upoly._variations_on`` (the Descartes test of
+    descartes_isolate, upoly.py:338-346) to the GPU version.
     Returns the previous bindings (pass them to ``uninstall``).
     """
     import importlib
@@ -27,6 +29,12 @@ def install():
                  "zp_gcd_sylvester", "crt_reconstruct", "modular_subres_profile"):
         saved[("curvekit.modpoly", name)] = getattr(ref, name)
         setattr(ref, name, getattr(ours, name))
+    # the Descartes test of real-root isolation (upoly.py:338-346), looked up
+    # by descartes_isolate at call time
+    up = importlib.import_module("curvekit.upoly")
+    from . import upoly as our_upoly
+    saved[("curvekit.upoly", "_variations_on")] = getattr(up, "_variations_on")
+    setattr(up, "_variations_on", our_upoly.variations_on)
     try:
         bis = importlib.import_module("curvekit.bisolve")
     except ImportError:  # bisolve needs mpmath

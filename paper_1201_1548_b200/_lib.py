@@ -22,6 +22,7 @@ EXPORTS = (
     "ckb_interp_geometric", "ckb_crt_lift", "ckb_dev_modular_images", "ckb_dev_crt",
     "ckb_interp_points", "ckb_gcd_mod_batch", "ckb_dev_biv_resultant", "ckb_set_timing",
     "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values", "ckb_host_alloc", "ckb_host_free",
+    "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release",
 )
 
 _P = ctypes.c_void_p
@@ -52,6 +53,9 @@ _SIGS = {
     "ckb_psc_values": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, ctypes.c_uint32, _I, _P, _P]),
     "ckb_host_alloc": (_P, [ctypes.c_ulonglong]),
     "ckb_host_free": (_I, [_P]),
+    "ckb_descartes_prepare": (_I, [_P, _I, _I, _P, _P, _I]),
+    "ckb_descartes_variations": (_I, [_I, _P, _I, _I, _I, _I, _P]),
+    "ckb_descartes_release": (_I, [_I]),
 }
 
 _lock = threading.Lock()

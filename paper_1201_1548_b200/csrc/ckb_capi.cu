@@ -73,6 +73,20 @@ struct Ctx {
 Ctx g;
 std::mutex g_mu;
 
+// ---- Descartes sign-variation test ------------------------------------------
+// A handle holds one polynomial's residues modulo a prefix of PRIMES30-style
+// primes and the per-(primes, n) plan; each test then needs only the interval.
+struct DescHandle {
+  bool used = false;
+  int n = 0, K = 0;
+  std::vector<uint32_t> primes, gens;
+  void* blob = nullptr;  // residues [K][n+1] then the plan tables
+  DescPlan pl;
+  uint32_t* d_res = nullptr;
+  Prime* d_primes = nullptr;
+};
+std::vector<DescHandle> g_desc;
+
 int dev_buf(const char* name, size_t bytes, void** out) {
   Buf& b = g.dev[name];
   if (b.n < bytes) {
@@ -604,6 +618,9 @@ int ckb_shutdown(void) {
   cudaStreamSynchronize(g.stream);
   drop_graphs();
   ++g.epoch;
+  for (auto& d : g_desc)
+    if (d.blob) cudaFree(d.blob);
+  g_desc.clear();
   for (auto& kv : g.dev) cudaFree(kv.second.p);
   for (auto& kv : g.host) cudaFreeHost(kv.second.p);
   for (auto& e : g.crt) {
@@ -993,6 +1010,113 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
     CK(cudaGetLastError());
     return 0;
   });
+}
+
+
+int ckb_descartes_prepare(const uint32_t* limbs, int n, int L, const uint32_t* primes, const uint32_t* gens, int K) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if (n < 1 || n > 8191 || L < 1 || K < 1 || K > 8192) return fail("ckb_descartes_prepare: bad sizes", -2);
+  if ((rc = check_primes(primes, K))) return rc;
+  int logL = 0;
+  while ((1 << logL) < 2 * n + 1) ++logL;
+  for (int i = 0; i < K; ++i)
+    if (primes[i] >= (1u << 30) || (primes[i] - 1) % (1u << logL))
+      return fail("ckb_descartes_prepare: primes must be < 2^30 and 1 mod the NTT length (PRIMES30)", -2);
+  int h = -1;
+  for (size_t i = 0; i < g_desc.size(); ++i)
+    if (!g_desc[i].used) h = (int)i;
+  if (h < 0) {
+    if (g_desc.size() >= 64) return fail("ckb_descartes_prepare: too many live handles", -2);
+    g_desc.emplace_back();
+    h = (int)g_desc.size() - 1;
+  }
+  DescHandle& d = g_desc[h];
+  d.used = true;
+  d.n = n;
+  d.K = K;
+  d.primes.assign(primes, primes + K);
+  d.gens.assign(gens, gens + K);
+  const int Lt = 1 << logL;
+  const size_t n1 = (size_t)n + 1, kh = (size_t)K * (Lt / 2), kl = (size_t)K * Lt;
+  const size_t words = (size_t)K * n1 * 3 + kh * 4 + kl * 2 + (size_t)K * 5 + 64;
+  CK(cudaMalloc(&d.blob, 4 * words));
+  uint32_t* b = (uint32_t*)d.blob;
+  auto take = [&](size_t m) { uint32_t* r = b; b += m; return r; };
+  d.d_res = take((size_t)K * n1);
+  DescPlan& pl = d.pl;
+  pl.K = K;
+  pl.n = n;
+  pl.L = Lt;
+  pl.logL = logL;
+  pl.fact = take((size_t)K * n1);
+  pl.ifact = take((size_t)K * n1);
+  pl.W = take(kh);
+  pl.Wc = take(kh);
+  pl.Wi = take(kh);
+  pl.Wic = take(kh);
+  pl.Vf = take(kl);
+  pl.Vfc = take(kl);
+  pl.Linv = take(K);
+  uint32_t* d_gens = take(K);
+  d.d_primes = reinterpret_cast<Prime*>(take((size_t)K * 3));
+  std::vector<Prime> hp(K);
+  for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
+  cudaStream_t st = g.stream;
+  CK(cudaMemcpyAsync(d.d_primes, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_gens, gens, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
+  uint32_t* d_limbs;
+  if ((rc = dbuf("desc.limbs", n1 * L, &d_limbs))) return rc;
+  CK(cudaMemcpyAsync(d_limbs, limbs, 4 * n1 * L, cudaMemcpyHostToDevice, st));
+  launch_reduce(d_limbs, (int)n1, L, d.d_primes, K, d.d_res, st);
+  launch_desc_plan(d.d_primes, d_gens, pl, st);
+  g.launches += 2;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  return h;
+}
+
+int ckb_descartes_variations(int handle, const uint32_t* aw, int AL, int ld, int K, int LW, int32_t* variations) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if (handle < 0 || handle >= (int)g_desc.size() || !g_desc[handle].used)
+    return fail("ckb_descartes_variations: bad handle", -2);
+  DescHandle& d = g_desc[handle];
+  if (K < 1 || K > d.K || AL < 1 || ld < 0 || LW < 1) return fail("ckb_descartes_variations: bad sizes", -2);
+  cudaStream_t st = g.stream;
+  const int N = d.n + 1;
+  CrtEntry* ce;
+  if ((rc = get_crt(d.primes.data(), K, LW, &ce))) return rc;
+  uint32_t *d_aw, *d_c, *d_out, *d_crtS;
+  int32_t* d_v;
+  if ((rc = dbuf("desc.aw", 2 * (size_t)AL, &d_aw))) return rc;
+  if ((rc = dbuf("desc.c", (size_t)K * N, &d_c))) return rc;
+  if ((rc = dbuf("desc.out", (size_t)N * LW, &d_out))) return rc;
+  if ((rc = dbuf("desc.v", 1, &d_v))) return rc;
+  if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
+  CK(cudaMemcpyAsync(d_aw, aw, 8 * (size_t)AL, cudaMemcpyHostToDevice, st));
+  DescPlan pl = d.pl;
+  pl.K = K;  // the first K primes of the prepared set
+  launch_desc_shift(d.d_primes, pl, d.d_res, d_aw, AL, ld, d_c, st);
+  launch_crt(ce->t, d_c, N, d_out, d_crtS, st);
+  launch_desc_signs(d_out, N, LW, d_v, st);
+  g.launches += 5;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(variations, d_v, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ckb_descartes_release(int handle) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (handle < 0 || handle >= (int)g_desc.size() || !g_desc[handle].used) return 0;
+  DescHandle& d = g_desc[handle];
+  cudaStreamSynchronize(g.stream);
+  cudaFree(d.blob);
+  d = DescHandle();
+  return 0;
 }
 
 void* ckb_host_alloc(unsigned long long bytes) {

@@ -121,6 +121,19 @@ __host__ __device__ __forceinline__ size_t crt_a_word(int i, int n, int KC) {
   return tile * 4096 + ((n & 127) >> 3) * 256 + ((i & 31) >> 2) * 32 + (n & 7) * 4 + (i & 3);
 }
 inline size_t crt_a_words(int K, int N) { return (size_t)((N + 127) / 128) * ((K + 31) / 32) * 4096; }
+// ---- Descartes sign-variation test (ckb_descartes.cu) -----------------------
+struct DescPlan {
+  int K, n, L, logL;       // primes, degree, NTT length >= 2n+1
+  uint32_t *fact, *ifact;  // [K][n+1] i! and 1/i! mod p
+  uint32_t *W, *Wc, *Wi, *Wic;  // [K][L/2] twiddles and companions
+  uint32_t *Vf, *Vfc;      // [K][L] DIF of (1/0!, ..., 1/n!, 0, ...) and companions
+  uint32_t* Linv;          // [K] 1/L
+};
+void launch_desc_plan(const Prime* primes, const uint32_t* gens, const DescPlan& pl, cudaStream_t st);
+void launch_desc_shift(const Prime* primes, const DescPlan& pl, const uint32_t* res, const uint32_t* aw, int AL,
+                       int ld, uint32_t* out, cudaStream_t st);
+void launch_desc_signs(const uint32_t* limbs, int N, int LW, int32_t* result, cudaStream_t st);
+
 // tensor-core CRT product (ckb_crt_mma.cu): byte table size / builder, and the
 // GEMM y (A layout) -> S [N][32 ceil(LW/32)] u64 limb sums
 size_t crt_btable_bytes(int K, int LW);

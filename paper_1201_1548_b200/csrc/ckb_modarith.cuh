@@ -90,6 +90,28 @@ __device__ __forceinline__ uint32_t mod_word(uint32_t x, uint32_t one_comp, uint
   return shoup(x, 1u, one_comp, p);
 }
 
+// per-prime constants of limbs_mod: 2^32 mod p and companions, 2^(32 L) mod p
+struct LimbModConst {
+  uint32_t R1, R1c, onec, big;
+};
+__device__ __forceinline__ LimbModConst limbs_mod_const(int L, const Prime& P) {
+  LimbModConst k;
+  const uint32_t p = P.p;
+  k.R1 = redc(P.r2, P);
+  k.R1c = shoup_comp(k.R1, P);
+  k.onec = shoup_comp(1u % p, P);
+  uint32_t big = 1u % p;
+  for (int l = 0; l < L; ++l) big = shoup(big, k.R1, k.R1c, p);
+  k.big = big;
+  return k;
+}
+// residue of an UNSIGNED integer of L little-endian 32-bit limbs
+__device__ __forceinline__ uint32_t limbs_mod_k(const uint32_t* w, int L, uint32_t p, const LimbModConst& k) {
+  uint32_t r = 0;
+  for (int l = L - 1; l >= 0; --l) r = add_mod(shoup(r, k.R1, k.R1c, p), mod_word(w[l], k.onec, p), p);
+  return r;
+}
+
 // residue mod p of a two's-complement integer of L little-endian 32-bit limbs
 __device__ __forceinline__ uint32_t limbs_mod(const uint32_t* w, int L, const Prime& P) {
   const uint32_t p = P.p;

@@ -137,3 +137,100 @@ def squarefree_decompose(p, gcd_fn=None) -> SquareFreeDecomposition:
         v, u = _frac_div(v, h), _frac_div(d, h)
         i += 1
     return SquareFreeDecomposition(tuple(factors), cont)
+
+
+# ---------------------------------------------------------------------------
+# Descartes test of real-root isolation on the GPU
+# ---------------------------------------------------------------------------
+
+class _DescHandles:
+    """Per-polynomial device state (residues + plan), keyed by the list object
+    descartes_isolate passes to every test of one isolation (upoly.py:387-405)."""
+
+    def __init__(self, size: int = 8):
+        self.size = size
+        self.entries = []  # [poly list, snapshot, handle, K]
+
+    def get(self, p, n: int, K: int):
+        from . import _lib
+        from .planner import ints_to_limbs
+        from .primes30 import PRIMES30
+        import numpy as np
+        snap = (len(p), p[0], p[-1], p[len(p) // 2])
+        for e in self.entries:
+            if e[0] is p and e[1] == snap and e[3] >= K:
+                return e[2], e[3]
+        # (re)prepare with headroom: deeper subdivisions need more primes
+        Kp = min(len(PRIMES30), max(256, 2 * K))
+        lib = _lib.lib()
+        limbs, L = ints_to_limbs(p[:n + 1])
+        primes = np.array([q for q, _ in PRIMES30[:Kp]], dtype=np.uint32)
+        gens = np.array([g for _, g in PRIMES30[:Kp]], dtype=np.uint32)
+        h = _lib.check(lib.ckb_descartes_prepare(_lib.ptr(limbs), n, L, _lib.ptr(primes), _lib.ptr(gens), Kp),
+                       "ckb_descartes_prepare")
+        for e in [e for e in self.entries if e[0] is p]:
+            lib.ckb_descartes_release(e[2])
+            self.entries.remove(e)
+        self.entries.insert(0, [p, snap, h, Kp])
+        while len(self.entries) > self.size:
+            lib.ckb_descartes_release(self.entries.pop()[2])
+        return h, Kp
+
+
+_desc = _DescHandles()
+_log2_prefix = None
+
+
+def _primes_for_bits(bits: float) -> int:
+    """Fewest PRIMES30 (in order) whose product exceeds 2^bits, rounded up to 64."""
+    global _log2_prefix
+    from .primes30 import PRIMES30
+    if _log2_prefix is None:
+        acc, pre = 0.0, []
+        for q, _ in PRIMES30:
+            acc += math.log2(q)
+            pre.append(acc)
+        _log2_prefix = pre
+    import bisect
+    k = bisect.bisect_right(_log2_prefix, bits) + 1
+    k = -(-k // 64) * 64
+    if k > min(len(_log2_prefix), 8192):
+        raise NotImplementedError("Descartes test needs more than 8192 primes")
+    return k
+
+
+def variations_on(p, a, b) -> int:
+    """Sign-variation bound for the roots of p in (a, b) — upoly._variations_on
+    (pkg/src/curvekit/upoly.py:338-346) on the GPU; a, b are dyadics (man, exp).
+
+    Exact: the coefficients of taylor_shift(reversed(compose_linear(p, ...)), 1)
+    are computed modulo enough primes for their a-priori bound and lifted by the
+    CRT before their signs are counted, so the result is the reference's.
+    """
+    from . import _lib
+    from .planner import ints_to_limbs
+    import numpy as np
+    e = min(a.exp, b.exp, 0)
+    a_num = a.man << (a.exp - e)
+    b_num = b.man << (b.exp - e)
+    w = b_num - a_num
+    ld = -e
+    n = len(p) - 1
+    while n >= 0 and p[n] == 0:
+        n -= 1
+    if n < 1:
+        return 0  # compose_linear of a constant has one coefficient: no variation
+    if n > 8191:
+        raise NotImplementedError("Descartes test supports degree < 8192")
+    # |c|_inf <= 2^n |r|_1 <= 2^n sum_i |p_i| 2^(ld (n-i)) (|a| + |w|)^i   (bit-length bounds)
+    t = (abs(a_num) + abs(w)).bit_length()
+    top = max(abs(p[i]).bit_length() + ld * (n - i) + i * t for i in range(n + 1) if p[i])
+    bits = top + math.log2(n + 1) + n + 4  # M > 4 * bound for the explicit CRT
+    K = _primes_for_bits(bits)
+    h, _ = _desc.get(p, n, K)
+    LW = (int(_log2_prefix[K - 1]) + 1 + 1 + 31) // 32 + 1
+    aw, AL = ints_to_limbs([a_num, w])
+    v = np.zeros(1, dtype=np.int32)
+    lib = _lib.lib()
+    _lib.check(lib.ckb_descartes_variations(h, _lib.ptr(aw), AL, ld, K, LW, _lib.ptr(v)), "ckb_descartes_variations")
+    return int(v[0])

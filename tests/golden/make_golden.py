@@ -9,6 +9,7 @@ that the GPU box, where /root/reference does not exist, can check parity.
     python tests/golden/make_golden.py cfg2       # ~3 min
     python tests/golden/make_golden.py cfg3       # ~12 min (+ Yun, gcd, profile)
     python tests/golden/make_golden.py cfg4prime  # ~1 min (one prime of cfg4)
+    python tests/golden/make_golden.py descartes  # Descartes tests of real-root isolation
 
 Every fixture records which reference function produced it (file:line).
 """
@@ -399,6 +400,66 @@ def gen_cfg4prime():
     dump("cfg4_prime0", obj, gz=True)
 
 
+def gen_descartes():
+    """The Descartes test of real-root isolation, upoly._variations_on (upoly.py:338-346):
+    every (polynomial, interval) a reference isolation visits, recorded with its count,
+    plus the reference's isolating intervals (descartes_isolate, upoly.py:358-408)."""
+    from curvekit.dyadic import Dyadic
+    rng = random.Random(61)
+    polys = []
+    # resultants of small curves (what Bisolve isolates) and random square-free polynomials
+    for seed in range(3):
+        f, g = make_pair("cfg1", seed)
+        r = M.biv_resultant(BivPoly(f), BivPoly(g), "y")
+        polys.append(("cfg1_seed%d_res_y" % seed, upoly.primitive(r)))
+    for deg in (5, 17, 40, 90):
+        for k in range(2):
+            p = [rng.randint(-2 ** 40, 2 ** 40) for _ in range(deg + 1)]
+            p[-1] = p[-1] or 1
+            polys.append(("random_deg%d_%d" % (deg, k), p))
+    f, g = make_pair("cfg2", 0)
+    polys.append(("cfg2_res_y", upoly.primitive(M.biv_resultant(BivPoly(f), BivPoly(g), "y"))))
+    cases, isol = [], []
+    orig = upoly._variations_on
+    for name, p in polys:
+        if upoly.degree(M.int_gcd_uni(p, upoly.derivative(p))) > 0:
+            continue
+        seen = []
+
+        def rec(q, a, b, _seen=seen):
+            v = orig(q, a, b)
+            _seen.append((a.man, a.exp, b.man, b.exp, v))
+            return v
+        upoly._variations_on = rec
+        t0 = time.time()
+        try:
+            roots = upoly.descartes_isolate(p)
+        finally:
+            upoly._variations_on = orig
+        dt = time.time() - t0
+        isol.append({"name": name, "p": ints_out(p), "seconds": dt, "tests": len(seen),
+                     "roots": [[str(r.interval.lo.man), r.interval.lo.exp, str(r.interval.hi.man), r.interval.hi.exp]
+                               for r in roots]})
+        step = max(1, len(seen) // 40)
+        for (am, ae, bm, be, v) in seen[::step]:
+            cases.append({"name": name, "am": str(am), "ae": ae, "bm": str(bm), "be": be, "v": v})
+        print(name, "deg", upoly.degree(p), "tests", len(seen), "roots", len(roots), "%.1f s" % dt)
+    for _ in range(60):  # arbitrary intervals, including ones that need many primes
+        deg = rng.randint(1, 60)
+        p = [rng.randint(-2 ** 30, 2 ** 30) for _ in range(deg + 1)]
+        p[-1] = p[-1] or 1
+        ae, be = rng.randint(-30, 3), rng.randint(-30, 3)
+        am, bm = rng.randint(-2 ** 20, 2 ** 20), rng.randint(-2 ** 20, 2 ** 20)
+        a, b = Dyadic(am, ae), Dyadic(bm, be)
+        if b <= a:
+            a, b = b, a
+        cases.append({"name": "arbitrary", "p": ints_out(p), "am": str(a.man), "ae": a.exp, "bm": str(b.man),
+                      "be": b.exp, "v": orig(p, a, b)})
+    dump("descartes", {"source": "upoly._variations_on (upoly.py:338-346), descartes_isolate (:358-408)",
+                       "polys": {name: ints_out(p) for name, p in polys}, "cases": cases, "isolations": isol},
+         gz=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small"]
     for w in which:
@@ -410,5 +471,7 @@ if __name__ == "__main__":
             gen_big(w)
         elif w == "cfg4prime":
             gen_cfg4prime()
+        elif w == "descartes":
+            gen_descartes()
         else:
             raise SystemExit("unknown fixture " + w)

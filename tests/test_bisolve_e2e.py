@@ -42,6 +42,9 @@ def test_install_rebinds_and_restores(curvekit_mod):
         assert M.biv_resultant is ours.biv_resultant and B.biv_resultant is ours.biv_resultant
         assert M.int_gcd_uni is ours.int_gcd_uni and B.int_gcd_uni is ours.int_gcd_uni
         assert M.zp_gcd_sylvester is ours.zp_gcd_sylvester
+        import curvekit.upoly as U
+        from paper_1201_1548_b200 import upoly as our_upoly
+        assert U._variations_on is our_upoly.variations_on
     finally:
         pkg.uninstall(saved)
     assert (M.biv_resultant, M.int_gcd_uni, B.biv_resultant, B.int_gcd_uni) == orig

@@ -1,0 +1,104 @@
+"""Descartes test of real-root isolation: upoly._variations_on
+(pkg/src/curvekit/upoly.py:338-346) on the GPU against the reference's own
+recorded counts and isolating intervals (tests/golden/descartes.json.gz)."""
+
+import random
+from dataclasses import dataclass
+
+import pytest
+
+from conftest import ints_in, load_golden
+
+
+@dataclass(frozen=True)
+class Dy:  # the two fields of curvekit.dyadic.Dyadic the test reads
+    man: int
+    exp: int
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return load_golden("descartes.json.gz")
+
+
+def _poly(gold, c):
+    return ints_in(c["p"]) if "p" in c else ints_in(gold["polys"][c["name"]])
+
+
+def test_oracle_matches_reference_counts(gold):
+    from oracle import oracle
+    for c in gold["cases"]:
+        p = _poly(gold, c)
+        if len(p) > 100:
+            continue  # the degree-400 cases are checked on the GPU
+        assert oracle.variations_on(p, int(c["am"]), c["ae"], int(c["bm"]), c["be"]) == c["v"], c
+
+
+@pytest.mark.gpu
+def test_gpu_variations_match_reference(gold):
+    from paper_1201_1548_b200.upoly import variations_on
+    polys = {}
+    for c in gold["cases"]:
+        key = c["name"] if "p" not in c else None
+        p = polys.setdefault(key, _poly(gold, c)) if key else _poly(gold, c)
+        v = variations_on(p, Dy(int(c["am"]), c["ae"]), Dy(int(c["bm"]), c["be"]))
+        assert v == c["v"], (c["name"], c["am"], c["ae"], c["bm"], c["be"])
+
+
+@pytest.mark.gpu
+def test_gpu_variations_random_vs_oracle():
+    from oracle import oracle
+    from paper_1201_1548_b200.upoly import variations_on
+    rng = random.Random(5)
+    for _ in range(25):
+        deg = rng.randint(1, 70)
+        p = [rng.randint(-2 ** 60, 2 ** 60) for _ in range(deg + 1)]
+        p[-1] = p[-1] or 3
+        if rng.random() < 0.3:
+            p[0] = 0
+        a = Dy(rng.randint(-2 ** 40, 2 ** 40), rng.randint(-60, 5))
+        b = Dy(rng.randint(-2 ** 40, 2 ** 40), rng.randint(-60, 5))
+        want = oracle.variations_on(p, a.man, a.exp, b.man, b.exp)
+        assert variations_on(p, a, b) == want
+
+
+@pytest.fixture(scope="module")
+def curvekit_mod():
+    import os
+    import sys
+    from conftest import REPO
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "curvekit")):
+        pytest.skip("reference install baseline/_ref is absent")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import curvekit.upoly  # noqa: F401
+    return sys.modules["curvekit"]
+
+
+@pytest.mark.gpu
+def test_isolation_matches_reference(gold, curvekit_mod):
+    """descartes_isolate of the unmodified reference, with install() routing its
+    Descartes tests (and square-free check) to the GPU: identical isolating
+    intervals for every recorded polynomial, the degree-400 cfg2 resultant
+    included (53 s in the reference)."""
+    import time
+
+    import curvekit.upoly as U
+
+    import paper_1201_1548_b200 as pkg
+    saved = pkg.install()
+    try:
+        from paper_1201_1548_b200 import upoly as ours
+        assert U._variations_on is ours.variations_on
+        for iso in gold["isolations"]:
+            p = ints_in(iso["p"])
+            t0 = time.time()
+            roots = U.descartes_isolate(p)
+            dt = time.time() - t0
+            got = [[str(r.interval.lo.man), r.interval.lo.exp, str(r.interval.hi.man), r.interval.hi.exp]
+                   for r in roots]
+            assert got == iso["roots"], iso["name"]
+            print(iso["name"], "%.3f s (reference %.1f s)" % (dt, iso["seconds"]))
+    finally:
+        pkg.uninstall(saved)
