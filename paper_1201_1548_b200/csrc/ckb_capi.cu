@@ -183,7 +183,7 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
       return 0;
     }
   }
-  if (g.crt.size() >= 4) {  // evict least recently used
+  if (g.crt.size() >= 8) {  // evict least recently used
     size_t v = 0;
     for (size_t i = 1; i < g.crt.size(); ++i)
       if (g.crt[i].last_use < g.crt[v].last_use) v = i;
