@@ -193,7 +193,15 @@ def _primes_for_bits(bits: float) -> int:
         _log2_prefix = pre
     import bisect
     k = bisect.bisect_right(_log2_prefix, bits) + 1
-    k = -(-k // 64) * 64
+    # a log-spaced ladder (64, 80, 96, 112, 128, 160, 192, 224, 256, 320, ...: four
+    # steps per doubling) so the cached CRT tables are reused across subdivision depths
+    j = 0
+    while True:
+        rung = -(-int(64 * 2 ** (j / 4)) // 16) * 16
+        if rung >= k:
+            k = rung
+            break
+        j += 1
     if k > min(len(_log2_prefix), 8192):
         raise NotImplementedError("Descartes test needs more than 8192 primes")
     return k
