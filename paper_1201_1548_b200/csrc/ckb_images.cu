@@ -11,6 +11,7 @@
 //     the general warp kernel (ckb_general.cu) recomputes exactly.
 #include "ckb_kernels.cuh"
 #include "ckb_resultant.cuh"
+#include "ckb_ntt.cuh"
 
 namespace ckb {
 
@@ -163,6 +164,25 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
   for (int h = POLY / 2; h >= 1; h >>= 1) {
     const bool upper = (l & h) != 0;
     const int widx = (l & (h - 1)) * (POLY / (2 * h));
+#ifndef CKB_NO_BF_SPLIT
+    if (h > 1) {
+      // split butterflies: the lower lane of a pair does the whole butterfly of
+      // A[i], the upper lane that of B[i] (one product per butterfly instead of
+      // one per lane), then they trade the halves that belong to the other lane
+      const uint32_t wp = som[widx], wpc = som[POLY + widx];
+#pragma unroll
+      for (int i = 0; i <= MAXD; ++i) {
+        const uint32_t recv = __shfl_xor_sync(FULL, upper ? A[i] : B[i], h);
+        const uint32_t lo = upper ? recv : A[i], hi = upper ? B[i] : recv;  // the pair's lower / upper values
+        const uint32_t sum = red2p(lo + hi, p2);
+        const uint32_t dif = shoup_lazy(lo - hi + p2, wp, wpc, p);
+        const uint32_t recv2 = __shfl_xor_sync(FULL, upper ? sum : dif, h);
+        A[i] = upper ? recv2 : sum;
+        B[i] = upper ? dif : recv2;
+      }
+      continue;
+    }
+#endif
     const uint32_t w = upper ? som[widx] : 1u;
     const uint32_t wc = upper ? som[POLY + widx] : (uint32_t)(0x100000000ull / p);  // companion of 1
 #pragma unroll
