@@ -55,9 +55,24 @@ def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=())
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    if out == OUT:
+        build_host(force)
     if verbose:
         print("built", out)
     return out
+
+
+def build_host(force: bool = False) -> str:
+    """The CPython helper that turns output limbs into Python ints (host glue)."""
+    import sysconfig
+    src = os.path.join(HERE, "host", "ckb_limbs.c")
+    dst = os.path.join(HERE, "ckb_limbs" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if force or not os.path.exists(dst) or os.path.getmtime(dst) < os.path.getmtime(src):
+        cmd = ["gcc", "-O2", "-shared", "-fPIC", "-I" + sysconfig.get_paths()["include"], src, "-o", dst]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"host helper build failed:\n{r.stderr}")
+    return dst
 
 
 if __name__ == "__main__":

@@ -262,10 +262,18 @@ def plan_resultant(fc, gc, tdf: int, tdg: int, dfx: int, dgx: int, start: int = 
 
 def limbs_to_ints(buf: np.ndarray, N: int, LW: int) -> list:
     """[N][LW] two's-complement u32 limbs -> list of Python ints."""
+    if _ckb_limbs is not None:
+        return _ckb_limbs.limbs_to_ints(memoryview(np.ascontiguousarray(buf, dtype=np.uint32)).cast("B"), N, LW)
     raw = np.ascontiguousarray(buf).tobytes()  # bytes slices beat memoryview slices here
     w = 4 * LW
     fb = int.from_bytes
     return [fb(raw[i * w:(i + 1) * w], "little", signed=True) for i in range(N)]
+
+
+try:  # the C helper built next to the library (paper_1201_1548_b200/host/ckb_limbs.c)
+    from . import ckb_limbs as _ckb_limbs
+except ImportError:  # pragma: no cover - pure-Python conversion (same result)
+    _ckb_limbs = None
 
 
 def ints_to_limbs(vals, L: int | None = None) -> tuple:
