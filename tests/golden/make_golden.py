@@ -460,6 +460,25 @@ def gen_descartes():
          gz=True)
 
 
+def gen_descartes_cfg3():
+    """Isolating intervals of cfg3's resultant R (square-free; upoly.descartes_isolate, upoly.py:358-408)."""
+    import math
+    gold = json.load(gzip.open(os.path.join(HERE, "cfg3_seed0.json.gz"), "rt"))
+    r = [int(c, 16) for c in gold["res"]]
+    c = 0
+    for v in r:
+        c = math.gcd(c, v)
+    p = [v // c for v in r]
+    t0 = time.time()
+    roots = upoly.descartes_isolate(p)
+    dt = time.time() - t0
+    print("cfg3 isolation", len(roots), "roots, %.1f s" % dt)
+    dump("descartes_cfg3", {"source": "upoly.descartes_isolate (upoly.py:358-408) on primitive(res_y) of cfg3 seed 0",
+                            "seconds": dt, "degree": len(p) - 1,
+                            "roots": [[str(x.interval.lo.man), x.interval.lo.exp, str(x.interval.hi.man),
+                                       x.interval.hi.exp] for x in roots]})
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small"]
     for w in which:
@@ -473,5 +492,7 @@ if __name__ == "__main__":
             gen_cfg4prime()
         elif w == "descartes":
             gen_descartes()
+        elif w == "descartes_cfg3":
+            gen_descartes_cfg3()
         else:
             raise SystemExit("unknown fixture " + w)

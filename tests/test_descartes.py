@@ -102,3 +102,32 @@ def test_isolation_matches_reference(gold, curvekit_mod):
             print(iso["name"], "%.3f s (reference %.1f s)" % (dt, iso["seconds"]))
     finally:
         pkg.uninstall(saved)
+
+
+@pytest.mark.gpu
+def test_cfg3_isolation_matches_reference(curvekit_mod):
+    """cfg3's degree-552 resultant: the reference's isolation takes ~170 s on one
+    core; through install() the same intervals come back in about a second."""
+    import math
+    import time
+
+    import curvekit.upoly as U
+
+    import paper_1201_1548_b200 as pkg
+    gold = load_golden("cfg3_seed0.json.gz")
+    want = load_golden("descartes_cfg3.json")
+    r = [int(c, 16) for c in gold["res"]]
+    c = 0
+    for v in r:
+        c = math.gcd(c, v)
+    p = [v // c for v in r]
+    saved = pkg.install()
+    try:
+        t0 = time.time()
+        roots = U.descartes_isolate(p)
+        dt = time.time() - t0
+    finally:
+        pkg.uninstall(saved)
+    got = [[str(x.interval.lo.man), x.interval.lo.exp, str(x.interval.hi.man), x.interval.hi.exp] for x in roots]
+    assert got == want["roots"]
+    print("cfg3 isolation %.2f s (reference %.1f s)" % (dt, want["seconds"]))
