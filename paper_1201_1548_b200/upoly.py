@@ -148,10 +148,16 @@ class _DescHandles:
     descartes_isolate passes to every test of one isolation (upoly.py:387-405)."""
 
     def __init__(self, size: int = 8):
+        import threading
         self.size = size
         self.entries = []  # [poly list, snapshot, handle, K]
+        self.lock = threading.Lock()
 
     def get(self, p, n: int, K: int):
+        with self.lock:
+            return self._get(p, n, K)
+
+    def _get(self, p, n: int, K: int):
         from . import _lib
         from .planner import ints_to_limbs
         from .primes30 import PRIMES30
