@@ -236,12 +236,13 @@ def run_ours(args):
             times.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
     launches = int(lib.ckb_launch_count() - n0)
-    if rank == 0:  # the timed (graph-replayed) path still gives the reference's result
-        last = step()
-        torch.cuda.synchronize()
-        if last is not None:
-            got2 = modpoly._trim(limbs_to_ints(last.cpu().numpy().view(np.uint32).reshape(-1), N, LW))
-            assert got2 == ref, "replayed pipeline differs from the single-call API"
+    # the timed (graph-replayed) path still gives the reference's result; every
+    # rank takes part in the step (it contains the collective), rank 0 checks
+    last = step()
+    torch.cuda.synchronize()
+    if rank == 0 and last is not None:
+        got2 = modpoly._trim(limbs_to_ints(last.cpu().numpy().view(np.uint32).reshape(-1), N, LW))
+        assert got2 == ref, "replayed pipeline differs from the single-call API"
     barrier()
     torch.cuda.synchronize()
     tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
