@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CKB_ABI_VERSION 1
+#define CKB_ABI_VERSION 2
 #define CKB_STATUS_REPLAN 1 /* a prime had no admissible evaluation points: re-plan without it */
 
 int ckb_abi_version(void);
