@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CKB_ABI_VERSION 2
+#define CKB_ABI_VERSION 3
 #define CKB_STATUS_REPLAN 1 /* a prime had no admissible evaluation points: re-plan without it */
 
 int ckb_abi_version(void);
@@ -95,6 +95,19 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
  * neither leading coefficient vanishes at t (the reference skips the others). */
 int ckb_psc_values(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
                    const int16_t* gdeg, int n, int dgx, uint32_t p, int ncand, uint32_t* out, uint8_t* valid);
+
+/* Images of the dense modular bivariate gcd — the modular core that replaces
+ * the primitive PRS of curvekit.bivpoly.gcd_biv (pkg/src/curvekit/bivpoly.py:266-295;
+ * used by is_squarefree_biv / square_part :307-320 and bisolve.py:110).
+ *   limbs [C][L]: A's dense grid A[j][i] (x^i y^j, j <= m, i <= dax), B's grid
+ *          (j <= n, i <= dbx), then Gamma = gcd(lc_y A, lc_y B) (dgam + 1 coefficients);
+ *          C = (m+1)(dax+1) + (n+1)(dbx+1) + dgam + 1, m >= n >= 0
+ *   degs  [m+n+2] trimmed x-degree of each y-coefficient of A then B (-1 = zero)
+ *   out   [K][NP][Wo] (Wo > m): Gamma(x_t) * monic gcd(A(x_t, y), B(x_t, y)) mod p_k at
+ *          x_t = t + 1, low degree first; odeg [K][NP] its degree, -2 where lc_y A or
+ *          lc_y B vanishes at x_t (the point is unusable). */
+int ckb_biv_gcd_images(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dax, int dbx,
+                       int dgam, const uint32_t* primes, int K, int NP, uint32_t* out, int Wo, int32_t* odeg);
 
 /* Descartes test of real-root isolation — replaces upoly._variations_on
  * (pkg/src/curvekit/upoly.py:338-346; compose_linear :202-212, taylor_shift

@@ -18,6 +18,9 @@ def install():
     bivpoly.py:186,268), so they pick up the GPU gcd through the first rebinding.
     Also rebinds ``curvekit.upoly._variations_on`` (the Descartes test of
     descartes_isolate, upoly.py:338-346) to the GPU version.
+    Rebinds ``curvekit.bivpoly.gcd_biv`` (bivpoly.py:266-295; ``is_squarefree_biv`` and
+    ``square_part`` look it up at call time) and the name ``curvekit.bisolve``
+    bound at import (bisolve.py:21) to the modular GPU gcd.
     Returns the previous bindings (pass them to ``uninstall``).
     """
     import importlib
@@ -35,6 +38,10 @@ def install():
     from . import upoly as our_upoly
     saved[("curvekit.upoly", "_variations_on")] = getattr(up, "_variations_on")
     setattr(up, "_variations_on", our_upoly.variations_on)
+    bp = importlib.import_module("curvekit.bivpoly")
+    from . import bivpoly as our_bivpoly
+    saved[("curvekit.bivpoly", "gcd_biv")] = getattr(bp, "gcd_biv")
+    setattr(bp, "gcd_biv", our_bivpoly.gcd_biv)
     try:
         bis = importlib.import_module("curvekit.bisolve")
     except ImportError:  # bisolve needs mpmath
@@ -43,6 +50,8 @@ def install():
         for name in ("biv_resultant", "int_gcd_uni"):
             saved[("curvekit.bisolve", name)] = getattr(bis, name)
             setattr(bis, name, getattr(ours, name))
+        saved[("curvekit.bisolve", "gcd_biv")] = getattr(bis, "gcd_biv")
+        setattr(bis, "gcd_biv", our_bivpoly.gcd_biv)
     return saved
 
 

@@ -22,7 +22,7 @@ EXPORTS = (
     "ckb_interp_geometric", "ckb_crt_lift", "ckb_dev_modular_images", "ckb_dev_crt",
     "ckb_interp_points", "ckb_gcd_mod_batch", "ckb_dev_biv_resultant", "ckb_set_timing",
     "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values", "ckb_host_alloc", "ckb_host_free",
-    "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release",
+    "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release", "ckb_biv_gcd_images",
 )
 
 _P = ctypes.c_void_p
@@ -56,6 +56,7 @@ _SIGS = {
     "ckb_descartes_prepare": (_I, [_P, _I, _I, _P, _P, _I]),
     "ckb_descartes_variations": (_I, [_I, _P, _I, _I, _I, _I, _P]),
     "ckb_descartes_release": (_I, [_I]),
+    "ckb_biv_gcd_images": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P]),
 }
 
 _lock = threading.Lock()

@@ -898,6 +898,41 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
   return 0;
 }
 
+int ckb_biv_gcd_images(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dax, int dbx,
+                       int dgam, const uint32_t* primes, int K, int NP, uint32_t* out, int Wo, int32_t* odeg) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(primes, K))) return rc;
+  if (K == 0 || NP == 0) return 0;
+  if (m < n || n < 0 || dax < 0 || dbx < 0 || dgam < 0) return fail("ckb_biv_gcd_images: need m >= n >= 0", -2);
+  if (C != (m + 1) * (dax + 1) + (n + 1) * (dbx + 1) + dgam + 1) return fail("ckb_biv_gcd_images: bad C", -2);
+  if (Wo < m + 1) return fail("ckb_biv_gcd_images: Wo < m + 1", -2);
+  if ((size_t)8 * (m + 1) * 4 > 200 * 1024) return fail("ckb_biv_gcd_images: y-degree too large", -2);
+  cudaStream_t st = g.stream;
+  uint32_t *d_limbs, *d_res, *d_out;
+  int16_t* d_degs;
+  int32_t* d_odeg;
+  Prime* d_primes;
+  const size_t B = (size_t)K * NP;
+  if ((rc = dbuf("bg.limbs", (size_t)C * L, &d_limbs))) return rc;
+  if ((rc = dbuf("bg.res", (size_t)K * C, &d_res))) return rc;
+  if ((rc = dbuf("bg.degs", (size_t)(m + n + 2), &d_degs))) return rc;
+  if ((rc = dbuf("bg.out", B * Wo, &d_out))) return rc;
+  if ((rc = dbuf("bg.odeg", B, &d_odeg))) return rc;
+  if ((rc = upload_primes(primes, K, &d_primes))) return rc;
+  CK(cudaMemcpyAsync(d_limbs, limbs, 4 * (size_t)C * L, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_degs, degs, 2 * (size_t)(m + n + 2), cudaMemcpyHostToDevice, st));
+  launch_reduce(d_limbs, C, L, d_primes, K, d_res, st);
+  launch_biv_gcd_images(d_res, C, d_degs, m, n, dax, dbx, dgam, d_primes, K, NP, d_out, Wo, d_odeg, st);
+  g.launches += 2;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, 4 * B * Wo, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(odeg, d_odeg, 4 * B, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
 int ckb_psc_values(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
                    const int16_t* gdeg, int n, int dgx, uint32_t p, int ncand, uint32_t* out, uint8_t* valid) {
   std::lock_guard<std::mutex> lk(g_mu);

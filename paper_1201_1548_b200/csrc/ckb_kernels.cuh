@@ -152,6 +152,12 @@ void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_
 void launch_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const Prime* primes,
                           const int32_t* pidx, int B, uint32_t* out, cudaStream_t st);
 
+// ---- images of the dense modular bivariate gcd (bivpoly.py:266-295)
+// res [K][C] residues of A's grid, B's grid, Gamma; out [K*NP][Wo] Gamma(x_t) * monic
+// gcd(A(x_t, y), B(x_t, y)) at x_t = t + 1; odeg its degree or -2 (lc vanishes at x_t)
+void launch_biv_gcd_images(const uint32_t* res, int C, const int16_t* degs, int m, int n, int dax, int dbx, int dgam,
+                           const Prime* primes, int K, int NP, uint32_t* out, int Wo, int32_t* odeg, cudaStream_t st);
+
 // ---- principal subresultant coefficients at points t = 0..ncand-1 (modpoly.py:428-526)
 // out [n][ncand] psc_i(t) for i = 1..n; valid[t] = no leading coefficient vanishes at t
 void launch_psc(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,

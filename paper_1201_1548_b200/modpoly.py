@@ -226,6 +226,25 @@ def zp_interpolate_batch(problems) -> list:
     return [_trim([int(v) for v in out[i, :ns[i]]]) for i in range(B)]
 
 
+def zp_interpolate_arrays(xs: np.ndarray, vals: np.ndarray, primes) -> np.ndarray:
+    """Array form of a batch of _zp_interp problems (modpoly.py:164-185) sharing
+    one point set per prime: xs [k][n] distinct points mod primes[k], vals
+    [k][r][n] -> coefficients [k][r][n] (low first, canonical residues)."""
+    lib = _lib.lib()
+    k, r, n = vals.shape
+    if n > 12288:
+        raise NotImplementedError("at most 12288 points per interpolation problem")
+    B = k * r
+    xsb = np.ascontiguousarray(np.repeat(xs.astype(np.uint32), r, axis=0))
+    vsb = np.ascontiguousarray(vals.reshape(B, n).astype(np.uint32))
+    ns = np.full(B, n, dtype=np.int32)
+    parr, pidx = _prime_index([p for p in primes for _ in range(r)])
+    out = np.zeros((B, n), dtype=np.uint32)
+    _lib.check(lib.ckb_interp_points(_lib.ptr(xsb), _lib.ptr(vsb), _lib.ptr(ns), n, _lib.ptr(parr), len(parr),
+                                     _lib.ptr(pidx), B, _lib.ptr(out)), "ckb_interp_points")
+    return out.reshape(k, r, n)
+
+
 def zp_interpolate(points, values, p: int):
     """modpoly.py:188-189."""
     points, values = list(points), list(values)

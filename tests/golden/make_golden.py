@@ -479,6 +479,60 @@ def gen_descartes_cfg3():
                                        x.interval.hi.exp] for x in roots]})
 
 
+def gen_gcdbiv():
+    """gcd_biv / is_squarefree_biv / square_part (bivpoly.py:266-320) on known
+    answers (test_modpoly.py:264-269), planted common factors, singular curves."""
+    from curvekit.bivpoly import gcd_biv, is_squarefree_biv, square_part
+
+    def rnd(rng, d, bits, dens=1.0):
+        t = {}
+        for i in range(d + 1):
+            for j in range(d + 1 - i):
+                if rng.random() < dens:
+                    c = rng.randint(-(2**bits), 2**bits)
+                    if c:
+                        t[(i, j)] = c
+        return BivPoly(t or {(0, 1): 1})
+
+    circle = BivPoly({(2, 0): 1, (0, 2): 1, (0, 0): -1})
+    line = BivPoly({(0, 1): 1, (1, 0): -1})
+    cases = [(circle * line, circle * BivPoly({(0, 1): 1})), (circle, line), (circle, BivPoly()),
+             (BivPoly(), BivPoly({(0, 1): -3, (1, 0): 6})), (BivPoly({(2, 0): 4, (0, 0): -4}), BivPoly({(1, 0): 6, (0, 0): 6})),
+             (BivPoly({(2, 0): 4, (0, 0): -4}), circle * BivPoly({(1, 0): 2, (0, 0): 2})),
+             (circle * BivPoly({(0, 1): 2, (1, 0): 1}), line * BivPoly({(0, 1): 2, (1, 0): 1})),
+             (circle.scale(6) * BivPoly({(1, 0): 1, (0, 0): 1}), circle.scale(-4) * BivPoly({(2, 0): 1, (0, 0): -1}))]
+    rng = random.Random(31)
+    for d, dh, bits in [(3, 1, 6), (4, 2, 8), (5, 2, 10), (6, 3, 10), (8, 4, 16), (10, 5, 16), (12, 6, 32),
+                        (14, 3, 40), (16, 8, 24)]:
+        for _ in range(3):
+            h = rnd(rng, dh, bits)
+            cases.append((rnd(rng, d - dh, bits) * h, rnd(rng, d - dh, bits, 0.7) * h))
+    for d, bits in [(4, 8), (8, 16)]:  # coprime
+        cases.append((rnd(rng, d, bits), rnd(rng, d, bits)))
+    gcds = []
+    for f, g in cases:
+        t0 = time.time()
+        r = gcd_biv(f, g)
+        gcds.append({"f": terms_out(f), "g": terms_out(g), "gcd": terms_out(r), "seconds": time.time() - t0})
+    sq = []
+    for d, bits, sing in [(6, 10, False), (10, 16, False), (16, 32, False), (4, 8, True), (6, 10, True),
+                          (8, 12, True)]:
+        if sing:  # f1^2 f2: a repeated factor
+            f1 = rnd(rng, d // 2, bits)
+            f = f1 * f1 * rnd(rng, d // 2, bits)
+        else:
+            f = rnd(rng, d, bits)
+        t0 = time.time()
+        isq = is_squarefree_biv(f)
+        t1 = time.time()
+        spart = square_part(f)
+        sq.append({"f": terms_out(f), "squarefree": isq, "square_part": terms_out(spart),
+                   "seconds_squarefree": t1 - t0, "seconds_square_part": time.time() - t1})
+        print("sqfree", d, bits, sing, isq, "%.2f s" % (t1 - t0))
+    dump("gcd_biv", {"source": "curvekit.bivpoly.gcd_biv / is_squarefree_biv / square_part (bivpoly.py:266-320)",
+                     "gcd": gcds, "squarefree": sq})
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small"]
     for w in which:
@@ -492,6 +546,8 @@ if __name__ == "__main__":
             gen_cfg4prime()
         elif w == "descartes":
             gen_descartes()
+        elif w == "gcdbiv":
+            gen_gcdbiv()
         elif w == "descartes_cfg3":
             gen_descartes_cfg3()
         else:
