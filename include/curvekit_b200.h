@@ -49,6 +49,16 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
                       const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, uint32_t* out,
                       uint32_t* status, float* device_ms);
 
+/* A batch of 1-4 independent res_y problems in one call (SURVEY.md §8(f) #1:
+ * bisolve.biproject's res_y and res_x, bisolve.py:107-108): every argument of
+ * ckb_biv_resultant becomes an array indexed by problem (pointer arrays for the
+ * buffers); each problem's pipeline runs on its own stream so their kernels
+ * overlap, and the call returns once all are done.  status [P]. */
+int ckb_biv_resultant_batch(int P, const uint32_t* const* limbs, const int* C, const int* L,
+                            const int16_t* const* degs, const int* m, const int* n, const int* dfx, const int* dgx,
+                            const uint32_t* const* primes, const uint32_t* const* gens, const int* K, const int* N,
+                            const int* LW, uint32_t* const* out, uint32_t* status);
+
 /* K1: residues of every coefficient mod every prime — replaces
  * `[[c % p for c in cf] for cf in fc]` (modpoly.py:376-377).
  *   limbs [C][L] -> out [K][C] */

@@ -21,6 +21,8 @@ def install():
     Rebinds ``curvekit.bivpoly.gcd_biv`` (bivpoly.py:266-295; ``is_squarefree_biv`` and
     ``square_part`` look it up at call time) and the name ``curvekit.bisolve``
     bound at import (bisolve.py:21) to the modular GPU gcd.
+    Rebinds ``curvekit.bisolve.biproject`` to the batched projection
+    (paper_1201_1548_b200.bisolve: res_y and res_x in one GPU call).
     Returns the previous bindings (pass them to ``uninstall``).
     """
     import importlib
@@ -52,6 +54,11 @@ def install():
             setattr(bis, name, getattr(ours, name))
         saved[("curvekit.bisolve", "gcd_biv")] = getattr(bis, "gcd_biv")
         setattr(bis, "gcd_biv", our_bivpoly.gcd_biv)
+        # both resultants of the projection in one batched GPU call (bisolve.py:103-114,
+        # looked up by Bisolve.__init__ at bisolve.py:412)
+        from . import bisolve as our_bisolve
+        saved[("curvekit.bisolve", "biproject")] = getattr(bis, "biproject")
+        setattr(bis, "biproject", our_bisolve.biproject)
     return saved
 
 

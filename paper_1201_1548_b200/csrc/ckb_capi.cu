@@ -68,6 +68,9 @@ struct Ctx {
   int nsev = 0;
   uint64_t epoch = 0;  // bumped whenever a buffer or table a captured graph may reference is freed
   bool graphs = true;  // CKB_NO_GRAPHS=1 disables graph replay
+  std::string ns;      // buffer-name prefix: each problem of a batch owns its buffers
+  cudaStream_t bst[4] = {};  // streams of the batched entry (created on first use)
+  cudaEvent_t bev[4] = {};
 };
 
 Ctx g;
@@ -88,7 +91,7 @@ struct DescHandle {
 std::vector<DescHandle> g_desc;
 
 int dev_buf(const char* name, size_t bytes, void** out) {
-  Buf& b = g.dev[name];
+  Buf& b = g.dev[g.ns + name];
   if (b.n < bytes) {
     if (b.p) cudaFree(b.p);
     ++g.epoch;
@@ -103,7 +106,7 @@ int dev_buf(const char* name, size_t bytes, void** out) {
 }
 
 int host_buf(const char* name, size_t bytes, void** out) {
-  Buf& b = g.host[name];
+  Buf& b = g.host[g.ns + name];
   if (b.n < bytes) {
     if (b.p) cudaFreeHost(b.p);
     ++g.epoch;
@@ -638,6 +641,10 @@ int ckb_shutdown(void) {
   cudaEventDestroy(g.ev0);
   cudaEventDestroy(g.ev1);
   for (int i = 0; i < 8; ++i) cudaEventDestroy(g.sev[i]);
+  for (int i = 0; i < 4; ++i) {
+    if (g.bst[i]) cudaStreamDestroy(g.bst[i]);
+    if (g.bev[i]) cudaEventDestroy(g.bev[i]);
+  }
   cudaStreamDestroy(g.stream);
   g = Ctx();
   return 0;
@@ -645,16 +652,25 @@ int ckb_shutdown(void) {
 
 unsigned long long ckb_launch_count(void) { return g.launches; }
 
-int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
-                      const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, uint32_t* out,
-                      uint32_t* status, float* device_ms) {
-  std::lock_guard<std::mutex> lk(g_mu);
+}  // extern "C"
+
+namespace {
+
+// one res_y pipeline enqueued on a stream; finished by res_finish
+struct ResPending {
+  uint32_t* out;
+  uint8_t* ho;
+  size_t words;
+  bool out_direct;
+};
+
+int res_enqueue(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
+                const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, uint32_t* out, cudaStream_t st,
+                int slot, ResPending* pd) {
   int rc;
-  if ((rc = ensure_ready())) return rc;
   if (m < 1 || n < 1 || K < 1 || N < 1 || L < 1 || LW < 1) return fail("ckb_biv_resultant: bad sizes", -2);
   if (C != (m + 1) * (dfx + 1) + (n + 1) * (dgx + 1)) return fail("ckb_biv_resultant: C mismatch", -2);
   if ((rc = check_primes(primes, K))) return rc;
-  cudaStream_t st = g.stream;
   // stage inputs in pinned memory, then one async copy each
   const size_t nl = (size_t)C * L, nd = (size_t)(m + n + 2);
   void *h_in, *h_out;
@@ -681,11 +697,11 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   uint8_t* ho = (uint8_t*)h_out;
   void* dst_out = out_direct ? (void*)out : (void*)ho;
   std::vector<uint64_t> key = {2, (uint64_t)C, (uint64_t)L, (uint64_t)m, (uint64_t)n, (uint64_t)dfx, (uint64_t)dgx,
-                               (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)src_limbs, (uint64_t)dst_out};
+                               (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)src_limbs, (uint64_t)dst_out,
+                               (uint64_t)slot};
   key_push(key, degs, 2 * nd);
   key_push(key, primes, 4 * (size_t)K);
   key_push(key, gens, 4 * (size_t)K);
-  CK(cudaEventRecord(g.ev0, st));
   rc = graphed(key, st, [&]() -> int {
     int r;
     CK(cudaMemcpyAsync(d_limbs, src_limbs, 4 * nl, cudaMemcpyHostToDevice, st));
@@ -704,20 +720,99 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
     return 0;
   });
   if (rc) return rc;
-  CK(cudaEventRecord(g.ev1, st));
-  // spin on the completion event: a blocking synchronise adds a thread wake-up to
-  // every call's latency (the call is ~0.4 ms end to end)
+  pd->out = out;
+  pd->ho = ho;
+  pd->words = (size_t)N * LW;
+  pd->out_direct = out_direct;
+  return 0;
+}
+
+// spin on an event: a blocking synchronise adds a thread wake-up to every
+// call's latency (a cfg4 call is ~0.4 ms end to end)
+int spin_event(cudaEvent_t ev) {
   for (;;) {
-    const cudaError_t q = cudaEventQuery(g.ev1);
-    if (q == cudaSuccess) break;
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) return 0;
     if (q != cudaErrorNotReady) CK(q);
   }
-  if (!out_direct) memcpy(out, ho, 4 * (size_t)N * LW);
+}
+
+uint32_t res_finish(const ResPending& pd) {
+  if (!pd.out_direct) memcpy(pd.out, pd.ho, 4 * pd.words);
   uint32_t s;
-  memcpy(&s, ho + 4 * (size_t)N * LW, 4);
+  memcpy(&s, pd.ho + 4 * pd.words, 4);
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
+                      const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, uint32_t* out,
+                      uint32_t* status, float* device_ms) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  cudaStream_t st = g.stream;
+  ResPending pd;
+  CK(cudaEventRecord(g.ev0, st));
+  if ((rc = res_enqueue(limbs, C, L, degs, m, n, dfx, dgx, primes, gens, K, N, LW, out, st, 0, &pd))) return rc;
+  CK(cudaEventRecord(g.ev1, st));
+  if ((rc = spin_event(g.ev1))) return rc;
+  const uint32_t s = res_finish(pd);
   if (status) *status = s;
   if (device_ms) CK(cudaEventElapsedTime(device_ms, g.ev0, g.ev1));
   return s ? CKB_STATUS_REPLAN : 0;
+}
+
+int ckb_biv_resultant_batch(int P, const uint32_t* const* limbs, const int* C, const int* L,
+                            const int16_t* const* degs, const int* m, const int* n, const int* dfx, const int* dgx,
+                            const uint32_t* const* primes, const uint32_t* const* gens, const int* K, const int* N,
+                            const int* LW, uint32_t* const* out, uint32_t* status) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if (P < 1 || P > 4) return fail("ckb_biv_resultant_batch: 1 to 4 problems", -2);
+  for (int i = 0; i < P; ++i) {
+    if (!g.bst[i]) {
+      CK(cudaStreamCreateWithFlags(&g.bst[i], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&g.bev[i], cudaEventDisableTiming));
+    }
+  }
+  // cached tables first (built on the context stream, which get_plan / get_crt
+  // synchronise), so that enqueueing one problem cannot evict another's
+  for (int i = 0; i < P; ++i) {
+    InterpPlan pl;
+    CrtEntry* ce;
+    if (m[i] < 1 || n[i] < 1 || K[i] < 1) return fail("ckb_biv_resultant_batch: bad sizes", -2);
+    if ((rc = check_primes(primes[i], K[i]))) return rc;
+    if ((rc = get_plan(primes[i], gens[i], K[i], N[i], 8, &pl))) return rc;
+    if ((rc = get_crt(primes[i], K[i], LW[i], &ce))) return rc;
+  }
+  CK(cudaStreamSynchronize(g.stream));
+  // (with at most 4 problems every plan / CRT entry stays cached during the
+  // enqueue pass; buffers are per problem, so no problem's setup can free
+  // memory another problem's enqueued work uses)
+  ResPending pd[4];
+  const bool timing = g.timing;
+  g.timing = false;
+  for (int i = 0; i < P && rc == 0; ++i) {
+    g.ns = "b" + std::to_string(i) + ".";
+    rc = res_enqueue(limbs[i], C[i], L[i], degs[i], m[i], n[i], dfx[i], dgx[i], primes[i], gens[i], K[i], N[i],
+                     LW[i], out[i], g.bst[i], 1 + i, &pd[i]);
+    if (rc == 0 && cudaEventRecord(g.bev[i], g.bst[i]) != cudaSuccess) rc = fail("cudaEventRecord", -1);
+  }
+  g.ns.clear();
+  g.timing = timing;
+  for (int i = 0; i < P; ++i) cudaStreamSynchronize(g.bst[i]);
+  if (rc) return rc;
+  uint32_t any = 0;
+  for (int i = 0; i < P; ++i) {
+    status[i] = res_finish(pd[i]);
+    any |= status[i];
+  }
+  return any ? CKB_STATUS_REPLAN : 0;
 }
 
 int ckb_reduce(const uint32_t* limbs, int C, int L, const uint32_t* primes, int K, uint32_t* out) {

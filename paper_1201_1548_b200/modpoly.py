@@ -16,6 +16,7 @@ into Python ints.  ``prime_table``/``prime_stream`` are the reference's own
 
 from __future__ import annotations
 
+import ctypes
 import random
 from dataclasses import dataclass
 from functools import lru_cache
@@ -27,6 +28,8 @@ from . import _lib
 from .bivpoly import as_biv
 from .planner import (ints_to_limbs, limbs_to_ints, pack_grid, plan_resultant)
 from .primes30 import PRIMES30
+
+ctypes_ptr = ctypes.c_void_p
 
 __all__ = [
     "UnluckyPrime", "prime_table", "prime_stream", "ModPoly", "ResidueSystem",
@@ -460,6 +463,31 @@ def int_gcd_uni(f, g, seed: int = 0):
         batch = min(2 * batch, 64)
 
 
+def int_gcd_uni_batch(pairs) -> list:
+    """[int_gcd_uni(f, g) for (f, g) in pairs] with the first modular round of
+    every pair in one GPU batch: a pair whose images have degree 0 is coprime
+    (the common case) and is done; the others run int_gcd_uni."""
+    out = [None] * len(pairs)
+    todo = []
+    for i, (f, g) in enumerate(pairs):
+        f, g = _trim(list(f)), _trim(list(g))
+        if not f or not g or len(_primitive(f)) == 1 or len(_primitive(g)) == 1:
+            out[i] = int_gcd_uni(f, g)
+        else:
+            todo.append((i, _primitive(f), _primitive(g)))
+    triples, owners = [], []
+    for i, fp, gp in todo:
+        picked = [p for p, _ in PRIMES30[:16] if fp[-1] % p and gp[-1] % p][:2]
+        for p in picked:
+            triples.append(([a % p for a in fp], [a % p for a in gp], p))
+            owners.append(i)
+    gms = zp_gcd_batch(triples)
+    coprime = {i for i, gm in zip(owners, gms) if len(gm) == 1}
+    for i, fp, gp in todo:
+        out[i] = [1] if i in coprime else int_gcd_uni(fp, gp)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # bivariate resultants (modpoly.py:348-394)
 # ---------------------------------------------------------------------------
@@ -533,6 +561,67 @@ def _biv_resultant_gpu(fc, gc, tdf: int, tdg: int):
                           "bound_bits": plan.bound_bits, "modulus_bits": plan.modulus_bits}
         start += K  # a prime had no admissible point set: use the next primes
     raise ArithmeticError("no admissible evaluation points after re-planning")
+
+
+def biv_resultant_batch(problems, seed: int = 0) -> list:
+    """[biv_resultant(f, g, var) for (f, g, var) in problems], the GPU problems
+    of the list in ONE library call (ckb_biv_resultant_batch, up to 4 per call,
+    each pipeline on its own stream so their kernels overlap) — SURVEY.md §8(f) #1,
+    bisolve.biproject's two resultants (bisolve.py:107-108).  Errors and
+    degenerate branches are those of biv_resultant, problem by problem."""
+    results = [None] * len(problems)
+    gpu = []
+    for i, (f, g, var) in enumerate(problems):
+        f, g = as_biv(f), as_biv(g)
+        if f.is_zero() or g.is_zero():
+            raise ValueError("resultant of zero polynomial")
+        if var == "x":
+            f, g = f.swap(), g.swap()
+        elif var != "y":
+            raise ValueError("var must be 'x' or 'y'")
+        fc, gc = f.coeffs_wrt_y(), g.coeffs_wrt_y()
+        m, n = len(fc) - 1, len(gc) - 1
+        if m == 0 and n == 0:
+            results[i] = [1]
+        elif m == 0:
+            results[i] = _pow(fc[0], n)
+        elif n == 0:
+            results[i] = _pow(gc[0], m)
+        else:
+            gpu.append((i, fc, gc, f.total_degree(), g.total_degree()))
+    lib = _lib.lib()
+    for a in range(0, len(gpu), 4):
+        chunk = gpu[a:a + 4]
+        P = len(chunk)
+        packs = [pack_grid(fc, gc) for _, fc, gc, _, _ in chunk]
+        plans = [plan_resultant(fc, gc, tdf, tdg, pk.dfx, pk.dgx)
+                 for (_, fc, gc, tdf, tdg), pk in zip(chunk, packs)]
+        outs = [_lib.pinned.get(f"biv_out{j}", pl.N * pl.LW) for j, pl in enumerate(plans)]
+        status = np.zeros(P, dtype=np.uint32)
+
+        def ptrs(arrs):
+            return (ctypes_ptr * P)(*[_lib.ptr(x) for x in arrs])
+
+        def ints(vals):
+            return np.array(vals, dtype=np.int32)
+
+        cs, ls = ints([pk.C for pk in packs]), ints([pk.L for pk in packs])
+        ms, ns = ints([pk.m for pk in packs]), ints([pk.n for pk in packs])
+        dfs, dgs = ints([pk.dfx for pk in packs]), ints([pk.dgx for pk in packs])
+        ks, nn = ints([len(pl.primes) for pl in plans]), ints([pl.N for pl in plans])
+        lws = ints([pl.LW for pl in plans])
+        rc = _lib.check(lib.ckb_biv_resultant_batch(
+            P, ptrs([pk.limbs for pk in packs]), _lib.ptr(cs), _lib.ptr(ls), ptrs([pk.degs for pk in packs]),
+            _lib.ptr(ms), _lib.ptr(ns), _lib.ptr(dfs), _lib.ptr(dgs), ptrs([pl.primes for pl in plans]),
+            ptrs([pl.gens for pl in plans]), _lib.ptr(ks), _lib.ptr(nn), _lib.ptr(lws), ptrs(outs),
+            _lib.ptr(status)), "ckb_biv_resultant_batch")
+        for j, (i, fc, gc, tdf, tdg) in enumerate(chunk):
+            if status[j]:  # a prime had no admissible point set: the single call re-plans
+                results[i], _ = _biv_resultant_gpu(fc, gc, tdf, tdg)
+            else:
+                results[i] = _trim(limbs_to_ints(outs[j], plans[j].N, plans[j].LW))
+        del rc
+    return results
 
 
 # ---------------------------------------------------------------------------

@@ -111,3 +111,43 @@ def test_reference_squarefree_uses_gpu_gcd(curvekit_mod):
         assert _lib.launch_count() > n0, "the reference's Yun must reach the GPU gcd"
     finally:
         pkg.uninstall(saved)
+
+
+def _ps_key(ps):
+    dec = None if ps.decomposition is None else (str(ps.decomposition.content),
+                                                  [[list(map(str, f)), m] for f, m in ps.decomposition.factors])
+    roots = [(str(r.interval.lo.man), r.interval.lo.exp, str(r.interval.hi.man), r.interval.hi.exp)
+             for r in ps.roots]
+    return ps.axis, [str(c) for c in ps.resultant], dec, roots, [str(c) for c in ps.lead_gcd]
+
+
+@pytest.mark.gpu
+def test_batched_biproject_matches_reference(curvekit_mod):
+    """paper_1201_1548_b200.bisolve.biproject (both resultants in
+    one batched GPU call, both lead gcds in one gcd batch) returns the projection
+    sets of the reference's biproject (bisolve.py:103-114)."""
+    import curvekit.bisolve as B
+    from curvekit.bivpoly import BivPoly
+
+    import paper_1201_1548_b200 as pkg
+    from paper_1201_1548_b200 import bisolve as ours
+    gold = load_golden("cfg1_bisolve.json")
+    systems = [(BivPoly(terms_in(s["f"])), BivPoly(terms_in(s["g"]))) for s in gold["systems"][:3]]
+    want = [tuple(_ps_key(ps) for ps in B.biproject(f, g)) for f, g in systems]  # the unmodified reference
+    saved = pkg.install()
+    try:
+        assert B.biproject is ours.biproject
+        got = [tuple(_ps_key(ps) for ps in B.biproject(f, g)) for f, g in systems]
+    finally:
+        pkg.uninstall(saved)
+    assert got == want
+    # a common factor: both resultants vanish -> CommonFactorError carrying gcd_biv
+    circle = BivPoly({(2, 0): 1, (0, 2): 1, (0, 0): -1})
+    line = BivPoly({(0, 1): 1, (1, 0): -1})
+    saved = pkg.install()
+    try:
+        with pytest.raises(B.CommonFactorError) as ei:
+            B.biproject(circle * line, circle * BivPoly({(0, 1): 1}))
+    finally:
+        pkg.uninstall(saved)
+    assert ei.value.factor == circle

@@ -395,3 +395,37 @@ def test_interpolate_large_batch(mp):
             for c in reversed(co):
                 acc = (acc * x + c) % p
             assert acc == v
+
+
+def test_biv_resultant_batch_golden(mp, small):
+    """several res problems per library call (own streams),
+    identical to the reference's results; degenerate and mixed-size entries."""
+    from paper_1201_1548_b200 import _lib
+    probs, want = [], []
+    for case in small["random50"][:24]:
+        f, g = terms_in(case["f"]), terms_in(case["g"])
+        probs += [(f, g, "y"), (f, g, "x")]
+        want += [ints_in(case["res_y"]), ints_in(case["res_x"])]
+    for case in small["resultant_cases"]:
+        probs.append((terms_in(case["f"]), terms_in(case["g"]), case["var"]))
+        want.append(ints_in(case["res"]))
+    n0 = _lib.launch_count()
+    for rep in range(2):  # second pass replays the per-slot graphs
+        assert mp.biv_resultant_batch(probs) == want
+    assert _lib.launch_count() > n0
+    # a cfg2-size problem next to tiny ones in one call
+    from paper_1201_1548_b200.synth import make_pair
+    f2, g2 = make_pair("cfg2", 0)
+    gold = load_golden("cfg2_seed0.json.gz")
+    circle = {(2, 0): 1, (0, 2): 1, (0, 0): -1}
+    got = mp.biv_resultant_batch([(circle, {(0, 1): 2}, "y"), (f2, g2, "y"), (circle, {(0, 1): 1, (1, 0): -1}, "y")])
+    assert got[0] == [-4, 0, 4] and got[2] == [-1, 0, 2]
+    assert got[1] == [int(c, 16) for c in gold["res"]]
+    with pytest.raises(ValueError):
+        mp.biv_resultant_batch([(circle, {}, "y")])
+
+
+def test_int_gcd_uni_batch_golden(mp, small):
+    cases = small["int_gcd"]
+    got = mp.int_gcd_uni_batch([(ints_in(c["f"]), ints_in(c["g"])) for c in cases])
+    assert got == [ints_in(c["gcd"]) for c in cases]
