@@ -9,10 +9,12 @@ generator).  A step is one complete res_y (reduce -> plan -> fused
 evaluation + resultant per (prime, point) -> interpolation -> CRT to limbs).
   value  res_y per second with inputs resident in HBM (device time, CUDA
          events on the launching stream, L2 flushed between steps, max over
-         ranks); at N > 1 the primes are sharded and the residues all-gathered
-         over NCCL before the CRT on rank 0 (strong scaling).
+         ranks); at N > 1 the primes are sharded, one NCCL all-to-all gives
+         every rank all residues of its block of N/W coefficients and each rank
+         lifts its block by CRT (strong scaling; SURVEY §8e option B).
   e2e    the same metric through the C-ABI call with HOST buffers
-         (ckb_biv_resultant: H2D of the limbs, D2H of the result limbs), plus
+         (ckb_biv_resultant: H2D of the limbs, D2H of the result limbs; at
+         N > 1 per rank: H2D of the limbs, D2H of its coefficient block), plus
          the Python-level time of modpoly.biv_resultant (packing, planning and
          int conversion) reported beside it.
   --impl reference: the CPU reference path (the oracle port of
@@ -154,7 +156,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "u32 (mod p < 2^31), exact integers", "data": "synthetic",
             "config": cfg, "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -166,7 +168,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_1201_1548_b200 import _lib, modpoly, workmodel
-    from paper_1201_1548_b200.distributed import CudaBackend, plan_sharded, sharded_resultant_step
+    from paper_1201_1548_b200.distributed import (CudaBackend, gather_limbs, plan_sharded,
+                                                  sharded_resultant_step_a2a)
     from paper_1201_1548_b200.planner import limbs_to_ints, pack_grid, plan_resultant
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -174,7 +177,8 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     os.environ["CKB_DEVICE"] = str(local)
-    if world > 1:
+    sharded = world > 1 or args.sharded  # --sharded: the N > 1 code path on one rank (tests it)
+    if sharded:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     lib = _lib.lib()
@@ -189,29 +193,40 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier(device_ids=[local])
 
     hp_all = np.array(plan.primes, dtype=np.uint32)
     hg_all = np.array(plan.gens, dtype=np.uint32)
-    d_out1 = torch.empty((N, LW), dtype=torch.int32, device=dev) if world == 1 else None
+    d_out1 = torch.empty((N, LW), dtype=torch.int32, device=dev) if not sharded else None
 
     def step():
-        if world == 1:  # the whole pipeline in one C-ABI call (replayed as a CUDA graph)
+        if not sharded:  # the whole pipeline in one C-ABI call (replayed as a CUDA graph)
             _lib.check(lib.ckb_dev_biv_resultant(
                 backend.d_limbs.data_ptr(), pk.C, pk.L, backend.d_degs.data_ptr(), _lib.ptr(backend.h_degs),
                 pk.m, pk.n, pk.dfx, pk.dgx, _lib.ptr(hp_all), _lib.ptr(hg_all), K, N, LW, d_out1.data_ptr(),
                 backend.d_status.data_ptr(), stream.cuda_stream), "ckb_dev_biv_resultant")
             return d_out1
+        # primes sharded, residues exchanged by one all-to-all, every rank lifts
+        # its coefficient block by CRT (SURVEY §8e option B); the step ends with
+        # each rank's [N/W][LW] limbs in its HBM
         with torch.cuda.stream(stream):
-            return sharded_resultant_step(backend, plan, rank, world, None, stream.cuda_stream)
+            return sharded_resultant_step_a2a(backend, plan, rank, world, None, stream.cuda_stream)
+
+    def assemble(blk):  # outside the timed region: all limb blocks on rank 0
+        if not sharded:
+            return blk
+        with torch.cuda.stream(stream):
+            full = gather_limbs(blk, plan, rank, world)
+        torch.cuda.synchronize()
+        return full
 
     # correctness of the timed path against the single-call API (rank 0)
     t_cold = time.perf_counter()
     out = step()
     torch.cuda.synchronize()
     t_cold = time.perf_counter() - t_cold
-    torch.cuda.synchronize()
+    out = assemble(out)
     if rank == 0:
         got = modpoly._trim(limbs_to_ints(out.cpu().numpy().view(np.uint32).reshape(-1), N, LW))
         ref, _ = modpoly._biv_resultant_gpu(fc, gc, tdf, tdg)
@@ -238,7 +253,7 @@ def run_ours(args):
     launches = int(lib.ckb_launch_count() - n0)
     # the timed (graph-replayed) path still gives the reference's result; every
     # rank takes part in the step (it contains the collective), rank 0 checks
-    last = step()
+    last = assemble(step())
     torch.cuda.synchronize()
     if rank == 0 and last is not None:
         got2 = modpoly._trim(limbs_to_ints(last.cpu().numpy().view(np.uint32).reshape(-1), N, LW))
@@ -246,7 +261,7 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if sharded:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_per_step = float(tot.item()) / args.steps
     clocks = clk.summary()
@@ -275,9 +290,38 @@ def run_ours(args):
         lib.ckb_set_timing(0)
         stages = dict(zip(["reduce", "choose_c", "images", "interp", "crt"], (acc / reps).tolist()))
 
-    # e2e: through the C-ABI with host buffers (rank 0, single GPU), and the Python API
+    # e2e: through the C-ABI with host buffers (rank 0, single GPU), and the Python API;
+    # at N > 1 every rank copies the input limbs from pinned memory, runs the sharded
+    # step and reads its coefficient block back into pinned memory (max over ranks)
     e2e = None
-    if rank == 0:
+    if sharded:
+        h_in = torch.from_numpy(pk.limbs.view(np.int32).copy()).pin_memory()
+        h_out = torch.empty((-(-N // world), LW), dtype=torch.int32).pin_memory()
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        barrier()
+        et = 0.0
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            stream.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(stream):
+                backend.d_limbs.copy_(h_in, non_blocking=True)
+                blk = step()
+                h_out.copy_(blk, non_blocking=True)
+            stream.synchronize()
+            et += time.perf_counter() - t0
+        tt = torch.tensor([et], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_ms = 1e3 * float(tt.item()) / args.steps
+        e2e = {"value": 1e3 / e_ms, "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(pk.limbs.nbytes), "d2h_bytes_per_step": int(h_out.numel() * 4),
+               "path": "SPMD over NCCL: per rank H2D of the input limbs (pinned), sharded step, D2H of the "
+                       "rank's coefficient block (pinned); max over ranks, wall clock per step"}
+    if rank == 0 and not sharded:
         p1 = plan_resultant(fc, gc, tdf, tdg, pk.dfx, pk.dgx)
         # page-locked host buffers, as the e2e contract states (inputs copied from pinned memory)
         hlimbs = _lib.pinned.get("bench_in", pk.limbs.size)
@@ -335,7 +379,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32 (mod p < 2^30), exact integers", "data": "synthetic",
             "config": dict(cfg, primes=K, points_per_prime=N, images_per_res_y=images, out_words=LW,
-                           l2="flushed (256 MB write) before every timed step", parallelism=f"primes/{world}"),
+                           l2="flushed (256 MB write) before every timed step", parallelism=(f"primes/{world}" if not sharded else
+                                        f"primes/{world}, all-to-all, CRT coefficients/{world}")),
             "images_per_s": images * 1e3 / ms_per_step,
             "stages_ms": stages,
             "cold_first_call_ms": t_cold * 1e3,
@@ -358,14 +403,30 @@ def run_ours(args):
             "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line))
-    if world > 1:
+        emit(line)
+    if sharded:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    """The ONE JSON line, on the real stdout (library chatter was sent to stderr)."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # NCCL / CUDA libraries may print to fd 1 (e.g. "NCCL version ..."): route fd 1
+    # to stderr and keep a private handle on the real stdout for the JSON line
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -374,6 +435,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="run the multi-GPU (all-to-all) step even at N=1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -108,6 +108,47 @@ class CudaBackend:
         return out
 
 
+def coeff_slice(plan: ShardPlan, rank: int, world: int) -> tuple:
+    """Coefficients [a, b) whose CRT rank `rank` runs in the coefficient-sharded
+    exchange (contiguous blocks of ceil(N / world); the last may be short)."""
+    nc = -(-plan.N // world)
+    a = min(plan.N, rank * nc)
+    return a, min(plan.N, a + nc)
+
+
+def sharded_resultant_step_a2a(backend, plan: ShardPlan, rank: int, world: int, group=None, stream=None):
+    """One res_y with the coefficient-sharded CRT (SURVEY.md §8(e) option B).
+
+    Rank r computes the [K/W][N] residues of its primes, one all-to-all
+    transposes them so that rank r holds ALL K residues of its coefficient block
+    coeff_slice(r) (the block sent to rank s is the column block s of the local
+    residues, received in prime order because ranks own contiguous prime
+    blocks), and every rank lifts its block by CRT.  Returns this rank's
+    [nc][LW] limbs (rows past N, on the last rank, are zero coefficients).
+    """
+    import torch
+    import torch.distributed as dist
+    primes, gens = plan.shard(rank)
+    local = backend.modular_images(primes, gens, plan.N, stream)
+    nc = -(-plan.N // world)
+    if world == 1 and not dist.is_initialized():
+        recv = local
+    else:
+        reuse = getattr(backend, "buffer", None)
+        kr = plan.per_rank
+        shape = (world, kr, nc)
+        send = reuse("a2a_send", shape) if reuse else torch.empty(shape, dtype=local.dtype, device=local.device)
+        recv = reuse("a2a_recv", shape) if reuse else torch.empty(shape, dtype=local.dtype, device=local.device)
+        src = local
+        if world * nc != plan.N:  # zero coefficients pad the last block
+            src = torch.nn.functional.pad(local, (0, world * nc - plan.N))
+        # send[s] = column block s of the local residues (one strided copy)
+        send.copy_(src.view(kr, world, nc).permute(1, 0, 2))
+        dist.all_to_all_single(recv, send, group=group)
+        recv = recv.reshape(world * kr, nc)  # rows: rank-major prime blocks = plan.primes order
+    return backend.crt(recv, plan.primes, nc, plan.LW, stream)
+
+
 def sharded_resultant_step(backend, plan: ShardPlan, rank: int, world: int, group=None, stream=None):
     """One res_y: local primes -> all_gather -> CRT on rank 0 (returns limbs tensor or None)."""
     import torch.distributed as dist
@@ -126,11 +167,13 @@ def sharded_resultant_step(backend, plan: ShardPlan, rank: int, world: int, grou
     return backend.crt(gathered, plan.primes, plan.N, plan.LW, stream)
 
 
-def biv_resultant_distributed(f, g, var: str = "y", group=None) -> list | None:
+def biv_resultant_distributed(f, g, var: str = "y", group=None, exchange: str = "a2a") -> list | None:
     """res_var(f, g) over all ranks of the default process group (SPMD call).
 
     Every rank passes the same f, g; rank 0 returns the coefficient list,
-    the others return None.
+    the others return None.  exchange="a2a" (default): coefficient-sharded CRT
+    after an all-to-all, the limb blocks gathered to rank 0; "gather": residues
+    all-gathered, CRT on rank 0 (SURVEY.md §8(e) options B and A).
     """
     import torch
     import torch.distributed as dist
@@ -155,8 +198,23 @@ def biv_resultant_distributed(f, g, var: str = "y", group=None) -> list | None:
     backend = CudaBackend(fc, gc, device)
     s = torch.cuda.current_stream(device)
     with torch.cuda.stream(s):
-        out = sharded_resultant_step(backend, plan, rank, world, group, s.cuda_stream)
+        if exchange == "a2a":
+            blk = sharded_resultant_step_a2a(backend, plan, rank, world, group, s.cuda_stream)
+            out = gather_limbs(blk, plan, rank, world, group)
+        else:
+            out = sharded_resultant_step(backend, plan, rank, world, group, s.cuda_stream)
     if rank != 0:
         return None
     host = out.cpu().numpy().view(np.uint32).reshape(-1)
     return _trim(limbs_to_ints(host, plan.N, plan.LW))
+
+
+def gather_limbs(blk, plan: ShardPlan, rank: int, world: int, group=None):
+    """The [nc][LW] limb blocks of all ranks -> [N][LW] on rank 0 (None elsewhere)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1 and not dist.is_initialized():
+        return blk[:plan.N]
+    full = torch.empty((world * blk.shape[0], blk.shape[1]), dtype=blk.dtype, device=blk.device)
+    dist.all_gather_into_tensor(full, blk.contiguous(), group=group)
+    return full[:plan.N] if rank == 0 else None

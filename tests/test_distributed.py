@@ -40,10 +40,7 @@ class OracleBackend:
     def crt(self, coeffs, primes, N, LW, stream):
         from oracle import oracle
         res = coeffs.tolist()
-        vals = [oracle.crt_reconstruct(list(primes), [res[i][k] for i in range(len(primes))]) for k in range(N)]
-        while vals and vals[-1] == 0:
-            vals.pop()
-        return vals
+        return [oracle.crt_reconstruct(list(primes), [res[i][k] for i in range(len(primes))]) for k in range(N)]
 
 
 def _free_port():
@@ -54,13 +51,14 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, cases, q):
+def _worker(rank, world, port, cases, q, mode):
     import sys
     sys.path.insert(0, REPO)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import oracle
-    from paper_1201_1548_b200.distributed import plan_sharded, sharded_resultant_step
+    from paper_1201_1548_b200.distributed import (coeff_slice, plan_sharded, sharded_resultant_step,
+                                                  sharded_resultant_step_a2a)
     try:
         for f, g, want in cases:
             fc, gc = oracle.coeffs_wrt_y(f), oracle.coeffs_wrt_y(g)
@@ -68,17 +66,33 @@ def _worker(rank, world, port, cases, q):
             tdg = max(i + j for i, j in g)
             plan = plan_sharded(fc, gc, tdf, tdg, world)
             assert len(plan.primes) % world == 0 and plan.per_rank * world == len(plan.primes)
-            got = sharded_resultant_step(OracleBackend(fc, gc), plan, rank, world)
-            if rank == 0:
-                q.put(got == want)
-            else:
-                assert got is None
+            if mode == "gather":
+                got = sharded_resultant_step(OracleBackend(fc, gc), plan, rank, world)
+                if rank == 0:
+                    while got and got[-1] == 0:
+                        got.pop()
+                    q.put(got == want)
+                else:
+                    assert got is None
+            else:  # coefficient-sharded CRT after the all-to-all (option B)
+                blk = sharded_resultant_step_a2a(OracleBackend(fc, gc), plan, rank, world)
+                a, b = coeff_slice(plan, rank, world)
+                assert len(blk) == -(-plan.N // world) and not any(blk[b - a:])
+                blocks = [None] * world
+                dist.all_gather_object(blocks, blk[:b - a])
+                if rank == 0:
+                    got = [v for bl in blocks for v in bl]
+                    assert len(got) == plan.N
+                    while got and got[-1] == 0:
+                        got.pop()
+                    q.put(got == want)
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["gather", "a2a"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_resultant_gloo(world, small):
+def test_sharded_resultant_gloo(world, mode, small):
     cases = []
     for case in small["random50"][:6]:
         f, g = terms_in(case["f"]), terms_in(case["g"])
@@ -88,7 +102,7 @@ def test_sharded_resultant_gloo(world, small):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    mp.start_processes(_worker, args=(world, port, cases, q), nprocs=world, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(world, port, cases, q, mode), nprocs=world, join=True, start_method="spawn")
     results = [q.get(timeout=5) for _ in cases]
     assert results and all(results)
 
