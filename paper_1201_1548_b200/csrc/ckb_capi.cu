@@ -382,10 +382,11 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
   pl.logL = logL;
   const size_t kn = (size_t)K * N, kn1 = (size_t)K * (N + 1), kl = (size_t)K * L, kh = kl / 2;
   const size_t words =
-      kn * 10 + kn1 * 3 + kh * 4 + kl * 4 + (size_t)K * 5 + (size_t)K * 4 * S + (S > 1 ? 2 * (size_t)S * kn : 0) + 64;
+      kn * 10 + kn1 * 3 + kh * 4 + kl * 4 + (size_t)K * 5 + (size_t)K * 4 * S + (S > 1 ? 2 * (size_t)S * kn : 0) + 256;
   CK(cudaMalloc(&e.blob, 4 * words));
   uint32_t* b = (uint32_t*)e.blob;
-  auto take = [&](size_t n) { uint32_t* r = b; b += n; return r; };
+  // every table 16-byte aligned (the interpolation stages them with 16-byte cp.async)
+  auto take = [&](size_t n) { uint32_t* r = b; b += (n + 3) & ~(size_t)3; return r; };
   pl.yq = take(kn);
   pl.yqi = take(kn);
   pl.om = take((size_t)K * 4 * S);

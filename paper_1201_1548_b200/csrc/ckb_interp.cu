@@ -177,6 +177,23 @@ __global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const P
 // size M, one CTA per (prime, r), interleaved into P_{S k + r}.
 // threads per CTA = the radix-8 passes' L/8 groups, clamped to [32, 256]
 
+// cp.async (LDGSTS) copies global -> shared without a register round trip, so
+// every constant table of a CTA is requested at once at kernel entry and lands
+// while the input gather runs (one L2 latency instead of one per table)
+__device__ __forceinline__ void cp_async16(uint32_t* sdst, const uint32_t* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t* sdst, const uint32_t* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// n words (n % 4 == 0, both pointers 16-byte aligned) by the CTA
+__device__ __forceinline__ void stage16(uint32_t* sdst, const uint32_t* gsrc, int n, int tid, int T) {
+  for (int i = 4 * tid; i < n; i += 4 * T) cp_async16(sdst + i, gsrc + i);
+}
+
 template <int POLY_THREADS>
 __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, const Prime* __restrict__ primes,
                                                               const uint32_t* __restrict__ values,
@@ -184,21 +201,47 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
                                                               uint32_t* __restrict__ coeffs,
                                                               const uint32_t* __restrict__ crt_c,
                                                               const uint32_t* __restrict__ crt_cc) {
-  extern __shared__ uint32_t buf[];  // [L] data, then 4 x [L/2] twiddle tables
+  // shared: [L] data (one pad word per 8, sidx) | W, Wc, Wi, Wic [L/2 each] | Hf, Hfc, Mf, Mfc [L each] | sS, sSc [Mp each]
+  extern __shared__ __align__(16) uint32_t buf[];
   const int S = plan.S;
   const int pi = blockIdx.x / S, r = blockIdx.x % S, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pi];
   const uint32_t p = P.p;
   const int M = plan.N, L = plan.L, logL = plan.logL, half = L >> 1, Nfull = plan.Nfull;
+  const int Mp = (M + 3) & ~3, Lp = (L + 3) & ~3, hp = (half + 3) & ~3;  // 16-byte aligned regions
   const size_t oM = (size_t)pi * M, oL = (size_t)pi * L, oH = (size_t)pi * half;
-  uint32_t *W = buf + L, *Wc = W + half, *Wi = Wc + half, *Wic = Wi + half;
-  for (int j = tid; j < half; j += T) {
-    W[j] = plan.W[oH + j];
-    Wc[j] = plan.Wc[oH + j];
-    Wi[j] = plan.Wi[oH + j];
-    Wic[j] = plan.Wic[oH + j];
+  uint32_t *W = buf + ((padded_words(L) + 3) & ~3), *Wc = W + hp, *Wi = Wc + hp, *Wic = Wi + hp;
+  uint32_t *Hf = Wic + hp, *Hfc = Hf + Lp, *Mf = Hfc + Lp, *Mfc = Mf + Lp;
+  uint32_t *sS = Mfc + Lp, *sSc = sS + Mp;
+  // every per-plan constant this CTA needs, requested up front (16-byte copies
+  // when the per-prime table offsets are 16-byte aligned: L >= 8)
+  if (L >= 8) {
+    stage16(W, plan.W + oH, half, tid, T);
+    stage16(Wc, plan.Wc + oH, half, tid, T);
+    stage16(Wi, plan.Wi + oH, half, tid, T);
+    stage16(Wic, plan.Wic + oH, half, tid, T);
+    stage16(Hf, plan.Hf + oL, L, tid, T);
+    stage16(Hfc, plan.Hfc + oL, L, tid, T);
+    stage16(Mf, plan.Mf + oL, L, tid, T);
+    stage16(Mfc, plan.Mfc + oL, L, tid, T);
+  } else {
+    for (int j = tid; j < half; j += T) {
+      cp_async4(W + j, plan.W + oH + j);
+      cp_async4(Wc + j, plan.Wc + oH + j);
+      cp_async4(Wi + j, plan.Wi + oH + j);
+      cp_async4(Wic + j, plan.Wic + oH + j);
+    }
+    for (int j = tid; j < L; j += T) {
+      cp_async4(Hf + j, plan.Hf + oL + j);
+      cp_async4(Hfc + j, plan.Hfc + oL + j);
+      cp_async4(Mf + j, plan.Mf + oL + j);
+      cp_async4(Mfc + j, plan.Mfc + oL + j);
+    }
   }
-  const uint32_t *Hf = plan.Hf + oL, *Hfc = plan.Hfc + oL, *Mf = plan.Mf + oL, *Mfc = plan.Mfc + oL;
+  for (int e = tid; e < M; e += T) {
+    cp_async4(sS + e, plan.sS + oM + e);
+    cp_async4(sSc + e, plan.sSc + oM + e);
+  }
   const uint32_t* om = plan.om + (size_t)pi * 4 * S;
   const uint32_t c = cval[pi];
   // c^-r (the shifted point set; 1 almost always)
@@ -207,7 +250,7 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
   const uint32_t* zr = plan.zr + ((size_t)pi * S + r) * M;
   const uint32_t* zrc = plan.zrc + ((size_t)pi * S + r) * M;
   const uint32_t* v = values + (size_t)pi * M * S;
-  // a'_s = P_r(z_t) * zweight_t with t = M-1-s
+  // a'_s = P_r(z_t) * zweight_t with t = M-1-s (global loads overlap the copies above)
   for (int s = tid; s < L; s += T) {
     uint32_t a = 0u;
     if (s < M) {
@@ -221,32 +264,33 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
       if (c != 1u) g = shoup(g, cr, crc, p);
       a = shoup_lazy(g, zr[t], zrc[t], p);  // (1/S) y_t^-r z_t
     }
-    buf[s] = a;
+    buf[sidx<true>(s)] = a;
   }
+  cp_async_wait_all();
   __syncthreads();
-  ntt_dif8<POLY_THREADS>(buf, logL, W, Wc, p);
-  for (int u = tid; u < L; u += T) buf[u] = shoup_lazy(buf[u], Hf[u], Hfc[u], p);
+  ntt_dif8<POLY_THREADS, true>(buf, logL, W, Wc, p);
+  for (int u = tid; u < L; u += T) buf[sidx<true>(u)] = shoup_lazy(buf[sidx<true>(u)], Hf[u], Hfc[u], p);
   __syncthreads();
-  ntt_dit8<POLY_THREADS>(buf, logL, Wi, Wic, p);
+  ntt_dit8<POLY_THREADS, true>(buf, logL, Wi, Wic, p);
   uint32_t sv[MAX_PER_THREAD];
 #pragma unroll
   for (int q = 0; q < MAX_PER_THREAD; ++q) {
     const int e = tid + q * T;
-    sv[q] = (e < M) ? shoup_lazy(buf[M - 1 + e], plan.sS[oM + e], plan.sSc[oM + e], p) : 0u;
+    sv[q] = (e < M) ? shoup_lazy(buf[sidx<true>(M - 1 + e)], sS[e], sSc[e], p) : 0u;
   }
   __syncthreads();
-  for (int u = tid; u < L; u += T) buf[u] = 0u;
+  for (int u = tid; u < L; u += T) buf[sidx<true>(u)] = 0u;
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < MAX_PER_THREAD; ++q) {
     const int e = tid + q * T;
-    if (e < M) buf[M - 1 - e] = sv[q];
+    if (e < M) buf[sidx<true>(M - 1 - e)] = sv[q];
   }
   __syncthreads();
-  ntt_dif8<POLY_THREADS>(buf, logL, W, Wc, p);
-  for (int u = tid; u < L; u += T) buf[u] = shoup_lazy(buf[u], Mf[u], Mfc[u], p);
+  ntt_dif8<POLY_THREADS, true>(buf, logL, W, Wc, p);
+  for (int u = tid; u < L; u += T) buf[sidx<true>(u)] = shoup_lazy(buf[sidx<true>(u)], Mf[u], Mfc[u], p);
   __syncthreads();
-  ntt_dit8<POLY_THREADS>(buf, logL, Wi, Wic, p);
+  ntt_dit8<POLY_THREADS, true>(buf, logL, Wi, Wic, p);
   // P_r[k] = conv[M-1+k] / L * (c^S)^-k  ->  coefficient S k + r
   const uint32_t linv = plan.Linv[pi];
   const uint32_t linvc = shoup_comp(linv, P);
@@ -263,7 +307,7 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
   for (int k = tid; k < M; k += T) {
     const int idx = S * k + r;
     if (idx >= Nfull) continue;
-    uint32_t res = shoup(buf[M - 1 + k], fin, finc, p);
+    uint32_t res = shoup(buf[sidx<true>(M - 1 + k)], fin, finc, p);
     if (c != 1u) res = mul_mod(res, pow_mod(cS, (uint64_t)k, P), P);
     if (crt_c)
       coeffs[crt_a_word(pi, idx, KC)] = res;  // straight into the CRT GEMM's A layout
@@ -275,11 +319,14 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
 
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
                    uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c, const uint32_t* crt_cc) {
-  const size_t smem = (size_t)plan.L * 4 * 3;  // data + 4 twiddle tables of L/2
+  size_t smem = (size_t)plan.L * 4 * 3;  // data + 4 twiddle tables of L/2
   if (plan.S == 1) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_interp<<<plan.K, NTT_THREADS, smem, st>>>(plan, primes, values, cval, coeffs);
   } else {
+    const size_t Lp = (plan.L + 3) & ~3, hp = (plan.L / 2 + 3) & ~3, Mp = (plan.N + 3) & ~3;
+    const size_t Dp = ((size_t)padded_words(plan.L) + 3) & ~(size_t)3;
+    smem = (Dp + 4 * Lp + 4 * hp + 2 * Mp) * 4;  // padded data, twiddles, staged Hf, Hfc, Mf, Mfc, sS, sSc
     const int want = plan.L / 8;
 #define POLY_LAUNCH(TT)                                                                                       \
   if ((TT == 32 && want <= 32) || (TT == 64 && want == 64) || (TT == 128 && want == 128) ||                 \

@@ -53,6 +53,16 @@ __device__ __forceinline__ void ntt_dit(uint32_t* buf, int logL, const uint32_t*
   }
 }
 
+// Shared-memory index with one pad word per 8 (PAD = true): the radix-8
+// passes read 8 words at stride h/4 per lane; unpadded, the lanes of a warp
+// collide 4-8 ways on the banks for h <= 32 (ncu: 60% of the shared wavefronts
+// of k_interp_poly were conflicts).  i + i/8 makes stride-8 and the
+// (8-group x 8-lane) patterns conflict-free.
+template <bool PAD>
+__device__ __forceinline__ int sidx(int i) { return PAD ? i + (i >> 3) : i; }
+// words a padded buffer of n entries occupies
+__host__ __device__ __forceinline__ int padded_words(int n) { return n + (n >> 3) + 1; }
+
 // ---- register-blocked radix-8 passes (same transforms, 3 stages per pass) ----
 // DIF stage with half-size h on the pair (a, b) at in-block position pos:
 //   a <- a + b,  b <- (a - b) w^(pos L / 2h)
@@ -72,7 +82,7 @@ __device__ __forceinline__ void bf_dit(uint32_t& a, uint32_t& b, int widx, const
 
 // forward DIF: passes of three stages (h, h/2, h/4) on 8 registers, then a
 // radix-4 or radix-2 tail; T = blockDim.x (a power of two)
-template <int T>
+template <int T, bool PAD = false>
 __device__ __forceinline__ void ntt_dif8(uint32_t* buf, int logL, const uint32_t* W, const uint32_t* Wc, uint32_t p) {
   const int L = 1 << logL;
   const uint32_t p2 = 2u * p;
@@ -83,7 +93,7 @@ __device__ __forceinline__ void ntt_dif8(uint32_t* buf, int logL, const uint32_t
       const int j = g & (q4 - 1), base = (g >> (lh - 2)) << (lh + 1);
       uint32_t x[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = buf[base + j + k * q4];
+      for (int k = 0; k < 8; ++k) x[k] = buf[sidx<PAD>(base + j + k * q4)];
       const int s0 = logL - 1 - lh;  // twiddle stride L/(2h)
 #pragma unroll
       for (int k = 0; k < 4; ++k) bf_dif(x[k], x[k + 4], (j + k * q4) << s0, W, Wc, p, p2);
@@ -95,7 +105,7 @@ __device__ __forceinline__ void ntt_dif8(uint32_t* buf, int logL, const uint32_t
 #pragma unroll
       for (int k = 0; k < 8; k += 2) bf_dif(x[k], x[k + 1], j << (s0 + 2), W, Wc, p, p2);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) buf[base + j + k * q4] = x[k];
+      for (int k = 0; k < 8; ++k) buf[sidx<PAD>(base + j + k * q4)] = x[k];
     }
     __syncthreads();
   }
@@ -103,20 +113,20 @@ __device__ __forceinline__ void ntt_dif8(uint32_t* buf, int logL, const uint32_t
   if (lh == 1) {
     for (int g = threadIdx.x; g < (L >> 2); g += T) {
       const int base = g << 2;
-      uint32_t x0 = buf[base], x1 = buf[base + 1], x2 = buf[base + 2], x3 = buf[base + 3];
+      uint32_t x0 = buf[sidx<PAD>(base)], x1 = buf[sidx<PAD>(base + 1)], x2 = buf[sidx<PAD>(base + 2)], x3 = buf[sidx<PAD>(base + 3)];
       const int s0 = logL - 2;
       bf_dif(x0, x2, 0, W, Wc, p, p2);
       bf_dif(x1, x3, 1 << s0, W, Wc, p, p2);
       bf_dif(x0, x1, 0, W, Wc, p, p2);
       bf_dif(x2, x3, 0, W, Wc, p, p2);
-      buf[base] = x0; buf[base + 1] = x1; buf[base + 2] = x2; buf[base + 3] = x3;
+      buf[sidx<PAD>(base)] = x0; buf[sidx<PAD>(base + 1)] = x1; buf[sidx<PAD>(base + 2)] = x2; buf[sidx<PAD>(base + 3)] = x3;
     }
     __syncthreads();
   } else if (lh == 0) {
     for (int g = threadIdx.x; g < (L >> 1); g += T) {
-      uint32_t x0 = buf[2 * g], x1 = buf[2 * g + 1];
+      uint32_t x0 = buf[sidx<PAD>(2 * g)], x1 = buf[sidx<PAD>(2 * g + 1)];
       bf_dif(x0, x1, 0, W, Wc, p, p2);
-      buf[2 * g] = x0; buf[2 * g + 1] = x1;
+      buf[sidx<PAD>(2 * g)] = x0; buf[sidx<PAD>(2 * g + 1)] = x1;
     }
     __syncthreads();
   }
@@ -124,7 +134,7 @@ __device__ __forceinline__ void ntt_dif8(uint32_t* buf, int logL, const uint32_t
 
 // inverse DIT (no 1/L): a radix-2 or radix-4 head, then passes of three
 // stages (h, 2h, 4h) on 8 registers
-template <int T>
+template <int T, bool PAD = false>
 __device__ __forceinline__ void ntt_dit8(uint32_t* buf, int logL, const uint32_t* Wi, const uint32_t* Wic, uint32_t p) {
   const int L = 1 << logL;
   const uint32_t p2 = 2u * p;
@@ -132,22 +142,22 @@ __device__ __forceinline__ void ntt_dit8(uint32_t* buf, int logL, const uint32_t
   const int head = logL % 3;
   if (head == 1) {
     for (int g = threadIdx.x; g < (L >> 1); g += T) {
-      uint32_t x0 = buf[2 * g], x1 = buf[2 * g + 1];
+      uint32_t x0 = buf[sidx<PAD>(2 * g)], x1 = buf[sidx<PAD>(2 * g + 1)];
       bf_dit(x0, x1, 0, Wi, Wic, p, p2);
-      buf[2 * g] = x0; buf[2 * g + 1] = x1;
+      buf[sidx<PAD>(2 * g)] = x0; buf[sidx<PAD>(2 * g + 1)] = x1;
     }
     __syncthreads();
     lh = 1;
   } else if (head == 2) {
     for (int g = threadIdx.x; g < (L >> 2); g += T) {
       const int base = g << 2;
-      uint32_t x0 = buf[base], x1 = buf[base + 1], x2 = buf[base + 2], x3 = buf[base + 3];
+      uint32_t x0 = buf[sidx<PAD>(base)], x1 = buf[sidx<PAD>(base + 1)], x2 = buf[sidx<PAD>(base + 2)], x3 = buf[sidx<PAD>(base + 3)];
       const int s1 = logL - 2;
       bf_dit(x0, x1, 0, Wi, Wic, p, p2);
       bf_dit(x2, x3, 0, Wi, Wic, p, p2);
       bf_dit(x0, x2, 0, Wi, Wic, p, p2);
       bf_dit(x1, x3, 1 << s1, Wi, Wic, p, p2);
-      buf[base] = x0; buf[base + 1] = x1; buf[base + 2] = x2; buf[base + 3] = x3;
+      buf[sidx<PAD>(base)] = x0; buf[sidx<PAD>(base + 1)] = x1; buf[sidx<PAD>(base + 2)] = x2; buf[sidx<PAD>(base + 3)] = x3;
     }
     __syncthreads();
     lh = 2;
@@ -159,7 +169,7 @@ __device__ __forceinline__ void ntt_dit8(uint32_t* buf, int logL, const uint32_t
       const int j = g & (h - 1), base = (g >> lh) << (lh + 3);
       uint32_t x[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = buf[base + j + k * h];
+      for (int k = 0; k < 8; ++k) x[k] = buf[sidx<PAD>(base + j + k * h)];
       const int s0 = logL - 1 - lh;  // stride for half h
 #pragma unroll
       for (int k = 0; k < 8; k += 2) bf_dit(x[k], x[k + 1], j << s0, Wi, Wic, p, p2);
@@ -171,7 +181,7 @@ __device__ __forceinline__ void ntt_dit8(uint32_t* buf, int logL, const uint32_t
 #pragma unroll
       for (int k = 0; k < 4; ++k) bf_dit(x[k], x[k + 4], (j + k * h) << (s0 - 2), Wi, Wic, p, p2);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) buf[base + j + k * h] = x[k];
+      for (int k = 0; k < 8; ++k) buf[sidx<PAD>(base + j + k * h)] = x[k];
     }
     __syncthreads();
   }
