@@ -75,6 +75,11 @@ struct Ctx {
 
 Ctx g;
 std::mutex g_mu;
+}  // namespace
+namespace ckb {
+bool g_pdl = true;
+}
+namespace {
 
 // ---- Descartes sign-variation test ------------------------------------------
 // A handle holds one polynomial's residues modulo a prefix of PRIMES30-style
@@ -541,6 +546,10 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   if (!general && (rc = dbuf("tab", (size_t)K * images_tab_words(m, n, dfx, dgx), &d_tab))) return rc;
   if ((rc = dbuf("vals", (size_t)K * NI, &d_vals))) return rc;
   if ((rc = dbuf("cval", (size_t)K, &d_cval))) return rc;
+  uint32_t* d_fail;
+  if ((rc = dbuf("fail", (size_t)K * NI + 1, &d_fail))) return rc;
+  // zero the fail counter first so the kernels below run back to back (PDL)
+  if (!general) CK(cudaMemsetAsync(d_fail + (size_t)K * NI, 0, 4, st));
   stage_mark(st);
   if (general)
     launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
@@ -568,14 +577,12 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   a.K = K;
   a.values = d_vals;
   a.status = d_status;
-  if ((rc = dbuf("fail", (size_t)K * NI + 1, &a.fail_list))) return rc;
+  a.fail_list = d_fail;
   a.fail_count = a.fail_list + (size_t)K * NI;
-  if (general) {
+  if (general)
     launch_images_general(a, st);
-  } else {
-    CK(cudaMemsetAsync(a.fail_count, 0, 4, st));
+  else
     launch_images(a, st);
-  }
   stage_mark(st);
   launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr);
   stage_mark(st);
@@ -610,6 +617,8 @@ int ckb_init(int device) {
   {
     const char* e = getenv("CKB_NO_GRAPHS");
     g.graphs = !(e && e[0] == '1');
+    const char* q = getenv("CKB_NO_PDL");
+    ckb::g_pdl = !(q && q[0] == '1');
   }
   g.ready = true;
   return 0;

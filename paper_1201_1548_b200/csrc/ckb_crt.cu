@@ -26,6 +26,8 @@ namespace ckb {
 // ---------------------------------------------------------------------------
 __global__ void k_crt_ymul(CrtTables T, const uint32_t* __restrict__ r, int N, uint32_t* __restrict__ y) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  // pdl_launch();  (implicit at exit: measured better)
+  pdl_wait();
   if (k >= N) return;
   const uint32_t p = T.p[i];
   y[crt_a_word(i, k, (T.K + 31) / 32)] = red1(shoup_lazy(r[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
@@ -56,6 +58,8 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uns
                                                    uint32_t* __restrict__ out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = blockIdx.x * 4 + warp;
+  // pdl_launch();  (implicit at exit: measured better)
+  pdl_wait();
   if (k >= N) return;
   const unsigned FULL = 0xffffffffu;
   const int LW = T.LW;
@@ -175,11 +179,11 @@ void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out
   const uint32_t* y = coeffs;
   if (!input_is_y) {
     uint32_t* yb = scratch + (size_t)2 * N * LWp;
-    k_crt_ymul<<<dim3((N + 255) / 256, t.K), 256, 0, st>>>(t, coeffs, N, yb);
+    launch_pdl(k_crt_ymul, dim3((N + 255) / 256, t.K), dim3(256), 0, st, t, coeffs, N, yb);
     y = yb;
   }
   launch_crt_mma(t, y, N, S, st);
-  k_crt_carry<<<(N + 3) / 4, 128, 0, st>>>(t, N, S, y, LWp, out);
+  launch_pdl(k_crt_carry, dim3((N + 3) / 4), dim3(128), 0, st, t, N, S, y, LWp, out);
 }
 
 size_t crt_scratch_words(int K, int N, int LW) {

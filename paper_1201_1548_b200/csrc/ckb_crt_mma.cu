@@ -153,6 +153,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_crt_mma(int N, int KC, const uin
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // pdl_launch();  (implicit at exit: measured better)
+  pdl_wait();  // y (the interpolation's output) from here on
 
   if (tid == 0) {
     const uint8_t* gA = yA + (size_t)mt * KC * CHUNK;
@@ -223,7 +225,7 @@ void launch_crt_mma(const CrtTables& t, const uint32_t* y, int N, unsigned long 
   }
   const int NT = (t.LW + 31) / 32, KC = (t.K + 31) / 32;
   dim3 grid((N + BM - 1) / BM, NT);
-  k_crt_mma<<<grid, THREADS, smem, st>>>(N, KC, reinterpret_cast<const uint8_t*>(y), t.Bt, NT * 32, S);
+  launch_pdl(k_crt_mma, grid, dim3(THREADS), smem, st, N, KC, reinterpret_cast<const uint8_t*>(y), t.Bt, NT * 32, S);
 }
 
 }  // namespace ckb

@@ -71,6 +71,8 @@ __global__ void k_images_fallback(ImageArgs a, int W) {
   uint32_t* gb = sm + W;
   uint32_t* rr = sm + 2 * W;
   const int lane = threadIdx.x & 31;
+  // pdl_launch();  (implicit at exit: measured better)
+  pdl_wait();
   const uint32_t count = *a.fail_count;
   for (uint32_t idx = blockIdx.x; idx < count; idx += gridDim.x) {
     const uint32_t flat = a.fail_list[idx];
@@ -103,7 +105,7 @@ __global__ void k_images_fallback(ImageArgs a, int W) {
 
 void launch_images_fallback(const ImageArgs& a, cudaStream_t st) {
   const int W = (a.m > a.n ? a.m : a.n) + 2;
-  k_images_fallback<<<4 * 148, 32, (size_t)3 * W * 4, st>>>(a, W);
+  launch_pdl(k_images_fallback, dim3(4 * 148), dim3(32), (size_t)3 * W * 4, st, a, W);
 }
 
 __global__ void k_iota(uint32_t* list, uint32_t n) {

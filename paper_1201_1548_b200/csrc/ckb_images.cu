@@ -67,9 +67,9 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
   const int tin = active ? t - pi * a.N : 0;  // image index within the prime
   const int u = tin >> 3, l = t & (POLY - 1);
   const int tslot = pi - pi0;  // which staged table
+  // pdl_launch();  (implicit at exit: measured better)
   const Prime P = a.primes[pi];
-  const uint32_t c = a.cval[pi];
-  uint32_t y = a.yq[(size_t)pi * a.M + u];
+  uint32_t y = a.yq[(size_t)pi * a.M + u];  // plan (constant): before the wait
   // TA[e][i] = coefficient of x^e in the y-coefficient of degree da - i (top-aligned),
   // zero beyond each row; maskA[e] = chunks of registers with a term at x^e
   uint32_t* TA = sm + tslot * TW;
@@ -78,13 +78,6 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
   uint32_t* maskA = sm + a.span * TW;
   uint32_t* maskB = maskA + rows;
   uint32_t* som = maskB + rows + tslot * 2 * POLY;  // w^k and companions
-  {
-    // K1 wrote the tables in exactly this layout: coalesced 16-byte copies
-    const int nt = nspan * TW / 4;
-    const uint4* src = reinterpret_cast<const uint4*>(a.tab + (size_t)pi0 * TW);
-    uint4* dst = reinterpret_cast<uint4*>(sm);
-    for (int idx = threadIdx.x; idx < nt; idx += IMG_THREADS) dst[idx] = src[idx];
-  }
   for (int e = threadIdx.x; e < rows; e += IMG_THREADS) {
     uint32_t ma = 0, mb = 0;
     for (int i = 0; i <= MAXD; ++i) {
@@ -96,6 +89,15 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
   }
   for (int q = threadIdx.x; q < nspan * 2 * POLY; q += IMG_THREADS)
     maskB[rows + q] = a.om[(size_t)(pi0 + q / (2 * POLY)) * 4 * POLY + q % (2 * POLY)];
+  pdl_wait();  // K1's tables and k_choose_c's point scales from here on
+  const uint32_t c = a.cval[pi];
+  {
+    // K1 wrote the tables in exactly this layout: coalesced 16-byte copies
+    const int nt = nspan * TW / 4;
+    const uint4* src = reinterpret_cast<const uint4*>(a.tab + (size_t)pi0 * TW);
+    uint4* dst = reinterpret_cast<uint4*>(sm);
+    for (int idx = threadIdx.x; idx < nt; idx += IMG_THREADS) dst[idx] = src[idx];
+  }
   __syncthreads();
 
   // image (u, j): x = w^j c y_u.  Lane l of an 8-lane group evaluates the
@@ -242,6 +244,8 @@ __global__ void k_reduce_tab(const uint32_t* __restrict__ limbs, int C, int L, c
                              uint32_t* __restrict__ tab) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x, pi = blockIdx.y;
   const int TW = 2 * rows * SW;
+  // pdl_launch();  (implicit at exit: measured better)
+  pdl_wait();
   if (idx >= TW) return;
   const bool sw = m < n;
   const int sel = idx / (rows * SW), rem = idx % (rows * SW), e = rem / SW, i = rem % SW;
@@ -302,7 +306,7 @@ void launch_images(const ImageArgs& a, cudaStream_t st) {
     const size_t smem = (size_t)(b.span * (2 * rows * ImgLayout<D>::SW + 2 * POLY) + 2 * rows) * 4; \
     if (smem > 48 * 1024)                                                                            \
       cudaFuncSetAttribute(k_images<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    k_images<D><<<grid, IMG_THREADS, smem, st>>>(b);                                                 \
+    launch_pdl(k_images<D>, grid, dim3(IMG_THREADS), smem, st, b);                                   \
   }
   CKB_MAXD_LIST(LAUNCH)
 #undef LAUNCH

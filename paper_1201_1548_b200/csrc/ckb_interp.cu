@@ -242,6 +242,8 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
     cp_async4(sS + e, plan.sS + oM + e);
     cp_async4(sSc + e, plan.sSc + oM + e);
   }
+  // pdl_launch();  (implicit at exit: measured better)
+  pdl_wait();  // the images kernels' values and k_choose_c's point scales from here on
   const uint32_t* om = plan.om + (size_t)pi * 4 * S;
   const uint32_t c = cval[pi];
   // c^-r (the shifted point set; 1 almost always)
@@ -333,7 +335,8 @@ void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* 
       (TT == 256 && want >= 256)) {                                                                           \
     if (smem > 48 * 1024)                                                                                     \
       cudaFuncSetAttribute(k_interp_poly<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    k_interp_poly<TT><<<plan.K * plan.S, TT, smem, st>>>(plan, primes, values, cval, coeffs, crt_c, crt_cc); \
+    launch_pdl(k_interp_poly<TT>, dim3(plan.K * plan.S), dim3(TT), smem, st, plan, primes, values, cval, coeffs, \
+               crt_c, crt_cc);                                                                                \
   }
     POLY_LAUNCH(32) POLY_LAUNCH(64) POLY_LAUNCH(128) POLY_LAUNCH(256)
 #undef POLY_LAUNCH

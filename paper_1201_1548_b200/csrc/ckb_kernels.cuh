@@ -6,6 +6,33 @@
 
 namespace ckb {
 
+// ---- programmatic dependent launch (PDL) ----------------------------------
+// The pipeline kernels run back to back on one stream (inside a CUDA graph when
+// replayed).  Each is launched with programmatic stream serialization, so its
+// CTAs may start while the previous kernel's last wave drains; every such
+// kernel executes pdl_wait() (griddepcontrol.wait: the previous grid has
+// completed and its writes are visible) before touching the previous kernels'
+// outputs, and before it exits, which makes completion transitive along the
+// chain.  pdl_launch() lets the next kernel be scheduled once every CTA of
+// this one has started.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+extern bool g_pdl;  // CKB_NO_PDL=1 disables the attribute (A/B measurements)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- K1: coefficient reduction (modpoly.py:376-377) ------------------------
 // limbs: [C][L] two's-complement little-endian u32 words; out: [K][C] in [0,p)
 void launch_reduce(const uint32_t* limbs, int C, int L, const Prime* primes, int K, uint32_t* out,

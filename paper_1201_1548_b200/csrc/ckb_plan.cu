@@ -174,6 +174,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_choose_c(const Prime* __restri
                                                            int lcf_deg, int lcg_off, int lcg_deg,
                                                            uint32_t* __restrict__ cval, uint32_t* status) {
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, N = plan.N;
+  // pdl_launch();  (implicit at exit: measured better)
+  pdl_wait();
   const Prime P = primes[pi];
   const uint32_t p = P.p;
   const uint32_t* lcf = red + (size_t)pi * C + lcf_off;
@@ -216,7 +218,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_choose_c(const Prime* __restri
 
 void launch_choose_c(const Prime* primes, const InterpPlan& plan, const uint32_t* red, int C, int lcf_off,
                      int lcf_deg, int lcg_off, int lcg_deg, uint32_t* cval, uint32_t* status, cudaStream_t st) {
-  k_choose_c<<<plan.K, PLAN_THREADS, 0, st>>>(primes, plan, red, C, lcf_off, lcf_deg, lcg_off, lcg_deg, cval,
+  launch_pdl(k_choose_c, dim3(plan.K), dim3(PLAN_THREADS), 0, st, primes, plan, red, C, lcf_off, lcf_deg, lcg_off,
+             lcg_deg, cval,
                                                status);
 }
 
