@@ -9,6 +9,8 @@
 //     the loop; one Fermat inverse per image),
 //   * images whose remainder sequence is not generic appended to a list that
 //     the general warp kernel (ckb_general.cu) recomputes exactly.
+#include <algorithm>
+
 #include "ckb_kernels.cuh"
 #include "ckb_resultant.cuh"
 #include "ckb_ntt.cuh"
@@ -29,6 +31,31 @@ constexpr int img_minb(int maxd) { return maxd >= 56 ? CKB_IMG_MINB_BIG : CKB_IM
 constexpr int IMG_THREADS = CKB_IMG_THREADS;
 
 constexpr int POLY = 8;  // polyphase factor S: one 8-lane group per coset {w^j y_u}
+
+namespace {
+__device__ __forceinline__ uint32_t img_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void img_mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void img_mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void img_mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void img_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+}  // namespace
 
 // shared-memory row width of the transposed, top-aligned residue tables.  An
 // odd number of 16-byte chunks per row makes the 8 rows read by one lane
@@ -78,6 +105,21 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
   uint32_t* maskA = sm + a.span * TW;
   uint32_t* maskB = maskA + rows;
   uint32_t* som = maskB + rows + tslot * 2 * POLY;  // w^k and companions
+  // K1 wrote the tables in exactly this layout: ONE bulk copy (TMA engine,
+  // cp.async.bulk) lands them in shared memory while the threads build the
+  // chunk masks and their points; an mbarrier signals completion
+  __shared__ __align__(8) uint64_t tab_bar;
+  const uint32_t bar = img_smem_u32(&tab_bar);
+  if (threadIdx.x == 0) {
+    img_mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  pdl_wait();  // K1's tables and k_choose_c's point scales from here on
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)(nspan * TW) * 4u;  // TW * 4 is a multiple of 32
+    img_mbar_expect_tx(bar, bytes);
+    img_bulk_g2s(img_smem_u32(sm), a.tab + (size_t)pi0 * TW, bytes, bar);
+  }
   for (int e = threadIdx.x; e < rows; e += IMG_THREADS) {
     uint32_t ma = 0, mb = 0;
     for (int i = 0; i <= MAXD; ++i) {
@@ -89,24 +131,17 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
   }
   for (int q = threadIdx.x; q < nspan * 2 * POLY; q += IMG_THREADS)
     maskB[rows + q] = a.om[(size_t)(pi0 + q / (2 * POLY)) * 4 * POLY + q % (2 * POLY)];
-  pdl_wait();  // K1's tables and k_choose_c's point scales from here on
-  const uint32_t c = a.cval[pi];
-  {
-    // K1 wrote the tables in exactly this layout: coalesced 16-byte copies
-    const int nt = nspan * TW / 4;
-    const uint4* src = reinterpret_cast<const uint4*>(a.tab + (size_t)pi0 * TW);
-    uint4* dst = reinterpret_cast<uint4*>(sm);
-    for (int idx = threadIdx.x; idx < nt; idx += IMG_THREADS) dst[idx] = src[idx];
-  }
-  __syncthreads();
 
   // image (u, j): x = w^j c y_u.  Lane l of an 8-lane group evaluates the
   // polyphase component G_l = y^l F_l(y^8) of every y-coefficient; a 3-stage
   // DFT across the group then gives f(w^j y) for all j (j = bitrev(l)).
+  const uint32_t c = a.cval[pi];
   const uint32_t p = P.p;
   if (c != 1u) y = shoup(y, c, shoup_comp(c, P), p);  // y_u = c g^u
   const uint32_t y2 = mul_mod(y, y, P), y4 = mul_mod(y2, y2, P);
   const uint32_t z = mul_mod(y4, y4, P);  // Horner variable y^8
+  __syncthreads();     // masks, roots (and the barrier's initialisation) visible
+  img_mbar_wait(bar, 0);  // tables landed
   uint32_t yl = (l & 1) ? y : 1u;          // y^l, l < 8
   if (l & 2) yl = mul_mod(yl, y2, P);
   if (l & 4) yl = mul_mod(yl, y4, P);
@@ -236,29 +271,65 @@ size_t images_tab_words(int m, int n, int dfx, int dgx) {
   return (size_t)2 * rows * images_sw(maxd);
 }
 
-// one thread per table entry: TA[e][i] / TB[e][i] = coefficient of x^e in the
-// y-coefficient of degree d - i of A / B (A the higher y-degree input), 0 in
-// the padding; each real coefficient also lands in red[pi][c]
-__global__ void k_reduce_tab(const uint32_t* __restrict__ limbs, int C, int L, const Prime* __restrict__ primes,
-                             int m, int n, int dfx, int dgx, int rows, int SW, uint32_t* __restrict__ red,
-                             uint32_t* __restrict__ tab) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x, pi = blockIdx.y;
+// K1 for the pipeline, coefficient-major: a thread loads ONE input coefficient's
+// limbs into registers and reduces them modulo a block of RT_PRIMES primes
+// (per-prime constants staged in shared memory), writing each residue to
+// red[pi][c] (coalesced) and to its slot of the images kernel's table layout
+// TA[e][i] / TB[e][i] = coefficient of x^e in the y-coefficient of degree d - i
+// of A / B (A the higher y-degree input).  The padding of the tables is zeroed
+// by a memset first.  (One thread per table entry re-derived the per-prime
+// constants and paid an L2 round trip per entry: 157 us at cfg5.)
+constexpr int RT_PRIMES = 8;
+template <int LMAX>
+__global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__ limbs, int C, int L,
+                                                    const Prime* __restrict__ primes, int K, int m, int n, int dfx,
+                                                    int dgx, int rows, int SW, int rt, uint32_t* __restrict__ red,
+                                                    uint32_t* __restrict__ tab) {
+  __shared__ Prime ps[RT_PRIMES];
+  __shared__ LimbModConst kc[RT_PRIMES];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p0 = blockIdx.y * rt, np = min(rt, K - p0);
   const int TW = 2 * rows * SW;
-  // pdl_launch();  (implicit at exit: measured better)
   pdl_wait();
-  if (idx >= TW) return;
-  const bool sw = m < n;
-  const int sel = idx / (rows * SW), rem = idx % (rows * SW), e = rem / SW, i = rem % SW;
-  const bool isA = sel == 0;
-  const bool useg = isA == sw;  // A = g when swapped
-  const int d = useg ? n : m, str = useg ? dgx + 1 : dfx + 1, off = useg ? (m + 1) * (dfx + 1) : 0;
-  uint32_t r = 0u;
-  if (i <= d && e < str) {
-    const int c = off + (d - i) * str + e;
-    r = limbs_mod(limbs + (size_t)c * L, L, primes[pi]);
-    red[(size_t)pi * C + c] = r;
+  if (threadIdx.x < np) {
+    const Prime P = primes[p0 + threadIdx.x];
+    ps[threadIdx.x] = P;
+    kc[threadIdx.x] = limbs_mod_const(L, P);
   }
-  tab[(size_t)pi * TW + idx] = r;
+  uint32_t w[LMAX > 0 ? LMAX : 1];
+  int entry = 0;
+  bool neg = false;
+  const bool live = c < C;
+  if (live) {
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) {
+      w[l] = (l < L) ? limbs[(size_t)c * L + l] : 0u;
+      if (l == L - 1) neg = w[l] >> 31;
+    }
+    const int cf = (m + 1) * (dfx + 1);
+    const bool isf = c < cf;
+    const int cc = isf ? c : c - cf, str = isf ? dfx + 1 : dgx + 1;
+    const int j = cc / str, e = cc - j * str;
+    const bool isA = isf != (m < n);  // A = g when swapped (the reference swaps so that deg a >= deg b)
+    entry = (isA ? 0 : rows * SW) + e * SW + ((isf ? m : n) - j);
+  }
+  __syncthreads();
+  if (!live) return;
+  for (int q = 0; q < np; ++q) {
+    const uint32_t p = ps[q].p;
+    const LimbModConst k = kc[q];
+    uint32_t r = 0;
+    if (LMAX > 0) {
+#pragma unroll
+      for (int l = LMAX - 1; l >= 0; --l)
+        if (l < L) r = add_mod(shoup(r, k.R1, k.R1c, p), mod_word(w[l], k.onec, p), p);
+      if (neg) r = sub_mod(r, k.big, p);
+    } else {  // very wide coefficients: limbs straight from global memory
+      r = limbs_mod(limbs + (size_t)c * L, L, ps[q]);
+    }
+    red[(size_t)(p0 + q) * C + c] = r;
+    tab[(size_t)(p0 + q) * TW + entry] = r;
+  }
 }
 
 void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes, int K, int m, int n, int dfx,
@@ -268,7 +339,19 @@ void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes,
   const int rows = POLY * (dmax / POLY + 1);
   const int SW = images_sw(maxd);
   const int TW = 2 * rows * SW;
-  k_reduce_tab<<<dim3((TW + 127) / 128, K), 128, 0, st>>>(limbs, C, L, primes, m, n, dfx, dgx, rows, SW, red, tab);
+  cudaMemsetAsync(tab, 0, (size_t)K * TW * 4, st);
+  // primes per CTA: up to RT_PRIMES, fewer when that would leave the grid under ~2 CTAs per SM
+  const int cb = (C + 127) / 128;
+  const int rt = std::max(1, std::min(RT_PRIMES, cb * K / 296));
+  const dim3 grid(cb, (K + rt - 1) / rt);
+  if (L <= 4)
+    launch_pdl(k_reduce_tab<4>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, red, tab);
+  else if (L <= 8)
+    launch_pdl(k_reduce_tab<8>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, red, tab);
+  else if (L <= 16)
+    launch_pdl(k_reduce_tab<16>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, red, tab);
+  else
+    launch_pdl(k_reduce_tab<0>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, red, tab);
 }
 
 int images_maxd(int m, int n) {
