@@ -82,14 +82,14 @@ __device__ __forceinline__ void step1(uint32_t (&D)[MAXD + 1], const uint32_t (&
 // of deg k.  The three multipliers are formed with one REDC each, so they
 // carry a factor R^-1 and the single reduction of the update another; the
 // caller compensates the R^-2 with R^{2k} (res(V, c X) = c^{deg V} res(V, X)).
-// Returns the Montgomery form of lc(V).
+// Returns lc(V) (canonical: the running products absorb one R^-1 per step,
+// compensated once at the end).
 template <int MAXD>
 __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int k,
                                           const Prime& P) {
   const uint32_t p = P.p;
   const uint32_t lb = red4(V[0], p), la = red4(D[0], p);
   const uint32_t nla = la ? p - la : 0u;
-  const uint32_t lbm = to_mont(lb, P);
   // R^-1 (lb^2, -lb la, -la') with la' = lb D[1] - la V[1] the lc of the intermediate remainder
   const uint32_t d1 = red4(D[1], p), v1 = red4(V[1], p);
   const uint32_t w1m = redc((uint64_t)lb * lb, P);
@@ -123,7 +123,7 @@ __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_
   }
   D[MAXD - 1] = 0u;
   D[MAXD] = 0u;
-  return lbm;
+  return lb;
 }
 
 // res(A, B) for top-aligned A (deg da) and B (deg db), da >= db >= 1 with
@@ -183,9 +183,13 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
     den = mmul(den, mmul(Q, Q, P), P);
   }
   if (bad) return CKB_FAIL;
-  // each fused remainder with divisor degree k was stored as R^-2 prem: undo
-  // with R^{2 sum k} = R^{db (db - 1)} (in Montgomery form: mpow of R^2 mod p)
-  const uint32_t corr = mpow(P.r2, db * (db - 1), one, P);
+  // Compensation, one power of R: each fused remainder with divisor degree k
+  // was stored as R^-2 prem (factor R^{2 sum k} = R^{db (db - 1)}), and the
+  // running products took the canonical L_i (T_j carries R^-j, Q_J carries
+  // R^-J(J+1)/2 with J = db - 1 steps), which scales num / den by R^{J(J-1)};
+  // together R^{db (db - 1) - (db - 1)(db - 2)} = R^{2 (db - 1)}
+  // (in Montgomery form: mpow of R^2 mod p)
+  const uint32_t corr = mpow(P.r2, 2 * (db - 1), one, P);
   // num / den (Fermat inverse in the Montgomery domain), leave the domain
   uint32_t inv = one, b = den;
   uint32_t ex = p - 2;
