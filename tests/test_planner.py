@@ -133,3 +133,24 @@ def test_log2_bound_matches_exact_bound():
         for p in primes:
             mod *= p
         assert mod > 4 * planner.det_coeff_bound(fc, gc)
+
+
+def test_limbs_roundtrip_c_helper_and_python():
+    """ints -> two's-complement limbs -> ints through the C helper (30-bit digit
+    repacking) and the pure-Python fallback, 1 to 5,632 bits, signs and edges."""
+    import random
+
+    from paper_1201_1548_b200 import planner
+    rng = random.Random(5)
+    for bits in (1, 5, 29, 30, 31, 32, 33, 59, 60, 61, 63, 64, 65, 100, 3000, 5632):
+        vals = [rng.randint(-(2 ** bits), 2 ** bits) for _ in range(200)]
+        vals += [0, -1, 1, 2 ** bits - 1, -(2 ** bits), -(2 ** (bits - 1)), 2 ** (bits - 1)]
+        L = (bits + 2 + 31) // 32 + 1
+        limbs, _ = planner.ints_to_limbs(vals, L)
+        assert planner.limbs_to_ints(limbs, len(vals), L) == vals, bits
+        saved = planner._ckb_limbs
+        planner._ckb_limbs = None
+        try:
+            assert planner.limbs_to_ints(limbs, len(vals), L) == vals, bits
+        finally:
+            planner._ckb_limbs = saved
