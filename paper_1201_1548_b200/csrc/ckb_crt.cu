@@ -63,6 +63,17 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uns
   if (k >= N) return;
   const unsigned FULL = 0xffffffffu;
   const int LW = T.LW;
+  const unsigned long long* Sk = S + (size_t)k * LWp;
+  // the first chunk's limb sums and modulus limbs are loaded before q is known
+  // (their latency overlaps the q reduction)
+  unsigned long long pre_s[8];
+  uint32_t pre_m[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int l = lane * 8 + j;
+    pre_s[j] = l < LW ? Sk[l] : 0ull;
+    pre_m[j] = l < LW ? T.Ml[l] : 0u;
+  }
   // q = round(sum_i y_i / p_i); lane 0's value is broadcast so every lane agrees bitwise
   const int KC = (T.K + 31) / 32;
   double qs = 0.0;
@@ -72,7 +83,6 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uns
   qs = __shfl_sync(FULL, qs, 0);
   const unsigned long long q = (unsigned long long)llrint(qs);
   const bool ambk = fabs((qs - floor(qs)) - 0.5) < 1e-3;  // near a half-integer: exact fold needed
-  const unsigned long long* Sk = S + (size_t)k * LWp;
   uint32_t* ok = out + (size_t)k * LW;
   long long cin_hi = 0;            // carry into the chunk (signed 128-bit, fits in hi:lo)
   unsigned long long cin_lo = 0;
@@ -86,8 +96,8 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uns
       unsigned long long s_lo = 0, qm = 0;
       long long s_hi = 0;
       if (l < LW) {
-        s_lo = Sk[l];
-        qm = q * (unsigned long long)T.Ml[l];
+        s_lo = c0 == 0 ? pre_s[j] : Sk[l];
+        qm = q * (unsigned long long)(c0 == 0 ? pre_m[j] : T.Ml[l]);
       }
       I128 t;
       t.lo = s_lo - qm;

@@ -67,14 +67,14 @@ __device__ uint32_t warp_resultant(uint32_t* a, int la, uint32_t* b, int lb, uin
 // recompute the fast kernel's failed images
 __global__ void k_images_fallback(ImageArgs a, int W) {
   extern __shared__ uint32_t sm[];
-  uint32_t* fa = sm;
-  uint32_t* gb = sm + W;
-  uint32_t* rr = sm + 2 * W;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t* fa = sm + (size_t)warp * 3 * W;  // one warp per failed image
+  uint32_t* gb = fa + W;
+  uint32_t* rr = fa + 2 * W;
   // pdl_launch();  (implicit at exit: measured better)
   pdl_wait();
   const uint32_t count = *a.fail_count;
-  for (uint32_t idx = blockIdx.x; idx < count; idx += gridDim.x) {
+  for (uint32_t idx = blockIdx.x * nw + warp; idx < count; idx += gridDim.x * nw) {
     const uint32_t flat = a.fail_list[idx];
     const int pi = (int)(flat / (uint32_t)a.N);
     const Prime P = a.primes[pi];
@@ -104,8 +104,10 @@ __global__ void k_images_fallback(ImageArgs a, int W) {
 }
 
 void launch_images_fallback(const ImageArgs& a, cudaStream_t st) {
+  // one CTA of 4 warps per SM (the same 592 warps as 592 one-warp CTAs, a quarter of the CTA launches:
+  // the list is usually empty and the launch is pure overhead)
   const int W = (a.m > a.n ? a.m : a.n) + 2;
-  launch_pdl(k_images_fallback, dim3(4 * 148), dim3(32), (size_t)3 * W * 4, st, a, W);
+  launch_pdl(k_images_fallback, dim3(148), dim3(128), (size_t)4 * 3 * W * 4, st, a, W);
 }
 
 __global__ void k_iota(uint32_t* list, uint32_t n) {
@@ -119,7 +121,9 @@ void launch_images_general(const ImageArgs& a, cudaStream_t st) {
   const uint32_t n = (uint32_t)a.K * (uint32_t)a.N;
   k_iota<<<(n + 255) / 256, 256, 0, st>>>(a.fail_list, n);
   const int W = (a.m > a.n ? a.m : a.n) + 2;
-  k_images_fallback<<<32 * 148, 32, (size_t)3 * W * 4, st>>>(a, W);
+  const size_t smem = (size_t)4 * 3 * W * 4;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_images_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_images_fallback<<<8 * 148, 128, smem, st>>>(a, W);
 }
 
 // batched zp_resultant_uni: one warp per pair
