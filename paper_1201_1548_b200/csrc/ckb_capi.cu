@@ -551,13 +551,18 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   // zero the fail counter first so the kernels below run back to back (PDL)
   if (!general) CK(cudaMemsetAsync(d_fail + (size_t)K * NI, 0, 4, st));
   stage_mark(st);
+  const int lcf_off = m * (dfx + 1), lcg_off = (m + 1) * (dfx + 1) + n * (dgx + 1);
+  const bool merged = !general && reduce_tab_chooses(h_degs[m], h_degs[m + 1 + n]);
   if (general)
     launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
+  else if (merged)  // K1 and the point scales in one launch
+    launch_reduce_tab(d_limbs, C, L, d_primes, K, m, n, dfx, dgx, d_red, d_tab, st, &pl, lcf_off, h_degs[m],
+                      lcg_off, h_degs[m + 1 + n], d_cval, d_status);
   else
     launch_reduce_tab(d_limbs, C, L, d_primes, K, m, n, dfx, dgx, d_red, d_tab, st);
   stage_mark(st);
-  const int lcf_off = m * (dfx + 1), lcg_off = (m + 1) * (dfx + 1) + n * (dgx + 1);
-  launch_choose_c(d_primes, pl, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], d_cval, d_status, st);
+  if (!merged)
+    launch_choose_c(d_primes, pl, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], d_cval, d_status, st);
   stage_mark(st);
   ImageArgs a;
   a.red = d_red;

@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "ckb_kernels.cuh"
+#include "ckb_choose.cuh"
 #include "ckb_resultant.cuh"
 #include "ckb_ntt.cuh"
 
@@ -280,17 +281,37 @@ size_t images_tab_words(int m, int n, int dfx, int dgx) {
 // by a memset first.  (One thread per table entry re-derived the per-prime
 // constants and paid an L2 round trip per entry: 157 us at cfg5.)
 constexpr int RT_PRIMES = 8;
+constexpr int RT_LC_MAX = 256;  // leading-coefficient x-degrees the merged choose role stages
+// Roles by CTA index: the first nred CTAs reduce (coefficient block x prime
+// block); the K CTAs after them each choose one prime's point scale
+// (choose_c_prime), reducing the two leading coefficients straight from the
+// limbs — so the separate k_choose_c launch disappears from the pipeline.
 template <int LMAX>
 __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__ limbs, int C, int L,
                                                     const Prime* __restrict__ primes, int K, int m, int n, int dfx,
-                                                    int dgx, int rows, int SW, int rt, uint32_t* __restrict__ red,
-                                                    uint32_t* __restrict__ tab) {
+                                                    int dgx, int rows, int SW, int rt, int cb, int nred,
+                                                    uint32_t* __restrict__ red, uint32_t* __restrict__ tab,
+                                                    InterpPlan plan, int lcf_off, int lcf_deg, int lcg_off,
+                                                    int lcg_deg, uint32_t* __restrict__ cval, uint32_t* status) {
   __shared__ Prime ps[RT_PRIMES];
   __shared__ LimbModConst kc[RT_PRIMES];
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int p0 = blockIdx.y * rt, np = min(rt, K - p0);
-  const int TW = 2 * rows * SW;
   pdl_wait();
+  if ((int)blockIdx.x >= nred) {  // choose role
+    __shared__ uint32_t lc[2 * RT_LC_MAX];
+    const int pi = blockIdx.x - nred;
+    const Prime P = primes[pi];
+    for (int i = threadIdx.x; i <= lcf_deg + 1 + lcg_deg; i += blockDim.x) {
+      const int c = i <= lcf_deg ? lcf_off + i : lcg_off + (i - lcf_deg - 1);
+      lc[i] = limbs_mod(limbs + (size_t)c * L, L, P);
+    }
+    __syncthreads();
+    choose_c_prime(P, pi, plan, lc, lcf_deg < 0 ? 0 : lcf_deg, lc + lcf_deg + 1, lcg_deg < 0 ? 0 : lcg_deg, cval,
+                   status);
+    return;
+  }
+  const int c = (blockIdx.x % cb) * blockDim.x + threadIdx.x;
+  const int p0 = (blockIdx.x / cb) * rt, np = min(rt, K - p0);
+  const int TW = 2 * rows * SW;
   if (threadIdx.x < np) {
     const Prime P = primes[p0 + threadIdx.x];
     ps[threadIdx.x] = P;
@@ -332,8 +353,11 @@ __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__
   }
 }
 
+bool reduce_tab_chooses(int lcf_deg, int lcg_deg) { return lcf_deg + lcg_deg + 2 <= 2 * RT_LC_MAX; }
+
 void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes, int K, int m, int n, int dfx,
-                       int dgx, uint32_t* red, uint32_t* tab, cudaStream_t st) {
+                       int dgx, uint32_t* red, uint32_t* tab, cudaStream_t st, const InterpPlan* plan, int lcf_off,
+                       int lcf_deg, int lcg_off, int lcg_deg, uint32_t* cval, uint32_t* status) {
   const int maxd = images_maxd(m, n);
   const int dmax = dfx > dgx ? dfx : dgx;
   const int rows = POLY * (dmax / POLY + 1);
@@ -343,15 +367,22 @@ void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes,
   // primes per CTA: up to RT_PRIMES, fewer when that would leave the grid under ~2 CTAs per SM
   const int cb = (C + 127) / 128;
   const int rt = std::max(1, std::min(RT_PRIMES, cb * K / 296));
-  const dim3 grid(cb, (K + rt - 1) / rt);
+  const int nred = cb * ((K + rt - 1) / rt);
+  const int nch = plan ? K : 0;  // + one choose CTA per prime
+  InterpPlan pl = plan ? *plan : InterpPlan{};
+  const dim3 grid(nred + nch);
+#define RT_LAUNCH(LM)                                                                                             \
+  launch_pdl(k_reduce_tab<LM>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, cb, \
+             nred, red, tab, pl, lcf_off, lcf_deg, lcg_off, lcg_deg, cval, status)
   if (L <= 4)
-    launch_pdl(k_reduce_tab<4>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, red, tab);
+    RT_LAUNCH(4);
   else if (L <= 8)
-    launch_pdl(k_reduce_tab<8>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, red, tab);
+    RT_LAUNCH(8);
   else if (L <= 16)
-    launch_pdl(k_reduce_tab<16>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, red, tab);
+    RT_LAUNCH(16);
   else
-    launch_pdl(k_reduce_tab<0>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, red, tab);
+    RT_LAUNCH(0);
+#undef RT_LAUNCH
 }
 
 int images_maxd(int m, int n) {

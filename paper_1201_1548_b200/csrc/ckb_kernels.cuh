@@ -108,8 +108,13 @@ void launch_images_general(const ImageArgs& a, cudaStream_t st);
 // K1 for the pipeline: residues straight into the images kernel's transposed,
 // top-aligned, zero-padded table layout (and the plain [K][C] layout)
 size_t images_tab_words(int m, int n, int dfx, int dgx);
+// with plan != nullptr the same launch also chooses every prime's point scale
+// (k_choose_c's work, one extra CTA per prime) when reduce_tab_chooses(...)
+bool reduce_tab_chooses(int lcf_deg, int lcg_deg);
 void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes, int K, int m, int n, int dfx,
-                       int dgx, uint32_t* red, uint32_t* tab, cudaStream_t st);
+                       int dgx, uint32_t* red, uint32_t* tab, cudaStream_t st, const InterpPlan* plan = nullptr,
+                       int lcf_off = 0, int lcf_deg = 0, int lcg_off = 0, int lcg_deg = 0, uint32_t* cval = nullptr,
+                       uint32_t* status = nullptr);
 // fast generic kernel followed by the general warp kernel on its fail list
 void launch_images(const ImageArgs& a, cudaStream_t st);
 void launch_images_fallback(const ImageArgs& a, cudaStream_t st);

@@ -8,6 +8,7 @@
 // coefficient).  For geometric points the interpolation matrix has closed
 // form (q-binomial theorem), so every table below is a prefix product.
 #include "ckb_kernels.cuh"
+#include "ckb_choose.cuh"
 
 namespace ckb {
 
@@ -166,54 +167,18 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(const Prime* __restrict__
   }
 }
 
-// per call: the point scale c of every prime (modpoly.py:380-390 skips the
-// points where a leading coefficient vanishes; here the whole progression is
-// shifted by c instead, keeping the cached plan valid)
+// per call: the point scale c of every prime (choose_c_prime, ckb_choose.cuh);
+// the pipeline's fast path runs the same function inside the merged K1 kernel
 __global__ void __launch_bounds__(PLAN_THREADS) k_choose_c(const Prime* __restrict__ primes, InterpPlan plan,
                                                            const uint32_t* __restrict__ red, int C, int lcf_off,
                                                            int lcf_deg, int lcg_off, int lcg_deg,
                                                            uint32_t* __restrict__ cval, uint32_t* status) {
-  const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, N = plan.N;
+  const int pi = blockIdx.x;
   // pdl_launch();  (implicit at exit: measured better)
   pdl_wait();
   const Prime P = primes[pi];
-  const uint32_t p = P.p;
-  const uint32_t* lcf = red + (size_t)pi * C + lcf_off;
-  const uint32_t* lcg = red + (size_t)pi * C + lcg_off;
-  if (lcf_deg <= 0 && lcg_deg <= 0) {  // constant leading coefficients
-    if (tid == 0) {
-      cval[pi] = 1u;
-      if (lcf[0] == 0u || lcg[0] == 0u) atomicOr(status, 1u);
-    }
-    return;
-  }
-  // image points x = w^j c y_u, j < S, u < N (polyphase cosets)
-  const int S = plan.S;
-  const uint32_t* yq = plan.yq + (size_t)pi * N;
-  const uint32_t* om = plan.om + (size_t)pi * 4 * S;
-  for (int attempt = 0; attempt < 64; ++attempt) {
-    const uint32_t c = (uint32_t)(attempt + 1) % p;
-    const uint32_t cc = shoup_comp(c, P);
-    int bad = 0;
-    for (int t = tid; t < N * S; t += T) {
-      const int u = t / S, j = t % S;
-      const uint32_t x = shoup(shoup(yq[u], om[j], om[S + j], p), c, cc, p);
-      const uint32_t xc = shoup_comp(x, P);
-      uint32_t vf = 0, vg = 0;
-      for (int i = lcf_deg; i >= 0; --i) vf = add_mod(shoup(vf, x, xc, p), lcf[i], p);
-      for (int i = lcg_deg; i >= 0; --i) vg = add_mod(shoup(vg, x, xc, p), lcg[i], p);
-      if (vf == 0u || vg == 0u) bad = 1;
-    }
-    bad = __syncthreads_or(bad);
-    if (!bad) {
-      if (tid == 0) cval[pi] = c;
-      return;
-    }
-  }
-  if (tid == 0) {
-    cval[pi] = 1u;
-    atomicOr(status, 1u);
-  }
+  choose_c_prime(P, pi, plan, red + (size_t)pi * C + lcf_off, lcf_deg, red + (size_t)pi * C + lcg_off, lcg_deg, cval,
+                 status);
 }
 
 void launch_choose_c(const Prime* primes, const InterpPlan& plan, const uint32_t* red, int C, int lcf_off,

@@ -429,3 +429,20 @@ def test_int_gcd_uni_batch_golden(mp, small):
     cases = small["int_gcd"]
     got = mp.int_gcd_uni_batch([(ints_in(c["f"]), ints_in(c["g"])) for c in cases])
     assert got == [ints_in(c["gcd"]) for c in cases]
+
+
+def test_point_scale_when_leading_coefficient_vanishes_at_roots_of_unity(mp, oracle_mod):
+    """lc_y(f) = x^8 - 1 vanishes at the first coset {w^j} of every prime's planned
+    points, so every prime must shift its point set (c != 1; the reference skips such
+    points, modpoly.py:380-390).  Also with lc_y(g) = x^16 - 1 and a constant lc."""
+    rng = random.Random(17)
+    for lcf, lcg in (([-1] + [0] * 7 + [1], [3]), ([-1] + [0] * 7 + [1], [-1] + [0] * 15 + [1]),
+                     ([5], [-1] + [0] * 15 + [1])):
+        for my, ny in ((6, 5), (12, 12)):
+            f = {(i, j): rng.randint(-999, 999) for j in range(my) for i in range(10)}
+            g = {(i, j): rng.randint(-999, 999) for j in range(ny) for i in range(7)}
+            f.update({(i, my): c for i, c in enumerate(lcf) if c})
+            g.update({(i, ny): c for i, c in enumerate(lcg) if c})
+            f = {k: v for k, v in f.items() if v}
+            g = {k: v for k, v in g.items() if v}
+            assert mp.biv_resultant(f, g, "y") == oracle_mod.biv_resultant(f, g, "y")
