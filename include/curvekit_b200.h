@@ -132,6 +132,11 @@ int ckb_biv_gcd_images(const uint32_t* limbs, int C, int L, const int16_t* degs,
 int ckb_descartes_prepare(const uint32_t* limbs, int n, int L, const uint32_t* primes, const uint32_t* gens, int K);
 int ckb_descartes_variations(int handle, const uint32_t* aw, int AL, int ld, int K, int LW, int32_t* variations);
 int ckb_descartes_release(int handle);
+/* B intervals of one handle in one call (a breadth-first isolation tests a whole
+ * subdivision level at once): aw [B][2][AL], ld [B], variations [B]; K and LW
+ * must cover the largest bound of the batch (1 <= B <= 4096). */
+int ckb_descartes_variations_batch(int handle, const uint32_t* aw, int AL, const int32_t* ld, int B, int K, int LW,
+                                   int32_t* variations);
 
 /* Device-pointer stages for the multi-GPU driver (one process per GPU); primes
  * and gens are HOST arrays (they key the cached interpolation plan).

@@ -17,7 +17,9 @@ def install():
     ``bivpoly`` import ``int_gcd_uni`` lazily (upoly.py:258,372,538,569;
     bivpoly.py:186,268), so they pick up the GPU gcd through the first rebinding.
     Also rebinds ``curvekit.upoly._variations_on`` (the Descartes test of
-    descartes_isolate, upoly.py:338-346) to the GPU version.
+    descartes_isolate, upoly.py:338-346) to the GPU version, and
+    ``curvekit.upoly.descartes_isolate`` (upoly.py:358-408) to a breadth-first
+    version that tests a whole subdivision level per GPU call.
     Rebinds ``curvekit.bivpoly.gcd_biv`` (bivpoly.py:266-295; ``is_squarefree_biv`` and
     ``square_part`` look it up at call time) and the name ``curvekit.bisolve``
     bound at import (bisolve.py:21) to the modular GPU gcd.
@@ -40,6 +42,10 @@ def install():
     from . import upoly as our_upoly
     saved[("curvekit.upoly", "_variations_on")] = getattr(up, "_variations_on")
     setattr(up, "_variations_on", our_upoly.variations_on)
+    # breadth-first isolation: one batched GPU call per subdivision level
+    # (upoly.py:358-408; isolate_decomposition :411-421 and :573 look it up at call time)
+    saved[("curvekit.upoly", "descartes_isolate")] = getattr(up, "descartes_isolate")
+    setattr(up, "descartes_isolate", our_upoly.descartes_isolate)
     bp = importlib.import_module("curvekit.bivpoly")
     from . import bivpoly as our_bivpoly
     saved[("curvekit.bivpoly", "gcd_biv")] = getattr(bp, "gcd_biv")

@@ -23,7 +23,7 @@ EXPORTS = (
     "ckb_interp_points", "ckb_gcd_mod_batch", "ckb_dev_biv_resultant", "ckb_set_timing",
     "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values", "ckb_host_alloc", "ckb_host_free",
     "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release", "ckb_biv_gcd_images",
-    "ckb_biv_resultant_batch",
+    "ckb_biv_resultant_batch", "ckb_descartes_variations_batch",
 )
 
 _P = ctypes.c_void_p
@@ -58,6 +58,7 @@ _SIGS = {
     "ckb_descartes_variations": (_I, [_I, _P, _I, _I, _I, _I, _P]),
     "ckb_descartes_release": (_I, [_I]),
     "ckb_biv_resultant_batch": (_I, [_I] + [_P] * 15),
+    "ckb_descartes_variations_batch": (_I, [_I, _P, _I, _P, _I, _I, _I, _P]),
     "ckb_biv_gcd_images": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P]),
 }
 

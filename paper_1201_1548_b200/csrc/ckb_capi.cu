@@ -219,25 +219,9 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
     }
   }
   if (M[LW]) return fail("CRT output width too small for the prime product", -2);
-  std::vector<uint32_t> hc(K), hcc(K), Mi((size_t)K * LW), Mh(LW);
+  std::vector<uint32_t> Mh(LW);
   std::vector<double> pinvd(K);
-  for (int i = 0; i < K; ++i) {
-    const uint32_t p = primes[i];
-    // M / p_i by long division, and (M/p_i) mod p_i as prod_{l != i} p_l
-    uint64_t rem = 0;
-    for (int l = LW - 1; l >= 0; --l) {
-      const uint64_t cur = (rem << 32) | M[l];
-      Mi[(size_t)i * LW + l] = (uint32_t)(cur / p);
-      rem = cur % p;
-    }
-    uint64_t mod = 1 % p;
-    for (int j = 0; j < K; ++j)
-      if (j != i) mod = mod * (primes[j] % p) % p;
-    if (mod == 0) return fail("CRT primes are not pairwise distinct", -2);
-    hc[i] = h_powmod(mod, p - 2, p);
-    hcc[i] = (uint32_t)(((uint64_t)hc[i] << 32) / p);
-    pinvd[i] = 1.0 / (double)p;
-  }
+  for (int i = 0; i < K; ++i) pinvd[i] = 1.0 / (double)primes[i];
   {
     uint32_t carry = 0;
     for (int l = LW - 1; l >= 0; --l) {
@@ -247,7 +231,7 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
   }
   const size_t nb = 4 * (size_t)K * 3 + 8 * (size_t)K + 4 * (size_t)K * LW + 8 * (size_t)LW + 64;
   CK(cudaMalloc(&e.d_primes, sizeof(Prime) * K));
-  CK(cudaMalloc(&e.d_blob, nb));
+  CK(cudaMalloc(&e.d_blob, nb + 16));
   uint8_t* b = (uint8_t*)e.d_blob;
   double* d_pinvd = (double*)b;  // 8-byte aligned first
   uint32_t* d_p = (uint32_t*)(b + 8 * (size_t)K);
@@ -256,14 +240,24 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
   uint32_t* d_Mi = d_cc + K;
   uint32_t* d_Ml = d_Mi + (size_t)K * LW;
   uint32_t* d_Mh = d_Ml + LW;
+  uint32_t* d_bad = d_Mh + LW;  // one flag word (in the blob's spare bytes)
   CK(cudaMemcpy(e.d_primes, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_pinvd, pinvd.data(), 8 * (size_t)K, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_p, primes, 4 * (size_t)K, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_c, hc.data(), 4 * (size_t)K, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_cc, hcc.data(), 4 * (size_t)K, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_Mi, Mi.data(), 4 * (size_t)K * LW, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_Ml, M.data(), 4 * (size_t)LW, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_Mh, Mh.data(), 4 * (size_t)LW, cudaMemcpyHostToDevice));
+  CK(cudaMemset(d_bad, 0, 4));
+  // M / p_i and (M / p_i)^-1 mod p_i on the device (one thread per prime)
+  launch_crt_tables(d_p, K, d_Ml, LW, d_Mi, d_c, d_cc, d_bad, g.stream);
+  CK(cudaGetLastError());
+  uint32_t hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, d_bad, 4, cudaMemcpyDeviceToHost, g.stream));
+  CK(cudaStreamSynchronize(g.stream));
+  if (hbad) {
+    cudaFree(e.d_primes);
+    cudaFree(e.d_blob);
+    return fail("CRT primes are not pairwise distinct", -2);
+  }
   e.t.K = K;
   e.t.LW = LW;
   e.t.p = d_p;
@@ -1222,36 +1216,46 @@ int ckb_descartes_prepare(const uint32_t* limbs, int n, int L, const uint32_t* p
   return h;
 }
 
-int ckb_descartes_variations(int handle, const uint32_t* aw, int AL, int ld, int K, int LW, int32_t* variations) {
+int ckb_descartes_variations_batch(int handle, const uint32_t* aw, int AL, const int32_t* ld, int B, int K, int LW,
+                                   int32_t* variations) {
   std::lock_guard<std::mutex> lk(g_mu);
   int rc;
   if ((rc = ensure_ready())) return rc;
   if (handle < 0 || handle >= (int)g_desc.size() || !g_desc[handle].used)
     return fail("ckb_descartes_variations: bad handle", -2);
   DescHandle& d = g_desc[handle];
-  if (K < 1 || K > d.K || AL < 1 || ld < 0 || LW < 1) return fail("ckb_descartes_variations: bad sizes", -2);
+  if (K < 1 || K > d.K || AL < 1 || LW < 1 || B < 1 || B > 4096) return fail("ckb_descartes_variations: bad sizes", -2);
+  for (int b = 0; b < B; ++b)
+    if (ld[b] < 0) return fail("ckb_descartes_variations: negative ld", -2);
   cudaStream_t st = g.stream;
   const int N = d.n + 1;
   CrtEntry* ce;
   if ((rc = get_crt(d.primes.data(), K, LW, &ce))) return rc;
   uint32_t *d_aw, *d_c, *d_out, *d_crtS;
-  int32_t* d_v;
-  if ((rc = dbuf("desc.aw", 2 * (size_t)AL, &d_aw))) return rc;
-  if ((rc = dbuf("desc.c", (size_t)K * N, &d_c))) return rc;
-  if ((rc = dbuf("desc.out", (size_t)N * LW, &d_out))) return rc;
-  if ((rc = dbuf("desc.v", 1, &d_v))) return rc;
-  if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
-  CK(cudaMemcpyAsync(d_aw, aw, 8 * (size_t)AL, cudaMemcpyHostToDevice, st));
+  int32_t *d_v, *d_ld;
+  const size_t NB = (size_t)N * B;  // every interval's coefficients side by side: one CRT
+  if ((rc = dbuf("desc.aw", 2 * (size_t)AL * B, &d_aw))) return rc;
+  if ((rc = dbuf("desc.ld", (size_t)B, &d_ld))) return rc;
+  if ((rc = dbuf("desc.c", (size_t)K * NB, &d_c))) return rc;
+  if ((rc = dbuf("desc.out", NB * LW, &d_out))) return rc;
+  if ((rc = dbuf("desc.v", (size_t)B, &d_v))) return rc;
+  if ((rc = dbuf("crtS", crt_scratch_words(K, (int)NB, LW), &d_crtS))) return rc;
+  CK(cudaMemcpyAsync(d_aw, aw, 8 * (size_t)AL * B, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_ld, ld, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
   DescPlan pl = d.pl;
   pl.K = K;  // the first K primes of the prepared set
-  launch_desc_shift(d.d_primes, pl, d.d_res, d_aw, AL, ld, d_c, st);
-  launch_crt(ce->t, d_c, N, d_out, d_crtS, st);
-  launch_desc_signs(d_out, N, LW, d_v, st);
+  launch_desc_shift(d.d_primes, pl, d.d_res, d_aw, AL, d_ld, B, d_c, st);
+  launch_crt(ce->t, d_c, (int)NB, d_out, d_crtS, st);
+  launch_desc_signs(d_out, N, LW, B, d_v, st);
   g.launches += 5;
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(variations, d_v, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(variations, d_v, 4 * (size_t)B, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return 0;
+}
+
+int ckb_descartes_variations(int handle, const uint32_t* aw, int AL, int ld, int K, int LW, int32_t* variations) {
+  return ckb_descartes_variations_batch(handle, aw, AL, &ld, 1, K, LW, variations);
 }
 
 int ckb_descartes_release(int handle) {

@@ -109,12 +109,18 @@ void launch_desc_plan(const Prime* primes, const uint32_t* gens, const DescPlan&
   k_desc_plan<<<pl.K, DT, smem, st>>>(primes, gens, pl);
 }
 
-// c_k mod p for every prime: res [K][n+1] residues of p; aw [2][AL] limbs of a, w
+// c_k mod p for every prime and every interval b (grid.y): res [K][n+1]
+// residues of p; aw [B][2][AL] limbs of a, w; lds [B]; out [K][B (n+1)]
+// (interval b's coefficients at columns b (n+1) + k: one CRT lifts them all)
 __global__ void __launch_bounds__(DT) k_desc_shift(const Prime* __restrict__ primes, DescPlan pl,
-                                                   const uint32_t* __restrict__ res, const uint32_t* __restrict__ aw,
-                                                   int AL, int ld, uint32_t* __restrict__ out) {
+                                                   const uint32_t* __restrict__ res, const uint32_t* __restrict__ aws,
+                                                   int AL, const int32_t* __restrict__ lds,
+                                                   uint32_t* __restrict__ outs) {
   extern __shared__ uint32_t sm[];  // X [L], Y [L], twiddles 4 x [L/2]
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, n = pl.n, L = pl.L, half = L >> 1;
+  const int b = blockIdx.y, B = gridDim.y;
+  const uint32_t* aw = aws + (size_t)b * 2 * AL;
+  const int ld = lds[b];
   const Prime P = primes[pi];
   const uint32_t p = P.p;
   uint32_t* X = sm;
@@ -180,21 +186,24 @@ __global__ void __launch_bounds__(DT) k_desc_shift(const Prime* __restrict__ pri
   __syncthreads();
   ntt_dit8<DT>(Y, pl.logL, Wi, Wic, p);
   // c_k = 1/k! * conv[n-k] / L
-  for (int k = tid; k <= n; k += T)
-    out[(size_t)pi * (n + 1) + k] = mul_mod(mul_mod(red1(Y[n - k], p), linv, P), ifact[k], P);
+  uint32_t* out = outs + (size_t)pi * B * (n + 1) + (size_t)b * (n + 1);
+  for (int k = tid; k <= n; k += T) out[k] = mul_mod(mul_mod(red1(Y[n - k], p), linv, P), ifact[k], P);
 }
 
 void launch_desc_shift(const Prime* primes, const DescPlan& pl, const uint32_t* res, const uint32_t* aw, int AL,
-                       int ld, uint32_t* out, cudaStream_t st) {
+                       const int32_t* ld, int B, uint32_t* out, cudaStream_t st) {
   const size_t smem = (size_t)pl.L * 4 * 4;  // X, Y, 4 half-length twiddle tables
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_desc_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_desc_shift<<<pl.K, DT, smem, st>>>(primes, pl, res, aw, AL, ld, out);
+  k_desc_shift<<<dim3(pl.K, B), DT, smem, st>>>(primes, pl, res, aw, AL, ld, out);
 }
 
 // sign variations of the lifted coefficients limbs [N][LW] (two's complement),
-// upoly.sign_variations (:215-224): zeros are skipped, count sign changes
-__global__ void __launch_bounds__(1024) k_desc_signs(const uint32_t* __restrict__ limbs, int N, int LW,
-                                                     int32_t* __restrict__ result) {
+// upoly.sign_variations (:215-224): zeros are skipped, count sign changes; one
+// CTA per interval (rows b N .. b N + N - 1)
+__global__ void __launch_bounds__(1024) k_desc_signs(const uint32_t* __restrict__ limbs_all, int N, int LW,
+                                                     int32_t* __restrict__ results) {
+  const uint32_t* limbs = limbs_all + (size_t)blockIdx.x * N * LW;
+  int32_t* result = results + blockIdx.x;
   __shared__ int cnt[1024];
   __shared__ int8_t sg[16384];
   const int tid = threadIdx.x, T = blockDim.x;
@@ -242,8 +251,8 @@ __global__ void __launch_bounds__(1024) k_desc_signs(const uint32_t* __restrict_
   }
 }
 
-void launch_desc_signs(const uint32_t* limbs, int N, int LW, int32_t* result, cudaStream_t st) {
-  k_desc_signs<<<1, 1024, 0, st>>>(limbs, N, LW, result);
+void launch_desc_signs(const uint32_t* limbs, int N, int LW, int B, int32_t* result, cudaStream_t st) {
+  k_desc_signs<<<B, 1024, 0, st>>>(limbs, N, LW, result);
 }
 
 }  // namespace ckb

@@ -162,9 +162,10 @@ struct DescPlan {
   uint32_t* Linv;          // [K] 1/L
 };
 void launch_desc_plan(const Prime* primes, const uint32_t* gens, const DescPlan& pl, cudaStream_t st);
+// B intervals at once: aw [B][2][AL], ld [B] (device) -> out [K][B N]; signs: B results
 void launch_desc_shift(const Prime* primes, const DescPlan& pl, const uint32_t* res, const uint32_t* aw, int AL,
-                       int ld, uint32_t* out, cudaStream_t st);
-void launch_desc_signs(const uint32_t* limbs, int N, int LW, int32_t* result, cudaStream_t st);
+                       const int32_t* ld, int B, uint32_t* out, cudaStream_t st);
+void launch_desc_signs(const uint32_t* limbs, int N, int LW, int B, int32_t* result, cudaStream_t st);
 
 // tensor-core CRT product (ckb_crt_mma.cu): byte table size / builder, and the
 // GEMM y (A layout) -> S [N][32 ceil(LW/32)] u64 limb sums
@@ -176,6 +177,9 @@ void launch_crt_mma(const CrtTables& t, const uint32_t* y, int N, unsigned long 
 void launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
                 cudaStream_t st, bool input_is_y = false);
 size_t crt_scratch_words(int K, int N, int LW);  // scratch size for launch_crt
+// M/p_i limbs [K][LW] and c_i = (M/p_i)^-1 mod p_i (+ Shoup companions) from M's limbs; bad |= 1 on repeated primes
+void launch_crt_tables(const uint32_t* primes, int K, const uint32_t* M, int LW, uint32_t* Mi, uint32_t* c,
+                       uint32_t* cc, uint32_t* bad, cudaStream_t st);
 
 // ---- K6: batched gcd mod p (modpoly.py:115-122), interpolation at arbitrary points
 void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_t* gb, const int32_t* db, int Wg,

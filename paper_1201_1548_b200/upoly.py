@@ -248,3 +248,110 @@ def variations_on(p, a, b) -> int:
     lib = _lib.lib()
     _lib.check(lib.ckb_descartes_variations(h, _lib.ptr(aw), AL, ld, K, LW, _lib.ptr(v)), "ckb_descartes_variations")
     return int(v[0])
+
+
+def _variation_bits(p, n: int, a_num: int, w: int, ld: int) -> float:
+    # |c|_inf <= 2^n |r|_1 <= 2^n sum_i |p_i| 2^(ld (n-i)) (|a| + |w|)^i   (bit-length bounds)
+    t = (abs(a_num) + abs(w)).bit_length()
+    top = max(abs(p[i]).bit_length() + ld * (n - i) + i * t for i in range(n + 1) if p[i])
+    return top + math.log2(n + 1) + n + 4  # M > 4 * bound for the explicit CRT
+
+
+def variations_batch(p, intervals) -> list:
+    """[variations_on(p, a, b) for (a, b) in intervals] with whole batches of
+    intervals in one library call (ckb_descartes_variations_batch: every
+    interval's Taylor shift for every prime in one launch, one CRT over all
+    their coefficients, one sign count per interval)."""
+    from . import _lib
+    from .planner import ints_to_limbs
+    import numpy as np
+    intervals = list(intervals)
+    n = len(p) - 1
+    while n >= 0 and p[n] == 0:
+        n -= 1
+    if n < 1:
+        return [0] * len(intervals)
+    if n > 8191:
+        raise NotImplementedError("Descartes test supports degree < 8192")
+    params = []
+    for a, b in intervals:
+        e = min(a.exp, b.exp, 0)
+        a_num = a.man << (a.exp - e)
+        b_num = b.man << (b.exp - e)
+        params.append((a_num, b_num - a_num, -e))
+    out = [0] * len(intervals)
+    lib = _lib.lib()
+    i0 = 0
+    while i0 < len(params):
+        # chunk so that the CRT input and output stay within ~1 GB of HBM
+        bits = max(_variation_bits(p, n, a_num, w, ld) for a_num, w, ld in params[i0:i0 + 256])
+        K = _primes_for_bits(bits)
+        LW = (int(_log2_prefix[K - 1]) + 1 + 1 + 31) // 32 + 1
+        B = max(1, min(256, len(params) - i0, (1 << 28) // ((n + 1) * (K + 2 * LW))))
+        chunk = params[i0:i0 + B]
+        h, _ = _desc.get(p, n, K)
+        aw, AL = ints_to_limbs([v for a_num, w, _ in chunk for v in (a_num, w)])
+        lds = np.array([ld for _, _, ld in chunk], dtype=np.int32)
+        v = np.zeros(len(chunk), dtype=np.int32)
+        _lib.check(lib.ckb_descartes_variations_batch(h, _lib.ptr(aw), AL, _lib.ptr(lds), len(chunk), K, LW,
+                                                      _lib.ptr(v)), "ckb_descartes_variations_batch")
+        out[i0:i0 + len(chunk)] = [int(x) for x in v]
+        i0 += len(chunk)
+    return out
+
+
+def descartes_isolate(p, check_squarefree: bool = True, multiplicity: int = 1) -> list:
+    """curvekit.upoly.descartes_isolate (pkg/src/curvekit/upoly.py:358-408), breadth first.
+
+    The reference pops one interval at a time off a stack and runs one Descartes
+    test per pop; the subdivision of an interval depends only on that interval
+    (its test and its own split point), so the set of leaves — the isolating
+    intervals — does not depend on the traversal order.  Here every interval of
+    a subdivision level is tested in ONE batched GPU call (variations_batch);
+    split points, the zero root, sorting and _make_disjoint are the reference's
+    own code, so the returned brackets are identical.  Needs curvekit (it
+    returns the reference's AlgebraicNumber objects).
+    """
+    import importlib
+    U = importlib.import_module("curvekit.upoly")
+    if any(isinstance(c, Fraction) for c in p):
+        p = U.clear_denominators(p)
+    p = U.primitive(U.trim(list(p)))
+    if not p:
+        raise ValueError("zero polynomial")
+    if check_squarefree:
+        from .modpoly import int_gcd_uni
+        if U.degree(int_gcd_uni(p, U.derivative(p))) > 0:
+            raise ValueError("polynomial is not square-free")
+    roots = []
+    work = list(p)
+    if U.degree(work) <= 0:
+        return []
+    if work[0] == 0:
+        i = next(i for i, c in enumerate(work) if c)
+        work = work[i:]
+        roots.append(U.AlgebraicNumber(tuple(p), U.RealInterval.point(U.ZERO), multiplicity, exact=Fraction(0)))
+    if U.degree(work) > 0:
+        defining = tuple(U.primitive(work))
+        k = U.cauchy_bound_log2(work)
+        bound = U.Dyadic(1, k)
+        level = [(-bound, bound)]
+        while level:
+            vs = variations_batch(work, level)
+            nxt = []
+            for (a, b), v in zip(level, vs):
+                if v == 0:
+                    continue
+                if v == 1:
+                    roots.append(U.AlgebraicNumber(defining, U.RealInterval(a, b), multiplicity))
+                    continue
+                for m in U._interior_points(a, b):
+                    if U.eval_dyadic(work, m).sign() != 0:
+                        break
+                else:  # pragma: no cover
+                    raise ArithmeticError("no non-root subdivision point found")
+                nxt.append((a, m))
+                nxt.append((m, b))
+            level = nxt
+    roots.sort(key=lambda r: r.interval.midpoint().as_fraction())
+    return U._make_disjoint(roots)

@@ -131,3 +131,40 @@ def test_cfg3_isolation_matches_reference(curvekit_mod):
     got = [[str(x.interval.lo.man), x.interval.lo.exp, str(x.interval.hi.man), x.interval.hi.exp] for x in roots]
     assert got == want["roots"]
     print("cfg3 isolation %.2f s (reference %.1f s)" % (dt, want["seconds"]))
+
+
+@pytest.mark.gpu
+def test_batched_variations_and_breadth_first_isolation(gold, curvekit_mod):
+    """variations_batch (one launch for many intervals) equals the single-interval
+    test, and the breadth-first descartes_isolate that install() binds returns the
+    brackets of the reference's depth-first loop (run here with the GPU test)."""
+    import curvekit.upoly as U
+
+    import paper_1201_1548_b200 as pkg
+    from paper_1201_1548_b200 import upoly as ours
+    polys = {}
+    for c in gold["cases"]:
+        key = c["name"] if "p" not in c else repr(c["p"])[:64]
+        polys.setdefault(key, []).append(c)
+    for key, cases in polys.items():
+        p = _poly(gold, cases[0])
+        ivs = [(Dy(int(c["am"]), c["ae"]), Dy(int(c["bm"]), c["be"])) for c in cases]
+        assert ours.variations_batch(p, ivs) == [c["v"] for c in cases], key
+    saved = pkg.install()
+    try:
+        assert U.descartes_isolate is ours.descartes_isolate
+        dfs = saved[("curvekit.upoly", "descartes_isolate")]  # the reference's own loop
+        for iso in gold["isolations"]:
+            p = ints_in(iso["p"])
+            a = [(str(r.interval.lo.man), r.interval.lo.exp, str(r.interval.hi.man), r.interval.hi.exp, r.multiplicity)
+                 for r in ours.descartes_isolate(p, multiplicity=2)]
+            b = [(str(r.interval.lo.man), r.interval.lo.exp, str(r.interval.hi.man), r.interval.hi.exp, r.multiplicity)
+                 for r in dfs(p, multiplicity=2)]
+            assert a == b, iso["name"]
+        with pytest.raises(ValueError):
+            ours.descartes_isolate([])
+        with pytest.raises(ValueError):
+            ours.descartes_isolate([1, -2, 1])  # (x - 1)^2 is not square-free
+        assert [r.exact for r in ours.descartes_isolate([0, 1])] == [0]
+    finally:
+        pkg.uninstall(saved)
