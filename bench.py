@@ -57,11 +57,31 @@ def workload(config):
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 
+_NVML_POLL = r"""
+import sys, time
+import pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+bits = [pynvml.nvmlClocksThrottleReasonHwSlowdown, pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+        pynvml.nvmlClocksThrottleReasonSwThermalSlowdown, pynvml.nvmlClocksThrottleReasonSwPowerCap]
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+out = sys.stdout
+while True:
+    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+    out.write("%d %d %d %s\n" % (time.monotonic_ns(), sm, mx, "".join("1" if rs & b else "0" for b in bits)))
+    out.flush()
+    time.sleep(0.002)
+"""
+
+
 class Clocks:
     """SM clock and throttle reasons sampled DURING the timed region.
 
-    NVML (nvidia-ml-py) is polled every ~1 ms from a thread (costs ~0.3% of a 0.33 ms step), so even a few-ms
-    timed region gets many samples; without NVML, `nvidia-smi -lms 100`."""
+    A separate process polls NVML (nvidia-ml-py) every ~2 ms with monotonic
+    timestamps (no contention with this process's GIL); the samples inside the
+    timed window are kept (faster polling measurably perturbs a 0.06 ms step:
+    cfg2 +6% at 0.5 ms).  Without NVML: `nvidia-smi -lms 100`."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -69,76 +89,85 @@ class Clocks:
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []      # nvidia-smi rows
-        self.samples = []   # (sm_mhz, max_mhz, reasons) from NVML
+        self.rows = []      # nvidia-smi rows, or NVML lines "t sm max bits"
         self.proc = None
-        self.nvml = None
-        self.stop = threading.Event()
+        self.nvml = False
+        self.t0 = self.t1 = None
+
+    def _start(self, cmd, nvml):
+        self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.nvml = nvml
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
 
     def __enter__(self):
-        try:
-            if os.environ.get("CKB_BENCH_NO_NVML"):
-                raise ImportError
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            bits = [pynvml.nvmlClocksThrottleReasonHwSlowdown, pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
-                    pynvml.nvmlClocksThrottleReasonSwThermalSlowdown, pynvml.nvmlClocksThrottleReasonSwPowerCap]
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            self.nvml = pynvml
-
-            def poll():
-                while not self.stop.is_set():
-                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                    rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                    self.samples.append((sm, mx, [n for n, b_ in zip(self.NAMES, bits) if rs & b_]))
-                    time.sleep(0.001)
-            self.thread = threading.Thread(target=poll, daemon=True)
-            self.thread.start()
-            time.sleep(0.002)
-            return self
-        except Exception:  # no NVML: nvidia-smi sampling
-            self.nvml = None
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
+        started = False
+        if not os.environ.get("CKB_BENCH_NO_NVML"):
+            try:
+                import pynvml  # noqa: F401
+                self._start([sys.executable, "-c", _NVML_POLL, str(self.index)], True)
+                deadline = time.time() + 20
+                while not self.rows and self.proc.poll() is None and time.time() < deadline:
+                    time.sleep(0.01)
+                started = bool(self.rows)
+                if not started:
+                    self._stop()
+            except (ImportError, OSError):
+                started = False
+        if not started:
+            try:
+                self.rows = []
+                self._start(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                             "--format=csv,noheader,nounits", "-lms", "100"], False)
+            except OSError:
+                self.proc = None
+        self.t0 = time.monotonic_ns()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append(line.strip())
 
-    def __exit__(self, *a):
-        if self.nvml is not None:
-            self.stop.set()
-            self.thread.join(timeout=1)
-            return
+    def _stop(self):
         if self.proc:
-            time.sleep(0.25)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def __exit__(self, *a):
+        self.t1 = time.monotonic_ns()
+        if self.proc and not self.nvml:
+            time.sleep(0.25)
+        elif self.proc:
+            time.sleep(0.002)  # let the poller report past the end of the window
+        self._stop()
+
     def summary(self):
-        if self.samples:
-            sm = [s[0] for s in self.samples]
-            reasons = sorted({r for s in self.samples for r in s[2]})
-            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
-                    "sm_min_mhz": min(sm), "reasons": reasons, "samples": len(sm), "source": "nvml"}
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        reasons = sorted({self.NAMES[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        if self.nvml:
+            pts = []
+            for r in self.rows:
+                f = r.split()
+                if len(f) == 4 and f[0].isdigit():
+                    pts.append((int(f[0]), int(f[1]), int(f[2]), f[3]))
+            inside = [x for x in pts if self.t0 <= x[0] <= self.t1]
+            # a window shorter than the poll period still gets its nearest samples
+            use = inside or sorted(pts, key=lambda x: abs(x[0] - (self.t0 + self.t1) // 2))[:2]
+            if use:
+                sm = [x[1] for x in use]
+                reasons = sorted({n for x in use for n, bit in zip(self.NAMES, x[3]) if bit == "1"})
+                return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(x[2] for x in use), "sm_min_mhz": min(sm),
+                        "reasons": reasons, "samples": len(use), "samples_in_window": len(inside),
+                        "window_ms": (self.t1 - self.t0) / 1e6, "source": "nvml (separate process)"}
+        rows = [[x.strip() for x in r.split(",")] for r in self.rows if "," in r]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[k] for r in rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "source": "nvidia-smi"}
+                "reasons": reasons, "samples": len(rows), "source": "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
