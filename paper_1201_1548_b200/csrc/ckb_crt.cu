@@ -160,23 +160,29 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uns
       ones &= (o[j] == 0xffffffffu);
       zeros &= (o[j] == 0u);
     }
-    // sequential carry-ins along the lanes (c is small: |c| < 2^63)
-    long long my_cin = 0;  // carry into this lane's segment (fits in 64 bits)
-    long long run = (long long)cin_lo;  // carry entering lane 0 (|.| < 2^63)
-    (void)cin_hi;
-    for (int s = 0; s < 32; ++s) {
-      if (lane == s) {
-        my_cin = run;
-        // value added to limbs 0..1: seg_lo + run (signed); carry kappa into limb 2
-        const unsigned long long u = seg_lo + (unsigned long long)run;
-        long long kappa = (run >= 0) ? (long long)(u < seg_lo) : -(long long)(u > seg_lo);
-        long long delta = 0;
-        if (kappa == 1 && ones) delta = 1;
-        if (kappa == -1 && zeros) delta = -1;
-        run = (long long)c.lo + delta;  // this lane's carry-out
-      }
-      run = __shfl_sync(FULL, run, s);
+    // carry-ins along the lanes: lane s's carry-out is c + delta_s(cin_s), delta in
+    // {-1, 0, 1} (nonzero only when the carry-in overflows the low 64 bits AND
+    // limbs 2..7 are all ones / all zeros).  Fixed-point iteration from lane 0's
+    // known carry-in: after t rounds lanes 0..t-1 are exact, and a round in
+    // which nothing changes is exact everywhere (the chain is anchored at lane
+    // 0); typically 1-3 rounds instead of 32 sequential steps.
+    long long my_cin = 0;
+    long long co = (long long)c.lo;  // this lane's carry-out, current estimate
+    for (int it = 0; it < 33; ++it) {
+      const long long up = __shfl_up_sync(FULL, co, 1);
+      const long long cin = (lane == 0) ? (long long)cin_lo : up;
+      const unsigned long long u = seg_lo + (unsigned long long)cin;
+      const long long kappa = (cin >= 0) ? (long long)(u < seg_lo) : -(long long)(u > seg_lo);
+      long long delta = 0;
+      if (kappa == 1 && ones) delta = 1;
+      if (kappa == -1 && zeros) delta = -1;
+      const long long nco = (long long)c.lo + delta;
+      const bool changed = nco != co;
+      co = nco;
+      my_cin = cin;
+      if (!__any_sync(FULL, changed)) break;
     }
+    const long long run = __shfl_sync(FULL, co, 31);  // carry out of lane 31 = into the next chunk
     // apply the carry-in
     {
       const unsigned long long u = seg_lo + (unsigned long long)my_cin;

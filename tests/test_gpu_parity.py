@@ -193,6 +193,9 @@ def test_crt_lift_roundtrip_large(mp, K, extra):
     for p in primes:
         M *= p
     vals = [rng.randint(-(M // 2) + 1, M // 2) for _ in range(300 + extra)] + [0, 1, -1, M // 2, -(M // 2) + 1]
+    # every magnitude: long runs of sign-extension limbs exercise the carry propagation across lanes and chunks
+    vals += [s * rng.randint(1, 2 ** b) for b in range(0, M.bit_length() - 2, 23) for s in (-1, 1)]
+    vals += [s * (2 ** b - 1) for b in range(1, M.bit_length() - 2, 61) for s in (-1, 1)]
     res = np.array([[v % p for v in vals] for p in primes], dtype=np.uint32)
     assert mp.crt_lift(res, primes) == vals
 
