@@ -451,6 +451,8 @@ def run_ours(args):
                                         f"primes/{world}, all-to-all, CRT coefficients/{world}")),
             "images_per_s": images * 1e3 / ms_per_step,
             "stages_ms": stages,
+            "stages_note": ("CUDA events between the stages of one single-GPU pipeline call (timing mode: no graph)"
+                            + ("" if world == 1 else "; measured on rank 0's GPU alone")),
             "cold_first_call_ms": t_cold * 1e3,
             "cold_note": "first res_y of the process: builds the cached interpolation plan and CRT tables "
                          "(input-independent, keyed by primes and N, like an FFT plan); value is warm",
