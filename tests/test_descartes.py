@@ -168,3 +168,22 @@ def test_batched_variations_and_breadth_first_isolation(gold, curvekit_mod):
         assert [r.exact for r in ours.descartes_isolate([0, 1])] == [0]
     finally:
         pkg.uninstall(saved)
+
+
+@pytest.mark.gpu
+def test_variations_batch_chunking_vs_oracle():
+    """More intervals than one library call takes (chunks of <= 256), mixed widths
+    and exponents (different prime counts per interval within a chunk)."""
+    from oracle import oracle
+    from paper_1201_1548_b200.upoly import variations_batch
+    rng = random.Random(23)
+    for deg in (7, 33):
+        p = [rng.randint(-2 ** 50, 2 ** 50) for _ in range(deg + 1)]
+        p[-1] = p[-1] or 5
+        ivs = []
+        for _ in range(600):
+            a = Dy(rng.randint(-2 ** 30, 2 ** 30), rng.randint(-70, 3))
+            b = Dy(a.man * 2 ** max(0, a.exp - (a.exp - 1)) + rng.randint(1, 2 ** 20), a.exp)
+            ivs.append((a, b))
+        want = [oracle.variations_on(p, a.man, a.exp, b.man, b.exp) for a, b in ivs]
+        assert variations_batch(p, ivs) == want
