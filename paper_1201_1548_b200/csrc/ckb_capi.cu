@@ -585,7 +585,8 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   stage_mark(st);
   launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr);
   stage_mark(st);
-  g.launches += 5;
+  // reduce (+ choose when merged), [choose], images (general: iota + warp kernel), fallback, interpolation
+  g.launches += general ? 5 : (merged ? 4 : 5);
   CK(cudaGetLastError());
   return 0;
 }
