@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CKB_ABI_VERSION 3
+#define CKB_ABI_VERSION 4
 #define CKB_STATUS_REPLAN 1 /* a prime had no admissible evaluation points: re-plan without it */
 
 int ckb_abi_version(void);
@@ -165,6 +165,10 @@ int ckb_host_free(void* p);
  * calls; ckb_stage_times returns the durations (ms) of reduce, plan, images,
  * interpolation, CRT for the last call (count returned). */
 int ckb_set_timing(int on);
+/* Internal graph replay on (1, default) or off (0): off while a caller captures
+ * the library's launches into its own CUDA graph (e.g. a whole multi-GPU step
+ * with its NCCL collective), so they are recorded as plain kernel nodes. */
+int ckb_set_graphs(int on);
 int ckb_stage_times(float* ms, int max);
 
 /* Roofline denominators measured on the current device (csrc/ckb_peak.cu):

@@ -23,7 +23,7 @@ EXPORTS = (
     "ckb_interp_points", "ckb_gcd_mod_batch", "ckb_dev_biv_resultant", "ckb_set_timing",
     "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values", "ckb_host_alloc", "ckb_host_free",
     "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release", "ckb_biv_gcd_images",
-    "ckb_biv_resultant_batch", "ckb_descartes_variations_batch",
+    "ckb_biv_resultant_batch", "ckb_descartes_variations_batch", "ckb_set_graphs",
 )
 
 _P = ctypes.c_void_p
@@ -49,6 +49,7 @@ _SIGS = {
     "ckb_dev_crt": (_I, [_P, _I, _I, _P, _I, _P, _P]),
     "ckb_dev_biv_resultant": (_I, [_P, _I, _I, _P, _P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P, _P]),
     "ckb_set_timing": (_I, [_I]),
+    "ckb_set_graphs": (_I, [_I]),
     "ckb_stage_times": (_I, [_P, _I]),
     "ckb_measure_peak": (_I, [_P, _I]),
     "ckb_psc_values": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, ctypes.c_uint32, _I, _P, _P]),

@@ -1283,6 +1283,13 @@ int ckb_host_free(void* p) {
   return 0;
 }
 
+int ckb_set_graphs(int on) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  const char* e = getenv("CKB_NO_GRAPHS");
+  g.graphs = on != 0 && !(e && e[0] == '1');
+  return 0;
+}
+
 int ckb_set_timing(int on) {
   std::lock_guard<std::mutex> lk(g_mu);
   g.timing = on != 0;
