@@ -28,44 +28,45 @@ def install():
     Returns the previous bindings (pass them to ``uninstall``).
     """
     import importlib
-
-    from . import modpoly as ours
-    ref = importlib.import_module("curvekit.modpoly")
     saved = {}
-    for name in ("biv_resultant", "int_gcd_uni", "zp_resultant_uni", "zp_interpolate",
-                 "zp_gcd_sylvester", "crt_reconstruct", "modular_subres_profile"):
-        saved[("curvekit.modpoly", name)] = getattr(ref, name)
-        setattr(ref, name, getattr(ours, name))
-    # the Descartes test of real-root isolation (upoly.py:338-346), looked up
-    # by descartes_isolate at call time
-    up = importlib.import_module("curvekit.upoly")
-    from . import upoly as our_upoly
-    saved[("curvekit.upoly", "_variations_on")] = getattr(up, "_variations_on")
-    setattr(up, "_variations_on", our_upoly.variations_on)
-    # breadth-first isolation: one batched GPU call per subdivision level
-    # (upoly.py:358-408; isolate_decomposition :411-421 and :573 look it up at call time)
-    saved[("curvekit.upoly", "descartes_isolate")] = getattr(up, "descartes_isolate")
-    setattr(up, "descartes_isolate", our_upoly.descartes_isolate)
-    bp = importlib.import_module("curvekit.bivpoly")
-    from . import bivpoly as our_bivpoly
-    saved[("curvekit.bivpoly", "gcd_biv")] = getattr(bp, "gcd_biv")
-    setattr(bp, "gcd_biv", our_bivpoly.gcd_biv)
-    try:
-        bis = importlib.import_module("curvekit.bisolve")
-    except ImportError:  # bisolve needs mpmath
-        bis = None
-    if bis is not None:
-        for name in ("biv_resultant", "int_gcd_uni"):
-            saved[("curvekit.bisolve", name)] = getattr(bis, name)
-            setattr(bis, name, getattr(ours, name))
-        saved[("curvekit.bisolve", "gcd_biv")] = getattr(bis, "gcd_biv")
-        setattr(bis, "gcd_biv", our_bivpoly.gcd_biv)
-        # both resultants of the projection in one batched GPU call (bisolve.py:103-114,
-        # looked up by Bisolve.__init__ at bisolve.py:412)
-        from . import bisolve as our_bisolve
-        saved[("curvekit.bisolve", "biproject")] = getattr(bis, "biproject")
-        setattr(bis, "biproject", our_bisolve.biproject)
+    for mod, name, repl in _bindings():
+        try:
+            m = importlib.import_module(mod)
+        except ImportError:  # curvekit.bisolve needs mpmath
+            continue
+        cur = getattr(m, name)
+        # installing twice must still hand back the reference's own function
+        orig = _ORIGINALS.get((mod, name), cur) if cur is repl else cur
+        _ORIGINALS.setdefault((mod, name), orig)
+        saved[(mod, name)] = orig
+        setattr(m, name, repl)
     return saved
+
+
+_ORIGINALS = {}
+
+
+def _bindings():
+    """(module, name, replacement) for every rebinding install() makes."""
+    from . import bisolve as our_bisolve
+    from . import bivpoly as our_bivpoly
+    from . import modpoly as ours
+    from . import upoly as our_upoly
+    out = [("curvekit.modpoly", name, getattr(ours, name))
+           for name in ("biv_resultant", "int_gcd_uni", "zp_resultant_uni", "zp_interpolate",
+                        "zp_gcd_sylvester", "crt_reconstruct", "modular_subres_profile")]
+    # the Descartes test (upoly.py:338-346) and the breadth-first isolation
+    # (upoly.py:358-408; isolate_decomposition :411-421 and :573 look it up at call time)
+    out += [("curvekit.upoly", "_variations_on", our_upoly.variations_on),
+            ("curvekit.upoly", "descartes_isolate", our_upoly.descartes_isolate),
+            ("curvekit.bivpoly", "gcd_biv", our_bivpoly.gcd_biv)]
+    # names bisolve.py binds at import (:21, :26), and the projection (:103-114,
+    # looked up by _Solver.__init__ at :412)
+    out += [("curvekit.bisolve", "biv_resultant", ours.biv_resultant),
+            ("curvekit.bisolve", "int_gcd_uni", ours.int_gcd_uni),
+            ("curvekit.bisolve", "gcd_biv", our_bivpoly.gcd_biv),
+            ("curvekit.bisolve", "biproject", our_bisolve.biproject)]
+    return out
 
 
 def uninstall(saved):

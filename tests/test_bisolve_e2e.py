@@ -151,3 +151,17 @@ def test_batched_biproject_matches_reference(curvekit_mod):
     finally:
         pkg.uninstall(saved)
     assert ei.value.factor == circle
+
+
+def test_install_twice_then_uninstall_restores_reference(curvekit_mod):
+    import curvekit.bisolve as B
+    import curvekit.modpoly as M
+    import curvekit.upoly as U
+
+    import paper_1201_1548_b200 as pkg
+    orig = (M.biv_resultant, U.descartes_isolate, B.biproject)
+    first = pkg.install()
+    second = pkg.install()  # already installed: must still return the reference's functions
+    assert second == first
+    pkg.uninstall(second)
+    assert (M.biv_resultant, U.descartes_isolate, B.biproject) == orig
