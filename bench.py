@@ -310,20 +310,22 @@ def run_ours(args):
         # all-to-all) as ONE CUDA graph: at 8 ranks a step is ~0.1 ms of device
         # work, comparable to enqueueing its parts from Python
         lib.ckb_set_graphs(0)
-        graph = torch.cuda.CUDAGraph()
-        c0 = lib.ckb_launch_count()
-        with torch.cuda.graph(graph, stream=stream):
-            graph_out = step()
-        graph_launches = int(lib.ckb_launch_count() - c0)  # library kernels per replay
+        try:
+            graph = torch.cuda.CUDAGraph()
+            c0 = lib.ckb_launch_count()
+            with torch.cuda.graph(graph, stream=stream):
+                graph_out = step()
+            graph_launches = int(lib.ckb_launch_count() - c0)  # library kernels per replay
+        except Exception as exc:  # noqa: BLE001 - fall back to enqueueing the parts (same on every rank)
+            print(f"step graph capture failed, enqueueing the step's parts: {exc}", file=sys.stderr)
+            graph, graph_launches = None, 0
         lib.ckb_set_graphs(1)
         torch.cuda.synchronize()
         barrier()
-        plain_step = step
-
-        def step():  # noqa: F811 - replay the captured step
-            graph.replay()
-            return graph_out
-        del plain_step
+        if graph is not None:
+            def step():  # noqa: F811 - replay the captured step
+                graph.replay()
+                return graph_out
     n0 = lib.ckb_launch_count()
     times = []
     with Clocks(local) as clk:
@@ -467,7 +469,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32 (mod p < 2^30), exact integers", "data": "synthetic",
             "config": dict(cfg, primes=K, points_per_prime=N, images_per_res_y=images, out_words=LW,
-                           l2="flushed (256 MB write) before every timed step", parallelism=(f"primes/{world}" if not sharded else
+                           l2="flushed (256 MB write) before every timed step",
+                           step_graph=bool(graph is not None), parallelism=(f"primes/{world}" if not sharded else
                                         f"primes/{world}, all-to-all, CRT coefficients/{world}")),
             "images_per_s": images * 1e3 / ms_per_step,
             "stages_ms": stages,
