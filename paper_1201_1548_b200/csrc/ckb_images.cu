@@ -160,7 +160,32 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
   // opaque to the optimiser: keeps both in registers instead of letting
   // ptxas rematerialise the companion (7 instructions) in every chunk
   asm volatile("" : "+r"(negp), "+r"(zcp));
-  for (int e2 = emax; e2 >= 0; --e2) {
+  {
+    // the top row starts every chain: a plain load (z * 0 + c would cost a product per register)
+    const int e = l + POLY * emax;
+    const uint4* ta = reinterpret_cast<const uint4*>(TA + e * SW);
+    const uint4* tb = reinterpret_cast<const uint4*>(TB + e * SW);
+    const uint32_t mA = __reduce_or_sync(0xffffffffu, maskA[e]);
+    const uint32_t mB = __reduce_or_sync(0xffffffffu, maskB[e]);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      if (mA & (1u << c)) {
+        const uint4 v = ta[c];
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (4 * c + k <= MAXD) A[4 * c + k] = vv[k];
+      }
+      if (mB & (1u << c)) {
+        const uint4 v = tb[c];
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (4 * c + k <= MAXD) B[4 * c + k] = vv[k];
+      }
+    }
+  }
+  for (int e2 = emax - 1; e2 >= 0; --e2) {
     const int e = l + POLY * e2;
     const uint4* ta = reinterpret_cast<const uint4*>(TA + e * SW);
     const uint4* tb = reinterpret_cast<const uint4*>(TB + e * SW);

@@ -27,13 +27,14 @@ def eval_products(degs_f, degs_g) -> int:
 def eval_products_poly(degs_f, degs_g, S: int = POLY) -> int:
     """Products per image of the polyphase evaluation: each lane of an S-lane
     coset runs Horner in y^S over its share of the coefficients (ceil((D+1)/S)
-    terms of a degree-D poly), then one product by y^r and log2(S) - 1 DFT
-    stages with products (the last stage's twiddle is 1)."""
+    terms of a degree-D poly: one product fewer than terms, the top term is a
+    load), then one product by y^r and log2(S) - 1 DFT stages with products (the
+    last stage's twiddle is 1)."""
     stages = S.bit_length() - 2
     tot = 0
     for d in list(degs_f) + list(degs_g):
         if d >= 0:
-            tot += -(-(d + 1) // S) + 1 + stages
+            tot += -(-(d + 1) // S) - 1 + 1 + stages
     return tot
 
 
