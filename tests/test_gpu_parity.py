@@ -6,6 +6,7 @@ cfg3) and, at cfg4 size, through the specialisation property
 res_y(f, g)(a) = res(f(a, y), g(a, y)) modulo independent primes.
 """
 
+import ctypes
 import hashlib
 import random
 
@@ -449,3 +450,38 @@ def test_point_scale_when_leading_coefficient_vanishes_at_roots_of_unity(mp, ora
             f = {k: v for k, v in f.items() if v}
             g = {k: v for k, v in g.items() if v}
             assert mp.biv_resultant(f, g, "y") == oracle_mod.biv_resultant(f, g, "y")
+
+
+def test_c_abi_rejects_bad_arguments():
+    """The C-ABI validates its inputs: bad sizes, handles and shapes return < 0
+    with a message (no device work, no crash), and the library stays usable."""
+    from paper_1201_1548_b200 import _lib
+    lib = _lib.lib()
+    z = np.zeros(16, dtype=np.uint32)
+    d = np.zeros(16, dtype=np.int16)
+    primes = np.array([1000000007], dtype=np.uint32)
+    st = np.zeros(4, dtype=np.uint32)
+    # C does not match (m+1)(dfx+1) + (n+1)(dgx+1)
+    rc = lib.ckb_biv_resultant(_lib.ptr(z), 5, 1, _lib.ptr(d), 1, 1, 1, 1, _lib.ptr(primes), _lib.ptr(primes), 1, 4,
+                               1, _lib.ptr(z), _lib.ptr(st), None)
+    assert rc < 0 and b"C mismatch" in lib.ckb_last_error()
+    # an even "prime"
+    bad = np.array([1000000008], dtype=np.uint32)
+    assert lib.ckb_reduce(_lib.ptr(z), 1, 1, _lib.ptr(bad), 1, _lib.ptr(z)) < 0
+    # unknown Descartes handle, batch of zero intervals
+    v = np.zeros(4, dtype=np.int32)
+    lds = np.zeros(4, dtype=np.int32)
+    assert lib.ckb_descartes_variations_batch(12345, _lib.ptr(z), 1, _lib.ptr(lds), 1, 1, 1, _lib.ptr(v)) < 0
+    # bivariate gcd images need m >= n
+    od = np.zeros(16, dtype=np.int32)
+    assert lib.ckb_biv_gcd_images(_lib.ptr(z), 5, 1, _lib.ptr(d), 0, 1, 1, 1, 0, _lib.ptr(primes), 1, 2,
+                                  _lib.ptr(z), 2, _lib.ptr(od)) < 0
+    # batched resultants: 0 or more than 4 problems
+    ptrs = (ctypes.c_void_p * 1)(None)
+    ints = np.zeros(8, dtype=np.int32)
+    assert lib.ckb_biv_resultant_batch(0, ptrs, _lib.ptr(ints), _lib.ptr(ints), ptrs, _lib.ptr(ints), _lib.ptr(ints),
+                                       _lib.ptr(ints), _lib.ptr(ints), ptrs, ptrs, _lib.ptr(ints), _lib.ptr(ints),
+                                       _lib.ptr(ints), ptrs, _lib.ptr(st)) < 0
+    # still usable afterwards
+    from paper_1201_1548_b200 import modpoly
+    assert modpoly.biv_resultant({(2, 0): 1, (0, 2): 1, (0, 0): -1}, {(0, 1): 2}) == [-4, 0, 4]
