@@ -67,8 +67,10 @@ struct ImgLayout {
   static constexpr int SW = ((NCH & 1) ? NCH : NCH + 1) * 4;   // words per x-power row
 };
 
-template <int MAXD>
-__global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArgs a) {
+// NT = threads (images) per CTA; ALIGNED: grid (ceil(N/NT), K), a CTA never
+// straddles primes (one staged table: the register-heavy buckets fit more CTAs)
+template <int MAXD, int NT = IMG_THREADS, bool ALIGNED = false>
+__global__ void __launch_bounds__(NT, ALIGNED ? 1 : img_minb(MAXD)) k_images(ImageArgs a) {
   using LY = ImgLayout<MAXD>;
   constexpr int NCH = LY::NCH, SW = LY::SW;
   extern __shared__ __align__(16) uint32_t sm[];
@@ -85,14 +87,16 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
   // consecutive images, so the grid has no per-prime padding and ends in an
   // (almost) full wave.  The tables of every prime the CTA spans are staged
   // (two at most once N >= 128; the launch sizes shared memory for the worst case).
-  const int g0 = blockIdx.x * IMG_THREADS;
+  const int g0 = ALIGNED ? blockIdx.y * a.N + blockIdx.x * NT : blockIdx.x * NT;
   const int total = a.K * a.N;
-  const int pi0 = g0 / a.N, pi1 = min(a.K - 1, (g0 + IMG_THREADS - 1) / a.N);
+  const int pi0 = ALIGNED ? blockIdx.y : g0 / a.N;
+  const int pi1 = ALIGNED ? blockIdx.y : min(a.K - 1, (g0 + NT - 1) / a.N);
   // per-thread point data first: its global-load latency overlaps the table copy
   const int t = g0 + threadIdx.x;
-  const bool active = t < total;  // inactive lanes still join the shuffles
-  const int pi = active ? t / a.N : pi1;
-  const int tin = active ? t - pi * a.N : 0;  // image index within the prime
+  // inactive lanes still join the shuffles
+  const bool active = ALIGNED ? (int)(blockIdx.x * NT + threadIdx.x) < a.N : t < total;
+  const int pi = ALIGNED ? pi0 : (active ? t / a.N : pi1);
+  const int tin = ALIGNED ? (active ? t - pi * a.N : 0) : (active ? t - pi * a.N : 0);  // image index within the prime
   const int u = tin >> 3, l = t & (POLY - 1);
   const int tslot = pi - pi0;  // which staged table
   // pdl_launch();  (implicit at exit: measured better)
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
     img_mbar_expect_tx(bar, bytes);
     img_bulk_g2s(img_smem_u32(sm), a.tab + (size_t)pi0 * TW, bytes, bar);
   }
-  for (int e = threadIdx.x; e < rows; e += IMG_THREADS) {
+  for (int e = threadIdx.x; e < rows; e += NT) {
     uint32_t ma = 0, mb = 0;
     for (int i = 0; i <= MAXD; ++i) {
       if (i <= da && Adeg[da - i] >= e) ma |= 1u << (i >> 2);
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(IMG_THREADS, img_minb(MAXD)) k_images(ImageArg
     maskA[e] = ma;
     maskB[e] = mb;
   }
-  for (int q = threadIdx.x; q < nspan * 2 * POLY; q += IMG_THREADS)
+  for (int q = threadIdx.x; q < nspan * 2 * POLY; q += NT)
     maskB[rows + q] = a.om[(size_t)(pi0 + q / (2 * POLY)) * 4 * POLY + q % (2 * POLY)];
 
   // image (u, j): x = w^j c y_u.  Lane l of an 8-lane group evaluates the
@@ -432,8 +436,39 @@ bool images_fast_ok(int m, int n, int dfx, int dgx, int NI, int K) {
   return maxd > 0 && images_smem_bytes(maxd, dfx, dgx, NI, K) <= 200 * 1024;
 }
 
+// the register-heavy buckets (MAXD >= 56: ~200 registers) in prime-aligned CTAs
+// of 64 images: one staged table per CTA, so registers AND shared memory allow 5
+// CTAs (10 warps) per SM instead of 2 x 128 threads (8 warps).  CKB_IMG_ALIGN=0 disables.
+static bool images_aligned(int maxd) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CKB_IMG_ALIGN");
+    on = e ? atoi(e) : 1;
+  }
+  return on && maxd >= 56;
+}
+
 void launch_images(const ImageArgs& a, cudaStream_t st) {
   const int maxd = images_maxd(a.m, a.n);
+  if (images_aligned(maxd)) {
+    constexpr int NTA = 64;
+    ImageArgs b = a;
+    b.span = 1;
+    const dim3 grid((unsigned)((a.N + NTA - 1) / NTA), (unsigned)a.K);
+    const int dmax = a.dfx > a.dgx ? a.dfx : a.dgx;
+    const int rows = POLY * (dmax / POLY + 1);
+#define LAUNCH_AL(D)                                                                                     \
+  if (maxd == D) {                                                                                       \
+    const size_t smem = (size_t)((2 * rows * ImgLayout<D>::SW + 2 * POLY) + 2 * rows) * 4;              \
+    if (smem > 48 * 1024)                                                                                \
+      cudaFuncSetAttribute(k_images<D, NTA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    launch_pdl(k_images<D, NTA, true>, grid, dim3(NTA), smem, st, b);                                     \
+  }
+    LAUNCH_AL(56) LAUNCH_AL(64)
+#undef LAUNCH_AL
+    launch_images_fallback(a, st);
+    return;
+  }
   dim3 grid((unsigned)(((size_t)a.K * a.N + IMG_THREADS - 1) / IMG_THREADS));
   ImageArgs b = a;
   b.span = (IMG_THREADS - 1 + a.N - 1) / a.N + 1;  // primes a window of IMG_THREADS images can touch
