@@ -445,6 +445,7 @@ static bool images_aligned(int maxd) {
     const char* e = getenv("CKB_IMG_ALIGN");
     on = e ? atoi(e) : 1;
   }
+  // smaller buckets measured slower aligned (cfg4 images 270 -> 289 us: per-prime padding, no occupancy gain)
   return on && maxd >= 56;
 }
 
