@@ -194,7 +194,11 @@ __device__ __forceinline__ void stage16(uint32_t* sdst, const uint32_t* gsrc, in
   for (int i = 4 * tid; i < n; i += 4 * T) cp_async16(sdst + i, gsrc + i);
 }
 
-template <int POLY_THREADS>
+// STAGE: the pointwise tables (Hf, Hfc, Mf, Mfc, sS, sSc — each element read once
+// per CTA) are staged in shared memory with the twiddles; by default they are
+// read from global memory (L2) where used, which keeps shared memory to the data
+// and twiddles (staging them cost occupancy: 3 CTAs per SM at L = 2048)
+template <int POLY_THREADS, bool STAGE = true>
 __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, const Prime* __restrict__ primes,
                                                               const uint32_t* __restrict__ values,
                                                               const uint32_t* __restrict__ cval,
@@ -211,8 +215,14 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
   const int Mp = (M + 3) & ~3, Lp = (L + 3) & ~3, hp = (half + 3) & ~3;  // 16-byte aligned regions
   const size_t oM = (size_t)pi * M, oL = (size_t)pi * L, oH = (size_t)pi * half;
   uint32_t *W = buf + ((padded_words(L) + 3) & ~3), *Wc = W + hp, *Wi = Wc + hp, *Wic = Wi + hp;
-  uint32_t *Hf = Wic + hp, *Hfc = Hf + Lp, *Mf = Hfc + Lp, *Mfc = Mf + Lp;
-  uint32_t *sS = Mfc + Lp, *sSc = sS + Mp;
+  uint32_t *sHf = Wic + hp, *sHfc = sHf + Lp, *sMf = sHfc + Lp, *sMfc = sMf + Lp;
+  uint32_t *ssS = sMfc + Lp, *ssSc = ssS + Mp;
+  const uint32_t* Hf = STAGE ? sHf : plan.Hf + oL;
+  const uint32_t* Hfc = STAGE ? sHfc : plan.Hfc + oL;
+  const uint32_t* Mf = STAGE ? sMf : plan.Mf + oL;
+  const uint32_t* Mfc = STAGE ? sMfc : plan.Mfc + oL;
+  const uint32_t* sS = STAGE ? ssS : plan.sS + oM;
+  const uint32_t* sSc = STAGE ? ssSc : plan.sSc + oM;
   // every per-plan constant this CTA needs, requested up front (16-byte copies
   // when the per-prime table offsets are 16-byte aligned: L >= 8)
   if (L >= 8) {
@@ -220,10 +230,12 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
     stage16(Wc, plan.Wc + oH, half, tid, T);
     stage16(Wi, plan.Wi + oH, half, tid, T);
     stage16(Wic, plan.Wic + oH, half, tid, T);
-    stage16(Hf, plan.Hf + oL, L, tid, T);
-    stage16(Hfc, plan.Hfc + oL, L, tid, T);
-    stage16(Mf, plan.Mf + oL, L, tid, T);
-    stage16(Mfc, plan.Mfc + oL, L, tid, T);
+    if (STAGE) {
+      stage16(sHf, plan.Hf + oL, L, tid, T);
+      stage16(sHfc, plan.Hfc + oL, L, tid, T);
+      stage16(sMf, plan.Mf + oL, L, tid, T);
+      stage16(sMfc, plan.Mfc + oL, L, tid, T);
+    }
   } else {
     for (int j = tid; j < half; j += T) {
       cp_async4(W + j, plan.W + oH + j);
@@ -231,16 +243,16 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
       cp_async4(Wi + j, plan.Wi + oH + j);
       cp_async4(Wic + j, plan.Wic + oH + j);
     }
-    for (int j = tid; j < L; j += T) {
-      cp_async4(Hf + j, plan.Hf + oL + j);
-      cp_async4(Hfc + j, plan.Hfc + oL + j);
-      cp_async4(Mf + j, plan.Mf + oL + j);
-      cp_async4(Mfc + j, plan.Mfc + oL + j);
+    for (int j = tid; j < L && STAGE; j += T) {
+      cp_async4(sHf + j, plan.Hf + oL + j);
+      cp_async4(sHfc + j, plan.Hfc + oL + j);
+      cp_async4(sMf + j, plan.Mf + oL + j);
+      cp_async4(sMfc + j, plan.Mfc + oL + j);
     }
   }
-  for (int e = tid; e < M; e += T) {
-    cp_async4(sS + e, plan.sS + oM + e);
-    cp_async4(sSc + e, plan.sSc + oM + e);
+  for (int e = tid; e < M && STAGE; e += T) {
+    cp_async4(ssS + e, plan.sS + oM + e);
+    cp_async4(ssSc + e, plan.sSc + oM + e);
   }
   // pdl_launch();  (implicit at exit: measured better)
   pdl_wait();  // the images kernels' values and k_choose_c's point scales from here on
@@ -328,15 +340,30 @@ void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* 
   } else {
     const size_t Lp = (plan.L + 3) & ~3, hp = (plan.L / 2 + 3) & ~3, Mp = (plan.N + 3) & ~3;
     const size_t Dp = ((size_t)padded_words(plan.L) + 3) & ~(size_t)3;
-    smem = (Dp + 4 * Lp + 4 * hp + 2 * Mp) * 4;  // padded data, twiddles, staged Hf, Hfc, Mf, Mfc, sS, sSc
+    // pointwise tables straight from L2 (measured: cfg4 28.3 -> 26.1 us, cfg2 13.7 -> 13.1 us, cfg5
+    // 617 -> 544 us against staging them; CKB_INTERP_STAGE=1 stages them)
+    static int force = -2;
+    if (force == -2) {
+      const char* e = getenv("CKB_INTERP_STAGE");
+      force = e ? atoi(e) : -1;
+    }
+    const bool stage = force == 1;
+    smem = (Dp + 4 * hp + (stage ? 4 * Lp + 2 * Mp : 0)) * 4;  // padded data, twiddles[, staged tables]
     const int want = plan.L / 8;
 #define POLY_LAUNCH(TT)                                                                                       \
   if ((TT == 32 && want <= 32) || (TT == 64 && want == 64) || (TT == 128 && want == 128) ||                 \
       (TT == 256 && want >= 256)) {                                                                           \
-    if (smem > 48 * 1024)                                                                                     \
-      cudaFuncSetAttribute(k_interp_poly<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    launch_pdl(k_interp_poly<TT>, dim3(plan.K * plan.S), dim3(TT), smem, st, plan, primes, values, cval, coeffs, \
-               crt_c, crt_cc);                                                                                \
+    if (stage) {                                                                                              \
+      if (smem > 48 * 1024)                                                                                   \
+        cudaFuncSetAttribute(k_interp_poly<TT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      launch_pdl(k_interp_poly<TT, true>, dim3(plan.K * plan.S), dim3(TT), smem, st, plan, primes, values, cval,  \
+                 coeffs, crt_c, crt_cc);                                                                      \
+    } else {                                                                                                  \
+      if (smem > 48 * 1024)                                                                                   \
+        cudaFuncSetAttribute(k_interp_poly<TT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      launch_pdl(k_interp_poly<TT, false>, dim3(plan.K * plan.S), dim3(TT), smem, st, plan, primes, values, cval, \
+                 coeffs, crt_c, crt_cc);                                                                      \
+    }                                                                                                         \
   }
     POLY_LAUNCH(32) POLY_LAUNCH(64) POLY_LAUNCH(128) POLY_LAUNCH(256)
 #undef POLY_LAUNCH
