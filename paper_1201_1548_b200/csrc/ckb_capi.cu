@@ -338,6 +338,7 @@ struct PlanEntry {
   int N = 0, S = 1;
   InterpPlan pl;
   void* blob = nullptr;
+  void* ab = nullptr;  // tensor-core interpolation matrix (polyphase plans), or nullptr
   uint64_t last_use = 0;
 };
 std::vector<PlanEntry> g_plans;
@@ -364,6 +365,7 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
     for (size_t i = 1; i < g_plans.size(); ++i)
       if (g_plans[i].last_use < g_plans[v].last_use) v = i;
     cudaFree(g_plans[v].blob);
+    if (g_plans[v].ab) cudaFree(g_plans[v].ab);
     g_plans.erase(g_plans.begin() + v);
     ++g.epoch;
   }
@@ -418,6 +420,20 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
   CK(cudaMemcpy(d_primes, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice));
   launch_plan_base(d_primes, d_gens, pl, g.stream);
   launch_plan_ntt(d_primes, d_gens, pl, g.stream);
+  pl.Ab = nullptr;
+  {
+    // the interpolation as a tensor-core product: the per-prime inverse
+    // Vandermonde in bytes (input independent), when it is small enough
+    // (cfg4: 42 MB; K-chunks <= 4 for the kernel's shared memory).  CKB_INTERP_MMA=0 disables.
+    const char* env = getenv("CKB_INTERP_MMA");
+    int kch, mt;
+    const size_t ab = interp_mma_bytes(K, N, &kch, &mt);
+    if (S > 1 && !(env && env[0] == '0') && kch <= 4 && ab <= ((size_t)512 << 20)) {
+      CK(cudaMalloc(&e.ab, ab));
+      pl.Ab = (uint8_t*)e.ab;
+      launch_interp_lagrange(d_primes, pl, pl.Ab, g.stream);
+    }
+  }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(g.stream));
   e.last_use = ++g.tick;
@@ -583,7 +599,9 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   else
     launch_images(a, st);
   stage_mark(st);
-  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr);
+  uint8_t* d_ixb = nullptr;
+  if (pl.Ab && (rc = dbuf("ixb", interp_mma_scratch_bytes(pl), &d_ixb))) return rc;
+  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr, d_ixb);
   stage_mark(st);
   // reduce (+ choose when merged), [choose], images (general: iota + warp kernel), fallback, interpolation
   g.launches += general ? 5 : (merged ? 4 : 5);
@@ -643,7 +661,10 @@ int ckb_shutdown(void) {
   }
   for (auto& e : g_pcache) cudaFree(e.d);
   g_pcache.clear();
-  for (auto& e : g_plans) cudaFree(e.blob);
+  for (auto& e : g_plans) {
+    cudaFree(e.blob);
+    if (e.ab) cudaFree(e.ab);
+  }
   g_plans.clear();
   g.dev.clear();
   g.host.clear();

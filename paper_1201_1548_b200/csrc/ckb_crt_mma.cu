@@ -228,4 +228,258 @@ void launch_crt_mma(const CrtTables& t, const uint32_t* y, int N, unsigned long 
   launch_pdl(k_crt_mma, grid, dim3(THREADS), smem, st, N, KC, reinterpret_cast<const uint8_t*>(y), t.Bt, NT * 32, S);
 }
 
+// ===========================================================================
+// Interpolation as a tensor-core product (polyphase plans).
+//
+// For one prime the 8 coset phases interpolate at the SAME geometric points
+// z_u = q^u (u < M), so every phase is one product with the same matrix:
+//     P_r[k] = sum_u A[k][u] X_r[u],   A = inverse Vandermonde of the z_u
+//     (A[k][u] = coefficient k of the Lagrange basis polynomial L_u),
+//     X_r[u] = (1/S) (c y_u)^-r sum_j w^-jr v[u S + j]   (phase separation)
+// — the same values the NTT correlations of k_interp_poly produce.  Both
+// operands are split into bytes, A[k][u] = sum_a 2^8a A_a and X = sum_b 2^8b
+// X_b, so one u8 GEMM with rows (k, a), columns (r, b) and K = u gives
+// D[(k,a)][(r,b)] = sum_u A_a X_b < M 255^2 < 2^25, recombined mod p in the
+// epilogue.  A is input-independent: built once per plan (bytes in the
+// no-swizzle K-major core-matrix layout, like the CRT tables) and streamed by
+// the bulk-copy engine; X is built per call by k_interp_xprep.
+// ===========================================================================
+namespace {
+constexpr uint32_t IDESC_N32 = (2u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+constexpr int IA_TILE = 128 * 128;  // A bytes per (M-tile, K-chunk)
+constexpr int IB_TILE = 32 * 128;   // B bytes per K-chunk
+__device__ __forceinline__ size_t ia_byte(int row, int u, int KCH) {  // row = 4k + a
+  const size_t tile = (size_t)(row >> 7) * KCH + (u >> 7);
+  return tile * IA_TILE + ((row & 127) >> 3) * 1024 + ((u & 127) >> 4) * 128 + (row & 7) * 16 + (u & 15);
+}
+__device__ __forceinline__ size_t ib_byte(int n, int u) {  // n = 4r + b
+  return (size_t)(u >> 7) * IB_TILE + (n >> 3) * 1024 + ((u & 127) >> 4) * 128 + (n & 7) * 16 + (u & 15);
+}
+__device__ __forceinline__ void mma_i8_n32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC_N32), "r"(acc));
+}
+}  // namespace
+
+// plan: A bytes for every prime (one CTA per prime, one thread per point u):
+// L_u = M~(z) / ((z - z_u) M~'(z_u)) by synthetic division
+__global__ void k_interp_lagrange(const Prime* __restrict__ primes, InterpPlan plan, int KCH, int MT,
+                                  uint8_t* __restrict__ Ab) {
+  const int pi = blockIdx.x, M = plan.N;
+  const Prime P = primes[pi];
+  const uint32_t p = P.p;
+  const uint32_t* Mt = plan.Mt + (size_t)pi * (M + 1);  // M~ = prod_u (z - z_u), degree M
+  uint8_t* A = Ab + (size_t)pi * MT * KCH * IA_TILE;
+  for (int u = threadIdx.x; u < M; u += blockDim.x) {
+    const uint32_t x = plan.xq[(size_t)pi * M + u], xc = shoup_comp(x, P);
+    // M~'(x) by Horner on the derivative
+    uint32_t d = 0u;
+    for (int j = M; j >= 1; --j) d = add_mod(shoup(d, x, xc, p), mul_mod(Mt[j], (uint32_t)j % p, P), p);
+    const uint32_t inv = inv_mod(d, P), invc = shoup_comp(inv, P);
+    // quotient Q = M~ / (z - x): Q_{M-1} = Mt[M], Q_{j-1} = Mt[j] + x Q_j
+    uint32_t q = Mt[M];
+    for (int k = M - 1; k >= 0; --k) {
+      const uint32_t a = shoup(q, inv, invc, p);  // A[k][u] = Q_k / M~'(x)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) A[ia_byte(4 * k + b, u, KCH)] = (uint8_t)(a >> (8 * b));
+      if (k > 0) q = add_mod(Mt[k], shoup(q, x, xc, p), p);
+    }
+  }
+}
+
+// X bytes of one point u of prime pi (phase separation and weights) into B (shared or global)
+__device__ __forceinline__ void interp_x_bytes(const Prime& P, int pi, int u, const InterpPlan& plan,
+                                               const uint32_t* __restrict__ values, uint32_t c, uint32_t cinv,
+                                               uint32_t inv8, uint8_t* B) {
+  const int M = plan.N, S = plan.S;
+  const uint32_t p = P.p;
+  uint32_t X[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  if (u < M) {
+    const uint32_t* om = plan.om + (size_t)pi * 4 * S;  // w^k, companions, w^-k, companions
+    const uint32_t* v = values + ((size_t)pi * M + u) * S;
+    uint32_t vv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) vv[j] = v[j];
+    // weight (1/S) (c y_u)^-r, r = 0..7
+    uint32_t step = plan.yqi[(size_t)pi * M + u];
+    if (c != 1u) step = mul_mod(step, cinv, P);
+    const uint32_t stepc = shoup_comp(step, P);
+    // g_r = sum_j w^-jr v_j: radix-2 DIT on the bit-reversed inputs, natural-order outputs
+    // (5 twiddle products instead of 64)
+    uint32_t x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = vv[((m & 1) << 2) | (m & 2) | ((m >> 2) & 1)];
+#pragma unroll
+    for (int h = 1; h < 8; h <<= 1) {
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        if (l & h) continue;
+        const int e = (l & (h - 1)) * (8 / (2 * h));  // w^-e
+        const uint32_t t = e ? shoup(x[l + h], om[2 * S + e], om[3 * S + e], p) : x[l + h];
+        const uint32_t a0 = x[l];
+        x[l] = add_mod(a0, t, p);
+        x[l + h] = sub_mod(a0, t, p);
+      }
+    }
+    uint32_t wr = inv8;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      X[r] = mul_mod(x[r], wr, P);
+      wr = shoup(wr, step, stepc, p);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) B[ib_byte(4 * r + b, u)] = (uint8_t)(X[r] >> (8 * b));
+}
+
+__device__ __forceinline__ uint32_t inv8_mod(const Prime& P) {  // ((p + 1) / 2)^3 = 1/8
+  const uint32_t h = (P.p + 1u) >> 1;
+  return mul_mod(mul_mod(h, h, P), h, P);
+}
+
+// per call: X bytes (phase separation and weights) for every prime and point
+// (standalone form; k_interp_mma builds them in shared memory itself)
+__global__ void k_interp_xprep(const Prime* __restrict__ primes, InterpPlan plan, const uint32_t* __restrict__ values,
+                               const uint32_t* __restrict__ cval, int KCH, uint8_t* __restrict__ Bb) {
+  const int pi = blockIdx.y, u = blockIdx.x * blockDim.x + threadIdx.x, M = plan.N, S = plan.S;
+  pdl_wait();  // the images' values
+  if (u >= KCH * 128) return;
+  const Prime P = primes[pi];
+  const uint32_t c = cval[pi];
+  interp_x_bytes(P, pi, u, plan, values, c, c != 1u ? inv_mod(c, P) : 1u, inv8_mod(P), Bb + (size_t)pi * KCH * IB_TILE);
+}
+
+// per call: the product, one CTA per (M-tile of 32 coefficients, prime); the
+// epilogue recombines the bytes mod p and writes the CRT's y layout (or canonical)
+__global__ void __launch_bounds__(128, 1) k_interp_mma(const Prime* __restrict__ primes, InterpPlan plan,
+                                                       const uint8_t* __restrict__ Ab,
+                                                       const uint32_t* __restrict__ values,
+                                                       int KCH, int MT, const uint32_t* __restrict__ cval,
+                                                       uint32_t* __restrict__ coeffs, const uint32_t* __restrict__ crt_c) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;                        // [KCH][16 KB]
+  uint8_t* sB = smem + (size_t)KCH * IA_TILE;  // [KCH][4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)KCH * IB_TILE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mt = blockIdx.x, pi = blockIdx.y, M = plan.N, S = plan.S, Nfull = plan.Nfull;
+  const uint32_t full = smem_u32(bars), fin = smem_u32(bars + 1);
+  if (tid == 0) {
+    mbar_init(full, 1);
+    mbar_init(fin, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "n"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  // the A tiles (plan constants) stream in while the CTA builds X
+  if (tid == 0) {
+    mbar_expect_tx(full, (uint32_t)KCH * IA_TILE);
+    bulk_g2s(smem_u32(sA), Ab + ((size_t)pi * MT + mt) * KCH * IA_TILE, (uint32_t)KCH * IA_TILE, full);
+  }
+  pdl_wait();  // the images' values
+  {
+    // X for every point of this prime, straight into the B operand's shared-memory layout
+    const Prime P = primes[pi];
+    const uint32_t c = cval[pi];
+    const uint32_t cinv = c != 1u ? inv_mod(c, P) : 1u, inv8 = inv8_mod(P);
+    for (int u = tid; u < KCH * 128; u += 128) interp_x_bytes(P, pi, u, plan, values, c, cinv, inv8, sB);
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic-proxy writes -> tensor-core reads
+  __syncthreads();
+  if (tid == 0) {
+    mbar_wait(full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    for (int kc = 0; kc < KCH; ++kc) {
+      const uint32_t abase = smem_u32(sA + (size_t)kc * IA_TILE), bbase = smem_u32(sB + (size_t)kc * IB_TILE);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        mma_i8_n32(tmem, desc_kmajor(abase + ks * 256), desc_kmajor(bbase + ks * 256), (kc | ks) != 0);
+    }
+    mma_commit(fin);
+  }
+  __syncwarp();
+  mbar_wait(fin, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // epilogue: lane = row (k, a) = 4 k_local + a; columns (r, b) = 4 r + b
+  uint32_t r32[32];
+  CKB_LD32(r32, tmem + ((uint32_t)(warp * 32) << 16));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  const Prime P = primes[pi];
+  const uint32_t p = P.p;
+  const uint64_t m64 = ~0ull / p;
+  const int a = lane & 3, k = mt * 32 + warp * 8 + (lane >> 2);
+  const uint32_t ra = pow_mod(2u % p, (uint64_t)(8 * a), P), rac = shoup_comp(ra, P);  // 2^8a mod p
+  uint32_t out[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const uint64_t T = (uint64_t)r32[4 * r] + ((uint64_t)r32[4 * r + 1] << 8) + ((uint64_t)r32[4 * r + 2] << 16) +
+                       ((uint64_t)r32[4 * r + 3] << 24);  // < 2^50
+    uint64_t q = __umul64hi(T, m64), t = T - q * p;
+    while (t >= p) t -= p;
+    uint32_t x = shoup((uint32_t)t, ra, rac, p);
+    x = add_mod(x, __shfl_xor_sync(0xffffffffu, x, 1), p);
+    x = add_mod(x, __shfl_xor_sync(0xffffffffu, x, 2), p);
+    out[r] = x;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(32));
+  if (a != 0 || k >= M) return;
+  const uint32_t c = cval[pi];
+  uint32_t sc = 1u;  // (c^S)^-k
+  if (c != 1u) sc = pow_mod(pow_mod(inv_mod(c, P), (uint64_t)S, P), (uint64_t)k, P);
+  if (crt_c) sc = mul_mod(sc, crt_c[pi], P);
+  const uint32_t scc = shoup_comp(sc, P);
+  const int KC = (plan.K + 31) / 32;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int idx = S * k + r;
+    if (idx >= Nfull) continue;
+    const uint32_t res = shoup(out[r], sc, scc, p);
+    if (crt_c)
+      coeffs[crt_a_word(pi, idx, KC)] = res;
+    else
+      coeffs[(size_t)pi * Nfull + idx] = res;
+  }
+}
+
+size_t interp_mma_bytes(int K, int M, int* KCH, int* MT) {
+  *KCH = (M + 127) / 128;
+  *MT = (4 * M + 127) / 128;
+  return (size_t)K * (*MT) * (*KCH) * IA_TILE;
+}
+
+void launch_interp_lagrange(const Prime* primes, const InterpPlan& plan, uint8_t* Ab, cudaStream_t st) {
+  int KCH, MT;
+  const size_t bytes = interp_mma_bytes(plan.K, plan.N, &KCH, &MT);
+  cudaMemsetAsync(Ab, 0, bytes, st);
+  k_interp_lagrange<<<plan.K, 128, 0, st>>>(primes, plan, KCH, MT, Ab);
+}
+
+void launch_interp_mma(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
+                       uint32_t* coeffs, uint8_t* Bb, cudaStream_t st, const uint32_t* crt_c) {
+  int KCH, MT;
+  interp_mma_bytes(plan.K, plan.N, &KCH, &MT);
+  (void)Bb;  // X is built in shared memory by k_interp_mma (k_interp_xprep: the standalone form)
+  const size_t smem = (size_t)KCH * (IA_TILE + IB_TILE) + 64;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_interp_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  launch_pdl(k_interp_mma, dim3(MT, plan.K), dim3(128), smem, st, primes, plan, (const uint8_t*)plan.Ab, values,
+             KCH, MT, cval, coeffs, crt_c);
+}
+
 }  // namespace ckb

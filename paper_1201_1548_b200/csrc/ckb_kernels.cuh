@@ -72,6 +72,7 @@ struct InterpPlan {
   uint32_t* Linv;     // [K]       1/L mod p
   uint32_t* zr;       // [K][S][N] (1/S) y_t^-r z_t (polyphase plans), companions zrc
   uint32_t* zrc;
+  uint8_t* Ab;        // polyphase plans: inverse-Vandermonde bytes for the tensor-core interpolation, or nullptr
 };
 // build every table of the plan: base tables (ckb_plan.cu), then twiddles and
 // the transforms of the two constant convolution operands (ckb_interp.cu)
@@ -128,9 +129,17 @@ void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t*
 // values at the planned points -> coeffs [K][Nfull] (canonical residues); with
 // crt_c (polyphase plans only) each prime's row is pre-multiplied by crt_c[i]
 // for the explicit CRT (then launch_crt must be told the input is already y)
+// ixb: per-call scratch of interp_mma_scratch_bytes(plan): with plan.Ab set, the
+// interpolation runs as a tensor-core product (ckb_crt_mma.cu) instead of NTTs
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
                    uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c = nullptr,
-                   const uint32_t* crt_cc = nullptr);
+                   const uint32_t* crt_cc = nullptr, uint8_t* ixb = nullptr);
+// tensor-core interpolation (ckb_crt_mma.cu): plan bytes (KCH K-chunks, MT M-tiles), plan build, per-call launch
+size_t interp_mma_bytes(int K, int M, int* KCH, int* MT);
+inline size_t interp_mma_scratch_bytes(const InterpPlan& pl) { return (size_t)pl.K * ((pl.N + 127) / 128) * 32 * 128; }
+void launch_interp_lagrange(const Prime* primes, const InterpPlan& plan, uint8_t* Ab, cudaStream_t st);
+void launch_interp_mma(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
+                       uint32_t* coeffs, uint8_t* Bb, cudaStream_t st, const uint32_t* crt_c);
 
 // ---- K5: explicit CRT + symmetric lift to two's-complement limbs -----------
 struct CrtTables {
