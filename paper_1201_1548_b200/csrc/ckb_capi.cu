@@ -424,11 +424,11 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
   {
     // the interpolation as a tensor-core product: the per-prime inverse
     // Vandermonde in bytes (input independent), when it is small enough
-    // (cfg4: 42 MB; K-chunks <= 4 for the kernel's shared memory).  CKB_INTERP_MMA=0 disables.
+    // (cfg4: 37 MB; <= 16 K-steps of 32 bytes for the kernel's shared memory).  CKB_INTERP_MMA=0 disables.
     const char* env = getenv("CKB_INTERP_MMA");
     int kch, mt;
     const size_t ab = interp_mma_bytes(K, N, &kch, &mt);
-    if (S > 1 && !(env && env[0] == '0') && kch <= 4 && ab <= ((size_t)512 << 20)) {
+    if (S > 1 && !(env && env[0] == '0') && kch <= 16 && ab <= ((size_t)512 << 20)) {
       CK(cudaMalloc(&e.ab, ab));
       pl.Ab = (uint8_t*)e.ab;
       launch_interp_lagrange(d_primes, pl, pl.Ab, g.stream);

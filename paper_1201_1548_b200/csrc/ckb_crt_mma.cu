@@ -246,14 +246,21 @@ void launch_crt_mma(const CrtTables& t, const uint32_t* y, int N, unsigned long 
 // ===========================================================================
 namespace {
 constexpr uint32_t IDESC_N32 = (2u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-constexpr int IA_TILE = 128 * 128;  // A bytes per (M-tile, K-chunk)
-constexpr int IB_TILE = 32 * 128;   // B bytes per K-chunk
-__device__ __forceinline__ size_t ia_byte(int row, int u, int KCH) {  // row = 4k + a
-  const size_t tile = (size_t)(row >> 7) * KCH + (u >> 7);
-  return tile * IA_TILE + ((row & 127) >> 3) * 1024 + ((u & 127) >> 4) * 128 + (row & 7) * 16 + (u & 15);
+// K in steps of 32 bytes (one MMA each), so K is padded to a multiple of 32 only:
+// per step, 8-row groups of 2 core matrices (SBO 256 B, LBO 128 B)
+constexpr int IA_TILE = 128 * 32;  // A bytes per (M-tile, K-step)
+constexpr int IB_TILE = 32 * 32;   // B bytes per K-step
+__device__ __forceinline__ size_t ia_byte(int row, int u, int KCH) {  // row = 4k + a; KCH = K-steps
+  const size_t tile = (size_t)(row >> 7) * KCH + (u >> 5);
+  return tile * IA_TILE + ((row & 127) >> 3) * 256 + ((u & 31) >> 4) * 128 + (row & 7) * 16 + (u & 15);
 }
 __device__ __forceinline__ size_t ib_byte(int n, int u) {  // n = 4r + b
-  return (size_t)(u >> 7) * IB_TILE + (n >> 3) * 1024 + ((u & 127) >> 4) * 128 + (n & 7) * 16 + (u & 15);
+  return (size_t)(u >> 5) * IB_TILE + (n >> 3) * 256 + ((u & 31) >> 4) * 128 + (n & 7) * 16 + (u & 15);
+}
+__device__ __forceinline__ uint64_t desc_kmajor_s256(uint32_t addr) {  // LBO 128 B, SBO 256 B
+  const uint64_t lo = ((addr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16);
+  const uint64_t hi = (uint64_t)(256 >> 4) | (1ull << 14);
+  return lo | (hi << 32);
 }
 __device__ __forceinline__ void mma_i8_n32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
   asm volatile(
@@ -347,7 +354,7 @@ __global__ void k_interp_xprep(const Prime* __restrict__ primes, InterpPlan plan
                                const uint32_t* __restrict__ cval, int KCH, uint8_t* __restrict__ Bb) {
   const int pi = blockIdx.y, u = blockIdx.x * blockDim.x + threadIdx.x, M = plan.N, S = plan.S;
   pdl_wait();  // the images' values
-  if (u >= KCH * 128) return;
+  if (u >= KCH * 32) return;
   const Prime P = primes[pi];
   const uint32_t c = cval[pi];
   interp_x_bytes(P, pi, u, plan, values, c, c != 1u ? inv_mod(c, P) : 1u, inv8_mod(P), Bb + (size_t)pi * KCH * IB_TILE);
@@ -393,19 +400,16 @@ __global__ void __launch_bounds__(128, 1) k_interp_mma(const Prime* __restrict__
     const Prime P = primes[pi];
     const uint32_t c = cval[pi];
     const uint32_t cinv = c != 1u ? inv_mod(c, P) : 1u, inv8 = inv8_mod(P);
-    for (int u = tid; u < KCH * 128; u += 128) interp_x_bytes(P, pi, u, plan, values, c, cinv, inv8, sB);
+    for (int u = tid; u < KCH * 32; u += 128) interp_x_bytes(P, pi, u, plan, values, c, cinv, inv8, sB);
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic-proxy writes -> tensor-core reads
   __syncthreads();
   if (tid == 0) {
     mbar_wait(full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    for (int kc = 0; kc < KCH; ++kc) {
-      const uint32_t abase = smem_u32(sA + (size_t)kc * IA_TILE), bbase = smem_u32(sB + (size_t)kc * IB_TILE);
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks)
-        mma_i8_n32(tmem, desc_kmajor(abase + ks * 256), desc_kmajor(bbase + ks * 256), (kc | ks) != 0);
-    }
+    for (int ks = 0; ks < KCH; ++ks)
+      mma_i8_n32(tmem, desc_kmajor_s256(smem_u32(sA + (size_t)ks * IA_TILE)),
+                 desc_kmajor_s256(smem_u32(sB + (size_t)ks * IB_TILE)), ks != 0);
     mma_commit(fin);
   }
   __syncwarp();
@@ -455,7 +459,7 @@ __global__ void __launch_bounds__(128, 1) k_interp_mma(const Prime* __restrict__
 }
 
 size_t interp_mma_bytes(int K, int M, int* KCH, int* MT) {
-  *KCH = (M + 127) / 128;
+  *KCH = (M + 31) / 32;  // K-steps of 32 bytes
   *MT = (4 * M + 127) / 128;
   return (size_t)K * (*MT) * (*KCH) * IA_TILE;
 }

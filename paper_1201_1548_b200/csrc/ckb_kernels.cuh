@@ -136,7 +136,7 @@ void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* 
                    const uint32_t* crt_cc = nullptr, uint8_t* ixb = nullptr);
 // tensor-core interpolation (ckb_crt_mma.cu): plan bytes (KCH K-chunks, MT M-tiles), plan build, per-call launch
 size_t interp_mma_bytes(int K, int M, int* KCH, int* MT);
-inline size_t interp_mma_scratch_bytes(const InterpPlan& pl) { return (size_t)pl.K * ((pl.N + 127) / 128) * 32 * 128; }
+inline size_t interp_mma_scratch_bytes(const InterpPlan& pl) { return (size_t)pl.K * ((pl.N + 31) / 32) * 32 * 32; }
 void launch_interp_lagrange(const Prime* primes, const InterpPlan& plan, uint8_t* Ab, cudaStream_t st);
 void launch_interp_mma(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
                        uint32_t* coeffs, uint8_t* Bb, cudaStream_t st, const uint32_t* crt_c);
