@@ -424,7 +424,8 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
   {
     // the interpolation as a tensor-core product: the per-prime inverse
     // Vandermonde in bytes (input independent), when it is small enough
-    // (cfg4: 37 MB; <= 16 K-steps of 32 bytes for the kernel's shared memory).  CKB_INTERP_MMA=0 disables.
+    // (cfg4: 37 MB; <= 16 K-steps of 32 bytes for the kernel's shared memory).  At cfg5 (1.3 GB of
+    // matrix bytes) the NTT path measured faster: 546 vs 601 us.  CKB_INTERP_MMA=0 disables.
     const char* env = getenv("CKB_INTERP_MMA");
     int kch, mt;
     const size_t ab = interp_mma_bytes(K, N, &kch, &mt);
