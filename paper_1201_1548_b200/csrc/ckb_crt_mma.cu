@@ -1,5 +1,7 @@
-// K5 on the tensor cores: the explicit-CRT product X = sum_i y_i (M/p_i) as an
-// unsigned 8-bit GEMM on tcgen05 (kind::i8, s32 accumulators in TMEM).
+// The tensor-core stages (tcgen05 kind::i8, s32 accumulators in TMEM):
+//   * K5, the explicit-CRT product X = sum_i y_i (M/p_i) as an unsigned 8-bit GEMM;
+//   * K4, the interpolation as a product with the plan's inverse Vandermonde
+//     (k_interp_mma, second half of this file).
 //
 // Reference: _CrtAccumulator / crt_reconstruct (pkg/src/curvekit/modpoly.py:264-300);
 // see ckb_crt.cu for the explicit-CRT identity this evaluates.
