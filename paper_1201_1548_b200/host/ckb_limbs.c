@@ -102,8 +102,197 @@ static PyObject* limbs_to_ints(PyObject* self, PyObject* args) {
   return out;
 }
 
+/* ------------------------------------------------------------------------
+ * terms_grid(terms_f, terms_g, swap): the input side of the same glue.
+ *
+ * Reads two {(i, j): c} term dicts (the reference's BivPoly.terms,
+ * bivpoly.py:18-25; i = power of x, j = power of y; swap exchanges them for
+ * res_x) in one C pass each and returns what planner.pack_grid and
+ * planner.plan_resultant would derive from coeffs_wrt_y (bivpoly.py:71-80):
+ *   (limbs: bytes, L, m, n, dfx, dgx, tdf, tdg, degs: bytes (int16),
+ *    norm1: list[float] | None, lcf: list[int], lcg: list[int])
+ * with the limb grid in pack_grid's layout (f's y-rows padded to dfx + 1
+ * coefficients, then g's to dgx + 1; L two's-complement u32 limbs each) and
+ * norm1 the per-row 1-norms as doubles (None if one overflows a double).
+ * Returns None when the input is not in that plain form (non-dict, non-int
+ * keys or coefficients, negative exponents): the caller takes the Python path.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  Py_ssize_t rows; /* deg_y + 1 */
+  Py_ssize_t dx;   /* max x-degree over rows */
+  long td;         /* total degree */
+  int16_t* deg;    /* [rows] trimmed x-degree per row, -1 for an empty row */
+  double* norm;    /* [rows] */
+  int norm_ok;
+} GridSide;
+
+static int key_ij(PyObject* key, int swap, long* i, long* j) {
+  if (!PyTuple_CheckExact(key) || PyTuple_GET_SIZE(key) != 2) return 0;
+  PyObject* a = PyTuple_GET_ITEM(key, 0);
+  PyObject* b = PyTuple_GET_ITEM(key, 1);
+  if (!PyLong_CheckExact(a) || !PyLong_CheckExact(b)) return 0;
+  const long x = PyLong_AsLong(a), y = PyLong_AsLong(b);
+  if ((x == -1 || y == -1) && PyErr_Occurred()) {
+    PyErr_Clear();
+    return 0;
+  }
+  if (x < 0 || y < 0 || x > 1000000 || y > 1000000) return 0;
+  *i = swap ? y : x;
+  *j = swap ? x : y;
+  return 1;
+}
+
+/* pass 1: shape, degrees, 1-norms and the widest coefficient; 0 = not plain */
+static int scan_side(PyObject* terms, int swap, GridSide* s, size_t* maxbits) {
+  Py_ssize_t pos = 0;
+  PyObject *k, *v;
+  long i, j, maxj = -1, maxi = -1;
+  s->td = -1;
+  while (PyDict_Next(terms, &pos, &k, &v)) {
+    if (!PyLong_CheckExact(v) || !key_ij(k, swap, &i, &j)) return 0;
+    if (_PyLong_Sign(v) == 0) continue;
+    if (j > maxj) maxj = j;
+    if (i > maxi) maxi = i;
+    if (i + j > s->td) s->td = i + j;
+  }
+  s->rows = maxj + 1;
+  s->dx = maxi < 0 ? 0 : maxi;
+  s->deg = (int16_t*)PyMem_Malloc(sizeof(int16_t) * (size_t)(s->rows > 0 ? s->rows : 1));
+  s->norm = (double*)PyMem_Calloc((size_t)(s->rows > 0 ? s->rows : 1), sizeof(double));
+  if (!s->deg || !s->norm) return -1;
+  for (Py_ssize_t r = 0; r < s->rows; ++r) s->deg[r] = -1;
+  s->norm_ok = 1;
+  pos = 0;
+  while (PyDict_Next(terms, &pos, &k, &v)) {
+    key_ij(k, swap, &i, &j);
+    if (_PyLong_Sign(v) == 0) continue;
+    if (i > s->deg[j]) s->deg[j] = (int16_t)i;
+    const size_t nb = _PyLong_NumBits(v);
+    if (nb > *maxbits) *maxbits = nb;
+    if (s->norm_ok) {
+      const double d = PyLong_AsDouble(v);
+      if (d == -1.0 && PyErr_Occurred()) {
+        PyErr_Clear();
+        s->norm_ok = 0;
+      } else {
+        s->norm[j] += d < 0 ? -d : d;
+      }
+    }
+  }
+  return 1;
+}
+
+/* pass 2: every nonzero coefficient into its grid slot */
+static int write_side(PyObject* terms, int swap, Py_ssize_t dx, Py_ssize_t L, unsigned char* base) {
+  Py_ssize_t pos = 0;
+  PyObject *k, *v;
+  long i, j;
+  while (PyDict_Next(terms, &pos, &k, &v)) {
+    key_ij(k, swap, &i, &j);
+    if (_PyLong_Sign(v) == 0) continue;
+    unsigned char* dst = base + ((size_t)j * (size_t)(dx + 1) + (size_t)i) * (size_t)(4 * L);
+#if PY_VERSION_HEX >= 0x030D0000
+    if (_PyLong_AsByteArray((PyLongObject*)v, dst, (size_t)(4 * L), 1, 1, 1) < 0) return 0;
+#else
+    if (_PyLong_AsByteArray((PyLongObject*)v, dst, (size_t)(4 * L), 1, 1) < 0) return 0;
+#endif
+  }
+  return 1;
+}
+
+static PyObject* lead_row(PyObject* terms, int swap, long row, int16_t deg) {
+  PyObject* out = PyList_New(deg + 1);
+  if (!out) return NULL;
+  PyObject* zero = PyLong_FromLong(0);
+  for (Py_ssize_t t = 0; t <= deg; ++t) {
+    Py_INCREF(zero);
+    PyList_SET_ITEM(out, t, zero);
+  }
+  Py_DECREF(zero);
+  Py_ssize_t pos = 0;
+  PyObject *k, *v;
+  long i, j;
+  while (PyDict_Next(terms, &pos, &k, &v)) {
+    key_ij(k, swap, &i, &j);
+    if (j != row || _PyLong_Sign(v) == 0) continue;
+    Py_INCREF(v);
+    PyList_SetItem(out, i, v); /* steals v, releases the zero */
+  }
+  return out;
+}
+
+static PyObject* norms_list(const GridSide* f, const GridSide* g) {
+  if (!f->norm_ok || !g->norm_ok) Py_RETURN_NONE;
+  PyObject* out = PyList_New(f->rows + g->rows);
+  if (!out) return NULL;
+  for (Py_ssize_t r = 0; r < f->rows; ++r) PyList_SET_ITEM(out, r, PyFloat_FromDouble(f->norm[r]));
+  for (Py_ssize_t r = 0; r < g->rows; ++r) PyList_SET_ITEM(out, f->rows + r, PyFloat_FromDouble(g->norm[r]));
+  return out;
+}
+
+static PyObject* terms_grid(PyObject* self, PyObject* args) {
+  PyObject *tf, *tg;
+  int swap;
+  if (!PyArg_ParseTuple(args, "OOp", &tf, &tg, &swap)) return NULL;
+  if (!PyDict_CheckExact(tf) || !PyDict_CheckExact(tg)) Py_RETURN_NONE;
+  GridSide f = {0}, g = {0};
+  size_t maxbits = 0;
+  PyObject* ret = NULL;
+  int okf = scan_side(tf, swap, &f, &maxbits);
+  int okg = okf == 1 ? scan_side(tg, swap, &g, &maxbits) : okf;
+  if (okf < 0 || okg < 0) {
+    PyErr_NoMemory();
+    goto done;
+  }
+  if (!okf || !okg || f.rows == 0 || g.rows == 0) {
+    Py_INCREF(Py_None);
+    ret = Py_None;
+    goto done;
+  }
+  {
+    const Py_ssize_t L = (Py_ssize_t)((maxbits + 1 + 31) / 32) > 0 ? (Py_ssize_t)((maxbits + 1 + 31) / 32) : 1;
+    const Py_ssize_t cf = f.rows * (f.dx + 1), C = cf + g.rows * (g.dx + 1);
+    PyObject* limbs = PyBytes_FromStringAndSize(NULL, C * L * 4);
+    if (!limbs) goto done;
+    unsigned char* buf = (unsigned char*)PyBytes_AS_STRING(limbs);
+    memset(buf, 0, (size_t)(C * L * 4));
+    if (!write_side(tf, swap, f.dx, L, buf) || !write_side(tg, swap, g.dx, L, buf + (size_t)cf * L * 4)) {
+      Py_DECREF(limbs);
+      goto done;
+    }
+    PyObject* degs = PyBytes_FromStringAndSize(NULL, (f.rows + g.rows) * 2);
+    if (!degs) {
+      Py_DECREF(limbs);
+      goto done;
+    }
+    memcpy(PyBytes_AS_STRING(degs), f.deg, (size_t)f.rows * 2);
+    memcpy(PyBytes_AS_STRING(degs) + f.rows * 2, g.deg, (size_t)g.rows * 2);
+    PyObject* norms = norms_list(&f, &g);
+    PyObject* lcf = lead_row(tf, swap, (long)(f.rows - 1), f.deg[f.rows - 1]);
+    PyObject* lcg = lead_row(tg, swap, (long)(g.rows - 1), g.deg[g.rows - 1]);
+    if (norms && lcf && lcg)
+      ret = Py_BuildValue("(NnnnnnllNNNN)", limbs, L, f.rows - 1, g.rows - 1, f.dx, g.dx, f.td, g.td, degs, norms,
+                          lcf, lcg);
+    else {
+      Py_DECREF(limbs);
+      Py_DECREF(degs);
+      Py_XDECREF(norms);
+      Py_XDECREF(lcf);
+      Py_XDECREF(lcg);
+    }
+  }
+done:
+  PyMem_Free(f.deg);
+  PyMem_Free(f.norm);
+  PyMem_Free(g.deg);
+  PyMem_Free(g.norm);
+  return ret;
+}
+
 static PyMethodDef methods[] = {
     {"limbs_to_ints", limbs_to_ints, METH_VARARGS, "[N][LW] two's-complement u32 limbs -> list of ints"},
+    {"terms_grid", terms_grid, METH_VARARGS,
+     "(terms_f, terms_g, swap) -> packed limb grid, shape, degrees, row 1-norms, leading rows (or None)"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "ckb_limbs", NULL, -1, methods};

@@ -26,7 +26,7 @@ import numpy as np
 
 from . import _lib
 from .bivpoly import as_biv
-from .planner import (ints_to_limbs, limbs_to_ints, pack_grid, plan_resultant)
+from .planner import (ints_to_limbs, limbs_to_ints, pack_grid, pack_terms, plan_packed, plan_resultant)
 from .primes30 import PRIMES30
 
 ctypes_ptr = ctypes.c_void_p
@@ -520,6 +520,10 @@ def biv_resultant(f, g, var: str = "y", seed: int = 0) -> list:
     interpolation, mixed-radix CRT with limbs out) runs in one call of
     ``ckb_biv_resultant`` on the GPU.
     """
+    # plain term dicts go straight to the limb grid (one C pass, no coeffs_wrt_y)
+    pk = pack_terms(f, g, var == "x") if var in ("x", "y") else None
+    if pk is not None and pk.m > 0 and pk.n > 0:
+        return _biv_resultant_gpu(None, None, pk.tdf, pk.tdg, pk)[0]
     f, g = as_biv(f), as_biv(g)
     if f.is_zero() or g.is_zero():
         raise ValueError("resultant of zero polynomial")
@@ -540,13 +544,18 @@ def biv_resultant(f, g, var: str = "y", seed: int = 0) -> list:
     return res
 
 
-def _biv_resultant_gpu(fc, gc, tdf: int, tdg: int):
+def _biv_resultant_gpu(fc, gc, tdf: int, tdg: int, packed=None):
+    """One ckb_biv_resultant call; ``packed`` from pack_terms replaces fc/gc."""
     lib = _lib.lib()
-    m, n = len(fc) - 1, len(gc) - 1
-    packed = pack_grid(fc, gc)
+    if packed is None:
+        packed = pack_grid(fc, gc)
+    m, n = packed.m, packed.n
     start = 0
     for _attempt in range(4):
-        plan = plan_resultant(fc, gc, tdf, tdg, packed.dfx, packed.dgx, start)
+        if packed.norms is not None:
+            plan = plan_packed(packed, start)
+        else:
+            plan = plan_resultant(fc, gc, tdf, tdg, packed.dfx, packed.dgx, start)
         K, N, LW = len(plan.primes), plan.N, plan.LW
         out = _lib.pinned.get("biv_out", N * LW)  # page-locked: the result lands here directly
         status = np.zeros(1, dtype=np.uint32)
@@ -572,6 +581,10 @@ def biv_resultant_batch(problems, seed: int = 0) -> list:
     results = [None] * len(problems)
     gpu = []
     for i, (f, g, var) in enumerate(problems):
+        pk = pack_terms(f, g, var == "x") if var in ("x", "y") else None
+        if pk is not None and pk.m > 0 and pk.n > 0:
+            gpu.append((i, None, None, pk.tdf, pk.tdg, pk))
+            continue
         f, g = as_biv(f), as_biv(g)
         if f.is_zero() or g.is_zero():
             raise ValueError("resultant of zero polynomial")
@@ -588,14 +601,14 @@ def biv_resultant_batch(problems, seed: int = 0) -> list:
         elif n == 0:
             results[i] = _pow(gc[0], m)
         else:
-            gpu.append((i, fc, gc, f.total_degree(), g.total_degree()))
+            gpu.append((i, fc, gc, f.total_degree(), g.total_degree(), None))
     lib = _lib.lib()
     for a in range(0, len(gpu), 4):
         chunk = gpu[a:a + 4]
         P = len(chunk)
-        packs = [pack_grid(fc, gc) for _, fc, gc, _, _ in chunk]
-        plans = [plan_resultant(fc, gc, tdf, tdg, pk.dfx, pk.dgx)
-                 for (_, fc, gc, tdf, tdg), pk in zip(chunk, packs)]
+        packs = [pk if pk is not None else pack_grid(fc, gc) for _, fc, gc, _, _, pk in chunk]
+        plans = [plan_packed(pk) if pk.norms is not None else plan_resultant(fc, gc, tdf, tdg, pk.dfx, pk.dgx)
+                 for (_, fc, gc, tdf, tdg, _), pk in zip(chunk, packs)]
         outs = [_lib.pinned.get(f"biv_out{j}", pl.N * pl.LW) for j, pl in enumerate(plans)]
         status = np.zeros(P, dtype=np.uint32)
 
@@ -615,9 +628,9 @@ def biv_resultant_batch(problems, seed: int = 0) -> list:
             _lib.ptr(ms), _lib.ptr(ns), _lib.ptr(dfs), _lib.ptr(dgs), ptrs([pl.primes for pl in plans]),
             ptrs([pl.gens for pl in plans]), _lib.ptr(ks), _lib.ptr(nn), _lib.ptr(lws), ptrs(outs),
             _lib.ptr(status)), "ckb_biv_resultant_batch")
-        for j, (i, fc, gc, tdf, tdg) in enumerate(chunk):
+        for j, (i, fc, gc, tdf, tdg, _) in enumerate(chunk):
             if status[j]:  # a prime had no admissible point set: the single call re-plans
-                results[i], _ = _biv_resultant_gpu(fc, gc, tdf, tdg)
+                results[i], _ = _biv_resultant_gpu(fc, gc, tdf, tdg, packs[j])
             else:
                 results[i] = _trim(limbs_to_ints(outs[j], plans[j].N, plans[j].LW))
         del rc

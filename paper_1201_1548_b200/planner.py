@@ -36,6 +36,12 @@ class Packed:
     n: int
     dfx: int
     dgx: int
+    # filled by pack_terms: per-row 1-norms (doubles), total degrees, leading rows
+    norms: list | None = None
+    tdf: int = -1
+    tdg: int = -1
+    lcf: list | None = None
+    lcg: list | None = None
 
 
 @dataclass
@@ -141,29 +147,84 @@ def log2_coeff_bound(fc, gc) -> float:
     return min(ref, row, col)
 
 
+def log2_bound_from_norms(nf, ng) -> float:
+    """log2_coeff_bound from per-row 1-norms given as doubles (pack_terms).
+
+    Same three bounds; the column sums of the Sylvester matrix are windows of
+    n (f) and m (g) consecutive rows, i.e. full convolutions with a box, summed
+    directly (all terms positive: relative error <= (m + n) eps, no prefix-sum
+    cancellation), so the result is within ~1e-12 bits of the exact one, far
+    inside the planner's one-bit margin."""
+    nf = np.asarray(nf, dtype=np.float64)
+    ng = np.asarray(ng, dtype=np.float64)
+    m, n = len(nf) - 1, len(ng) - 1
+    s = np.convolve(nf, np.ones(n)) + np.convolve(ng, np.ones(m))
+    s2 = np.convolve(nf * nf, np.ones(n)) + np.convolve(ng * ng, np.ones(m))
+    ref = float(np.log2(np.maximum(s, 1.0)).sum())
+    col = 0.5 * float(np.log2(np.maximum(s2, 1.0)).sum())
+    row = 0.5 * (n * np.log2(max(1.0, float((nf * nf).sum()))) + m * np.log2(max(1.0, float((ng * ng).sum()))))
+    return min(ref, float(row), col)
+
+
 def choose_primes_log2(bound_log2: float, lcf, lcg, start: int = 0, table=PRIMES30):
-    """Primes (descending, from ``start``) until log2(prod) > log2(4 B) + 1."""
-    from math import log2
+    """Primes (descending, from ``start``) until log2(prod) > log2(4 B) + 1.
+
+    A prime annihilates a leading y-coefficient polynomial (modpoly.py:378-379)
+    iff it divides the gcd of that polynomial's coefficients, so the scan tests
+    two integers per prime (none at all when both gcds are 1, the usual case)."""
+    from math import gcd
     target = bound_log2 + 3.0
+    gf, gg = gcd(*lcf), gcd(*lcg)
+    check = gf != 1 or gg != 1
+    logs, cum, parr, garr = _log2_table(table)
+    # the count from the running log-sum, valid when no prime of the run is skipped
+    import bisect
+    k = bisect.bisect_right(cum, cum[start] + target)  # first index whose prefix exceeds the target
+    if not check or (k <= len(table) and not ((_mod_many(gf, parr[start:k]) == 0)
+                                              | (_mod_many(gg, parr[start:k]) == 0)).any()):
+        if k > len(table):
+            raise ArithmeticError("prime table exhausted in resultant computation")
+        return parr[start:k].tolist(), garr[start:k].tolist()
     primes, gens = [], []
     acc = 0.0
     i = start
-    const = len(lcf) == 1 and len(lcg) == 1
-    a, b = (lcf[0], lcg[0]) if const else (None, None)
     while acc <= target:
         if i >= len(table):
             raise ArithmeticError("prime table exhausted in resultant computation")
         p, g = table[i]
-        i += 1
-        if const:
-            if a % p == 0 or b % p == 0:
-                continue
-        elif _lc_vanishes(lcf, p) or _lc_vanishes(lcg, p):
+        if check and (gf % p == 0 or gg % p == 0):
+            i += 1
             continue
         primes.append(p)
         gens.append(g)
-        acc += log2(p)
+        acc += logs[i]
+        i += 1
     return primes, gens
+
+
+_LOG2 = {}
+
+
+def _mod_many(x: int, ps: np.ndarray) -> np.ndarray:
+    """|x| mod p for every p < 2^31 of ``ps``: Horner over x's 31-bit limbs (int64 lanes)."""
+    x = abs(x)
+    r = np.zeros(len(ps), dtype=np.int64)
+    for sh in range(((x.bit_length() + 30) // 31 - 1) * 31, -1, -31):
+        r = ((r << 31) + ((x >> sh) & 0x7FFFFFFF)) % ps
+    return r
+
+
+def _log2_table(table):
+    """(log2 p, prefix sums of log2 p from 0, primes, generators) of a prime table."""
+    t = _LOG2.get(id(table))
+    if t is None or len(t[0]) != len(table):
+        from itertools import accumulate
+        from math import log2
+        logs = [log2(p) for p, _ in table]
+        t = (logs, [0.0] + list(accumulate(logs)), np.array([p for p, _ in table], dtype=np.int64),
+             np.array([g for _, g in table], dtype=np.int64))
+        _LOG2[id(table)] = t
+    return t
 
 
 def point_count(fc, gc, dfx: int, dgx: int, tdf: int, tdg: int) -> int:
@@ -247,11 +308,40 @@ def pack_grid(fc, gc) -> Packed:
     return Packed(np.ascontiguousarray(limbs), degs, C, L, m, n, dfx, dgx)
 
 
+def pack_terms(f, g, swap: bool = False):
+    """pack_grid straight from two term dicts ({(i, j): c}, the reference's
+    BivPoly.terms, bivpoly.py:18-25) in one C pass (host/ckb_limbs.c
+    terms_grid), with what plan_packed needs; None when the C helper is absent
+    or the input is not plain ints (the caller takes coeffs_wrt_y + pack_grid)."""
+    if _ckb_limbs is None:
+        return None
+    tf = f if isinstance(f, dict) else getattr(f, "terms", None)
+    tg = g if isinstance(g, dict) else getattr(g, "terms", None)
+    if type(tf) is not dict or type(tg) is not dict:
+        return None
+    r = _ckb_limbs.terms_grid(tf, tg, bool(swap))
+    if r is None or r[9] is None:
+        return None
+    limbs, L, m, n, dfx, dgx, tdf, tdg, degs, norms, lcf, lcg = r
+    C = (m + 1) * (dfx + 1) + (n + 1) * (dgx + 1)
+    return Packed(np.frombuffer(limbs, dtype=np.uint32), np.frombuffer(degs, dtype=np.int16), C, L, m, n, dfx, dgx,
+                  norms, tdf, tdg, lcf, lcg)
+
+
 def plan_resultant(fc, gc, tdf: int, tdg: int, dfx: int, dgx: int, start: int = 0) -> Plan:
+    return _plan(log2_coeff_bound(fc, gc), point_count(fc, gc, dfx, dgx, tdf, tdg), fc[-1], gc[-1], start)
+
+
+def plan_packed(pk: Packed, start: int = 0) -> Plan:
+    """plan_resultant for a grid from pack_terms (its norms, degrees and leading rows)."""
+    m, n = pk.m, pk.n
+    N = min(pk.dfx * n + pk.dgx * m, n * pk.tdf + m * pk.tdg - m * n) + 1  # point_count
+    return _plan(log2_bound_from_norms(pk.norms[:m + 1], pk.norms[m + 1:]), N, pk.lcf, pk.lcg, start)
+
+
+def _plan(blog: float, N: int, lcf, lcg, start: int) -> Plan:
     from math import log2
-    blog = log2_coeff_bound(fc, gc)
-    N = point_count(fc, gc, dfx, dgx, tdf, tdg)
-    primes, gens = choose_primes_log2(blog, fc[-1], gc[-1], start)
+    primes, gens = choose_primes_log2(blog, lcf, lcg, start)
     # bit length of the modulus (LW words must hold M): the float sum is within
     # ~1e-12 of log2 M; rounding it up by 1e-6 can only add a spare word
     mbits = int(sum(log2(p) for p in primes) + 1e-6) + 1

@@ -154,3 +154,66 @@ def test_limbs_roundtrip_c_helper_and_python():
             assert planner.limbs_to_ints(limbs, len(vals), L) == vals, bits
         finally:
             planner._ckb_limbs = saved
+
+
+def _pack_both(f, g, swap):
+    F, G = (BivPoly(f), BivPoly(g)) if isinstance(f, dict) else (f, g)
+    if swap:
+        F, G = F.swap(), G.swap()
+    fc, gc = F.coeffs_wrt_y(), G.coeffs_wrt_y()
+    return planner.pack_terms(f, g, swap), planner.pack_grid(fc, gc), fc, gc, F, G
+
+
+def test_pack_terms_matches_coeffs_path():
+    """The one-pass C packer (host/ckb_limbs.c terms_grid) gives pack_grid's grid
+    and plan_resultant's plan, for dicts and BivPoly objects, both variables."""
+    if planner._ckb_limbs is None:
+        import pytest
+        pytest.skip("host helper not built")
+    from paper_1201_1548_b200.synth import make_pair
+    rng = random.Random(5)
+    cases = [make_pair(c, 0) for c in ("cfg1", "cfg2", "cfg4")]
+    for _ in range(40):
+        f, g = {}, {}
+        for t in (f, g):
+            dx, dy = rng.randint(0, 9), rng.randint(1, 9)
+            bits = rng.choice([3, 31, 32, 63, 64, 65, 200])
+            for i in range(dx + 1):
+                for j in range(dy + 1):
+                    if rng.random() < 0.6:
+                        t[(i, j)] = rng.randint(-2 ** bits, 2 ** bits)  # zeros included
+            t[(rng.randint(0, dx), dy)] = rng.choice([1, -1]) * rng.randint(1, 2 ** bits)
+        cases.append((f, g))
+    n = 0
+    for f, g in cases:
+        for swap in (False, True):
+            for wrap in (False, True):
+                a, b = (BivPoly(f), BivPoly(g)) if wrap else (f, g)
+                pk, ref, fc, gc, F, G = _pack_both(a, b, swap)
+                if ref.m == 0 or ref.n == 0:
+                    continue
+                assert pk is not None
+                assert (pk.C, pk.L, pk.m, pk.n, pk.dfx, pk.dgx) == (ref.C, ref.L, ref.m, ref.n, ref.dfx, ref.dgx)
+                assert np.array_equal(pk.limbs, ref.limbs) and np.array_equal(pk.degs, ref.degs)
+                assert (pk.tdf, pk.tdg, pk.lcf, pk.lcg) == (F.total_degree(), G.total_degree(), fc[-1], gc[-1])
+                p1 = planner.plan_packed(pk)
+                p2 = planner.plan_resultant(fc, gc, F.total_degree(), G.total_degree(), ref.dfx, ref.dgx)
+                assert np.array_equal(p1.primes, p2.primes) and (p1.N, p1.LW) == (p2.N, p2.LW)
+                assert abs(planner.log2_bound_from_norms(pk.norms[:pk.m + 1], pk.norms[pk.m + 1:])
+                           - planner.log2_coeff_bound(fc, gc)) < 1e-9
+                n += 1
+    assert n > 100
+
+
+def test_pack_terms_declines_what_it_cannot_read():
+    if planner._ckb_limbs is None:
+        import pytest
+        pytest.skip("host helper not built")
+    one = {(0, 1): 1, (0, 0): 2}
+    assert planner.pack_terms({(0, 1): 1.5}, one) is None           # non-int coefficient
+    assert planner.pack_terms({(0, 1): True}, one) is None          # bool is not a plain int
+    assert planner.pack_terms({(-1, 1): 3}, one) is None            # negative exponent
+    assert planner.pack_terms({(0, 1): np.int64(3)}, one) is None   # numpy scalar
+    assert planner.pack_terms({(0, 1): 10 ** 400}, one) is None     # 1-norm overflows a double
+    assert planner.pack_terms({}, one) is None                      # zero polynomial
+    assert planner.pack_terms([1, 2], one) is None
