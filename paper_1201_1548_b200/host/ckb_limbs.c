@@ -15,23 +15,38 @@
  * 30-bit digits (_PyLong_FromDigits copies and normalises them): O(limbs),
  * no per-byte loop (_PyLong_FromByteArray costs ~1 us per 5,000-bit
  * coefficient; this ~0.1 us). */
-static PyObject* limbs_to_long(const uint32_t* c, Py_ssize_t len, digit* dg, uint32_t* mag) {
+static PyObject* limbs_to_long(const uint32_t* c, Py_ssize_t len, digit* dg) {
   const int neg = (int)(c[len - 1] >> 31);
-  const uint32_t* m = c;
-  if (neg) { /* magnitude = ~c + 1 */
-    uint64_t carry = 1;
-    for (Py_ssize_t i = 0; i < len; ++i) {
-      const uint64_t v = (uint64_t)(~c[i]) + carry;
-      mag[i] = (uint32_t)v;
+  /* magnitude = (c ^ flip) + carry0, negated on the fly for a negative value */
+  const uint32_t flip = neg ? 0xffffffffu : 0u;
+  uint64_t carry = neg ? 1u : 0u;
+  Py_ssize_t nd = 0;
+  Py_ssize_t i = 0;
+  /* 15 limbs = 480 bits = 16 digits: a fixed shift pattern the compiler unrolls */
+  for (; i + 15 <= len; i += 15) {
+    uint32_t s[15];
+#pragma GCC unroll 15
+    for (int k = 0; k < 15; ++k) {
+      const uint64_t v = (uint64_t)(c[i + k] ^ flip) + carry;
+      s[k] = (uint32_t)v;
       carry = v >> 32;
     }
-    m = mag;
+    digit* d = dg + nd;
+#pragma GCC unroll 16
+    for (int t = 0; t < 16; ++t) {
+      const int bit = 30 * t, w = bit >> 5, o = bit & 31;
+      uint64_t v = (uint64_t)s[w] >> o;
+      if (o > 2 && w + 1 < 15) v |= (uint64_t)s[w + 1] << (32 - o);
+      d[t] = (digit)(v & PyLong_MASK);
+    }
+    nd += 16;
   }
-  Py_ssize_t nd = 0;
   uint64_t acc = 0;
   int bits = 0;
-  for (Py_ssize_t i = 0; i < len; ++i) {
-    acc |= (uint64_t)m[i] << bits;
+  for (; i < len; ++i) {
+    const uint64_t v = (uint64_t)(c[i] ^ flip) + carry;
+    carry = v >> 32;
+    acc |= (uint64_t)(uint32_t)v << bits;
     bits += 32;
     while (bits >= PyLong_SHIFT) {
       dg[nd++] = (digit)(acc & PyLong_MASK);
@@ -63,10 +78,7 @@ static PyObject* limbs_to_ints(PyObject* self, PyObject* args) {
   const uint32_t* w = (const uint32_t*)view.buf;
 #ifdef CKB_FAST_DIGITS
   digit* dg = (digit*)PyMem_Malloc(sizeof(digit) * (size_t)(lw * 32 / PyLong_SHIFT + 2));
-  uint32_t* mag = (uint32_t*)PyMem_Malloc(sizeof(uint32_t) * (size_t)lw);
-  if (!dg || !mag) {
-    PyMem_Free(dg);
-    PyMem_Free(mag);
+  if (!dg) {
     Py_DECREF(out);
     PyBuffer_Release(&view);
     return PyErr_NoMemory();
@@ -79,14 +91,13 @@ static PyObject* limbs_to_ints(PyObject* self, PyObject* args) {
     /* drop limbs that only repeat the sign, keeping the sign bit in the top one */
     while (len > 1 && c[len - 1] == ext && ((c[len - 2] >> 31) ? 0xffffffffu : 0u) == ext) --len;
 #ifdef CKB_FAST_DIGITS
-    PyObject* v = limbs_to_long(c, len, dg, mag);
+    PyObject* v = limbs_to_long(c, len, dg);
 #else
     PyObject* v = _PyLong_FromByteArray((const unsigned char*)c, (size_t)(4 * len), 1, 1);
 #endif
     if (!v) {
 #ifdef CKB_FAST_DIGITS
       PyMem_Free(dg);
-      PyMem_Free(mag);
 #endif
       Py_DECREF(out);
       PyBuffer_Release(&view);
@@ -96,7 +107,6 @@ static PyObject* limbs_to_ints(PyObject* self, PyObject* args) {
   }
 #ifdef CKB_FAST_DIGITS
   PyMem_Free(dg);
-  PyMem_Free(mag);
 #endif
   PyBuffer_Release(&view);
   return out;
