@@ -250,14 +250,45 @@ def variations_on(p, a, b) -> int:
     return int(v[0])
 
 
-def _variation_bits(p, n: int, a_num: int, w: int, ld: int) -> float:
-    # |c|_inf <= 2^n |r|_1 <= 2^n sum_i |p_i| 2^(ld (n-i)) (|a| + |w|)^i   (bit-length bounds)
+def _variation_bits(pb, n: int, a_num: int, w: int, ld: int) -> float:
+    # |c|_inf <= 2^n |r|_1 <= 2^n sum_i |p_i| 2^(ld (n-i)) (|a| + |w|)^i   (bit-length bounds);
+    # pb = _coeff_bits(p): the max over i of pb_i + ld (n - i) + i t, evaluated as one numpy max
+    import numpy as np
     t = (abs(a_num) + abs(w)).bit_length()
-    top = max(abs(p[i]).bit_length() + ld * (n - i) + i * t for i in range(n + 1) if p[i])
+    top = int((pb + np.arange(n + 1, dtype=np.int64) * (t - ld)).max()) + ld * n
     return top + math.log2(n + 1) + n + 4  # M > 4 * bound for the explicit CRT
 
 
-def variations_batch(p, intervals) -> list:
+def _coeff_bits(p, n: int):
+    """Bit lengths of |p_0..p_n| (int64; zero coefficients far below any term)."""
+    import numpy as np
+    return np.array([abs(c).bit_length() if c else -(1 << 60) for c in p[:n + 1]], dtype=np.int64)
+
+
+_ZQ = (1 << 61) - 1  # prime
+
+
+def _nonzero_at(p, pmod, x, U) -> bool:
+    """U.eval_dyadic(p, x).sign() != 0 (upoly.py:168-179), decided modulo the
+    prime q = 2^61 - 1 first: with x = man 2^e, p(x) = 0 iff the integer
+    sum_i p_i man^i 2^(k (n - i)) (k = -e > 0; or p(man 2^e) for e >= 0) is 0,
+    and a nonzero residue of it proves it nonzero (2 is invertible mod q).  A
+    zero residue (probability ~2^-61, or a real root) takes the exact path."""
+    q = _ZQ
+    xq = x.man % q
+    if x.exp >= 0:
+        xq = xq * pow(2, x.exp, q) % q
+    else:
+        xq = xq * pow(pow(2, -x.exp, q), q - 2, q) % q
+    acc = 0
+    for c in reversed(pmod):
+        acc = (acc * xq + c) % q
+    if acc:
+        return True
+    return U.eval_dyadic(p, x).sign() != 0
+
+
+def variations_batch(p, intervals, pbits=None) -> list:
     """[variations_on(p, a, b) for (a, b) in intervals] with whole batches of
     intervals in one library call (ckb_descartes_variations_batch: every
     interval's Taylor shift for every prime in one launch, one CRT over all
@@ -273,6 +304,7 @@ def variations_batch(p, intervals) -> list:
         return [0] * len(intervals)
     if n > 8191:
         raise NotImplementedError("Descartes test supports degree < 8192")
+    pb = pbits if pbits is not None else _coeff_bits(p, n)  # (descartes_isolate passes it once per polynomial)
     params = []
     for a, b in intervals:
         e = min(a.exp, b.exp, 0)
@@ -284,7 +316,7 @@ def variations_batch(p, intervals) -> list:
     i0 = 0
     while i0 < len(params):
         # chunk so that the CRT input and output stay within ~1 GB of HBM
-        bits = max(_variation_bits(p, n, a_num, w, ld) for a_num, w, ld in params[i0:i0 + 256])
+        bits = max(_variation_bits(pb, n, a_num, w, ld) for a_num, w, ld in params[i0:i0 + 256])
         K = _primes_for_bits(bits)
         LW = (int(_log2_prefix[K - 1]) + 1 + 1 + 31) // 32 + 1
         B = max(1, min(256, len(params) - i0, (1 << 28) // ((n + 1) * (K + 2 * LW))))
@@ -336,8 +368,13 @@ def descartes_isolate(p, check_squarefree: bool = True, multiplicity: int = 1) -
         k = U.cauchy_bound_log2(work)
         bound = U.Dyadic(1, k)
         level = [(-bound, bound)]
+        nw = len(work) - 1
+        while nw >= 0 and work[nw] == 0:
+            nw -= 1
+        pbits = _coeff_bits(work, nw)
+        pmod = [c % _ZQ for c in work]
         while level:
-            vs = variations_batch(work, level)
+            vs = variations_batch(work, level, pbits)
             nxt = []
             for (a, b), v in zip(level, vs):
                 if v == 0:
@@ -346,7 +383,7 @@ def descartes_isolate(p, check_squarefree: bool = True, multiplicity: int = 1) -
                     roots.append(U.AlgebraicNumber(defining, U.RealInterval(a, b), multiplicity))
                     continue
                 for m in U._interior_points(a, b):
-                    if U.eval_dyadic(work, m).sign() != 0:
+                    if _nonzero_at(work, pmod, m, U):
                         break
                 else:  # pragma: no cover
                     raise ArithmeticError("no non-root subdivision point found")
