@@ -32,9 +32,11 @@ for cfg in sys.argv[1:] or ["cfg2", "cfg4"]:
     for v in r:
         c = math.gcd(c, v)
     p = [v // c for v in r]
-    calls["n"] = 0
-    t0 = time.time()
-    roots = U.descartes_isolate(p)
-    dt = time.time() - t0
-    print(f"{cfg}: degree {len(p) - 1}, {len(roots)} real roots, {calls['n']} Descartes tests, {dt:.2f} s")
+    for rep in ("cold", "warm"):
+        calls["n"] = 0
+        t0 = time.time()
+        roots = U.descartes_isolate(p)
+        dt = time.time() - t0
+        print(f"{cfg} ({rep}): degree {len(p) - 1}, {len(roots)} real roots, {calls['n']} single Descartes tests, "
+              f"{dt:.3f} s")
 pkg.uninstall(saved)
