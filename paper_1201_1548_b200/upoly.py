@@ -266,16 +266,6 @@ def _coeff_bits(p, n: int):
 
 
 _ZQ = (1 << 61) - 1  # prime
-_LOOKAHEAD_TESTS = 32  # tests per batched call the look-ahead may fill
-
-
-def _lookahead(width: int) -> int:
-    """Levels tested per call for a frontier of `width` intervals: the largest
-    d with width (2^d - 1) <= _LOOKAHEAD_TESTS (at least 1)."""
-    d = 1
-    while width * ((1 << (d + 1)) - 1) <= _LOOKAHEAD_TESTS:
-        d += 1
-    return d
 
 
 def _nonzero_at(p, pmod, x, U) -> bool:
@@ -349,9 +339,8 @@ def descartes_isolate(p, check_squarefree: bool = True, multiplicity: int = 1) -
     test per pop; the subdivision of an interval depends only on that interval
     (its test and its own split point), so the set of leaves — the isolating
     intervals — does not depend on the traversal order.  Here every interval of
-    a subdivision level is tested in ONE batched GPU call (variations_batch),
-    and while the level is narrow its descendants a few levels down too
-    (_lookahead: the same tests, fewer calls); split points, the zero root, sorting and _make_disjoint are the reference's
+    a subdivision level is tested in ONE batched GPU call (variations_batch);
+    split points, the zero root, sorting and _make_disjoint are the reference's
     own code, so the returned brackets are identical.  Needs curvekit (it
     returns the reference's AlgebraicNumber objects).
     """
@@ -378,49 +367,28 @@ def descartes_isolate(p, check_squarefree: bool = True, multiplicity: int = 1) -
         defining = tuple(U.primitive(work))
         k = U.cauchy_bound_log2(work)
         bound = U.Dyadic(1, k)
+        level = [(-bound, bound)]
         nw = len(work) - 1
         while nw >= 0 and work[nw] == 0:
             nw -= 1
         pbits = _coeff_bits(work, nw)
         pmod = [c % _ZQ for c in work]
-
-        def split(a, b):  # the reference's subdivision point (upoly.py:349-356, 398-403)
-            for m in U._interior_points(a, b):
-                if _nonzero_at(work, pmod, m, U):
-                    return m
-            raise ArithmeticError("no non-root subdivision point found")  # pragma: no cover
-
-        frontier = [(-bound, bound)]
-        while frontier:
-            # Look ahead: while the frontier is narrow (deep bisection toward close
-            # roots), also test its descendants `depth - 1` levels down in the same
-            # call.  Every test is one the reference would make or a descendant of
-            # one; the walk below keeps exactly the reference's decisions.
-            depth = _lookahead(len(frontier))
-            layers = [frontier]
-            for _ in range(depth - 1):
-                nxt = []
-                for a, b in layers[-1]:
-                    m = split(a, b)
-                    nxt += [(a, m), (m, b)]
-                layers.append(nxt)
-            vs = variations_batch(work, [iv for layer in layers for iv in layer], pbits)
-            off, alive, frontier = 0, range(len(layers[0])), []
-            for d, layer in enumerate(layers):
-                below = []
-                for k in alive:
-                    v = vs[off + k]
-                    a, b = layer[k]
-                    if v == 0:
-                        continue
-                    if v == 1:
-                        roots.append(U.AlgebraicNumber(defining, U.RealInterval(a, b), multiplicity))
-                    elif d + 1 < len(layers):
-                        below += [2 * k, 2 * k + 1]
-                    else:
-                        m = split(a, b)
-                        frontier += [(a, m), (m, b)]
-                off += len(layer)
-                alive = below
+        while level:
+            vs = variations_batch(work, level, pbits)
+            nxt = []
+            for (a, b), v in zip(level, vs):
+                if v == 0:
+                    continue
+                if v == 1:
+                    roots.append(U.AlgebraicNumber(defining, U.RealInterval(a, b), multiplicity))
+                    continue
+                for m in U._interior_points(a, b):
+                    if _nonzero_at(work, pmod, m, U):
+                        break
+                else:  # pragma: no cover
+                    raise ArithmeticError("no non-root subdivision point found")
+                nxt.append((a, m))
+                nxt.append((m, b))
+            level = nxt
     roots.sort(key=lambda r: r.interval.midpoint().as_fraction())
     return U._make_disjoint(roots)

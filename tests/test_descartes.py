@@ -187,48 +187,3 @@ def test_variations_batch_chunking_vs_oracle():
             ivs.append((a, b))
         want = [oracle.variations_on(p, a.man, a.exp, b.man, b.exp) for a, b in ivs]
         assert variations_batch(p, ivs) == want
-
-
-@pytest.mark.parametrize("budget", [1, 6, 32, 200])
-def test_lookahead_walk_matches_reference_loop(curvekit_mod, monkeypatch, budget):
-    """CPU: the breadth-first isolation with look-ahead (several subdivision
-    levels per batched call) returns the reference's own descartes_isolate
-    brackets, with the reference's CPU Descartes test standing in for the GPU
-    batch — the walk and the split points are what is checked here."""
-    import curvekit.upoly as U
-
-    import paper_1201_1548_b200 as pkg
-    from paper_1201_1548_b200 import upoly as ours
-    ref_loop = pkg._ORIGINALS.get(("curvekit.upoly", "descartes_isolate"), U.descartes_isolate)
-    assert ref_loop is not ours.descartes_isolate
-    calls = []
-
-    def cpu_batch(p, intervals, pbits=None):
-        calls.append(len(intervals))
-        return [U._variations_on(p, a, b) for a, b in intervals]
-
-    monkeypatch.setattr(ours, "variations_batch", cpu_batch)
-    monkeypatch.setattr(ours, "_LOOKAHEAD_TESTS", budget)
-    rng = random.Random(budget)
-    polys = []
-    for _ in range(6):  # products of linear factors with close rational roots, times a random factor
-        p = [1]
-        for _ in range(rng.randint(2, 6)):
-            num, den = rng.randint(-40, 40), rng.choice([1, 3, 7, 64, 1000])
-            p = [a - b for a, b in zip([0] + [den * c for c in p], [num * c for c in p] + [0])]
-        q = [rng.randint(-9, 9) for _ in range(rng.randint(1, 5))] + [1]
-        polys.append([sum(p[i] * q[j - i] for i in range(len(p)) if 0 <= j - i < len(q))
-                      for j in range(len(p) + len(q) - 1)])
-    n = 0
-    for p in polys:
-        try:
-            want = ref_loop(p)
-        except ValueError:  # not square-free
-            continue
-        got = ours.descartes_isolate(p, check_squarefree=False)
-        key = [(r.interval.lo, r.interval.hi) for r in want]
-        assert [(r.interval.lo, r.interval.hi) for r in got] == key
-        n += 1
-    assert n >= 3
-    if budget == 1:
-        assert max(calls) >= 1  # no look-ahead: one level per call
