@@ -187,3 +187,38 @@ def test_variations_batch_chunking_vs_oracle():
             ivs.append((a, b))
         want = [oracle.variations_on(p, a.man, a.exp, b.man, b.exp) for a, b in ivs]
         assert variations_batch(p, ivs) == want
+
+
+def test_breadth_first_walk_matches_reference_loop(curvekit_mod, monkeypatch):
+    """CPU: the breadth-first isolation (one batched call per subdivision level,
+    split points checked modulo 2^61 - 1 first) returns the reference's own
+    descartes_isolate brackets, with the reference's CPU Descartes test standing
+    in for the GPU batch — the walk and the split points are what is checked."""
+    import curvekit.upoly as U
+
+    import paper_1201_1548_b200 as pkg
+    from paper_1201_1548_b200 import upoly as ours
+    ref_loop = pkg._ORIGINALS.get(("curvekit.upoly", "descartes_isolate"), U.descartes_isolate)
+    assert ref_loop is not ours.descartes_isolate
+
+    def cpu_batch(p, intervals, pbits=None):
+        return [U._variations_on(p, a, b) for a, b in intervals]
+
+    monkeypatch.setattr(ours, "variations_batch", cpu_batch)
+    rng = random.Random(11)
+    n = 0
+    for _ in range(8):  # products of linear factors with close rational roots, times a random factor
+        p = [1]
+        for _ in range(rng.randint(2, 6)):
+            num, den = rng.randint(-40, 40), rng.choice([1, 3, 7, 64, 1000])
+            p = [a - b for a, b in zip([0] + [den * c for c in p], [num * c for c in p] + [0])]
+        q = [rng.randint(-9, 9) for _ in range(rng.randint(1, 5))] + [1]
+        p = [sum(p[i] * q[j - i] for i in range(len(p)) if 0 <= j - i < len(q)) for j in range(len(p) + len(q) - 1)]
+        try:
+            want = ref_loop(p)
+        except ValueError:  # not square-free
+            continue
+        got = ours.descartes_isolate(p, check_squarefree=False)
+        assert [(r.interval.lo, r.interval.hi) for r in got] == [(r.interval.lo, r.interval.hi) for r in want]
+        n += 1
+    assert n >= 3
