@@ -14,6 +14,9 @@ from paper_1201_1548_b200 import modpoly as mp  # noqa: E402
 from paper_1201_1548_b200 import upoly as ours  # noqa: E402
 from paper_1201_1548_b200.synth import make_pair  # noqa: E402
 
+if os.environ.get("NO_GC"):
+    import gc
+    gc.disable()
 saved = pkg.install()
 calls = {"n": 0}
 orig = ours.variations_on
@@ -32,7 +35,7 @@ for cfg in sys.argv[1:] or ["cfg2", "cfg4"]:
     for v in r:
         c = math.gcd(c, v)
     p = [v // c for v in r]
-    for rep in ("cold", "warm"):
+    for rep in ("cold", "warm", "warm", "warm", "warm"):
         calls["n"] = 0
         t0 = time.time()
         roots = U.descartes_isolate(p)
