@@ -15,20 +15,6 @@ import pytest
 
 from conftest import REPO, load_golden, terms_in
 
-REF = os.path.join(REPO, "baseline", "_ref")
-
-
-@pytest.fixture(scope="module")
-def curvekit_mod():
-    if not os.path.isdir(os.path.join(REF, "curvekit")):
-        pytest.skip("reference install baseline/_ref is absent")
-    if REF not in sys.path:
-        sys.path.insert(0, REF)
-    pytest.importorskip("mpmath")
-    import curvekit.bisolve  # noqa: F401
-    import curvekit.modpoly  # noqa: F401
-    return sys.modules["curvekit"]
-
 
 def test_install_rebinds_and_restores(curvekit_mod):
     import curvekit.bisolve as B

@@ -10,18 +10,6 @@ import pytest
 
 from conftest import REPO, load_golden, terms_in
 
-REF = os.path.join(REPO, "baseline", "_ref")
-
-
-@pytest.fixture(scope="module")
-def ref_bivpoly():
-    if not os.path.isdir(os.path.join(REF, "curvekit")):
-        pytest.skip("reference install baseline/_ref is absent")
-    if REF not in sys.path:
-        sys.path.insert(0, REF)
-    import curvekit.bivpoly as BP
-    return BP
-
 
 def _cols(terms):
     from paper_1201_1548_b200.bivpoly import BivPoly

@@ -62,18 +62,6 @@ def test_gpu_variations_random_vs_oracle():
         assert variations_on(p, a, b) == want
 
 
-@pytest.fixture(scope="module")
-def curvekit_mod():
-    import os
-    import sys
-    from conftest import REPO
-    ref = os.path.join(REPO, "baseline", "_ref")
-    if not os.path.isdir(os.path.join(ref, "curvekit")):
-        pytest.skip("reference install baseline/_ref is absent")
-    if ref not in sys.path:
-        sys.path.insert(0, ref)
-    import curvekit.upoly  # noqa: F401
-    return sys.modules["curvekit"]
 
 
 @pytest.mark.gpu

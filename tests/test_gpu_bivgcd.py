@@ -55,13 +55,8 @@ def test_squarefree_and_square_part(golden):
         print(f"is_squarefree_biv deg {f.total_degree()}: {dt:.3f} s (reference {case['seconds_squarefree']:.2f} s)")
 
 
-def test_installed_into_reference(golden):
-    ref = os.path.join(REPO, "baseline", "_ref")
-    if not os.path.isdir(os.path.join(ref, "curvekit")):
-        pytest.skip("reference install baseline/_ref is absent")
-    if ref not in sys.path:
-        sys.path.insert(0, ref)
-    import curvekit.bivpoly as BP
+def test_installed_into_reference(golden, ref_bivpoly):
+    BP = ref_bivpoly
 
     import paper_1201_1548_b200 as pkg
     from paper_1201_1548_b200 import bivpoly as ours
