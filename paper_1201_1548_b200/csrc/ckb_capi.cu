@@ -75,6 +75,9 @@ struct Ctx {
 
 Ctx g;
 std::mutex g_mu;
+// dynamic shared memory a per-problem kernel may ask for; beyond it the
+// operands live in a global scratch slice per problem (L2-resident in practice)
+constexpr size_t kSmemLimit = 200 * 1024;
 }  // namespace
 namespace ckb {
 bool g_pdl = true;
@@ -873,7 +876,7 @@ int ckb_uni_resultant_batch(const uint32_t* fa, const int32_t* da, const uint32_
   int rc;
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, P))) return rc;
-  if (W < 1 || W > 4096) return fail("ckb_uni_resultant_batch: need 1 <= W <= 4096", -2);
+  if (W < 1) return fail("ckb_uni_resultant_batch: need W >= 1", -2);
   if (B == 0) return 0;
   cudaStream_t st = g.stream;
   uint32_t *d_fa, *d_gb, *d_out;
@@ -891,7 +894,9 @@ int ckb_uni_resultant_batch(const uint32_t* fa, const int32_t* da, const uint32_
   CK(cudaMemcpyAsync(d_da, da, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_db, db, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_pi, pidx, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
-  launch_uni_resultant(d_fa, d_da, d_gb, d_db, W, d_primes, d_pi, B, d_out, st);
+  uint32_t* d_gs = nullptr;  // operands beyond shared memory: a global slice per pair
+  if ((size_t)3 * W * 4 > kSmemLimit && (rc = dbuf("u.gs", (size_t)B * 3 * W, &d_gs))) return rc;
+  launch_uni_resultant(d_fa, d_da, d_gb, d_db, W, d_primes, d_pi, B, d_out, d_gs, st);
   g.launches += 1;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)B, cudaMemcpyDeviceToHost, st));
@@ -968,7 +973,6 @@ int ckb_gcd_mod_batch(const uint32_t* fa, const int32_t* da, int Wf, const uint3
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, P))) return rc;
   if (B == 0) return 0;
-  if ((size_t)2 * (Wf > Wg ? Wf : Wg) * 4 > 200 * 1024) return fail("ckb_gcd_mod_batch: degree too large", -2);
   cudaStream_t st = g.stream;
   uint32_t *d_fa, *d_gb, *d_out;
   int32_t *d_da, *d_db, *d_pi, *d_odeg;
@@ -986,7 +990,10 @@ int ckb_gcd_mod_batch(const uint32_t* fa, const int32_t* da, int Wf, const uint3
   CK(cudaMemcpyAsync(d_da, da, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_db, db, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_pi, pidx, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
-  launch_gcd_mod(d_fa, d_da, Wf, d_gb, d_db, Wg, d_primes, d_pi, B, d_out, Wo, d_odeg, st);
+  uint32_t* d_gs = nullptr;
+  const size_t gw = (size_t)2 * (Wf > Wg ? Wf : Wg);
+  if (gw * 4 > kSmemLimit && (rc = dbuf("g.gs", (size_t)B * gw, &d_gs))) return rc;
+  launch_gcd_mod(d_fa, d_da, Wf, d_gb, d_db, Wg, d_primes, d_pi, B, d_out, Wo, d_odeg, d_gs, st);
   g.launches += 1;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)B * Wo, cudaMemcpyDeviceToHost, st));
@@ -1002,7 +1009,6 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(primes, P))) return rc;
   if (B == 0) return 0;
-  if (W > 12288) return fail("ckb_interp_points: at most 12288 points", -2);
   cudaStream_t st = g.stream;
   uint32_t *d_xs, *d_vs, *d_out;
   int32_t *d_ns, *d_pi;
@@ -1017,7 +1023,9 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
   CK(cudaMemcpyAsync(d_vs, vs, 4 * (size_t)B * W, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_ns, ns, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_pi, pidx, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
-  launch_interp_points(d_xs, d_vs, d_ns, W, d_primes, d_pi, B, d_out, st);
+  uint32_t* d_gs = nullptr;
+  if ((size_t)(4 * W + 2) * 4 > kSmemLimit && (rc = dbuf("ip.gs", (size_t)B * (4 * W + 2), &d_gs))) return rc;
+  launch_interp_points(d_xs, d_vs, d_ns, W, d_primes, d_pi, B, d_out, d_gs, st);
   g.launches += 1;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)B * W, cudaMemcpyDeviceToHost, st));
@@ -1179,12 +1187,15 @@ int ckb_descartes_prepare(const uint32_t* limbs, int n, int L, const uint32_t* p
   std::lock_guard<std::mutex> lk(g_mu);
   int rc;
   if ((rc = ensure_ready())) return rc;
-  if (n < 1 || n > 8191 || L < 1 || K < 1 || K > 8192) return fail("ckb_descartes_prepare: bad sizes", -2);
+  if (n < 1 || L < 1 || K < 1 || K > 8192) return fail("ckb_descartes_prepare: bad sizes", -2);
   if ((rc = check_primes(primes, K))) return rc;
   int logL = 0;
   while ((1 << logL) < 2 * n + 1) ++logL;
+  // degrees whose correlation length exceeds the primes' 2^14 roots of unity: direct O(n^2) correlations
+  const char* fd = getenv("CKB_DESC_DIRECT");  // force the direct mode (parity tests of that path at small n)
+  const bool direct = logL > DESC_NTT_LOG2_MAX || (fd && fd[0] == '1');
   for (int i = 0; i < K; ++i)
-    if (primes[i] >= (1u << 30) || (primes[i] - 1) % (1u << logL))
+    if (primes[i] >= (1u << 30) || (!direct && (primes[i] - 1) % (1u << logL)))
       return fail("ckb_descartes_prepare: primes must be < 2^30 and 1 mod the NTT length (PRIMES30)", -2);
   int h = -1;
   for (size_t i = 0; i < g_desc.size(); ++i)
@@ -1194,16 +1205,25 @@ int ckb_descartes_prepare(const uint32_t* limbs, int n, int L, const uint32_t* p
     g_desc.emplace_back();
     h = (int)g_desc.size() - 1;
   }
-  DescHandle& d = g_desc[h];
-  d.used = true;
+  DescHandle d;  // committed to the slot only once everything succeeded
   d.n = n;
   d.K = K;
   d.primes.assign(primes, primes + K);
   d.gens.assign(gens, gens + K);
-  const int Lt = 1 << logL;
-  const size_t n1 = (size_t)n + 1, kh = (size_t)K * (Lt / 2), kl = (size_t)K * Lt;
-  const size_t words = (size_t)K * n1 * 3 + kh * 4 + kl * 2 + (size_t)K * 5 + 64;
-  CK(cudaMalloc(&d.blob, 4 * words));
+  const int Lt = direct ? n + 1 : 1 << logL;
+  const size_t n1 = (size_t)n + 1, kh = direct ? 0 : (size_t)K * (Lt / 2), kl = (size_t)K * Lt;
+  const size_t words = (size_t)K * n1 * 3 + kh * 4 + kl * (direct ? 1 : 2) + (size_t)K * 5 + 64;
+  auto bail = [&](int code) {
+    if (d.blob) cudaFree(d.blob);
+    return code;
+  };
+  {
+    cudaError_t e = cudaMalloc(&d.blob, 4 * words);
+    if (e != cudaSuccess) {
+      d.blob = nullptr;
+      return fail(std::string("ckb_descartes_prepare: cudaMalloc: ") + cudaGetErrorString(e));
+    }
+  }
   uint32_t* b = (uint32_t*)d.blob;
   auto take = [&](size_t m) { uint32_t* r = b; b += m; return r; };
   d.d_res = take((size_t)K * n1);
@@ -1211,7 +1231,8 @@ int ckb_descartes_prepare(const uint32_t* limbs, int n, int L, const uint32_t* p
   pl.K = K;
   pl.n = n;
   pl.L = Lt;
-  pl.logL = logL;
+  pl.logL = direct ? 0 : logL;
+  pl.direct = direct ? 1 : 0;
   pl.fact = take((size_t)K * n1);
   pl.ifact = take((size_t)K * n1);
   pl.W = take(kh);
@@ -1219,23 +1240,28 @@ int ckb_descartes_prepare(const uint32_t* limbs, int n, int L, const uint32_t* p
   pl.Wi = take(kh);
   pl.Wic = take(kh);
   pl.Vf = take(kl);
-  pl.Vfc = take(kl);
+  pl.Vfc = direct ? nullptr : take(kl);
   pl.Linv = take(K);
   uint32_t* d_gens = take(K);
   d.d_primes = reinterpret_cast<Prime*>(take((size_t)K * 3));
   std::vector<Prime> hp(K);
   for (int i = 0; i < K; ++i) hp[i] = h_prime(primes[i]);
   cudaStream_t st = g.stream;
-  CK(cudaMemcpyAsync(d.d_primes, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_gens, gens, 4 * (size_t)K, cudaMemcpyHostToDevice, st));
   uint32_t* d_limbs;
-  if ((rc = dbuf("desc.limbs", n1 * L, &d_limbs))) return rc;
-  CK(cudaMemcpyAsync(d_limbs, limbs, 4 * n1 * L, cudaMemcpyHostToDevice, st));
-  launch_reduce(d_limbs, (int)n1, L, d.d_primes, K, d.d_res, st);
-  launch_desc_plan(d.d_primes, d_gens, pl, st);
-  g.launches += 2;
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(st));
+  if ((rc = dbuf("desc.limbs", n1 * L, &d_limbs))) return bail(rc);
+  cudaError_t e = cudaMemcpyAsync(d.d_primes, hp.data(), sizeof(Prime) * K, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_gens, gens, 4 * (size_t)K, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_limbs, limbs, 4 * n1 * L, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    launch_reduce(d_limbs, (int)n1, L, d.d_primes, K, d.d_res, st);
+    launch_desc_plan(d.d_primes, d_gens, pl, st);
+    g.launches += 2;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return bail(fail(std::string("ckb_descartes_prepare: ") + cudaGetErrorString(e)));
+  d.used = true;
+  g_desc[h] = d;
   return h;
 }
 
@@ -1267,7 +1293,9 @@ int ckb_descartes_variations_batch(int handle, const uint32_t* aw, int AL, const
   CK(cudaMemcpyAsync(d_ld, ld, 4 * (size_t)B, cudaMemcpyHostToDevice, st));
   DescPlan pl = d.pl;
   pl.K = K;  // the first K primes of the prepared set
-  launch_desc_shift(d.d_primes, pl, d.d_res, d_aw, AL, d_ld, B, d_c, st);
+  uint32_t* d_dscr = nullptr;
+  if (pl.direct && (rc = dbuf("desc.direct", desc_direct_scratch_words(K, d.n, B), &d_dscr))) return rc;
+  launch_desc_shift(d.d_primes, pl, d.d_res, d_aw, AL, d_ld, B, d_c, d_dscr, st);
   launch_crt(ce->t, d_c, (int)NB, d_out, d_crtS, st);
   launch_desc_signs(d_out, N, LW, B, d_v, st);
   g.launches += 5;

@@ -51,9 +51,10 @@ __device__ void desc_scan_mul(uint32_t* buf, int n, const Prime& P, uint32_t* sh
 __global__ void __launch_bounds__(DT) k_desc_plan(const Prime* __restrict__ primes, const uint32_t* __restrict__ gens,
                                                   DescPlan pl) {
   extern __shared__ uint32_t sm[];  // [L] work, [DT] scan scratch
-  uint32_t* buf = sm;
-  uint32_t* sh = sm + pl.L;
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, n = pl.n, L = pl.L, half = L >> 1;
+  // direct mode (degrees beyond the NTT): the scans run in a global slice
+  uint32_t* buf = pl.direct ? pl.Vf + (size_t)pi * (n + 1) : sm;
+  uint32_t* sh = pl.direct ? sm : sm + pl.L;
   const Prime P = primes[pi];
   const uint32_t p = P.p;
   uint32_t* fact = pl.fact + (size_t)pi * (n + 1);
@@ -72,6 +73,7 @@ __global__ void __launch_bounds__(DT) k_desc_plan(const Prime* __restrict__ prim
   desc_scan_mul(buf, n + 1, P, sh);  // buf[m] = (1/n!) * n (n-1) ... (n-m+1) = 1/(n-m)!
   for (int i = tid; i <= n; i += T) ifact[n - i] = buf[i];
   __syncthreads();
+  if (pl.direct) return;  // the direct correlations need only the factorials
   // twiddles
   const uint32_t w = pow_mod(gens[pi] % p, (uint64_t)(p - 1) >> pl.logL, P);
   const uint32_t wi = inv_mod(w, P);
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(DT) k_desc_plan(const Prime* __restrict__ prim
 }
 
 void launch_desc_plan(const Prime* primes, const uint32_t* gens, const DescPlan& pl, cudaStream_t st) {
-  const size_t smem = ((size_t)pl.L + DT) * 4;
+  const size_t smem = ((pl.direct ? 0 : (size_t)pl.L) + DT) * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_desc_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_desc_plan<<<pl.K, DT, smem, st>>>(primes, gens, pl);
 }
@@ -112,11 +114,14 @@ void launch_desc_plan(const Prime* primes, const uint32_t* gens, const DescPlan&
 // c_k mod p for every prime and every interval b (grid.y): res [K][n+1]
 // residues of p; aw [B][2][AL] limbs of a, w; lds [B]; out [K][B (n+1)]
 // (interval b's coefficients at columns b (n+1) + k: one CRT lifts them all)
+// TWS: the four twiddle tables staged in shared memory (L <= 2^13); at L = 2^14
+// X and Y alone take 128 KB, so the twiddles are read from global memory (L2)
+template <bool TWS>
 __global__ void __launch_bounds__(DT) k_desc_shift(const Prime* __restrict__ primes, DescPlan pl,
                                                    const uint32_t* __restrict__ res, const uint32_t* __restrict__ aws,
                                                    int AL, const int32_t* __restrict__ lds,
                                                    uint32_t* __restrict__ outs) {
-  extern __shared__ uint32_t sm[];  // X [L], Y [L], twiddles 4 x [L/2]
+  extern __shared__ uint32_t sm[];  // X [L], Y [L], (TWS) twiddles 4 x [L/2]
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, n = pl.n, L = pl.L, half = L >> 1;
   const int b = blockIdx.y, B = gridDim.y;
   const uint32_t* aw = aws + (size_t)b * 2 * AL;
@@ -125,13 +130,17 @@ __global__ void __launch_bounds__(DT) k_desc_shift(const Prime* __restrict__ pri
   const uint32_t p = P.p;
   uint32_t* X = sm;
   uint32_t* Y = sm + L;
-  uint32_t *W = sm + 2 * L, *Wc = W + half, *Wi = Wc + half, *Wic = Wi + half;
   const size_t oH = (size_t)pi * half;
-  for (int j = tid; j < half; j += T) {
-    W[j] = pl.W[oH + j];
-    Wc[j] = pl.Wc[oH + j];
-    Wi[j] = pl.Wi[oH + j];
-    Wic[j] = pl.Wic[oH + j];
+  const uint32_t *W = pl.W + oH, *Wc = pl.Wc + oH, *Wi = pl.Wi + oH, *Wic = pl.Wic + oH;
+  if (TWS) {
+    uint32_t *sW = sm + 2 * L, *sWc = sW + half, *sWi = sWc + half, *sWic = sWi + half;
+    for (int j = tid; j < half; j += T) {
+      sW[j] = W[j];
+      sWc[j] = Wc[j];
+      sWi[j] = Wi[j];
+      sWic[j] = Wic[j];
+    }
+    W = sW, Wc = sWc, Wi = sWi, Wic = sWic;
   }
   const uint32_t* fact = pl.fact + (size_t)pi * (n + 1);
   const uint32_t* ifact = pl.ifact + (size_t)pi * (n + 1);
@@ -190,11 +199,94 @@ __global__ void __launch_bounds__(DT) k_desc_shift(const Prime* __restrict__ pri
   for (int k = tid; k <= n; k += T) out[k] = mul_mod(mul_mod(red1(Y[n - k], p), linv, P), ifact[k], P);
 }
 
+// ---- direct mode: degrees whose NTT length exceeds the primes' 2^14 -------------
+// the same two correlations as k_desc_shift, each output an O(n) dot product
+// (thread per output, operands in a global slice per (prime, interval)):
+//   conv1[i] = sum_{j <= i} X'_{i-j} Y_j,   conv2[i] = sum_{j <= i} Y2_{i-j} / j!
+__device__ __forceinline__ uint32_t desc_dot(const uint32_t* __restrict__ u, const uint32_t* __restrict__ v, int i,
+                                             const Prime& P) {
+  // sum_{j=0}^{i} u[i-j] v[j]: products < 2^60 (p < 2^30), 16 of them summed in 64 bits
+  // before one reduction to [0, p) by REDC (result carries R^-1, the caller compensates)
+  const uint32_t p = P.p;
+  uint32_t acc = 0u;
+  int j = 0;
+  while (j <= i) {
+    const int e = min(i + 1, j + 15);
+    uint64_t t = 0;
+    for (; j < e; ++j) t += (uint64_t)u[i - j] * v[j];
+    t = t % ((uint64_t)p << 32);  // keep t < p 2^32 for the REDC (16 * 2^60 < 2^64)
+    acc = add_mod(acc, redc(t, P), p);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(DT) k_desc_direct_prep(const Prime* __restrict__ primes, DescPlan pl,
+                                                         const uint32_t* __restrict__ res,
+                                                         const uint32_t* __restrict__ aws, int AL,
+                                                         const int32_t* __restrict__ lds, uint32_t* __restrict__ scr) {
+  const int pi = blockIdx.y, b = blockIdx.z, B = gridDim.z, n = pl.n;
+  const int m = blockIdx.x * DT + threadIdx.x;
+  if (m > n) return;
+  const Prime P = primes[pi];
+  const uint32_t* aw = aws + (size_t)b * 2 * AL;
+  const uint32_t a = limbs_mod(aw, AL, P);
+  const uint32_t s = pow_mod(2u % P.p, (uint64_t)lds[b], P);
+  const uint32_t* fact = pl.fact + (size_t)pi * (n + 1);
+  const uint32_t* ifact = pl.ifact + (size_t)pi * (n + 1);
+  uint32_t* X = scr + ((size_t)pi * B + b) * 3 * (n + 1);
+  uint32_t* Y = X + (n + 1);
+  X[m] = mul_mod(mul_mod(res[(size_t)pi * (n + 1) + n - m], pow_mod(s, (uint64_t)m, P), P), fact[n - m], P);
+  Y[m] = mul_mod(pow_mod(a, (uint64_t)m, P), ifact[m], P);
+}
+
+// conv1 -> Y2 (a third region of the slice: conv1 reads all of X and Y)
+__global__ void __launch_bounds__(DT) k_desc_direct_conv1(const Prime* __restrict__ primes, DescPlan pl,
+                                                          const uint32_t* __restrict__ aws, int AL,
+                                                          uint32_t* __restrict__ scr) {
+  const int pi = blockIdx.y, b = blockIdx.z, B = gridDim.z, n = pl.n;
+  const int m = blockIdx.x * DT + threadIdx.x;
+  if (m > n) return;
+  const Prime P = primes[pi];
+  const uint32_t wv = limbs_mod(aws + (size_t)b * 2 * AL + AL, AL, P);
+  uint32_t* X = scr + ((size_t)pi * B + b) * 3 * (n + 1);
+  const uint32_t R1 = redc((uint64_t)P.r2, P);  // 2^32 mod p: undoes desc_dot's R^-1
+  const uint32_t t = mul_mod(desc_dot(X, X + (n + 1), n - m, P), R1, P);
+  // r_m = t_m w^m / m!;  Y2_m = (n-m)! r_m
+  const uint32_t r = mul_mod(mul_mod(t, pow_mod(wv, (uint64_t)m, P), P), pl.ifact[(size_t)pi * (n + 1) + m], P);
+  X[2 * (n + 1) + m] = mul_mod(r, pl.fact[(size_t)pi * (n + 1) + n - m], P);
+}
+
+__global__ void __launch_bounds__(DT) k_desc_direct_conv2(const Prime* __restrict__ primes, DescPlan pl,
+                                                          const uint32_t* __restrict__ scr, uint32_t* __restrict__ outs) {
+  const int pi = blockIdx.y, b = blockIdx.z, B = gridDim.z, n = pl.n;
+  const int k = blockIdx.x * DT + threadIdx.x;
+  if (k > n) return;
+  const Prime P = primes[pi];
+  const uint32_t* ifact = pl.ifact + (size_t)pi * (n + 1);
+  const uint32_t* Y2 = scr + ((size_t)pi * B + b) * 3 * (n + 1) + 2 * (n + 1);
+  const uint32_t v = mul_mod(desc_dot(Y2, ifact, n - k, P), redc((uint64_t)P.r2, P), P);
+  outs[(size_t)pi * B * (n + 1) + (size_t)b * (n + 1) + k] = mul_mod(v, ifact[k], P);  // c_k = conv2[n-k] / k!
+}
+
 void launch_desc_shift(const Prime* primes, const DescPlan& pl, const uint32_t* res, const uint32_t* aw, int AL,
-                       const int32_t* ld, int B, uint32_t* out, cudaStream_t st) {
-  const size_t smem = (size_t)pl.L * 4 * 4;  // X, Y, 4 half-length twiddle tables
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_desc_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_desc_shift<<<dim3(pl.K, B), DT, smem, st>>>(primes, pl, res, aw, AL, ld, out);
+                       const int32_t* ld, int B, uint32_t* out, uint32_t* scratch, cudaStream_t st) {
+  if (pl.direct) {
+    const dim3 grid((unsigned)((pl.n + DT) / DT), (unsigned)pl.K, (unsigned)B);
+    k_desc_direct_prep<<<grid, DT, 0, st>>>(primes, pl, res, aw, AL, ld, scratch);
+    k_desc_direct_conv1<<<grid, DT, 0, st>>>(primes, pl, aw, AL, scratch);
+    k_desc_direct_conv2<<<grid, DT, 0, st>>>(primes, pl, scratch, out);
+    return;
+  }
+  const size_t full = (size_t)pl.L * 4 * 4;  // X, Y, 4 half-length twiddle tables
+  if (full <= 200 * 1024) {
+    if (full > 48 * 1024) cudaFuncSetAttribute(k_desc_shift<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)full);
+    k_desc_shift<true><<<dim3(pl.K, B), DT, full, st>>>(primes, pl, res, aw, AL, ld, out);
+  } else {
+    const size_t smem = (size_t)pl.L * 2 * 4;  // X, Y (128 KB at L = 2^14)
+    cudaError_t e = cudaFuncSetAttribute(k_desc_shift<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return;  // surfaces through cudaGetLastError in the caller
+    k_desc_shift<false><<<dim3(pl.K, B), DT, smem, st>>>(primes, pl, res, aw, AL, ld, out);
+  }
 }
 
 // sign variations of the lifted coefficients limbs [N][LW] (two's complement),
@@ -205,29 +297,24 @@ __global__ void __launch_bounds__(1024) k_desc_signs(const uint32_t* __restrict_
   const uint32_t* limbs = limbs_all + (size_t)blockIdx.x * N * LW;
   int32_t* result = results + blockIdx.x;
   __shared__ int cnt[1024];
-  __shared__ int8_t sg[16384];
   const int tid = threadIdx.x, T = blockDim.x;
-  for (int k = tid; k < N; k += T) {
-    const uint32_t* c = limbs + (size_t)k * LW;
-    int8_t s = 0;
-    if ((int32_t)c[LW - 1] < 0) {
-      s = -1;
-    } else {
-      for (int l = LW - 1; l >= 0; --l)
-        if (c[l]) {
-          s = 1;
-          break;
-        }
-    }
-    sg[k] = s;
-  }
-  __syncthreads();
-  // each thread: a contiguous segment; count changes inside, remember first/last nonzero sign
+  // each thread: a contiguous segment (signs read straight from the limbs, any N);
+  // count changes inside, remember the first/last nonzero sign
   const int seg = (N + T - 1) / T;
   const int s0 = min(N, tid * seg), s1 = min(N, s0 + seg);
   int first = 0, last = 0, c = 0;
   for (int k = s0; k < s1; ++k) {
-    const int s = sg[k];
+    const uint32_t* w = limbs + (size_t)k * LW;
+    int s = 0;
+    if ((int32_t)w[LW - 1] < 0) {
+      s = -1;
+    } else {
+      for (int l = LW - 1; l >= 0; --l)
+        if (w[l]) {
+          s = 1;
+          break;
+        }
+    }
     if (!s) continue;
     if (!first) first = s;
     if (last && s != last) ++c;

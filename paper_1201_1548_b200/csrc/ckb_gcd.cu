@@ -23,15 +23,17 @@ __global__ void __launch_bounds__(GCD_THREADS) k_gcd_mod(const uint32_t* __restr
                                                          const int32_t* __restrict__ db_, int Wg,
                                                          const Prime* __restrict__ primes,
                                                          const int32_t* __restrict__ pidx, uint32_t* __restrict__ out,
-                                                         int Wo, int32_t* __restrict__ odeg) {
-  extern __shared__ uint32_t sm[];
+                                                         int Wo, int32_t* __restrict__ odeg, uint32_t* __restrict__ gs) {
+  extern __shared__ uint32_t sm_[];
   __shared__ int s_da, s_db, s_swap;
   __shared__ uint32_t s_la, s_lb;
   const int b = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pidx[b]];
   const uint32_t p = P.p;
   const int W = max(Wf, Wg);
-  uint32_t* X = sm;      // two operand buffers of W words
+  // two operand buffers of W words: shared memory, or a global scratch slice beyond it
+  uint32_t* sm = gs ? gs + (size_t)b * 2 * W : sm_;
+  uint32_t* X = sm;
   uint32_t* Y = sm + W;
   int da = da_[b], db = db_[b];
   for (int i = tid; i < W; i += T) {
@@ -86,10 +88,10 @@ __global__ void __launch_bounds__(GCD_THREADS) k_gcd_mod(const uint32_t* __restr
 
 void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_t* gb, const int32_t* db, int Wg,
                     const Prime* primes, const int32_t* pidx, int B, uint32_t* out, int Wo, int32_t* odeg,
-                    cudaStream_t st) {
-  const size_t smem = (size_t)2 * (Wf > Wg ? Wf : Wg) * 4;
+                    uint32_t* gs, cudaStream_t st) {
+  const size_t smem = gs ? 0 : (size_t)2 * (Wf > Wg ? Wf : Wg) * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_gcd_mod, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_gcd_mod<<<B, GCD_THREADS, smem, st>>>(fa, da, Wf, gb, db, Wg, primes, pidx, out, Wo, odeg);
+  k_gcd_mod<<<B, GCD_THREADS, smem, st>>>(fa, da, Wf, gb, db, Wg, primes, pidx, out, Wo, odeg, gs);
 }
 
 // ---------------------------------------------------------------------------
@@ -99,10 +101,11 @@ __global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* _
                                                                const uint32_t* __restrict__ vs, const int32_t* __restrict__ ns,
                                                                int W, const Prime* __restrict__ primes,
                                                                const int32_t* __restrict__ pidx,
-                                                               uint32_t* __restrict__ out) {
-  extern __shared__ uint32_t sm[];
+                                                               uint32_t* __restrict__ out, uint32_t* __restrict__ gs) {
+  extern __shared__ uint32_t sm_[];
   const int b = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const int n = ns[b];
+  uint32_t* sm = gs ? gs + (size_t)b * (4 * W + 2) : sm_;  // global scratch beyond shared memory
   const Prime P = primes[pidx[b]];
   const uint32_t p = P.p;
   uint32_t* x = sm;            // points
@@ -160,10 +163,10 @@ __global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* _
 }
 
 void launch_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const Prime* primes,
-                          const int32_t* pidx, int B, uint32_t* out, cudaStream_t st) {
-  const size_t smem = (size_t)(4 * W + 2) * 4;
+                          const int32_t* pidx, int B, uint32_t* out, uint32_t* gs, cudaStream_t st) {
+  const size_t smem = gs ? 0 : (size_t)(4 * W + 2) * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp_points, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_interp_points<<<B, GCD_THREADS, smem, st>>>(xs, vs, ns, W, primes, pidx, out);
+  k_interp_points<<<B, GCD_THREADS, smem, st>>>(xs, vs, ns, W, primes, pidx, out, gs);
 }
 
 }  // namespace ckb

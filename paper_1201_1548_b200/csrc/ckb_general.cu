@@ -40,6 +40,7 @@ __device__ uint32_t warp_resultant(uint32_t* a, int la, uint32_t* b, int lb, uin
     int lr = la;
     while (lr >= lb) {
       const uint32_t c = mul_mod(r[lr - 1], inv, P);
+      __syncwarp();  // every lane has read r[lr - 1] before its owner updates it
       if (c) {
         const int k = lr - lb;
         const uint32_t nc = p - c;
@@ -130,12 +131,13 @@ void launch_images_general(const ImageArgs& a, cudaStream_t st) {
 __global__ void k_uni_resultant(const uint32_t* __restrict__ fa, const int32_t* __restrict__ da,
                                 const uint32_t* __restrict__ gb, const int32_t* __restrict__ db, int W,
                                 const Prime* __restrict__ primes, const int32_t* __restrict__ pidx,
-                                uint32_t* __restrict__ out) {
+                                uint32_t* __restrict__ out, uint32_t* __restrict__ gs) {
   extern __shared__ uint32_t sm[];
   const int b = blockIdx.x, lane = threadIdx.x;
-  uint32_t* x = sm;
-  uint32_t* y = sm + W;
-  uint32_t* r = sm + 2 * W;
+  // operands in shared memory, or (degrees beyond it) in a global scratch slice per pair
+  uint32_t* x = gs ? gs + (size_t)b * 3 * W : sm;
+  uint32_t* y = x + W;
+  uint32_t* r = x + 2 * W;
   const int la = da[b] + 1, lb = db[b] + 1;
   for (int i = lane; i < W; i += 32) {
     x[i] = i < la ? fa[(size_t)b * W + i] : 0u;
@@ -147,10 +149,11 @@ __global__ void k_uni_resultant(const uint32_t* __restrict__ fa, const int32_t* 
 }
 
 void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t* gb, const int32_t* db, int W,
-                          const Prime* primes, const int32_t* pidx, int B, uint32_t* out, cudaStream_t st) {
-  const size_t smem = (size_t)3 * W * 4;
+                          const Prime* primes, const int32_t* pidx, int B, uint32_t* out, uint32_t* gs,
+                          cudaStream_t st) {
+  const size_t smem = gs ? 0 : (size_t)3 * W * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_uni_resultant, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_uni_resultant<<<B, 32, smem, st>>>(fa, da, gb, db, W, primes, pidx, out);
+  k_uni_resultant<<<B, 32, smem, st>>>(fa, da, gb, db, W, primes, pidx, out, gs);
 }
 
 }  // namespace ckb

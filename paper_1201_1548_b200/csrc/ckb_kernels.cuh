@@ -123,7 +123,8 @@ void launch_images_fallback(const ImageArgs& a, cudaStream_t st);
 // batch of independent univariate resultants (modpoly.py:156-161)
 // fa/gb: [B][W] padded low-first coefficients; degrees da/db; per-pair prime index
 void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t* gb, const int32_t* db, int W,
-                          const Prime* primes, const int32_t* pidx, int B, uint32_t* out, cudaStream_t st);
+                          const Prime* primes, const int32_t* pidx, int B, uint32_t* out, uint32_t* gs,
+                          cudaStream_t st);  // gs: null = operands in shared memory, else 3 W words per pair
 
 // ---- K4: interpolation at the planned points (modpoly.py:164-185) -----------
 // values at the planned points -> coeffs [K][Nfull] (canonical residues); with
@@ -165,15 +166,20 @@ inline size_t crt_a_words(int K, int N) { return (size_t)((N + 127) / 128) * ((K
 // ---- Descartes sign-variation test (ckb_descartes.cu) -----------------------
 struct DescPlan {
   int K, n, L, logL;       // primes, degree, NTT length >= 2n+1
+  int direct;              // degree beyond the NTT primes (2n+1 > 2^14): direct O(n^2) correlations
   uint32_t *fact, *ifact;  // [K][n+1] i! and 1/i! mod p
-  uint32_t *W, *Wc, *Wi, *Wic;  // [K][L/2] twiddles and companions
-  uint32_t *Vf, *Vfc;      // [K][L] DIF of (1/0!, ..., 1/n!, 0, ...) and companions
+  uint32_t *W, *Wc, *Wi, *Wic;  // [K][L/2] twiddles and companions (NTT mode)
+  uint32_t *Vf, *Vfc;      // [K][L] DIF of (1/0!, ..., 1/n!, 0, ...) and companions (NTT mode);
+                           // direct mode: Vf = [K][n+1] scan scratch of the plan kernel
   uint32_t* Linv;          // [K] 1/L
 };
+constexpr int DESC_NTT_LOG2_MAX = 14;  // PRIMES30: p = 1 mod 2^14
 void launch_desc_plan(const Prime* primes, const uint32_t* gens, const DescPlan& pl, cudaStream_t st);
-// B intervals at once: aw [B][2][AL], ld [B] (device) -> out [K][B N]; signs: B results
+// B intervals at once: aw [B][2][AL], ld [B] (device) -> out [K][B N]; signs: B results.
+// Direct mode needs scratch of desc_direct_scratch_words(K, n, B) words.
 void launch_desc_shift(const Prime* primes, const DescPlan& pl, const uint32_t* res, const uint32_t* aw, int AL,
-                       const int32_t* ld, int B, uint32_t* out, cudaStream_t st);
+                       const int32_t* ld, int B, uint32_t* out, uint32_t* scratch, cudaStream_t st);
+inline size_t desc_direct_scratch_words(int K, int n, int B) { return (size_t)K * B * 3 * (n + 1); }
 void launch_desc_signs(const uint32_t* limbs, int N, int LW, int B, int32_t* result, cudaStream_t st);
 
 // tensor-core CRT product (ckb_crt_mma.cu): byte table size / builder, and the
@@ -193,9 +199,10 @@ void launch_crt_tables(const uint32_t* primes, int K, const uint32_t* M, int LW,
 // ---- K6: batched gcd mod p (modpoly.py:115-122), interpolation at arbitrary points
 void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_t* gb, const int32_t* db, int Wg,
                     const Prime* primes, const int32_t* pidx, int B, uint32_t* out, int Wo, int32_t* odeg,
-                    cudaStream_t st);
+                    uint32_t* gs, cudaStream_t st);  // gs: null or 2 max(Wf, Wg) words per pair
 void launch_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const Prime* primes,
-                          const int32_t* pidx, int B, uint32_t* out, cudaStream_t st);
+                          const int32_t* pidx, int B, uint32_t* out, uint32_t* gs,
+                          cudaStream_t st);  // gs: null or 4 W + 2 words per problem
 
 // ---- images of the dense modular bivariate gcd (bivpoly.py:266-295)
 // res [K][C] residues of A's grid, B's grid, Gamma; out [K*NP][Wo] Gamma(x_t) * monic

@@ -37,12 +37,12 @@ class ShardPlan:
         return self.primes[a:a + self.per_rank], self.gens[a:a + self.per_rank]
 
 
-def plan_sharded(fc, gc, tdf: int, tdg: int, world: int, table=PRIMES30) -> ShardPlan:
+def plan_sharded(fc, gc, tdf: int, tdg: int, world: int, table=PRIMES30, start: int = 0) -> ShardPlan:
     m, n = len(fc) - 1, len(gc) - 1
     dfx = max(0, max(len(c) - 1 for c in fc))
     dgx = max(0, max(len(c) - 1 for c in gc))
     N = point_count(fc, gc, dfx, dgx, tdf, tdg)
-    primes, gens = choose_primes_log2(log2_coeff_bound(fc, gc), fc[-1], gc[-1], 0, table)
+    primes, gens = choose_primes_log2(log2_coeff_bound(fc, gc), fc[-1], gc[-1], start, table)
     mod = 1
     for p in primes:
         mod *= p
@@ -94,6 +94,8 @@ class CudaBackend:
         hp = np.array(primes, dtype=np.uint32)
         hg = np.array(gens, dtype=np.uint32)
         out = self.buffer("images_out", (K, N))
+        # the status word accumulates (atomicOr) over the launch: clear it per step
+        self.d_status.zero_()
         self._lib.check(self.lib.ckb_dev_modular_images(
             self.d_limbs.data_ptr(), pk.C, pk.L, self.d_degs.data_ptr(), self._lib.ptr(self.h_degs), pk.m, pk.n,
             pk.dfx, pk.dgx, self._lib.ptr(hp), self._lib.ptr(hg), K, N, out.data_ptr(), self.d_status.data_ptr(),
@@ -194,19 +196,37 @@ def biv_resultant_distributed(f, g, var: str = "y", group=None, exchange: str = 
     if m == 0 or n == 0:
         return (_pow(fc[0], n) if m == 0 else _pow(gc[0], m)) if rank == 0 else None
     device = torch.device("cuda", torch.cuda.current_device())
-    plan = plan_sharded(fc, gc, f.total_degree(), g.total_degree(), world)
     backend = CudaBackend(fc, gc, device)
     s = torch.cuda.current_stream(device)
-    with torch.cuda.stream(s):
-        if exchange == "a2a":
-            blk = sharded_resultant_step_a2a(backend, plan, rank, world, group, s.cuda_stream)
-            out = gather_limbs(blk, plan, rank, world, group)
-        else:
-            out = sharded_resultant_step(backend, plan, rank, world, group, s.cuda_stream)
-    if rank != 0:
-        return None
-    host = out.cpu().numpy().view(np.uint32).reshape(-1)
-    return _trim(limbs_to_ints(host, plan.N, plan.LW))
+    start = 0
+    for _attempt in range(4):
+        plan = plan_sharded(fc, gc, f.total_degree(), g.total_degree(), world, start=start)
+        with torch.cuda.stream(s):
+            if exchange == "a2a":
+                blk = sharded_resultant_step_a2a(backend, plan, rank, world, group, s.cuda_stream)
+                out = gather_limbs(blk, plan, rank, world, group)
+            else:
+                out = sharded_resultant_step(backend, plan, rank, world, group, s.cuda_stream)
+        # a prime without an admissible point scale (bit 1) or a vanishing leading
+        # coefficient at a point (bit 2) on ANY rank invalidates the CRT: agree on
+        # the worst status and re-plan with the next primes, as the single-GPU path does
+        if status_any(backend.d_status, group):
+            start += len(plan.primes)
+            continue
+        if rank != 0:
+            return None
+        host = out.cpu().numpy().view(np.uint32).reshape(-1)
+        return _trim(limbs_to_ints(host, plan.N, plan.LW))
+    raise ArithmeticError("no admissible evaluation points after re-planning")
+
+
+def status_any(d_status, group=None) -> bool:
+    """Max of every rank's status word (one all-reduce; a local read at world 1)."""
+    import torch.distributed as dist
+    st = d_status.clone()
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(st, op=dist.ReduceOp.MAX, group=group)
+    return bool(int(st.item()))
 
 
 def gather_limbs(blk, plan: ShardPlan, rank: int, world: int, group=None):

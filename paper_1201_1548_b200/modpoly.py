@@ -174,8 +174,6 @@ def zp_resultant_batch(triples) -> list:
     A = [_trim([x % p for x in a]) for a, _, p in triples]
     Bb = [_trim([x % p for x in b]) for _, b, p in triples]
     W = max(1, max(max(len(a), len(b)) for a, b in zip(A, Bb)))
-    if W > 4096:
-        raise NotImplementedError("univariate resultant kernel supports degree < 4096")
     fa = np.zeros((B, W), dtype=np.uint32)
     gb = np.zeros((B, W), dtype=np.uint32)
     for i, (a, b) in enumerate(zip(A, Bb)):
@@ -213,8 +211,6 @@ def zp_interpolate_batch(problems) -> list:
             raise ValueError("duplicate interpolation points")
     B = len(problems)
     W = max(1, max(len(pts) for pts, _, _ in problems))
-    if W > 12288:
-        raise NotImplementedError("at most 12288 points per interpolation problem")
     xs = np.zeros((B, W), dtype=np.uint32)
     vs = np.zeros((B, W), dtype=np.uint32)
     ns = np.zeros(B, dtype=np.int32)
@@ -235,8 +231,6 @@ def zp_interpolate_arrays(xs: np.ndarray, vals: np.ndarray, primes) -> np.ndarra
     [k][r][n] -> coefficients [k][r][n] (low first, canonical residues)."""
     lib = _lib.lib()
     k, r, n = vals.shape
-    if n > 12288:
-        raise NotImplementedError("at most 12288 points per interpolation problem")
     B = k * r
     xsb = np.ascontiguousarray(np.repeat(xs.astype(np.uint32), r, axis=0))
     vsb = np.ascontiguousarray(vals.reshape(B, n).astype(np.uint32))

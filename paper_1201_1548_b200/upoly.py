@@ -162,7 +162,7 @@ class _DescHandles:
         from .planner import ints_to_limbs
         from .primes30 import PRIMES30
         import numpy as np
-        snap = (len(p), p[0], p[-1], p[len(p) // 2])
+        snap = tuple(p[:n + 1])  # the full coefficients: an in-place edit of the list re-prepares
         for e in self.entries:
             if e[0] is p and e[1] == snap and e[3] >= K:
                 return e[2], e[3]
@@ -234,8 +234,6 @@ def variations_on(p, a, b) -> int:
         n -= 1
     if n < 1:
         return 0  # compose_linear of a constant has one coefficient: no variation
-    if n > 8191:
-        raise NotImplementedError("Descartes test supports degree < 8192")
     # |c|_inf <= 2^n |r|_1 <= 2^n sum_i |p_i| 2^(ld (n-i)) (|a| + |w|)^i   (bit-length bounds)
     t = (abs(a_num) + abs(w)).bit_length()
     top = max(abs(p[i]).bit_length() + ld * (n - i) + i * t for i in range(n + 1) if p[i])
@@ -302,8 +300,6 @@ def variations_batch(p, intervals, pbits=None) -> list:
         n -= 1
     if n < 1:
         return [0] * len(intervals)
-    if n > 8191:
-        raise NotImplementedError("Descartes test supports degree < 8192")
     pb = pbits if pbits is not None else _coeff_bits(p, n)  # (descartes_isolate passes it once per polynomial)
     params = []
     for a, b in intervals:

@@ -113,6 +113,20 @@ def test_cfg4_specialisation(mp, oracle_mod):
     _specialisation_check(mp, oracle_mod, f, g, res, random.Random(4))
 
 
+def test_cfg4_full_golden(mp):
+    """Every coefficient of the headline configuration, bit for bit, against the
+    pinned oracle's full cfg4 resultant (tests/golden/make_oracle_golden.py;
+    the fixture itself is tied to the reference by test_oracle.py's
+    test_cfg4_full_golden_matches_reference_prime)."""
+    from paper_1201_1548_b200.synth import make_pair
+    gold = load_golden("cfg4_full.json.gz")
+    f, g = make_pair("cfg4", 0)
+    got = mp.biv_resultant(f, g, "y")
+    assert len(got) - 1 == gold["degree"] == 1600
+    assert hashlib.sha256(repr(got).encode()).hexdigest() == gold["sha256_repr"]
+    assert got == [int(c, 16) for c in gold["res"]]
+
+
 def test_cfg5_specialisation(mp, oracle_mod):
     """cfg5 (d = 64, 256-bit): ~1,150 primes x 4,097 points, NTT length 2^14."""
     from paper_1201_1548_b200.synth import make_pair

@@ -80,3 +80,17 @@ def test_oracle_cfg2_full():
     got = oracle.biv_resultant(f, g, "y")
     assert got == [int(c, 16) for c in gold["res"]]
     assert hashlib.sha256(repr(got).encode()).hexdigest()[:16] == gold["sha16_repr"] == "e19abb8388d2a501"
+
+
+def test_cfg4_full_golden_matches_reference_prime():
+    """The oracle's full cfg4 resultant (tests/golden/cfg4_full.json.gz) reduced
+    modulo the reference loop's own prime equals the polynomial the UNMODIFIED
+    reference interpolated at that prime (cfg4_prime0.json.gz), and its bit
+    length stays inside the reference's coefficient bound (modpoly.py:397-414)."""
+    gold = load_golden("cfg4_full.json.gz")
+    one = load_golden("cfg4_prime0.json.gz")
+    res = [int(c, 16) for c in gold["res"]]
+    assert hashlib.sha256(repr(res).encode()).hexdigest() == gold["sha256_repr"]
+    p = one["p"]
+    assert [c % p for c in res] == one["poly"] + [0] * (len(res) - len(one["poly"]))
+    assert max(abs(c).bit_length() for c in res) == gold["max_bits"] <= 5765
