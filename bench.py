@@ -232,6 +232,77 @@ def run_reference(args):
 # our arm
 # ---------------------------------------------------------------------------
 
+def run_devices(args, devices):
+    """--gpus N outside torchrun: ONE process drives N devices through the C-ABI
+    (ckb_init_devices + ckb_biv_resultant_multi: primes sharded over the
+    device contexts, NCCL residue exchange over NVLink, coefficient-sharded
+    CRT), i.e. the drop-in modpoly.biv_resultant with CKB_GPUS=N.  A step is one
+    complete call with host buffers (page-locked), so value and e2e coincide
+    here: value is the device time (CUDA events per context, max over
+    contexts, copies included), e2e the wall time of the call."""
+    import ctypes
+    from paper_1201_1548_b200 import _lib, modpoly
+    from paper_1201_1548_b200.planner import limbs_to_ints, plan_resultant
+
+    lib = _lib.load()
+    arr = (ctypes.c_int * len(devices))(*devices)
+    _lib.check(lib.ckb_init_devices(len(devices), ctypes.cast(arr, ctypes.c_void_p)), "ckb_init_devices")
+    _lib._ready = True
+    G = len(devices)
+    F, G_, cfg = workload(args.config)
+    fc, gc = F.coeffs_wrt_y(), G_.coeffs_wrt_y()
+    from paper_1201_1548_b200.planner import pack_grid
+    pk = pack_grid(fc, gc)
+    p1 = plan_resultant(fc, gc, F.total_degree(), G_.total_degree(), pk.dfx, pk.dgx)
+    K, N, LW = len(p1.primes), p1.N, p1.LW
+    hlimbs = _lib.pinned.get("bench_in", pk.limbs.size)
+    hlimbs[:] = pk.limbs.reshape(-1)
+    hout = _lib.pinned.get("bench_out", N * LW)
+    status = np.zeros(1, dtype=np.uint32)
+    ms = np.zeros(1, dtype=np.float32)
+    args_c = (_lib.ptr(hlimbs), pk.C, pk.L, _lib.ptr(pk.degs), pk.m, pk.n, pk.dfx, pk.dgx, _lib.ptr(p1.primes),
+              _lib.ptr(p1.gens), K, N, LW, G, _lib.ptr(hout), _lib.ptr(status), _lib.ptr(ms))
+    t_cold = time.perf_counter()
+    _lib.check(lib.ckb_biv_resultant_multi(*args_c), "ckb_biv_resultant_multi")
+    t_cold = time.perf_counter() - t_cold
+    got = modpoly._trim(limbs_to_ints(hout, N, LW))
+    for _ in range(args.warmup):
+        _lib.check(lib.ckb_biv_resultant_multi(*args_c), "ckb_biv_resultant_multi")
+    n0 = lib.ckb_launch_count()
+    dev_ms, wall = [], []
+    with Clocks(devices[0]) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            _lib.check(lib.ckb_biv_resultant_multi(*args_c), "ckb_biv_resultant_multi")
+            wall.append(time.perf_counter() - t0)
+            dev_ms.append(float(ms[0]))
+    launches = int(lib.ckb_launch_count() - n0)
+    again = modpoly._trim(limbs_to_ints(hout, N, LW))
+    assert again == got, "replayed multi-device call differs from its first result"
+    # the one-context result of the same library (bit-exact equality across device counts)
+    one = np.zeros(N * LW, dtype=np.uint32)
+    _lib.check(lib.ckb_biv_resultant(*args_c[:13], _lib.ptr(one), _lib.ptr(status), None), "ckb_biv_resultant")
+    assert modpoly._trim(limbs_to_ints(one, N, LW)) == got, "multi-device result differs from one device"
+    ms_step = sum(dev_ms) / len(dev_ms)
+    e_ms = 1e3 * statistics.median(wall)
+    line = {"metric": METRIC, "value": 1e3 / ms_step, "unit": UNIT, "n_gpus": G, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32 (mod p < 2^30), exact integers", "data": "synthetic",
+            "config": dict(cfg, primes=K, points_per_prime=N, out_words=LW, devices=list(devices),
+                           parallelism=f"one process, {G} device contexts: primes/{G}, "
+                                       f"{'NCCL' if _lib.uses_nccl() else 'peer-copy'} exchange, CRT coefficients/{G}",
+                           l2="inputs from page-locked host memory every step (H2D + D2H inside the timed call)"),
+            "value_note": "device time per call incl. its H2D/D2H (CUDA events per context, max over contexts)",
+            "cold_first_call_ms": t_cold * 1e3, "clocks": clk.summary(), "gpu_launches": launches,
+            "e2e": {"value": 1e3 / e_ms, "unit": UNIT, "ms_per_step": e_ms,
+                    "h2d_bytes_per_step": int(pk.limbs.nbytes + pk.degs.nbytes) * G,
+                    "d2h_bytes_per_step": int(N * LW * 4 + 4 * G),
+                    "path": "ckb_biv_resultant_multi (C-ABI, one process, page-locked host buffers)"},
+            "cpu_baseline": None}
+    emit(line)
+    return 0
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -530,11 +601,23 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="run the multi-GPU (all-to-all) step even at N=1")
     ap.add_argument("--no-step-graph", action="store_true", help="N > 1: enqueue the step's parts from Python")
+    ap.add_argument("--devices", default="", help="one process over these device ids (may repeat: contexts "
+                    "sharing a GPU, a correctness configuration); default with --gpus N outside torchrun: 0..N-1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.devices or (args.gpus > 1 and "WORLD_SIZE" not in os.environ):
+        # one process driving several devices (the drop-in's multi-GPU mode)
+        devices = [int(x) for x in args.devices.split(",")] if args.devices else list(range(args.gpus))
+        import torch
+        have = torch.cuda.device_count()
+        if max(devices) >= have:
+            print(f"bench.py: --gpus {args.gpus} needs devices {devices} but only {have} CUDA device(s) "
+                  "are visible", file=sys.stderr)
+            return 2
+        return run_devices(args, devices)
     return run_ours(args)
 
 

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CKB_ABI_VERSION 4
+#define CKB_ABI_VERSION 5
 #define CKB_STATUS_REPLAN 1 /* a prime had no admissible evaluation points: re-plan without it */
 
 int ckb_abi_version(void);
@@ -48,6 +48,25 @@ unsigned long long ckb_launch_count(void);
 int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
                       const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, uint32_t* out,
                       uint32_t* status, float* device_ms);
+
+/* Several devices in one process: contexts 0..n-1 on
+ * devices[0..n-1] (each with its own stream, buffers and cached tables); with
+ * distinct devices the residue exchange uses NCCL (ncclCommInitAll, loaded at
+ * run time) over NVLink, else peer copies.  A device may repeat (contexts that
+ * share one GPU: a correctness configuration).  ckb_init(device) is the n = 1
+ * case.  ckb_devices reports the context count and whether NCCL is in use. */
+int ckb_init_devices(int n, const int* devices);
+int ckb_devices(int* n_contexts, int* nccl);
+
+/* ckb_biv_resultant over the first G contexts (primes sharded, SURVEY §8e
+ * option B): context d runs the modular stages for its contiguous block of
+ * K/G primes; one exchange gives every context all K residues of its block of
+ * ceil(N/G) coefficients; each lifts its block by CRT and writes its rows of
+ * `out`.  Same arguments, result and status as ckb_biv_resultant; device_ms is
+ * the maximum over the contexts. */
+int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
+                            const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, int G, uint32_t* out,
+                            uint32_t* status, float* device_ms);
 
 /* A batch of 1-4 independent res_y problems in one call (SURVEY.md §8(f) #1:
  * bisolve.biproject's res_y and res_x, bisolve.py:107-108): every argument of

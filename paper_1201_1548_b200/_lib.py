@@ -24,6 +24,7 @@ EXPORTS = (
     "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values", "ckb_host_alloc", "ckb_host_free",
     "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release", "ckb_biv_gcd_images",
     "ckb_biv_resultant_batch", "ckb_descartes_variations_batch", "ckb_set_graphs",
+    "ckb_init_devices", "ckb_devices", "ckb_biv_resultant_multi",
 )
 
 _P = ctypes.c_void_p
@@ -61,6 +62,9 @@ _SIGS = {
     "ckb_biv_resultant_batch": (_I, [_I] + [_P] * 15),
     "ckb_descartes_variations_batch": (_I, [_I, _P, _I, _P, _I, _I, _I, _P]),
     "ckb_biv_gcd_images": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P]),
+    "ckb_init_devices": (_I, [_I, _P]),
+    "ckb_devices": (_I, [_P, _P]),
+    "ckb_biv_resultant_multi": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
 }
 
 _lock = threading.Lock()
@@ -99,18 +103,55 @@ def _device_index() -> int:
     return 0
 
 
+def _device_list():
+    """CKB_DEVICES="0,1,2,3" (explicit list; a device may repeat) or CKB_GPUS=N
+    (devices 0..N-1): the drop-in then shards every res_y over those GPUs."""
+    v = os.environ.get("CKB_DEVICES")
+    if v:
+        return [int(x) for x in v.split(",") if x.strip() != ""]
+    n = int(os.environ.get("CKB_GPUS", "1") or 1)
+    return list(range(n)) if n > 1 else None
+
+
 def lib():
-    """The initialised library (lazily binds a CUDA device)."""
+    """The initialised library (lazily binds the CUDA device(s))."""
     global _ready
     lb = load()
     if not _ready:
         with _lock:
             if not _ready:
-                rc = lb.ckb_init(_device_index())
+                devs = _device_list()
+                if devs:
+                    arr = (ctypes.c_int * len(devs))(*devs)
+                    rc = lb.ckb_init_devices(len(devs), ctypes.cast(arr, _P))
+                else:
+                    rc = lb.ckb_init(_device_index())
                 if rc != 0:
                     raise CkbError("ckb_init failed: " + lb.ckb_last_error().decode())
                 _ready = True
     return lb
+
+
+def use_devices(devices) -> int:
+    """Shard res_y over these devices from now on (one context per entry; the
+    first must be the device already in use, if any).  Returns the count."""
+    lb = lib()
+    arr = (ctypes.c_int * len(devices))(*devices)
+    check(lb.ckb_init_devices(len(devices), ctypes.cast(arr, _P)), "ckb_init_devices")
+    return len(devices)
+
+
+def n_devices() -> int:
+    """Device contexts the drop-in shards over (1 = single GPU)."""
+    n, nc = ctypes.c_int(0), ctypes.c_int(0)
+    lib().ckb_devices(ctypes.byref(n), ctypes.byref(nc))
+    return max(1, n.value)
+
+
+def uses_nccl() -> bool:
+    n, nc = ctypes.c_int(0), ctypes.c_int(0)
+    lib().ckb_devices(ctypes.byref(n), ctypes.byref(nc))
+    return bool(nc.value)
 
 
 def check(rc: int, what: str) -> int:

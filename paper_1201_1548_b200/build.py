@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = True, out: str = OUT, defines=())
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, force, obj, extra), SOURCES))
     if force or not os.path.exists(out) or os.path.getmtime(out) < _newest(objs):
-        cmd = [NVCC, *ARCH, "-shared", "-Xlinker", "--no-undefined", "-o", out, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-Xlinker", "--no-undefined", "-o", out, *objs, "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -18,6 +18,8 @@
 
 #include "../../include/curvekit_b200.h"
 #include "ckb_kernels.cuh"
+#include <dlfcn.h>
+#include <nccl.h>
 
 using namespace ckb;
 
@@ -73,7 +75,14 @@ struct Ctx {
   cudaEvent_t bev[4] = {};
 };
 
-Ctx g;
+// One context per device (index = position in the device list of
+// ckb_init_devices; ckb_init(device) sets up context 0 only).  Every entry point
+// works on context 0 unless the multi-device call has switched g_ci.
+constexpr int kMaxCtx = 8;
+Ctx g_ctxs[kMaxCtx];
+int g_ci = 0;     // current context
+int g_nctx = 0;   // contexts initialised by ckb_init_devices (1 after ckb_init)
+#define g (g_ctxs[g_ci])
 std::mutex g_mu;
 // dynamic shared memory a per-problem kernel may ask for; beyond it the
 // operands live in a global scratch slice per problem (L2-resident in practice)
@@ -121,7 +130,8 @@ int host_buf(const char* name, size_t bytes, void** out) {
     b.p = nullptr;
     b.n = 0;
     size_t want = bytes + bytes / 4 + 256;
-    CK(cudaMallocHost(&b.p, want));
+    // portable: every device's copy engine may read / write it (multi-device calls)
+    CK(cudaHostAlloc(&b.p, want, cudaHostAllocPortable));
     b.n = want;
   }
   *out = b.p;
@@ -303,7 +313,8 @@ struct PrimeEntry {
   std::vector<uint32_t> primes;
   Prime* d = nullptr;
 };
-std::vector<PrimeEntry> g_pcache;
+std::vector<PrimeEntry> g_pcache_[kMaxCtx];
+#define g_pcache (g_pcache_[g_ci])
 
 int get_primes_dev(const uint32_t* primes, int K, Prime** out) {
   for (auto& e : g_pcache)
@@ -344,7 +355,8 @@ struct PlanEntry {
   void* ab = nullptr;  // tensor-core interpolation matrix (polyphase plans), or nullptr
   uint64_t last_use = 0;
 };
-std::vector<PlanEntry> g_plans;
+std::vector<PlanEntry> g_plans_[kMaxCtx];
+#define g_plans (g_plans_[g_ci])
 
 // Nfull points per prime, polyphase factor S (1 or 8): the interpolation plan
 // has M = ceil(Nfull / S) points with ratio g^S
@@ -463,7 +475,8 @@ struct GraphEntry {
   int seen = 0;           // < 0: not capturable
   uint64_t last_use = 0;
 };
-std::vector<GraphEntry> g_graphs;
+std::vector<GraphEntry> g_graphs_[kMaxCtx];
+#define g_graphs (g_graphs_[g_ci])
 
 void drop_graphs() {
   for (auto& e : g_graphs)
@@ -613,23 +626,19 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   return 0;
 }
 
-}  // namespace
-
-extern "C" {
-
-int ckb_abi_version(void) { return CKB_ABI_VERSION; }
-
-const char* ckb_last_error(void) { return g_err.c_str(); }
-
-int ckb_init(int device) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (g.ready) {
-    if (device == g.device) return 0;
-    return fail("ckb_init: already initialised on another device", -3);
+// ---- per-device contexts -----------------------------------------------------
+struct CtxSwitch {  // restores context 0 when a multi-device call returns
+  ~CtxSwitch() {
+    g_ci = 0;
+    if (g_ctxs[0].ready) cudaSetDevice(g_ctxs[0].device);
   }
+};
+
+int init_ctx(int idx, int device) {
+  g_ci = idx;
   int n = 0;
   CK(cudaGetDeviceCount(&n));
-  if (device < 0 || device >= n) return fail("ckb_init: no such CUDA device", -3);
+  if (device < 0 || device >= n) return fail("ckb_init: no such CUDA device " + std::to_string(device), -3);
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&g.ev0));
@@ -646,16 +655,17 @@ int ckb_init(int device) {
   return 0;
 }
 
-int ckb_shutdown(void) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (!g.ready) return 0;
+void shutdown_ctx() {
+  if (!g.ready) return;
   cudaSetDevice(g.device);
   cudaStreamSynchronize(g.stream);
   drop_graphs();
   ++g.epoch;
-  for (auto& d : g_desc)
-    if (d.blob) cudaFree(d.blob);
-  g_desc.clear();
+  if (g_ci == 0) {
+    for (auto& d : g_desc)
+      if (d.blob) cudaFree(d.blob);
+    g_desc.clear();
+  }
   for (auto& kv : g.dev) cudaFree(kv.second.p);
   for (auto& kv : g.host) cudaFreeHost(kv.second.p);
   for (auto& e : g.crt) {
@@ -682,10 +692,162 @@ int ckb_shutdown(void) {
   }
   cudaStreamDestroy(g.stream);
   g = Ctx();
+}
+
+// ---- the residue exchange between device contexts --------------
+// Distinct devices: NCCL point-to-point over NVLink (ncclCommInitAll: one
+// communicator per device in this process), loaded with dlopen so the library
+// itself has no NCCL dependency on single-GPU hosts.  Contexts sharing a device
+// (a correctness configuration for one-GPU machines) or a host without NCCL:
+// peer copies ordered by events.
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+struct Exchange {
+  bool nccl = false;
+  NcclApi api;
+  ncclComm_t comms[kMaxCtx] = {};
+  int n = 0;
+  cudaEvent_t ready[kMaxCtx] = {};  // phase 1 done on context d (peer-copy exchange)
+};
+Exchange g_x;
+
+bool load_nccl(NcclApi& a) {
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* nm : names)
+    if ((a.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!a.h) return false;
+  a.CommInitAll = (decltype(a.CommInitAll))dlsym(a.h, "ncclCommInitAll");
+  a.CommDestroy = (decltype(a.CommDestroy))dlsym(a.h, "ncclCommDestroy");
+  a.GroupStart = (decltype(a.GroupStart))dlsym(a.h, "ncclGroupStart");
+  a.GroupEnd = (decltype(a.GroupEnd))dlsym(a.h, "ncclGroupEnd");
+  a.Send = (decltype(a.Send))dlsym(a.h, "ncclSend");
+  a.Recv = (decltype(a.Recv))dlsym(a.h, "ncclRecv");
+  a.GetErrorString = (decltype(a.GetErrorString))dlsym(a.h, "ncclGetErrorString");
+  return a.CommInitAll && a.CommDestroy && a.GroupStart && a.GroupEnd && a.Send && a.Recv && a.GetErrorString;
+}
+
+#define NC(call)                                                                                 \
+  do {                                                                                           \
+    ncclResult_t r_ = (call);                                                                    \
+    if (r_ != ncclSuccess) return fail(std::string(#call) + ": " + g_x.api.GetErrorString(r_)); \
+  } while (0)
+
+int setup_exchange(int n, const int* devices) {
+  if (g_x.n == n) return 0;
+  g_x.n = n;
+  for (int i = 0; i < n; ++i) {
+    g_ci = i;
+    CK(cudaSetDevice(g.device));
+    if (!g_x.ready[i]) CK(cudaEventCreateWithFlags(&g_x.ready[i], cudaEventDisableTiming));
+  }
+  bool distinct = n > 1;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j)
+      if (devices[i] == devices[j]) distinct = false;
+  if (!distinct) return 0;
+  for (int i = 0; i < n; ++i) {  // NVLink peer access both ways (the peer-copy exchange)
+    CK(cudaSetDevice(devices[i]));
+    for (int j = 0; j < n; ++j) {
+      int can = 0;
+      if (i != j && cudaDeviceCanAccessPeer(&can, devices[i], devices[j]) == cudaSuccess && can) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+        cudaGetLastError();
+      }
+    }
+  }
+  const char* off = getenv("CKB_NO_NCCL");
+  if (!(off && off[0] == '1') && load_nccl(g_x.api)) {
+    NC(g_x.api.CommInitAll(g_x.comms, n, devices));
+    g_x.nccl = true;
+  }
   return 0;
 }
 
-unsigned long long ckb_launch_count(void) { return g.launches; }
+void teardown_exchange() {
+  if (g_x.nccl)
+    for (int i = 0; i < g_x.n; ++i)
+      if (g_x.comms[i]) g_x.api.CommDestroy(g_x.comms[i]);
+  for (int i = 0; i < kMaxCtx; ++i)
+    if (g_x.ready[i]) {
+      if (g_ctxs[i].ready) cudaSetDevice(g_ctxs[i].device);
+      cudaEventDestroy(g_x.ready[i]);
+    }
+  NcclApi api = g_x.api;
+  g_x = Exchange();
+  g_x.api = api;  // the dlopen handle stays (NCCL does not support unloading cleanly)
+}
+
+}  // namespace
+
+extern "C" {
+
+int ckb_abi_version(void) { return CKB_ABI_VERSION; }
+
+const char* ckb_last_error(void) { return g_err.c_str(); }
+
+int ckb_init(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_ci = 0;
+  if (g.ready) {
+    if (device == g.device) return 0;
+    return fail("ckb_init: already initialised on another device", -3);
+  }
+  int rc = init_ctx(0, device);
+  if (rc == 0 && g_nctx < 1) g_nctx = 1;
+  return rc;
+}
+
+int ckb_init_devices(int n, const int* devices) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  CtxSwitch cs;
+  if (n < 1 || n > kMaxCtx) return fail("ckb_init_devices: 1 to 8 devices", -2);
+  if (g_nctx > 1 && n != g_nctx) return fail("ckb_init_devices: already initialised with another device list", -3);
+  int rc;
+  for (int i = 0; i < n; ++i) {
+    g_ci = i;
+    if (g.ready) {
+      if (g.device != devices[i]) return fail("ckb_init_devices: context " + std::to_string(i) + " is on another device", -3);
+      continue;
+    }
+    if ((rc = init_ctx(i, devices[i]))) return rc;
+  }
+  g_nctx = n;
+  return setup_exchange(n, devices);
+}
+
+int ckb_devices(int* n_contexts, int* nccl) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (n_contexts) *n_contexts = g_nctx;
+  if (nccl) *nccl = g_x.nccl ? 1 : 0;
+  return 0;
+}
+
+int ckb_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  teardown_exchange();
+  for (int i = kMaxCtx - 1; i >= 0; --i) {
+    g_ci = i;
+    shutdown_ctx();
+  }
+  g_ci = 0;
+  g_nctx = 0;
+  return 0;
+}
+
+unsigned long long ckb_launch_count(void) {
+  unsigned long long t = 0;
+  for (int i = 0; i < kMaxCtx; ++i) t += g_ctxs[i].launches;
+  return t;
+}
 
 }  // extern "C"
 
@@ -847,6 +1009,176 @@ int ckb_biv_resultant_batch(int P, const uint32_t* const* limbs, const int* C, c
     status[i] = res_finish(pd[i]);
     any |= status[i];
   }
+  return any ? CKB_STATUS_REPLAN : 0;
+}
+
+int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
+                            const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, int G, uint32_t* out,
+                            uint32_t* status, float* device_ms) {
+  // res_y over G device contexts (option B):
+  //   phase 1, context d: its contiguous block of primes [k0_d, k0_d + K_d) through
+  //            reduce -> point scales -> images -> interpolation, giving the
+  //            residues [K_d][N]; column block s (coefficients [a_s, a_s + w_s))
+  //            packed contiguously for context s;
+  //   exchange: every context receives ALL K residues of its coefficient block
+  //            (NCCL send/recv over NVLink, or peer copies);
+  //   phase 3, context s: CRT of its w_s coefficients with all K primes, limbs
+  //            straight into the caller's rows [a_s, a_s + w_s).
+  std::lock_guard<std::mutex> lk(g_mu);
+  CtxSwitch cs;
+  int rc;
+  g_ci = 0;
+  if ((rc = ensure_ready())) return rc;
+  if (G < 1 || G > g_nctx) return fail("ckb_biv_resultant_multi: G must be 1 .. ckb_init_devices' count", -2);
+  if (m < 1 || n < 1 || K < G || N < G || L < 1 || LW < 1) return fail("ckb_biv_resultant_multi: bad sizes", -2);
+  if (C != (m + 1) * (dfx + 1) + (n + 1) * (dgx + 1)) return fail("ckb_biv_resultant_multi: C mismatch", -2);
+  if ((rc = check_primes(primes, K))) return rc;
+  int k0[kMaxCtx + 1], a0[kMaxCtx + 1];
+  for (int d = 0; d <= G; ++d) {
+    k0[d] = (int)((int64_t)K * d / G);  // balanced contiguous prime blocks
+    const int nc = (N + G - 1) / G;
+    a0[d] = std::min(N, d * nc);        // coefficient blocks of ceil(N / G)
+  }
+  // host staging in context 0's portable pinned memory (every device DMAs from it)
+  const size_t nl = (size_t)C * L, nd = (size_t)(m + n + 2);
+  void *h_in, *h_out;
+  if ((rc = host_buf("m.in", 4 * nl + 2 * nd + 64, &h_in))) return rc;
+  if ((rc = host_buf("m.out", 4 * (size_t)N * LW + 4 * kMaxCtx + 64, &h_out))) return rc;
+  const bool in_direct = is_pinned(limbs), out_direct = is_pinned(out);
+  uint8_t* hb = (uint8_t*)h_in;
+  if (!in_direct) memcpy(hb, limbs, 4 * nl);
+  memcpy(hb + 4 * nl, degs, 2 * nd);
+  const void* src_limbs = in_direct ? (const void*)limbs : (const void*)hb;
+  uint8_t* ho = (uint8_t*)h_out;
+  uint32_t* dst_out = out_direct ? out : (uint32_t*)ho;
+  uint32_t* h_status = (uint32_t*)(ho + 4 * (size_t)N * LW);
+  struct Dev {
+    uint32_t *limbs, *coeffs, *send, *recv, *out, *status, *crtS;
+    int16_t* degs;
+    Prime* primes;
+    CrtEntry* ce;
+  } dv[kMaxCtx];
+  // per-context buffers and cached tables (plans, CRT tables) first: building
+  // them synchronises the context's stream
+  for (int d = 0; d < G; ++d) {
+    g_ci = d;
+    if ((rc = ensure_ready())) return rc;
+    const int kd = k0[d + 1] - k0[d], wd = a0[d + 1] - a0[d];
+    Dev& v = dv[d];
+    if ((rc = dbuf("m.limbs", nl, &v.limbs))) return rc;
+    if ((rc = dbuf("m.degs", nd, &v.degs))) return rc;
+    if ((rc = dbuf("m.coeffs", (size_t)kd * N, &v.coeffs))) return rc;
+    if ((rc = dbuf("m.send", (size_t)kd * N, &v.send))) return rc;
+    if ((rc = dbuf("m.recv", (size_t)K * wd, &v.recv))) return rc;
+    if ((rc = dbuf("m.out", (size_t)wd * LW, &v.out))) return rc;
+    if ((rc = dbuf("m.status", 4, &v.status))) return rc;
+    if ((rc = dbuf("m.crtS", crt_scratch_words(K, wd, LW), &v.crtS))) return rc;
+    if ((rc = get_primes_dev(primes + k0[d], kd, &v.primes))) return rc;
+    if ((rc = get_crt(primes, K, LW, &v.ce))) return rc;
+    InterpPlan pl;
+    if ((rc = get_plan(primes + k0[d], gens + k0[d], kd, N, 8, &pl))) return rc;
+  }
+  // phase 1 (each context's launches replayed as one CUDA graph after the first calls)
+  for (int d = 0; d < G; ++d) {
+    g_ci = d;
+    CK(cudaSetDevice(g.device));
+    cudaStream_t st = g.stream;
+    const int kd = k0[d + 1] - k0[d];
+    Dev& v = dv[d];
+    CK(cudaEventRecord(g.ev0, st));
+    std::vector<uint64_t> key = {5, (uint64_t)G, (uint64_t)C, (uint64_t)L, (uint64_t)m, (uint64_t)n, (uint64_t)dfx,
+                                 (uint64_t)dgx, (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)src_limbs,
+                                 (uint64_t)hb};
+    key_push(key, degs, 2 * nd);
+    key_push(key, primes + k0[d], 4 * (size_t)kd);
+    key_push(key, gens + k0[d], 4 * (size_t)kd);
+    rc = graphed(key, st, [&]() -> int {
+      int r;
+      CK(cudaMemcpyAsync(v.limbs, src_limbs, 4 * nl, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(v.degs, hb + 4 * nl, 2 * nd, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(v.status, 0, 4, st));
+      g.nsev = 0;
+      if ((r = modular_stage(v.limbs, C, L, v.degs, degs, m, n, dfx, dgx, v.primes, primes + k0[d], gens + k0[d], kd,
+                             N, v.coeffs, v.status, st)))
+        return r;
+      for (int s2 = 0; s2 < G; ++s2) {  // column block s2 -> contiguous [K_d][w_s2] at K_d a_s2
+        const int ws = a0[s2 + 1] - a0[s2];
+        if (ws > 0)
+          CK(cudaMemcpy2DAsync(v.send + (size_t)kd * a0[s2], 4 * (size_t)ws, v.coeffs + a0[s2], 4 * (size_t)N,
+                               4 * (size_t)ws, kd, cudaMemcpyDeviceToDevice, st));
+      }
+      return 0;
+    });
+    if (rc) return rc;
+    if (!g_x.nccl) CK(cudaEventRecord(g_x.ready[d], st));
+  }
+  // the exchange
+  if (g_x.nccl) {
+    NC(g_x.api.GroupStart());
+    for (int d = 0; d < G; ++d) {
+      const int kd = k0[d + 1] - k0[d], wd = a0[d + 1] - a0[d];
+      for (int s2 = 0; s2 < G; ++s2) {
+        const int ks = k0[s2 + 1] - k0[s2], ws = a0[s2 + 1] - a0[s2];
+        if (ws > 0)
+          NC(g_x.api.Send(dv[d].send + (size_t)kd * a0[s2], (size_t)kd * ws, ncclUint32, s2, g_x.comms[d],
+                          g_ctxs[d].stream));
+        if (wd > 0)
+          NC(g_x.api.Recv(dv[d].recv + (size_t)k0[s2] * wd, (size_t)ks * wd, ncclUint32, s2, g_x.comms[d],
+                          g_ctxs[d].stream));
+      }
+    }
+    NC(g_x.api.GroupEnd());
+  } else {
+    for (int s2 = 0; s2 < G; ++s2) {
+      g_ci = s2;
+      CK(cudaSetDevice(g.device));
+      const int ws = a0[s2 + 1] - a0[s2];
+      for (int d = 0; d < G; ++d) {
+        const int kd = k0[d + 1] - k0[d];
+        CK(cudaStreamWaitEvent(g.stream, g_x.ready[d], 0));
+        if (ws > 0)
+          CK(cudaMemcpyPeerAsync(dv[s2].recv + (size_t)k0[d] * ws, g.device, dv[d].send + (size_t)kd * a0[s2],
+                                 g_ctxs[d].device, 4 * (size_t)kd * ws, g.stream));
+      }
+    }
+  }
+  // phase 3: CRT of each context's coefficient block, limbs to the caller's rows
+  for (int s2 = 0; s2 < G; ++s2) {
+    g_ci = s2;
+    CK(cudaSetDevice(g.device));
+    cudaStream_t st = g.stream;
+    const int ws = a0[s2 + 1] - a0[s2];
+    Dev& v = dv[s2];
+    std::vector<uint64_t> key = {6, (uint64_t)G, (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)dst_out,
+                                 (uint64_t)h_status};
+    key_push(key, primes, 4 * (size_t)K);
+    rc = graphed(key, st, [&]() -> int {
+      if (ws > 0) {
+        launch_crt(v.ce->t, v.recv, ws, v.out, v.crtS, st);
+        g.launches += 3;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(dst_out + (size_t)a0[s2] * LW, v.out, 4 * (size_t)ws * LW, cudaMemcpyDeviceToHost, st));
+      }
+      CK(cudaMemcpyAsync(h_status + s2, v.status, 4, cudaMemcpyDeviceToHost, st));
+      return 0;
+    });
+    if (rc) return rc;
+    CK(cudaEventRecord(g.ev1, st));
+  }
+  float worst = 0.f;
+  uint32_t any = 0;
+  for (int d = 0; d < G; ++d) {
+    g_ci = d;
+    CK(cudaSetDevice(g.device));
+    if ((rc = spin_event(g.ev1))) return rc;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+    worst = std::max(worst, ms);
+    any |= h_status[d];
+  }
+  if (!out_direct) memcpy(out, ho, 4 * (size_t)N * LW);
+  if (status) *status = any;
+  if (device_ms) *device_ms = worst;
   return any ? CKB_STATUS_REPLAN : 0;
 }
 

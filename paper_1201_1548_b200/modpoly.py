@@ -554,10 +554,17 @@ def _biv_resultant_gpu(fc, gc, tdf: int, tdg: int, packed=None):
         out = _lib.pinned.get("biv_out", N * LW)  # page-locked: the result lands here directly
         status = np.zeros(1, dtype=np.uint32)
         ms = np.zeros(1, dtype=np.float32)
-        rc = _lib.check(lib.ckb_biv_resultant(
-            _lib.ptr(packed.limbs), packed.C, packed.L, _lib.ptr(packed.degs), m, n, packed.dfx, packed.dgx,
-            _lib.ptr(plan.primes), _lib.ptr(plan.gens), K, N, LW, _lib.ptr(out), _lib.ptr(status),
-            _lib.ptr(ms)), "ckb_biv_resultant")
+        G = min(_lib.n_devices(), K, N)
+        if G > 1:  # primes sharded over the device contexts, one residue exchange
+            rc = _lib.check(lib.ckb_biv_resultant_multi(
+                _lib.ptr(packed.limbs), packed.C, packed.L, _lib.ptr(packed.degs), m, n, packed.dfx, packed.dgx,
+                _lib.ptr(plan.primes), _lib.ptr(plan.gens), K, N, LW, G, _lib.ptr(out), _lib.ptr(status),
+                _lib.ptr(ms)), "ckb_biv_resultant_multi")
+        else:
+            rc = _lib.check(lib.ckb_biv_resultant(
+                _lib.ptr(packed.limbs), packed.C, packed.L, _lib.ptr(packed.degs), m, n, packed.dfx, packed.dgx,
+                _lib.ptr(plan.primes), _lib.ptr(plan.gens), K, N, LW, _lib.ptr(out), _lib.ptr(status),
+                _lib.ptr(ms)), "ckb_biv_resultant")
         if rc == 0:
             vals = _trim(limbs_to_ints(out, N, LW))
             return vals, {"K": K, "N": N, "LW": LW, "device_ms": float(ms[0]),
