@@ -69,8 +69,19 @@ struct ImgLayout {
 
 // NT = threads (images) per CTA; ALIGNED: grid (ceil(N/NT), K), a CTA never
 // straddles primes (one staged table: the register-heavy buckets fit more CTAs)
-template <int MAXD, int NT = IMG_THREADS, bool ALIGNED = false>
-__global__ void __launch_bounds__(NT, ALIGNED ? 1 : img_minb(MAXD)) k_images(ImageArgs a) {
+// EX: 0 any degrees; 1 da = db = MAXD; 2 da = MAXD, db = MAXD - 1 (the dense
+// res(f, g) and res(f, f_y) shapes: the elimination chain is unrolled exactly)
+// The unrolled chain lets ptxas keep more values live (cfg4: 178 registers
+// uncapped, 8 warps/SM): capped at 128 (16 warps/SM) for MAXD <= 40 and 170
+// for 48 it measured fastest (cfg4 images 270 -> 241 us; uncapped 337 us)
+#ifndef CKB_IMG_MINB_EX
+#define CKB_IMG_MINB_EX 0
+#endif
+constexpr int exact_minb(int maxd) {
+  return CKB_IMG_MINB_EX ? CKB_IMG_MINB_EX : maxd <= 24 ? 4 : maxd <= 32 ? 3 : maxd <= 40 ? 4 : maxd <= 48 ? 3 : img_minb(maxd);
+}
+template <int MAXD, int NT = IMG_THREADS, bool ALIGNED = false, int EX = 0>
+__global__ void __launch_bounds__(NT, ALIGNED ? 1 : (EX ? exact_minb(MAXD) : img_minb(MAXD))) k_images(ImageArgs a) {
   using LY = ImgLayout<MAXD>;
   constexpr int NCH = LY::NCH, SW = LY::SW;
   extern __shared__ __align__(16) uint32_t sm[];
@@ -274,7 +285,12 @@ __global__ void __launch_bounds__(NT, ALIGNED ? 1 : img_minb(MAXD)) k_images(Ima
     v = 0u;
   } else {
     const bool neg = sw && ((a.m * a.n) & 1);
-    v = resultant_generic<MAXD>(A, da, B, db, neg, P);
+    if constexpr (EX == 1)
+      v = resultant_generic<MAXD, MAXD>(A, da, B, db, neg, P);
+    else if constexpr (EX == 2)
+      v = resultant_generic<MAXD, MAXD - 1>(A, da, B, db, neg, P);
+    else
+      v = resultant_generic<MAXD>(A, da, B, db, neg, P);
     if (v == CKB_FAIL) {
       const uint32_t slot = atomicAdd(a.fail_count, 1u);
       a.fail_list[slot] = (uint32_t)((size_t)pi * a.N + idx);
@@ -449,8 +465,22 @@ static bool images_aligned(int maxd) {
   return on && maxd >= 56;
 }
 
+// the exactly unrolled elimination for the dense shapes (CKB_IMG_EXACT=0 disables)
+static int images_exact(int maxd, int m, int n) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CKB_IMG_EXACT");
+    on = e ? atoi(e) : 1;
+  }
+  if (!on) return 0;
+  const int da = m > n ? m : n, db = m > n ? n : m;
+  if (da != maxd) return 0;
+  return db == maxd ? 1 : db == maxd - 1 ? 2 : 0;
+}
+
 void launch_images(const ImageArgs& a, cudaStream_t st) {
   const int maxd = images_maxd(a.m, a.n);
+  const int ex = images_exact(maxd, a.m, a.n);
   if (images_aligned(maxd)) {
     constexpr int NTA = 64;
     ImageArgs b = a;
@@ -461,9 +491,9 @@ void launch_images(const ImageArgs& a, cudaStream_t st) {
 #define LAUNCH_AL(D)                                                                                     \
   if (maxd == D) {                                                                                       \
     const size_t smem = (size_t)((2 * rows * ImgLayout<D>::SW + 2 * POLY) + 2 * rows) * 4;              \
-    if (smem > 48 * 1024)                                                                                \
-      cudaFuncSetAttribute(k_images<D, NTA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    launch_pdl(k_images<D, NTA, true>, grid, dim3(NTA), smem, st, b);                                     \
+    auto kern = ex == 1 ? k_images<D, NTA, true, 1> : ex == 2 ? k_images<D, NTA, true, 2> : k_images<D, NTA, true, 0>; \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    launch_pdl(kern, grid, dim3(NTA), smem, st, b);                                                      \
   }
     LAUNCH_AL(56) LAUNCH_AL(64)
 #undef LAUNCH_AL
@@ -479,9 +509,10 @@ void launch_images(const ImageArgs& a, cudaStream_t st) {
 #define LAUNCH(D)                                                                                    \
   if (maxd == D) {                                                                                   \
     const size_t smem = (size_t)(b.span * (2 * rows * ImgLayout<D>::SW + 2 * POLY) + 2 * rows) * 4; \
-    if (smem > 48 * 1024)                                                                            \
-      cudaFuncSetAttribute(k_images<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    launch_pdl(k_images<D>, grid, dim3(IMG_THREADS), smem, st, b);                                   \
+    auto kern = ex == 1 ? k_images<D, IMG_THREADS, false, 1>                                         \
+                        : ex == 2 ? k_images<D, IMG_THREADS, false, 2> : k_images<D, IMG_THREADS, false, 0>; \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    launch_pdl(kern, grid, dim3(IMG_THREADS), smem, st, b);                                          \
   }
   CKB_MAXD_LIST(LAUNCH)
 #undef LAUNCH

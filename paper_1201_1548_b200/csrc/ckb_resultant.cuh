@@ -126,10 +126,33 @@ __device__ __forceinline__ uint32_t step2(uint32_t (&D)[MAXD + 1], const uint32_
   return lb;
 }
 
+// The fused remainders with the divisor degree K a COMPILE-TIME constant, the
+// whole chain unrolled (K, K-1, ..., 1, roles alternating): every chunk guard
+// and every `i < k` test folds, so a step issues exactly its k outputs (the
+// run-time loop issues whole chunks and predicates the tail off: ~3.5 wasted
+// outputs per step, 17% of the elimination at r = 80).
+template <int MAXD, int K, bool BA>  // BA: dividend B, divisor A
+__device__ __forceinline__ void chain_exact(uint32_t (&A)[MAXD + 1], uint32_t (&B)[MAXD + 1], uint32_t& T, uint32_t& Q,
+                                            uint32_t& num, bool& bad, const Prime& P) {
+  if constexpr (K >= 1) {
+    const uint32_t lm = BA ? step2<MAXD>(B, A, K, P) : step2<MAXD>(A, B, K, P);
+    T = mmul(T, lm, P);
+    Q = mmul(Q, T, P);
+    const uint32_t d0 = red4(BA ? B[0] : A[0], P.p);
+    bad |= (d0 == 0u);
+    if constexpr (K == 1) {
+      num = mmul(num, to_mont(d0, P), P);
+    } else {
+      chain_exact<MAXD, K - 1, !BA>(A, B, T, Q, num, bad, P);
+    }
+  }
+}
+
 // res(A, B) for top-aligned A (deg da) and B (deg db), da >= db >= 1 with
 // nonzero leading coefficients; `neg` carries the sign of an initial swap.
-// Returns CKB_FAIL on a non-generic remainder sequence.
-template <int MAXD>
+// Returns CKB_FAIL on a non-generic remainder sequence.  DB > 0: the caller
+// guarantees db == DB (the chain is unrolled for it).
+template <int MAXD, int DB = 0>
 __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], int da, uint32_t (&B)[MAXD + 1], int db,
                                                       bool neg, const Prime& P) {
   const uint32_t p = P.p;
@@ -154,6 +177,10 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
   int k = db - 1;
   if (k == 0) {
     num = mmul(num, to_mont(a0, P), P);  // lc(P_K)^(d_{K-1}), d_{K-1} = db = 1
+  } else if constexpr (DB > 1) {
+    chain_exact<MAXD, DB - 1, true>(A, B, T, Q, num, bad, P);
+    num = mmul(num, mmul(T, T, P), P);
+    den = mmul(den, mmul(Q, Q, P), P);
   } else {
     for (;;) {
       // dividend B (deg k+1), divisor A (deg k)

@@ -1,0 +1,13 @@
+# A/B of k_images variants: stage times from bench.py (cfg4, cfg3, cfg5)
+for cfg in cfg4 cfg3 cfg5; do
+  for v in default noexact exmb3 exmb4; do
+    case $v in
+      default) env="" ;;
+      noexact) env="CKB_IMG_EXACT=0" ;;
+      *) env="CKB_LIB=build/variants/lib$v.so" ;;
+    esac
+    steps=20; [ $cfg = cfg5 ] && steps=5
+    r=$(env $env timeout 600 python bench.py --config $cfg --steps $steps --no-cpu 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('%.4f'%d['ms_per_step'], 'images %.4f'%d['stages_ms']['images'], 'frac %.3f'%d['roofline']['frac'])")
+    echo "$cfg $v $r"
+  done
+done
