@@ -465,6 +465,19 @@ static bool images_aligned(int maxd) {
   return on && maxd >= 56;
 }
 
+// the kernel for a bucket: the exactly unrolled chains only up to MAXD 48 (at
+// 56 / 64 they exceed the register file and spill; the run-time exit sweep
+// measured faster there: cfg5 images 10.42 -> 9.97 ms)
+constexpr int EXACT_MAXD = 48;
+template <int D, int NT, bool AL>
+static void (*images_kernel(int ex))(ImageArgs) {
+  if constexpr (D > EXACT_MAXD) {
+    return k_images<D, NT, AL, 0>;
+  } else {
+    return ex == 1 ? k_images<D, NT, AL, 1> : ex == 2 ? k_images<D, NT, AL, 2> : k_images<D, NT, AL, 0>;
+  }
+}
+
 // the exactly unrolled elimination for the dense shapes (CKB_IMG_EXACT=0 disables)
 static int images_exact(int maxd, int m, int n) {
   static int on = -1;
@@ -474,7 +487,7 @@ static int images_exact(int maxd, int m, int n) {
   }
   if (!on) return 0;
   const int da = m > n ? m : n, db = m > n ? n : m;
-  if (da != maxd) return 0;
+  if (da != maxd || maxd > EXACT_MAXD) return 0;
   return db == maxd ? 1 : db == maxd - 1 ? 2 : 0;
 }
 
@@ -491,7 +504,7 @@ void launch_images(const ImageArgs& a, cudaStream_t st) {
 #define LAUNCH_AL(D)                                                                                     \
   if (maxd == D) {                                                                                       \
     const size_t smem = (size_t)((2 * rows * ImgLayout<D>::SW + 2 * POLY) + 2 * rows) * 4;              \
-    auto kern = ex == 1 ? k_images<D, NTA, true, 1> : ex == 2 ? k_images<D, NTA, true, 2> : k_images<D, NTA, true, 0>; \
+    auto kern = images_kernel<D, NTA, true>(ex);                                                         \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     launch_pdl(kern, grid, dim3(NTA), smem, st, b);                                                      \
   }
@@ -509,8 +522,7 @@ void launch_images(const ImageArgs& a, cudaStream_t st) {
 #define LAUNCH(D)                                                                                    \
   if (maxd == D) {                                                                                   \
     const size_t smem = (size_t)(b.span * (2 * rows * ImgLayout<D>::SW + 2 * POLY) + 2 * rows) * 4; \
-    auto kern = ex == 1 ? k_images<D, IMG_THREADS, false, 1>                                         \
-                        : ex == 2 ? k_images<D, IMG_THREADS, false, 2> : k_images<D, IMG_THREADS, false, 0>; \
+    auto kern = images_kernel<D, IMG_THREADS, false>(ex);                                            \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     launch_pdl(kern, grid, dim3(IMG_THREADS), smem, st, b);                                          \
   }

@@ -57,6 +57,55 @@ __device__ __forceinline__ uint32_t mont3(uint32_t x, uint32_t a, uint32_t y, ui
   return (uint32_t)(t >> 32) - __umulhi((uint32_t)t * pinv, p) + p;
 }
 
+// step2 with an exact trip count at run time: outputs i = 0 .. k-1 in
+// ascending order (each reads D[i+2] before it is overwritten), the loop
+// leaving through a uniform branch right after output k-1 and zeroing D[k]
+// (the one entry past the new degree the next step reads).  Code size is one
+// copy of the sweep per role (the compile-time chain unrolls every k: ~100 KB
+// of SASS, instruction-cache misses).
+#ifndef CKB_SWEEP_BLK
+#define CKB_SWEEP_BLK 1
+#endif
+// outputs I, I+1, ... while below k, in blocks of SB between the uniform exit
+// branches (SB = 1: exact; SB > 1: the block's tail is predicated)
+template <int MAXD, int I, int SB = CKB_SWEEP_BLK>
+__device__ __forceinline__ void sweep_exit(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int k, uint32_t w1m,
+                                           uint32_t w2m, uint32_t w3m, uint32_t pinv, uint32_t p) {
+  if constexpr (I < MAXD - 1) {
+    if (I >= k) {
+      D[I] = 0u;
+    } else if (SB == 1 || I + SB <= k) {
+#pragma unroll
+      for (int j = 0; j < SB; ++j)
+        if (I + j < MAXD - 1) D[I + j] = mont3(D[I + j + 2], w1m, V[I + j + 2], w2m, V[I + j + 1], w3m, pinv, p);
+      sweep_exit<MAXD, I + SB, SB>(D, V, k, w1m, w2m, w3m, pinv, p);
+    } else {  // k - I in [1, SB): the last outputs, then the zero
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (I + j < MAXD - 1) {
+          if (I + j < k) D[I + j] = mont3(D[I + j + 2], w1m, V[I + j + 2], w2m, V[I + j + 1], w3m, pinv, p);
+          else if (I + j == k) D[I + j] = 0u;
+        }
+      }
+    }
+  }
+}
+template <int MAXD>
+__device__ __forceinline__ uint32_t step2_exit(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int k,
+                                               const Prime& P) {
+  const uint32_t p = P.p;
+  const uint32_t lb = red4(V[0], p), la = red4(D[0], p);
+  const uint32_t nla = la ? p - la : 0u;
+  const uint32_t d1 = red4(D[1], p), v1 = red4(V[1], p);
+  const uint32_t w1m = redc((uint64_t)lb * lb, P);
+  const uint32_t w2m = redc((uint64_t)lb * nla, P);
+  const uint32_t l3 = redc((uint64_t)lb * d1 + (uint64_t)nla * v1, P);
+  const uint32_t w3m = l3 ? p - l3 : 0u;
+  const uint32_t pinv = P.pinv;
+  sweep_exit<MAXD, 0>(D, V, k, w1m, w2m, w3m, pinv, p);
+  return lb;
+}
+
 // single division-free step D <- lb D - lc(D) V (aligned tops); nom = nominal deg D
 template <int MAXD>
 __device__ __forceinline__ void step1(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int nom, uint32_t lb,
@@ -152,6 +201,9 @@ __device__ __forceinline__ void chain_exact(uint32_t (&A)[MAXD + 1], uint32_t (&
 // nonzero leading coefficients; `neg` carries the sign of an initial swap.
 // Returns CKB_FAIL on a non-generic remainder sequence.  DB > 0: the caller
 // guarantees db == DB (the chain is unrolled for it).
+#ifndef CKB_STEP_EXIT
+#define CKB_STEP_EXIT 1
+#endif
 template <int MAXD, int DB = 0>
 __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], int da, uint32_t (&B)[MAXD + 1], int db,
                                                       bool neg, const Prime& P) {
@@ -184,7 +236,7 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
   } else {
     for (;;) {
       // dividend B (deg k+1), divisor A (deg k)
-      uint32_t lm = step2<MAXD>(B, A, k, P);
+      uint32_t lm = CKB_STEP_EXIT ? step2_exit<MAXD>(B, A, k, P) : step2<MAXD>(B, A, k, P);
       T = mmul(T, lm, P);
       Q = mmul(Q, T, P);
       --k;
@@ -195,7 +247,7 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
         break;
       }
       // dividend A (deg k+1), divisor B (deg k)
-      lm = step2<MAXD>(A, B, k, P);
+      lm = CKB_STEP_EXIT ? step2_exit<MAXD>(A, B, k, P) : step2<MAXD>(A, B, k, P);
       T = mmul(T, lm, P);
       Q = mmul(Q, T, P);
       --k;

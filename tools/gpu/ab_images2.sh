@@ -1,0 +1,11 @@
+for cfg in cfg4 cfg3 cfg2 cfg5; do
+  for v in default noexact; do
+    case $v in
+      default) env="" ;;
+      noexact) env="CKB_IMG_EXACT=0" ;;
+    esac
+    steps=20; [ $cfg = cfg5 ] && steps=5
+    r=$(env $env timeout 600 python bench.py --config $cfg --steps $steps --no-cpu 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('%.4f'%d['ms_per_step'], 'images %.4f'%d['stages_ms']['images'], 'frac %.3f'%d['roofline']['frac'])")
+    echo "$cfg $v $r"
+  done
+done
