@@ -117,13 +117,28 @@ int ckb_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns,
                       const int32_t* pidx, int B, uint32_t* out);
 
 /* Principal subresultant coefficients psc_i(t) mod p, i = 1..n, at the points
- * t = 0..ncand-1 — the per-point determinants of modular_subres_profile
- * (_psc_det / _zp_det, modpoly.py:428-526).  fres [(m+1)][(dfx+1)], gres
- * [(n+1)][(dgx+1)]: residues of the y-coefficients (m >= n, as the reference
- * swaps), fdeg/gdeg their x-degrees.  out [n][ncand]; valid [ncand] = 1 where
- * neither leading coefficient vanishes at t (the reference skips the others). */
+ * t = 0..ncand-1 — the values _psc_det (modpoly.py:477-501) gives at each point
+ * of modular_subres_profile, read off one remainder sequence per point (one warp
+ * each).  fres [(m+1)][(dfx+1)], gres [(n+1)][(dgx+1)]:
+ * residues of the y-coefficients (m >= n, as the reference swaps), fdeg/gdeg
+ * their x-degrees.  out [n][ncand]; valid [ncand] = 1 where neither leading
+ * coefficient vanishes at t (the reference skips those t; their values are 0). */
 int ckb_psc_values(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
                    const int16_t* gdeg, int n, int dgx, uint32_t p, int ncand, uint32_t* out, uint8_t* valid);
+
+#define CKB_STATUS_UNLUCKY 2 /* UnluckyPrime(p) (modpoly.py:439, :451, :463) */
+
+/* The whole modular subresultant degree profile on the device — replaces the
+ * body of curvekit.modpoly.modular_subres_profile (modpoly.py:428-474) after its
+ * reduction and swap: the reference's points, every psc_i at every point
+ * (remainder sequences), every psc_i interpolated, and the gcd chain
+ * S_0 = rstar mod p, S_i = gcd(S_{i-1}, psc_i).  rmod [rlen]: rstar mod p
+ * (low first); rlen_int = rstar's length over Z (S_0 must keep it); dmax =
+ * max(deg_x f, deg_x g).  chain [n+1] = deg S_i.  Returns CKB_STATUS_UNLUCKY
+ * where the reference raises UnluckyPrime(p). */
+int ckb_subres_profile(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
+                       const int16_t* gdeg, int n, int dgx, const uint32_t* rmod, int rlen, int rlen_int, int dmax,
+                       uint32_t p, int32_t* chain);
 
 /* Images of the dense modular bivariate gcd — the modular core that replaces
  * the primitive PRS of curvekit.bivpoly.gcd_biv (pkg/src/curvekit/bivpoly.py:266-295;

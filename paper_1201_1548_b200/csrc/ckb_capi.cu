@@ -1406,8 +1406,8 @@ int ckb_psc_values(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, co
   int rc;
   if ((rc = ensure_ready())) return rc;
   if ((rc = check_primes(&p, 1))) return rc;
-  if (m < 0 || n < 0 || ncand < 1) return fail("ckb_psc_values: bad sizes", -2);
-  if ((size_t)(m + n + 2 + (m + n) * (m + n)) * 4 > 200 * 1024) return fail("ckb_psc_values: degree too large", -2);
+  if (m < 0 || n < 0 || m < n || ncand < 1) return fail("ckb_psc_values: bad sizes (need m >= n >= 0)", -2);
+  if (!psc_fits(m, n)) return fail("ckb_psc_values: degree too large", -2);
   cudaStream_t st = g.stream;
   const size_t nf = (size_t)(m + 1) * (dfx + 1), ng = (size_t)(n + 1) * (dgx + 1);
   uint32_t *d_f, *d_g, *d_out;
@@ -1424,13 +1424,91 @@ int ckb_psc_values(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, co
   CK(cudaMemcpyAsync(d_g, gres, 4 * ng, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_fd, fdeg, 2 * ((size_t)m + 1), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_gd, gdeg, 2 * ((size_t)n + 1), cudaMemcpyHostToDevice, st));
-  launch_psc(d_f, d_fd, m, dfx, d_g, d_gd, n, dgx, h_prime(p), ncand, d_out, d_valid, st);
+  launch_psc(d_f, d_fd, m, dfx, d_g, d_gd, n, dgx, h_prime(p), nullptr, ncand, d_out, d_valid, st);
   g.launches += 1;
   CK(cudaGetLastError());
   if (n > 0) CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)n * ncand, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(valid, d_valid, (size_t)ncand, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return 0;
+}
+
+int ckb_subres_profile(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
+                       const int16_t* gdeg, int n, int dgx, const uint32_t* rmod, int rlen, int rlen_int, int dmax,
+                       uint32_t p, int32_t* chain) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  if ((rc = check_primes(&p, 1))) return rc;
+  if (m < 1 || n < 1 || m < n || dmax < 0 || rlen < 1 || rlen_int < 1)
+    return fail("ckb_subres_profile: bad sizes (need m >= n >= 1, rstar nonzero)", -2);
+  if (!psc_fits(m, n)) return fail("ckb_subres_profile: degree too large", -2);
+  const int need = (m + n - 2) * dmax + 1;  // modpoly.py:447
+  const int W = need;
+  if (!gcd_chain_fits(rlen, W)) return fail("ckb_subres_profile: chain degrees too large", -2);
+  // candidates: need plus a margin for the skipped t (re-run with more if a
+  // leading coefficient vanishes unusually often); t never reaches p
+  const int64_t lim = (int64_t)p;
+  cudaStream_t st = g.stream;
+  const size_t nf = (size_t)(m + 1) * (dfx + 1), ng = (size_t)(n + 1) * (dgx + 1);
+  uint32_t *d_f, *d_g, *d_sel, *d_vals, *d_sr, *d_r, *d_status;
+  int16_t *d_fd, *d_gd;
+  int *d_count, *d_cnt, *d_chain;
+  int32_t *d_ns, *d_pi;
+  Prime* d_prime;
+  if ((rc = dbuf("sp.f", nf, &d_f))) return rc;
+  if ((rc = dbuf("sp.g", ng, &d_g))) return rc;
+  if ((rc = dbuf("sp.fd", (size_t)m + 1, &d_fd))) return rc;
+  if ((rc = dbuf("sp.gd", (size_t)n + 1, &d_gd))) return rc;
+  if ((rc = dbuf("sp.sel", (size_t)need, &d_sel))) return rc;
+  if ((rc = dbuf("sp.vals", (size_t)n * need, &d_vals))) return rc;
+  if ((rc = dbuf("sp.sr", (size_t)n * W, &d_sr))) return rc;
+  if ((rc = dbuf("sp.r", (size_t)rlen, &d_r))) return rc;
+  if ((rc = dbuf("sp.status", 4, &d_status))) return rc;
+  if ((rc = dbuf("sp.count", 1, &d_count))) return rc;
+  if ((rc = dbuf("sp.cnt", (size_t)n, &d_cnt))) return rc;
+  if ((rc = dbuf("sp.chain", (size_t)n + 1, &d_chain))) return rc;
+  if ((rc = dbuf("sp.ns", (size_t)n, &d_ns))) return rc;
+  if ((rc = dbuf("sp.pi", (size_t)n, &d_pi))) return rc;
+  if ((rc = upload_primes(&p, 1, &d_prime))) return rc;
+  std::vector<int32_t> cnt(n), zeros(n, 0);
+  for (int i = 1; i <= n; ++i) cnt[i - 1] = (m + n - 2 * i) * dmax + 1;  // modpoly.py:466
+  CK(cudaMemcpyAsync(d_f, fres, 4 * nf, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_g, gres, 4 * ng, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_fd, fdeg, 2 * ((size_t)m + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_gd, gdeg, 2 * ((size_t)n + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_r, rmod, 4 * (size_t)rlen, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_cnt, cnt.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_ns, cnt.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_pi, zeros.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_status, 0, 4, st));
+  const Prime P = h_prime(p);
+  const uint32_t* lcf = d_f + (size_t)m * (dfx + 1);
+  const uint32_t* lcg = d_g + (size_t)n * (dgx + 1);
+  int64_t ncand = need + 64;
+  for (;;) {
+    if (ncand > lim) ncand = lim;
+    launch_psc_points(lcf, fdeg[m], lcg, gdeg[n], P, (int)ncand, need, d_sel, d_count, st);
+    int count = 0;
+    CK(cudaMemcpyAsync(&count, d_count, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    g.launches += 1;
+    if (count >= need) break;
+    if (ncand >= lim) return CKB_STATUS_UNLUCKY;  // modpoly.py:450-451: t reached p
+    ncand *= 2;
+  }
+  launch_psc(d_f, d_fd, m, dfx, d_g, d_gd, n, dgx, P, d_sel, need, d_vals, nullptr, st);
+  uint32_t* d_gs = nullptr;  // every psc_i interpolated from its first cnt_i points, one launch
+  if ((size_t)(4 * W + 2) * 4 > kSmemLimit && (rc = dbuf("sp.gs", (size_t)n * (4 * W + 2), &d_gs))) return rc;
+  launch_interp_points(d_sel, d_vals, d_ns, W, d_prime, d_pi, n, d_sr, d_gs, st, 0);
+  launch_gcd_chain(d_r, rlen, rlen_int, d_sr, d_cnt, W, n, P, d_chain, d_status, st);
+  g.launches += 3;
+  CK(cudaGetLastError());
+  uint32_t status = 0;
+  CK(cudaMemcpyAsync(chain, d_chain, 4 * ((size_t)n + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&status, d_status, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return status ? CKB_STATUS_UNLUCKY : 0;
 }
 
 // ---- device-pointer entry points for the multi-GPU driver -------------------

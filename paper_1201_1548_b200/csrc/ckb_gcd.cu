@@ -97,11 +97,98 @@ void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_
 // ---------------------------------------------------------------------------
 // interpolation at arbitrary distinct points (one problem per CTA)
 // ---------------------------------------------------------------------------
+
+// inclusive multiplicative scan of buf[0..n) by one CTA; rev: suffix products
+__device__ void block_scan_mul(uint32_t* buf, int n, bool rev, const Prime& P) {
+  __shared__ uint32_t sh[GCD_THREADS];
+  const int T = blockDim.x, tid = threadIdx.x;
+  const int seg = (n + T - 1) / T;
+  const int s0 = min(n, tid * seg), s1 = min(n, s0 + seg);
+  auto at = [&](int i) -> uint32_t& { return buf[rev ? n - 1 - i : i]; };
+  uint32_t acc = 1u % P.p;
+  for (int i = s0; i < s1; ++i) {
+    acc = mul_mod(acc, at(i), P);
+    at(i) = acc;
+  }
+  sh[tid] = acc;
+  __syncthreads();
+  for (int off = 1; off < T; off <<= 1) {
+    const uint32_t v = (tid >= off) ? sh[tid - off] : 1u % P.p;
+    __syncthreads();
+    if (tid >= off) sh[tid] = mul_mod(sh[tid], v, P);
+    __syncthreads();
+  }
+  const uint32_t pre = tid ? sh[tid - 1] : 1u % P.p;
+  __syncthreads();
+  if (tid)
+    for (int i = s0; i < s1; ++i) at(i) = mul_mod(at(i), pre, P);
+  __syncthreads();
+}
+
+// Newton interpolation at x_i = x_0 + i: c (values, n >= 2) -> o (coefficients).
+// x is reused for the table 1/j; every row / Horner step is one pass over
+// contiguous per-thread segments with the left neighbour's old boundary value
+// passed through a two-slot array (one barrier per row).
+__device__ void interp_consecutive(uint32_t* x, uint32_t* c, uint32_t* o, uint32_t* o2, int n, const Prime& P) {
+  __shared__ uint32_t bnd[2][GCD_THREADS];
+  const int T = blockDim.x, tid = threadIdx.x;
+  const uint32_t p = P.p;
+  const uint32_t x0 = x[0];
+  __syncthreads();  // every thread has read x[0]
+  // 1/j = (j-1)! / j!:  o2[i] = i!, o[i] = 1/i! (suffix products from 1/(n-1)!)
+  for (int i = tid; i < n; i += T) o2[i] = i ? (uint32_t)i % p : 1u % p;
+  __syncthreads();
+  block_scan_mul(o2, n, false, P);
+  const uint32_t inv_last = inv_mod(o2[n - 1], P);
+  for (int i = tid; i < n; i += T) o[i] = (i == n - 1) ? inv_last : (uint32_t)(i + 1) % p;
+  __syncthreads();
+  block_scan_mul(o, n, true, P);  // o[i] = inv_last * (i+1) ... (n-1) = 1/i!
+  for (int j = tid; j < n; j += T) x[j] = j ? mul_mod(o[j], o2[j - 1], P) : 0u;  // 1/j
+  __syncthreads();
+  const int seg = (n + T - 1) / T;
+  const int s0 = min(n, tid * seg), s1 = min(n, s0 + seg);
+  // forward differences: row j, i >= j: c[i] = (c[i] - c[i-1]) / j
+  for (int j = 1; j < n; ++j) {
+    const int slot = j & 1;
+    if (s1 > s0) bnd[slot][tid] = c[s1 - 1];  // this thread's old last entry
+    __syncthreads();
+    const uint32_t prev = (tid > 0 && s0 > 0) ? bnd[slot][tid - 1] : 0u;
+    const uint32_t w = x[j], wc = shoup_comp(w, P);
+    for (int i = s1 - 1; i >= max(s0, j); --i) {
+      const uint32_t lo = i > s0 ? c[i - 1] : prev;
+      c[i] = shoup(sub_mod(c[i], lo, p), w, wc, p);
+    }
+  }
+  __syncthreads();
+  // Newton -> monomial: o = 0; for i = n-1 .. 0: o = o (x - x_i) + c_i  (x_i = x0 + i)
+  for (int k = tid; k <= n; k += T) o[k] = 0u;
+  __syncthreads();
+  const int seg2 = (n + 1 + T - 1) / T;
+  const int u0 = min(n + 1, tid * seg2), u1 = min(n + 1, u0 + seg2);
+  for (int i = n - 1; i >= 0; --i) {
+    const int slot = i & 1;
+    if (u1 > u0) bnd[slot][tid] = o[u1 - 1];
+    __syncthreads();
+    const uint32_t prev = (tid > 0 && u0 > 0) ? bnd[slot][tid - 1] : 0u;
+    const uint32_t xi = (uint32_t)(((uint64_t)x0 + (uint64_t)i) % p);
+    const uint32_t nxi = neg_mod(xi, p), nxic = shoup_comp(nxi, P);
+    const uint32_t ci = c[i];
+    for (int k = u1 - 1; k >= u0; --k) {
+      uint32_t v = shoup(o[k], nxi, nxic, p);  // -x_i o[k]
+      v = add_mod(v, k > u0 ? o[k - 1] : prev, p);
+      if (k == 0) v = add_mod(v, ci, p);
+      o[k] = v;
+    }
+  }
+  __syncthreads();
+  (void)o2;
+}
 __global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* __restrict__ xs,
                                                                const uint32_t* __restrict__ vs, const int32_t* __restrict__ ns,
                                                                int W, const Prime* __restrict__ primes,
                                                                const int32_t* __restrict__ pidx,
-                                                               uint32_t* __restrict__ out, uint32_t* __restrict__ gs) {
+                                                               uint32_t* __restrict__ out, uint32_t* __restrict__ gs,
+                                                               int xstride) {
   extern __shared__ uint32_t sm_[];
   const int b = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const int n = ns[b];
@@ -113,10 +200,21 @@ __global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* _
   uint32_t* o = sm + 2 * W;    // output (n + 1 words)
   uint32_t* o2 = sm + 3 * W + 1;
   for (int i = tid; i < n; i += T) {
-    x[i] = xs[(size_t)b * W + i];
+    x[i] = xs[(size_t)b * xstride + i];  // xstride 0: one point list shared by every problem
     c[i] = vs[(size_t)b * W + i];
   }
   __syncthreads();
+  // consecutive points x_i = x_0 + i (the reference's t = 0, 1, 2, ... when no t
+  // is skipped): the divided differences are forward differences and row j
+  // divides by j alone
+  int cons = 1;
+  for (int i = tid; i < n; i += T)
+    if (x[i] != (uint32_t)(((uint64_t)x[0] + (uint64_t)i) % p)) cons = 0;
+  if (__syncthreads_and(cons) && n >= 2) {
+    interp_consecutive(x, c, o, o2, n, P);
+    for (int k = tid; k < n; k += T) out[(size_t)b * W + k] = o[k];
+    return;
+  }
   // for j in 1..n-1: for i = n-1 .. j: c[i] = (c[i] - c[i-1]) / (x[i] - x[i-j]).
   // The reference takes one Fermat inverse per entry (modpoly.py:172-178); here
   // each thread inverts the denominators of its strided entries of a row at
@@ -163,10 +261,10 @@ __global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* _
 }
 
 void launch_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const Prime* primes,
-                          const int32_t* pidx, int B, uint32_t* out, uint32_t* gs, cudaStream_t st) {
+                          const int32_t* pidx, int B, uint32_t* out, uint32_t* gs, cudaStream_t st, int xstride) {
   const size_t smem = gs ? 0 : (size_t)(4 * W + 2) * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp_points, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_interp_points<<<B, GCD_THREADS, smem, st>>>(xs, vs, ns, W, primes, pidx, out, gs);
+  k_interp_points<<<B, GCD_THREADS, smem, st>>>(xs, vs, ns, W, primes, pidx, out, gs, xstride < 0 ? W : xstride);
 }
 
 }  // namespace ckb

@@ -201,8 +201,8 @@ void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_
                     const Prime* primes, const int32_t* pidx, int B, uint32_t* out, int Wo, int32_t* odeg,
                     uint32_t* gs, cudaStream_t st);  // gs: null or 2 max(Wf, Wg) words per pair
 void launch_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const Prime* primes,
-                          const int32_t* pidx, int B, uint32_t* out, uint32_t* gs,
-                          cudaStream_t st);  // gs: null or 4 W + 2 words per problem
+                          const int32_t* pidx, int B, uint32_t* out, uint32_t* gs, cudaStream_t st,
+                          int xstride = -1);  // gs: null or 4 W + 2 words per problem; xstride -1 = W
 
 // ---- images of the dense modular bivariate gcd (bivpoly.py:266-295)
 // res [K][C] residues of A's grid, B's grid, Gamma; out [K*NP][Wo] Gamma(x_t) * monic
@@ -210,10 +210,18 @@ void launch_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t*
 void launch_biv_gcd_images(const uint32_t* res, int C, const int16_t* degs, int m, int n, int dax, int dbx, int dgam,
                            const Prime* primes, int K, int NP, uint32_t* out, int Wo, int32_t* odeg, cudaStream_t st);
 
-// ---- principal subresultant coefficients at points t = 0..ncand-1 (modpoly.py:428-526)
-// out [n][ncand] psc_i(t) for i = 1..n; valid[t] = no leading coefficient vanishes at t
+// ---- the modular subresultant profile (ckb_psc.cu, modpoly.py:428-526) --------
+// points: the first `need` t with lc_f(t) lc_g(t) != 0 -> sel, *count = all such t < ncand
+void launch_psc_points(const uint32_t* lcf, int dlf, const uint32_t* lcg, int dlg, const Prime& P, int ncand,
+                       int need, uint32_t* sel, int* count, cudaStream_t st);
+// psc_i(t) for i = 1..n at pts[0..npts) (pts null: t = index) -> out [n][npts]; valid optional
 void launch_psc(const uint32_t* fres, const int16_t* fdeg, int m, int dfx, const uint32_t* gres,
-                const int16_t* gdeg, int n, int dgx, const Prime& P, int ncand, uint32_t* out, uint8_t* valid,
-                cudaStream_t st);
+                const int16_t* gdeg, int n, int dgx, const Prime& P, const uint32_t* pts, int npts, uint32_t* out,
+                uint8_t* valid, cudaStream_t st);
+bool psc_fits(int m, int n);
+// S_0 = rstar mod p, S_i = gcd(S_{i-1}, sr_i): chain [n+1] degrees; *status = 2: S_0 lost degree
+void launch_gcd_chain(const uint32_t* rmod, int rlen, int rlen_int, const uint32_t* sr, const int* cnt, int W, int n,
+                      const Prime& P, int* chain, uint32_t* status, cudaStream_t st);
+bool gcd_chain_fits(int rlen, int W);
 
 }  // namespace ckb

@@ -63,30 +63,17 @@ __device__ __forceinline__ uint32_t mont3(uint32_t x, uint32_t a, uint32_t y, ui
 // (the one entry past the new degree the next step reads).  Code size is one
 // copy of the sweep per role (the compile-time chain unrolls every k: ~100 KB
 // of SASS, instruction-cache misses).
-#ifndef CKB_SWEEP_BLK
-#define CKB_SWEEP_BLK 1
-#endif
-// outputs I, I+1, ... while below k, in blocks of SB between the uniform exit
-// branches (SB = 1: exact; SB > 1: the block's tail is predicated)
-template <int MAXD, int I, int SB = CKB_SWEEP_BLK>
+// outputs I, I+1, ... while below k, each followed by the uniform exit test;
+// the exit zeroes D[k] (also at k = MAXD - 1, past the last computable output)
+template <int MAXD, int I>
 __device__ __forceinline__ void sweep_exit(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int k, uint32_t w1m,
                                            uint32_t w2m, uint32_t w3m, uint32_t pinv, uint32_t p) {
-  if constexpr (I < MAXD - 1) {
+  if constexpr (I < MAXD) {
     if (I >= k) {
       D[I] = 0u;
-    } else if (SB == 1 || I + SB <= k) {
-#pragma unroll
-      for (int j = 0; j < SB; ++j)
-        if (I + j < MAXD - 1) D[I + j] = mont3(D[I + j + 2], w1m, V[I + j + 2], w2m, V[I + j + 1], w3m, pinv, p);
-      sweep_exit<MAXD, I + SB, SB>(D, V, k, w1m, w2m, w3m, pinv, p);
-    } else {  // k - I in [1, SB): the last outputs, then the zero
-#pragma unroll
-      for (int j = 0; j < SB; ++j) {
-        if (I + j < MAXD - 1) {
-          if (I + j < k) D[I + j] = mont3(D[I + j + 2], w1m, V[I + j + 2], w2m, V[I + j + 1], w3m, pinv, p);
-          else if (I + j == k) D[I + j] = 0u;
-        }
-      }
+    } else if constexpr (I < MAXD - 1) {
+      D[I] = mont3(D[I + 2], w1m, V[I + 2], w2m, V[I + 1], w3m, pinv, p);
+      sweep_exit<MAXD, I + 1>(D, V, k, w1m, w2m, w3m, pinv, p);
     }
   }
 }

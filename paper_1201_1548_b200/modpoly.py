@@ -648,10 +648,10 @@ def modular_subres_profile(f, g, rstar, p: int):
     ``rstar`` is the square-free part of res(f, g; y) over Z; the chain is
     S_0 = rstar mod p, S_i = gcd(S_{i-1}, psc_i mod p), with psc_i the i-th
     principal subresultant coefficient of f and g with respect to y.  On the
-    GPU: the residues (K1), every psc_i at every point (one warp per (point, i)
-    determinant, ckb_psc_values), the interpolation of every psc_i in one batch
-    (ckb_interp_points) and the gcd chain (ckb_gcd_mod_batch).  The points are
-    the reference's: t = 0, 1, 2, ... skipping zeros of the leading coefficients.
+    GPU: the residues (K1), then ONE library call (ckb_subres_profile) for the
+    reference's points, every psc_i at every point (one remainder sequence per
+    point instead of a determinant per (point, i)), the batched interpolation
+    of every psc_i and the gcd chain.
     """
     lib = _lib.lib()
     f, g = as_biv(f), as_biv(g)
@@ -677,49 +677,30 @@ def modular_subres_profile(f, g, rstar, p: int):
     if m < n:
         fc, gc, m, n = gc, fc, n, m
     dmax = max(f.deg_x(), g.deg_x(), 0)
-    need = (m + n - 2) * dmax + 1
-    # candidate points t = 0, 1, ...; the kernel flags where a leading coefficient vanishes
-    ncand = max(need, 1) + 32
-    while True:
-        if ncand > p:
-            ncand = p
-        dfx = max(0, max(len(c) - 1 for c in fc))
-        dgx = max(0, max(len(c) - 1 for c in gc))
-        fg = np.zeros((m + 1, dfx + 1), dtype=np.uint32)
-        gg = np.zeros((n + 1, dgx + 1), dtype=np.uint32)
-        for j, col in enumerate(fc):
-            fg[j, :len(col)] = col
-        for j, col in enumerate(gc):
-            gg[j, :len(col)] = col
-        fdeg = np.array([len(_trim(list(c))) - 1 for c in fc], dtype=np.int16)
-        gdeg = np.array([len(_trim(list(c))) - 1 for c in gc], dtype=np.int16)
-        out = np.zeros((max(n, 1), ncand), dtype=np.uint32)
-        valid = np.zeros(ncand, dtype=np.uint8)
-        _lib.check(lib.ckb_psc_values(_lib.ptr(fg), _lib.ptr(fdeg), m, dfx, _lib.ptr(gg), _lib.ptr(gdeg), n, dgx,
-                                      p, ncand, _lib.ptr(out), _lib.ptr(valid)), "ckb_psc_values")
-        sel = np.nonzero(valid)[0]
-        if need <= 0 or len(sel) >= need:
-            break
-        if ncand >= p:
-            raise UnluckyPrime(p)  # modpoly.py:450-451
-        ncand *= 2
-    points = sel[:max(need, 0)].tolist()
-    # S_0 = monic(rstar mod p): gcd(rstar, 0) on the GPU is the monic polynomial
-    s0 = zp_gcd_batch([(rmod, [], p)])[0] if _trim(list(rmod)) else []
-    if len(s0) - 1 != len(_trim(list(rstar))) - 1:
-        raise UnluckyPrime(p)  # modpoly.py:462-463
-    # interpolate every psc_i from its first cnt_i points (one batched launch)
-    probs = []
-    for i in range(1, n + 1):
-        cnt = (m + n - 2 * i) * dmax + 1
-        probs.append((points[:cnt], out[i - 1, sel[:cnt]].tolist(), p))
-    sris = zp_interpolate_batch(probs) if probs else []
-    chain = [len(s0) - 1]
-    d = []
-    cur = s0
-    for sri in sris:
-        if sri:
-            cur = zp_gcd_batch([(cur, sri, p)])[0]
-        chain.append(len(cur) - 1)
-        d.append(chain[-2] - chain[-1])
+    rlen_int = len(_trim(list(rstar)))
+    if n == 0:
+        # no psc to interpolate: the chain is S_0 alone (modpoly.py:462-474)
+        s0 = zp_gcd_batch([(rmod, [], p)])[0] if _trim(list(rmod)) else []
+        if len(s0) - 1 != rlen_int - 1:
+            raise UnluckyPrime(p)
+        return ModularSubresultantProfile(p, (len(s0) - 1,), ())
+    dfx = max(0, max(len(c) - 1 for c in fc))
+    dgx = max(0, max(len(c) - 1 for c in gc))
+    fg = np.zeros((m + 1, dfx + 1), dtype=np.uint32)
+    gg = np.zeros((n + 1, dgx + 1), dtype=np.uint32)
+    for j, col in enumerate(fc):
+        fg[j, :len(col)] = col
+    for j, col in enumerate(gc):
+        gg[j, :len(col)] = col
+    fdeg = np.array([len(_trim(list(c))) - 1 for c in fc], dtype=np.int16)
+    gdeg = np.array([len(_trim(list(c))) - 1 for c in gc], dtype=np.int16)
+    rm = np.array(rmod, dtype=np.uint32)
+    chain = np.zeros(n + 1, dtype=np.int32)
+    rc = _lib.check(lib.ckb_subres_profile(_lib.ptr(fg), _lib.ptr(fdeg), m, dfx, _lib.ptr(gg), _lib.ptr(gdeg), n,
+                                           dgx, _lib.ptr(rm), len(rmod), rlen_int, dmax, p, _lib.ptr(chain)),
+                    "ckb_subres_profile")
+    if rc == 2:
+        raise UnluckyPrime(p)  # modpoly.py:450-451, :462-463
+    chain = [int(v) for v in chain]
+    d = [chain[i - 1] - chain[i] for i in range(1, n + 1)]
     return ModularSubresultantProfile(p, tuple(chain), tuple(d))

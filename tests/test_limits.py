@@ -127,3 +127,16 @@ def test_isolate_degree_8192(curvekit_mod):
         iv = r.interval
         lo, hi = iv.lo.as_fraction(), iv.hi.as_fraction()
         assert lo <= Fraction(want) <= hi
+
+
+def test_interpolate_consecutive_points_vs_oracle(oracle_mod):
+    """Points x_0, x_0 + 1, ... take the forward-difference path of k_interp_points
+    (the reference's t = 0, 1, 2, ... of modular_subres_profile)."""
+    from paper_1201_1548_b200.modpoly import zp_interpolate_batch
+    rng = random.Random(21)
+    probs = []
+    for n, x0, p in ((2, 0, 7), (3, 5, 101), (700, 0, 1073692673), (1301, 123456, 2147483629), (257, 1000, 1009)):
+        probs.append((list(range(x0, x0 + n)), [rng.randrange(p) for _ in range(n)], p))
+    got = zp_interpolate_batch(probs)
+    for (pts, vals, p), c in zip(probs, got):
+        assert c == oracle_mod.zp_interp(pts, vals, p)

@@ -55,6 +55,17 @@ for world in (1, 2, 4, 8):
     be = CudaBackend(fc, gc, dev)
     primes, gens = plan.shard(0)
     t_img = timed(lambda: be.modular_images(primes, gens, plan.N, st.cuda_stream))
+    lib.ckb_set_timing(1)
+    acc = np.zeros(4)
+    for _ in range(args.reps):
+        with torch.cuda.stream(st):
+            flush.zero_()
+        be.modular_images(primes, gens, plan.N, st.cuda_stream)
+        sm = np.zeros(8, dtype=np.float32)
+        n = lib.ckb_stage_times(_lib.ptr(sm), 8)
+        acc += sm[:4] if n >= 4 else 0
+    lib.ckb_set_timing(0)
+    stages = " ".join(f"{k} {v * 1e3 / args.reps:.1f}" for k, v in zip(("reduce", "choose", "images", "interp"), acc))
     Nc = -(-plan.N // world)
     coeffs = torch.randint(0, 1 << 29, (len(plan.primes), Nc), dtype=torch.int32, device=dev)
     out = torch.empty((Nc, plan.LW), dtype=torch.int32, device=dev)
@@ -73,4 +84,4 @@ for world in (1, 2, 4, 8):
     t_crt_all = timed(crt_all)
     print(f"{args.config} world {world}: K {len(plan.primes)} ({plan.per_rank}/rank), images+interp {t_img * 1e3:.1f} us, "
           f"CRT of N/{world} coefficients {t_crt * 1e3:.1f} us (option B), CRT of all {t_crt_all * 1e3:.1f} us "
-          f"(option A, rank 0)", flush=True)
+          f"(option A, rank 0); stages (us): {stages}", flush=True)
