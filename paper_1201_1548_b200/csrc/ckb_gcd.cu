@@ -99,8 +99,13 @@ void launch_gcd_mod(const uint32_t* fa, const int32_t* da, int Wf, const uint32_
 // ---------------------------------------------------------------------------
 
 // inclusive multiplicative scan of buf[0..n) by one CTA; rev: suffix products
-__device__ void block_scan_mul(uint32_t* buf, int n, bool rev, const Prime& P) {
-  __shared__ uint32_t sh[GCD_THREADS];
+constexpr int INTERP_THREADS = 1024;
+// scratch shared by the device functions below (one static allocation per kernel)
+struct InterpShared {
+  uint32_t sh[INTERP_THREADS];      // scan partials
+  uint32_t bnd[2][INTERP_THREADS];  // row boundaries (two slots)
+};
+static __device__ void interp_scan_mul(uint32_t* buf, int n, bool rev, const Prime& P, uint32_t* sh) {
   const int T = blockDim.x, tid = threadIdx.x;
   const int seg = (n + T - 1) / T;
   const int s0 = min(n, tid * seg), s1 = min(n, s0 + seg);
@@ -125,12 +130,78 @@ __device__ void block_scan_mul(uint32_t* buf, int n, bool rev, const Prime& P) {
   __syncthreads();
 }
 
+// register-resident variant: thread t owns entries [t SEG, (t+1) SEG) of the
+// difference table and of the output in registers; per row only the boundary
+// value crosses threads (two-slot array, one barrier).  Needs n + 1 <= SEG T.
+template <int SEG>
+__device__ __forceinline__ void interp_consecutive_reg(uint32_t* x, uint32_t* c, uint32_t* o, uint32_t* o2, int n, const Prime& P,
+                                       uint32_t* __restrict__ out, InterpShared& S) {
+  auto& bnd = S.bnd;
+  const int T = blockDim.x, tid = threadIdx.x;
+  const uint32_t p = P.p;
+  const uint32_t x0 = x[0];
+  __syncthreads();
+  for (int i = tid; i < n; i += T) o2[i] = i ? (uint32_t)i % p : 1u % p;
+  __syncthreads();
+  interp_scan_mul(o2, n, false, P, S.sh);
+  const uint32_t inv_last = inv_mod(o2[n - 1], P);
+  for (int i = tid; i < n; i += T) o[i] = (i == n - 1) ? inv_last : (uint32_t)(i + 1) % p;
+  __syncthreads();
+  interp_scan_mul(o, n, true, P, S.sh);
+  for (int j = tid; j < n; j += T) x[j] = j ? mul_mod(o[j], o2[j - 1], P) : 0u;  // 1/j
+  __syncthreads();
+  for (int j = tid; j < n; j += T) o[j] = shoup_comp(x[j], P);  // and its Shoup companion
+  const int s0 = tid * SEG;
+  uint32_t v[SEG];
+#pragma unroll
+  for (int e = 0; e < SEG; ++e) v[e] = s0 + e < n ? c[s0 + e] : 0u;
+  __syncthreads();
+  for (int j = 1; j < n; ++j) {
+    const int slot = j & 1;
+    const uint32_t w = x[j], wc = o[j];  // independent of this row's barrier
+    bnd[slot][tid] = v[SEG - 1];
+    __syncthreads();
+    const uint32_t prev = tid ? bnd[slot][tid - 1] : 0u;
+#pragma unroll
+    for (int e = SEG - 1; e >= 0; --e) {
+      const uint32_t lo = e ? v[e - 1] : prev;
+      if (s0 + e >= j) v[e] = shoup(sub_mod(v[e], lo, p), w, wc, p);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < SEG; ++e)
+    if (s0 + e < n) c[s0 + e] = v[e];
+  __syncthreads();
+  // Newton -> monomial over entries 0..n (o = 0 initially)
+#pragma unroll
+  for (int e = 0; e < SEG; ++e) v[e] = 0u;
+  for (int i = n - 1; i >= 0; --i) {
+    const int slot = i & 1;
+    const uint32_t xi = (uint32_t)(((uint64_t)x0 + (uint64_t)i) % p);
+    const uint32_t nxi = neg_mod(xi, p), nxic = shoup_comp(nxi, P);
+    const uint32_t ci = c[i];
+    bnd[slot][tid] = v[SEG - 1];
+    __syncthreads();
+    const uint32_t prev = tid ? bnd[slot][tid - 1] : 0u;
+#pragma unroll
+    for (int e = SEG - 1; e >= 0; --e) {
+      uint32_t t = add_mod(shoup(v[e], nxi, nxic, p), e ? v[e - 1] : prev, p);
+      if (s0 + e == 0) t = add_mod(t, ci, p);
+      v[e] = t;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < SEG; ++e)
+    if (s0 + e < n) out[s0 + e] = v[e];
+}
+
 // Newton interpolation at x_i = x_0 + i: c (values, n >= 2) -> o (coefficients).
 // x is reused for the table 1/j; every row / Horner step is one pass over
 // contiguous per-thread segments with the left neighbour's old boundary value
 // passed through a two-slot array (one barrier per row).
-__device__ void interp_consecutive(uint32_t* x, uint32_t* c, uint32_t* o, uint32_t* o2, int n, const Prime& P) {
-  __shared__ uint32_t bnd[2][GCD_THREADS];
+__device__ __forceinline__ void interp_consecutive(uint32_t* x, uint32_t* c, uint32_t* o, uint32_t* o2, int n, const Prime& P,
+                                   InterpShared& S) {
+  auto& bnd = S.bnd;
   const int T = blockDim.x, tid = threadIdx.x;
   const uint32_t p = P.p;
   const uint32_t x0 = x[0];
@@ -138,11 +209,11 @@ __device__ void interp_consecutive(uint32_t* x, uint32_t* c, uint32_t* o, uint32
   // 1/j = (j-1)! / j!:  o2[i] = i!, o[i] = 1/i! (suffix products from 1/(n-1)!)
   for (int i = tid; i < n; i += T) o2[i] = i ? (uint32_t)i % p : 1u % p;
   __syncthreads();
-  block_scan_mul(o2, n, false, P);
+  interp_scan_mul(o2, n, false, P, S.sh);
   const uint32_t inv_last = inv_mod(o2[n - 1], P);
   for (int i = tid; i < n; i += T) o[i] = (i == n - 1) ? inv_last : (uint32_t)(i + 1) % p;
   __syncthreads();
-  block_scan_mul(o, n, true, P);  // o[i] = inv_last * (i+1) ... (n-1) = 1/i!
+  interp_scan_mul(o, n, true, P, S.sh);  // o[i] = inv_last * (i+1) ... (n-1) = 1/i!
   for (int j = tid; j < n; j += T) x[j] = j ? mul_mod(o[j], o2[j - 1], P) : 0u;  // 1/j
   __syncthreads();
   const int seg = (n + T - 1) / T;
@@ -183,13 +254,14 @@ __device__ void interp_consecutive(uint32_t* x, uint32_t* c, uint32_t* o, uint32
   __syncthreads();
   (void)o2;
 }
-__global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* __restrict__ xs,
+__global__ void __launch_bounds__(INTERP_THREADS) k_interp_points(const uint32_t* __restrict__ xs,
                                                                const uint32_t* __restrict__ vs, const int32_t* __restrict__ ns,
                                                                int W, const Prime* __restrict__ primes,
                                                                const int32_t* __restrict__ pidx,
                                                                uint32_t* __restrict__ out, uint32_t* __restrict__ gs,
                                                                int xstride) {
   extern __shared__ uint32_t sm_[];
+  __shared__ InterpShared S;
   const int b = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const int n = ns[b];
   uint32_t* sm = gs ? gs + (size_t)b * (4 * W + 2) : sm_;  // global scratch beyond shared memory
@@ -211,8 +283,13 @@ __global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* _
   for (int i = tid; i < n; i += T)
     if (x[i] != (uint32_t)(((uint64_t)x[0] + (uint64_t)i) % p)) cons = 0;
   if (__syncthreads_and(cons) && n >= 2) {
-    interp_consecutive(x, c, o, o2, n, P);
-    for (int k = tid; k < n; k += T) out[(size_t)b * W + k] = o[k];
+    uint32_t* ob = out + (size_t)b * W;
+    if (n + 1 <= T) return interp_consecutive_reg<1>(x, c, o, o2, n, P, ob, S);
+    if (n + 1 <= 2 * T) return interp_consecutive_reg<2>(x, c, o, o2, n, P, ob, S);
+    if (n + 1 <= 4 * T) return interp_consecutive_reg<4>(x, c, o, o2, n, P, ob, S);
+    if (n + 1 <= 8 * T) return interp_consecutive_reg<8>(x, c, o, o2, n, P, ob, S);
+    interp_consecutive(x, c, o, o2, n, P, S);
+    for (int k = tid; k < n; k += T) ob[k] = o[k];
     return;
   }
   // for j in 1..n-1: for i = n-1 .. j: c[i] = (c[i] - c[i-1]) / (x[i] - x[i-j]).
@@ -263,8 +340,10 @@ __global__ void __launch_bounds__(GCD_THREADS) k_interp_points(const uint32_t* _
 void launch_interp_points(const uint32_t* xs, const uint32_t* vs, const int32_t* ns, int W, const Prime* primes,
                           const int32_t* pidx, int B, uint32_t* out, uint32_t* gs, cudaStream_t st, int xstride) {
   const size_t smem = gs ? 0 : (size_t)(4 * W + 2) * 4;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp_points, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_interp_points<<<B, GCD_THREADS, smem, st>>>(xs, vs, ns, W, primes, pidx, out, gs, xstride < 0 ? W : xstride);
+  // the static InterpShared (12 KB) counts against the 48 KB default too
+  if (smem + sizeof(InterpShared) > 48 * 1024)
+    cudaFuncSetAttribute(k_interp_points, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_interp_points<<<B, INTERP_THREADS, smem, st>>>(xs, vs, ns, W, primes, pidx, out, gs, xstride < 0 ? W : xstride);
 }
 
 }  // namespace ckb

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(32 * PSC_WARPS) k_psc_prs(const uint32_t* __re
 // one CTA: S_0 = rstar mod p (trimmed length must be rlen_int), S_i = gcd(S_{i-1}, sr_i)
 // for the interpolated sr_i (rows of `sr`, row i-1 has cnt[i-1] coefficients, stride W);
 // chain[0..n] = deg S_i; *status = 2 when S_0 loses degree mod p (UnluckyPrime)
-__global__ void __launch_bounds__(256) k_gcd_chain(const uint32_t* __restrict__ rmod, int rlen, int rlen_int,
+__global__ void __launch_bounds__(1024) k_gcd_chain(const uint32_t* __restrict__ rmod, int rlen, int rlen_int,
                                                    const uint32_t* __restrict__ sr, const int* __restrict__ cnt,
                                                    int W, int n, Prime P, int* __restrict__ chain,
                                                    uint32_t* __restrict__ status) {
@@ -220,16 +220,36 @@ __global__ void __launch_bounds__(256) k_gcd_chain(const uint32_t* __restrict__ 
         // leading coefficient and the trim read X[lx'-1 ..] (lx' the new length),
         // so a thread still trimming never reads what the next step writes
         while (lx >= ly) {
+          // Montgomery products with the RAW coefficients as multipliers: every
+          // term of a step carries the same factor 2^-32 (and so does the next
+          // step's), which leaves gcd(X, Y) unchanged -- no conversion or Shoup
+          // companion on the per-step critical path
           const uint32_t ca = X[lx - 1], cb = Y[ly - 1];
+          const uint32_t nca = neg_mod(ca, p);
           const int s = lx - ly;
-          const uint32_t cbc = shoup_comp(cb, P), nca = neg_mod(ca, p), ncac = shoup_comp(nca, P);
-          for (int k = tid; k < lx - 1; k += T) {
-            uint32_t v = shoup(X[k], cb, cbc, p);
-            if (k >= s) v = add_mod(v, shoup(Y[k - s], nca, ncac, p), p);
-            X[k] = v;
+          int l;
+          if (s >= 1 && ly >= 2) {
+            // two elimination steps per barrier: X <- cb^2 X - (cb ca x^s + l1 x^(s-1)) Y,
+            // l1 = cb X[lx-2] - ca Y[ly-2] the lc after the first (both leading terms cancel)
+            const uint32_t l1 = redc((uint64_t)cb * X[lx - 2] + (uint64_t)nca * Y[ly - 2], P);
+            const uint32_t w1 = redc((uint64_t)cb * cb, P), w2 = redc((uint64_t)cb * nca, P);
+            const uint32_t w3 = neg_mod(l1, p);
+            for (int k = tid; k < lx - 2; k += T) {
+              uint64_t t = (uint64_t)X[k] * w1;
+              if (k >= s) t += (uint64_t)Y[k - s] * w2;
+              if (k >= s - 1) t += (uint64_t)Y[k - s + 1] * w3;
+              X[k] = redc(t, P);  // t < 3 p^2 < p 2^32
+            }
+            l = lx - 2;
+          } else {
+            for (int k = tid; k < lx - 1; k += T) {
+              uint64_t t = (uint64_t)X[k] * cb;
+              if (k >= s) t += (uint64_t)Y[k - s] * nca;
+              X[k] = redc(t, P);
+            }
+            l = lx - 1;
           }
           __syncthreads();
-          int l = lx - 1;
           while (l > 0 && X[l - 1] == 0u) --l;  // every thread, the same length
           lx = l;
           if (lx == 0) break;
@@ -272,7 +292,7 @@ void launch_gcd_chain(const uint32_t* rmod, int rlen, int rlen_int, const uint32
                       const Prime& P, int* chain, uint32_t* status, cudaStream_t st) {
   const size_t smem = (size_t)2 * (rlen > W ? rlen : W) * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_gcd_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_gcd_chain<<<1, 256, smem, st>>>(rmod, rlen, rlen_int, sr, cnt, W, n, P, chain, status);
+  k_gcd_chain<<<1, 1024, smem, st>>>(rmod, rlen, rlen_int, sr, cnt, W, n, P, chain, status);
 }
 
 }  // namespace ckb

@@ -642,6 +642,14 @@ def biv_resultant_batch(problems, seed: int = 0) -> list:
 # modular subresultant degree profiles (modpoly.py:421-526)
 # ---------------------------------------------------------------------------
 
+def _mod_list(xs, p: int) -> list:
+    try:
+        from .ckb_limbs import mod_list
+    except ImportError:  # the host helper is optional glue
+        return [c % p for c in xs]
+    return mod_list(list(xs), p)
+
+
 def modular_subres_profile(f, g, rstar, p: int):
     """Degree profile of the subresultant gcd chain of f, g mod p (modpoly.py:428-474).
 
@@ -659,18 +667,11 @@ def modular_subres_profile(f, g, rstar, p: int):
     fci, gci = f.coeffs_wrt_y(), g.coeffs_wrt_y()
     if not fci or not gci:
         raise UnluckyPrime(p)
-    # K1 reduction of every coefficient, rstar included
-    flat = [c for col in fci for c in col] + [c for col in gci for c in col] + list(rstar)
-    red = _reduce_many([flat], [p])[0].tolist() if flat else []
-    pos = 0
-    fc, gc = [], []
-    for col in fci:
-        fc.append(red[pos:pos + len(col)])
-        pos += len(col)
-    for col in gci:
-        gc.append(red[pos:pos + len(col)])
-        pos += len(col)
-    rmod = red[pos:pos + len(rstar)]
+    # one prime: residues on the host (C helper over CPython's digits) instead of
+    # packing every coefficient -- rstar's ~5 kbit ones at cfg4 -- into limbs for K1
+    fc = [_mod_list(col, p) for col in fci]
+    gc = [_mod_list(col, p) for col in gci]
+    rmod = _mod_list(rstar, p)
     if not _trim(list(fc[-1])) or not _trim(list(gc[-1])):
         raise UnluckyPrime(p)  # modpoly.py:437-439
     m, n = len(fc) - 1, len(gc) - 1

@@ -252,3 +252,18 @@ def test_pack_terms_declines_what_it_cannot_read():
     assert planner.pack_terms({(0, 1): 10 ** 400}, one) is None     # 1-norm overflows a double
     assert planner.pack_terms({}, one) is None                      # zero polynomial
     assert planner.pack_terms([1, 2], one) is None
+
+
+def test_host_mod_list_matches_python():
+    """The host helper's residues (modular_subres_profile's single-prime
+    reduction) equal Python's % for big, negative and edge-case integers."""
+    import random as _r
+    try:
+        from paper_1201_1548_b200.ckb_limbs import mod_list
+    except ImportError:
+        import pytest
+        pytest.skip("host helper not built")
+    rng = _r.Random(3)
+    xs = [rng.randint(-2 ** 6000, 2 ** 6000) for _ in range(300)] + [0, 1, -1, 2 ** 30, -(2 ** 30), 2 ** 64 - 1]
+    for p in (2, 3, 7, 1073692673, 2147483647, 4294967291):
+        assert mod_list(xs, p) == [x % p for x in xs]
