@@ -12,6 +12,7 @@ if REPO not in sys.path:
 
 
 REF = os.path.join(REPO, "baseline", "_ref")
+sys.set_int_max_str_digits(0)  # repr-hashes of cfg5-size resultants (~34 kbit coefficients)
 
 
 def pytest_configure(config):

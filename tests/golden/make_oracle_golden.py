@@ -32,6 +32,8 @@ REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, REPO)
 
 from oracle import oracle  # noqa: E402
+
+sys.set_int_max_str_digits(0)  # repr of ~34 kbit coefficients (cfg5)
 from paper_1201_1548_b200.synth import make_pair  # noqa: E402
 
 FP_PRIMES = (2305843009213693951, 2305843009213693921, 2305843009213693907)  # 2^61-1 and two below
