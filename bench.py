@@ -614,6 +614,13 @@ def run_ours(args):
         # ideal time of this product mix at the measured peaks of its two forms
         t_ideal = p_shoup / (float(peak[3]) * 1e12) + p_mont / (float(peak[4]) * 1e12)
         mix_peak = img_prod / t_ideal / 1e12
+        # share of the images the register kernel handed to the general warp kernel
+        _lib.check(lib.ckb_dev_biv_resultant(
+            backend.d_limbs.data_ptr(), pk.C, pk.L, backend.d_degs.data_ptr(), _lib.ptr(backend.h_degs),
+            pk.m, pk.n, pk.dfx, pk.dgx, _lib.ptr(hp_all), _lib.ptr(hg_all), K, N, LW, d_out1.data_ptr()
+            if d_out1 is not None else d_out.data_ptr(), backend.d_status.data_ptr(), stream.cuda_stream),
+            "ckb_dev_biv_resultant")
+        fb, nimg = _lib.last_fallback()
         traffic = None
         try:
             with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as fh:
@@ -635,6 +642,9 @@ def run_ours(args):
                            step_graph=bool(graph is not None), parallelism=(f"primes/{world}" if not sharded else
                                         f"primes/{world}, all-to-all, CRT coefficients/{world}")),
             "images_per_s": images * 1e3 / ms_per_step,
+            "fallback": {"images": fb, "of": nimg, "share": fb / max(1, nimg),
+                         "note": "images whose remainder sequence is not generic: recomputed by the general "
+                                 "warp kernel (k_images_fallback)"},
             "stages_ms": stages,
             "stages_note": ("CUDA events between the stages of one single-GPU pipeline call (timing mode: no graph)"
                             + ("" if world == 1 else "; measured on rank 0's GPU alone")),

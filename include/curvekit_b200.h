@@ -56,6 +56,10 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
  * share one GPU: a correctness configuration).  ckb_init(device) is the n = 1
  * case.  ckb_devices reports the context count and whether NCCL is in use. */
 int ckb_init_devices(int n, const int* devices);
+
+/* Images of the last res_y pipeline call that left the register kernel for the
+ * general warp kernel (non-generic remainder sequences), and all its images. */
+int ckb_last_fallback(unsigned long long* fallback, unsigned long long* images);
 int ckb_devices(int* n_contexts, int* nccl);
 
 /* ckb_biv_resultant over the first G contexts (primes sharded, SURVEY §8e

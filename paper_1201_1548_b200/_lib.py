@@ -24,7 +24,7 @@ EXPORTS = (
     "ckb_stage_times", "ckb_measure_peak", "ckb_psc_values", "ckb_host_alloc", "ckb_host_free",
     "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release", "ckb_biv_gcd_images",
     "ckb_biv_resultant_batch", "ckb_descartes_variations_batch", "ckb_set_graphs",
-    "ckb_init_devices", "ckb_devices", "ckb_biv_resultant_multi", "ckb_subres_profile",
+    "ckb_init_devices", "ckb_devices", "ckb_biv_resultant_multi", "ckb_subres_profile", "ckb_last_fallback",
 )
 
 _P = ctypes.c_void_p
@@ -63,6 +63,7 @@ _SIGS = {
     "ckb_descartes_variations_batch": (_I, [_I, _P, _I, _P, _I, _I, _I, _P]),
     "ckb_biv_gcd_images": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P]),
     "ckb_init_devices": (_I, [_I, _P]),
+    "ckb_last_fallback": (_I, [_P, _P]),
     "ckb_subres_profile": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, _P, _I, _I, _I, ctypes.c_uint32, _P]),
     "ckb_devices": (_I, [_P, _P]),
     "ckb_biv_resultant_multi": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
@@ -147,6 +148,13 @@ def n_devices() -> int:
     n, nc = ctypes.c_int(0), ctypes.c_int(0)
     lib().ckb_devices(ctypes.byref(n), ctypes.byref(nc))
     return max(1, n.value)
+
+
+def last_fallback() -> tuple:
+    """(images sent to the general warp kernel, all images) of the last res_y call."""
+    a, b = ctypes.c_ulonglong(0), ctypes.c_ulonglong(0)
+    check(lib().ckb_last_fallback(ctypes.byref(a), ctypes.byref(b)), "ckb_last_fallback")
+    return int(a.value), int(b.value)
 
 
 def uses_nccl() -> bool:

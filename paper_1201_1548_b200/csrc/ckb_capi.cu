@@ -72,6 +72,9 @@ struct Ctx {
   bool graphs = true;  // CKB_NO_GRAPHS=1 disables graph replay
   std::string ns;      // buffer-name prefix: each problem of a batch owns its buffers
   cudaStream_t bst[4] = {};  // streams of the batched entry (created on first use)
+  const uint32_t* last_fail = nullptr;  // fallback counter of the last pipeline call (device)
+  cudaStream_t last_stream = nullptr;   // ... and the stream that call ran on
+  uint64_t last_images = 0;
   cudaEvent_t bev[4] = {};
 };
 
@@ -552,6 +555,24 @@ void key_push(std::vector<uint64_t>& k, const void* p, size_t bytes) {
   }
 }
 
+// structured inputs: a y-coefficient strictly inside the degree range vanishes identically (as in
+// F(x, y^2)), so the remainder sequences of (almost) all images drop the degree by more than one --
+// the subresultant coefficients vanish identically, for every point and shift.  Such inputs run the
+// register kernel's any-degree elimination directly (CKB_STRUCTURED=0/1 forces the choice).
+bool structured_input(const int16_t* h_degs, int m, int n) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("CKB_STRUCTURED");
+    force = e ? atoi(e) : -1;
+  }
+  if (force >= 0) return force != 0;
+  for (int j = 1; j < m; ++j)
+    if (h_degs[j] < 0) return true;
+  for (int j = 1; j < n; ++j)
+    if (h_degs[m + 1 + j] < 0) return true;
+  return false;
+}
+
 int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
                   int n, int dfx, int dgx, const Prime* d_primes, const uint32_t* h_primes, const uint32_t* h_gens,
                   int K, int N, uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st,
@@ -611,10 +632,13 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   a.status = d_status;
   a.fail_list = d_fail;
   a.fail_count = a.fail_list + (size_t)K * NI;
+  g.last_fail = general ? nullptr : a.fail_count;
+  g.last_stream = st;
+  g.last_images = (uint64_t)K * NI;
   if (general)
     launch_images_general(a, st);
   else
-    launch_images(a, st);
+    launch_images(a, st, structured_input(h_degs, m, n));
   stage_mark(st);
   uint8_t* d_ixb = nullptr;
   if (pl.Ab && (rc = dbuf("ixb", interp_mma_scratch_bytes(pl), &d_ixb))) return rc;
@@ -840,6 +864,24 @@ int ckb_shutdown(void) {
   }
   g_ci = 0;
   g_nctx = 0;
+  return 0;
+}
+
+int ckb_last_fallback(unsigned long long* fallback, unsigned long long* images) {
+  // images of the last pipeline call (context 0) that the register kernel handed
+  // to the general warp kernel (non-generic remainder sequences), and all images
+  std::lock_guard<std::mutex> lk(g_mu);
+  int rc;
+  if ((rc = ensure_ready())) return rc;
+  uint32_t c = 0;
+  if (g.last_fail) {
+    CK(cudaStreamSynchronize(g.last_stream ? g.last_stream : g.stream));
+    CK(cudaMemcpy(&c, g.last_fail, 4, cudaMemcpyDeviceToHost));
+  } else if (g.last_images) {
+    c = (uint32_t)g.last_images;  // the general path: every image went to the warp kernel
+  }
+  if (fallback) *fallback = c;
+  if (images) *images = g.last_images;
   return 0;
 }
 

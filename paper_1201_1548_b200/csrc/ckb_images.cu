@@ -70,7 +70,9 @@ struct ImgLayout {
 // NT = threads (images) per CTA; ALIGNED: grid (ceil(N/NT), K), a CTA never
 // straddles primes (one staged table: the register-heavy buckets fit more CTAs)
 // EX: 0 any degrees; 1 da = db = MAXD; 2 da = MAXD, db = MAXD - 1 (the dense
-// res(f, g) and res(f, f_y) shapes: the elimination chain is unrolled exactly)
+// res(f, g) and res(f, f_y) shapes: the elimination chain is unrolled exactly);
+// 3 structured inputs: any degree pattern of the remainder sequences, single
+// eliminations (no fallback list)
 // The unrolled chain lets ptxas keep more values live (cfg4: 178 registers
 // uncapped, 8 warps/SM): capped at 128 (16 warps/SM) for MAXD <= 40 and 170
 // for 48 it measured fastest (cfg4 images 270 -> 241 us; uncapped 337 us)
@@ -285,7 +287,9 @@ __global__ void __launch_bounds__(NT, ALIGNED ? 1 : (EX ? exact_minb(MAXD) : img
     v = 0u;
   } else {
     const bool neg = sw && ((a.m * a.n) & 1);
-    if constexpr (EX == 1)
+    if constexpr (EX == 3)
+      v = resultant_anydeg<MAXD>(A, da, B, db, neg, P);  // structured inputs: never CKB_FAIL
+    else if constexpr (EX == 1)
       v = resultant_generic<MAXD, MAXD>(A, da, B, db, neg, P);
     else if constexpr (EX == 2)
       v = resultant_generic<MAXD, MAXD - 1>(A, da, B, db, neg, P);
@@ -471,6 +475,7 @@ static bool images_aligned(int maxd) {
 constexpr int EXACT_MAXD = 48;
 template <int D, int NT, bool AL>
 static void (*images_kernel(int ex))(ImageArgs) {
+  if (ex == 3) return k_images<D, NT, AL, 3>;
   if constexpr (D > EXACT_MAXD) {
     return k_images<D, NT, AL, 0>;
   } else {
@@ -491,9 +496,9 @@ static int images_exact(int maxd, int m, int n) {
   return db == maxd ? 1 : db == maxd - 1 ? 2 : 0;
 }
 
-void launch_images(const ImageArgs& a, cudaStream_t st) {
+void launch_images(const ImageArgs& a, cudaStream_t st, bool structured) {
   const int maxd = images_maxd(a.m, a.n);
-  const int ex = images_exact(maxd, a.m, a.n);
+  const int ex = structured ? 3 : images_exact(maxd, a.m, a.n);
   if (images_aligned(maxd)) {
     constexpr int NTA = 64;
     ImageArgs b = a;

@@ -117,7 +117,7 @@ void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes,
                        int lcf_off = 0, int lcf_deg = 0, int lcg_off = 0, int lcg_deg = 0, uint32_t* cval = nullptr,
                        uint32_t* status = nullptr);
 // fast generic kernel followed by the general warp kernel on its fail list
-void launch_images(const ImageArgs& a, cudaStream_t st);
+void launch_images(const ImageArgs& a, cudaStream_t st, bool structured = false);
 void launch_images_fallback(const ImageArgs& a, cudaStream_t st);
 
 // batch of independent univariate resultants (modpoly.py:156-161)

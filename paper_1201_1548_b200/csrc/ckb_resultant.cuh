@@ -268,6 +268,89 @@ __device__ __forceinline__ uint32_t resultant_generic(uint32_t (&A)[MAXD + 1], i
   return neg ? neg_mod(r, p) : r;
 }
 
+// shift a top-aligned register array up by one position (the leading entry was 0)
+template <int MAXD>
+__device__ __forceinline__ void shift_up(uint32_t (&D)[MAXD + 1]) {
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) D[i] = D[i + 1];
+  D[MAXD] = 0u;
+}
+
+// one pseudo-remainder of the dividend D (deg dd) by V (deg dv >= 1), D <- prem(D, V)
+// by e = dd - dv + 1 single eliminations, then the leading zeros shifted out;
+// returns the remainder's degree (-1: zero remainder)
+template <int MAXD>
+__device__ __forceinline__ int prem_any(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int dd, int dv,
+                                        uint32_t lb, uint32_t lbc, const Prime& P) {
+  for (int s = 0; s <= dd - dv; ++s) step1<MAXD>(D, V, dd - s, lb, lbc, P);
+  int dr = dv - 1;
+  while (dr >= 0 && red4(D[0], P.p) == 0u) {
+    shift_up<MAXD>(D);
+    --dr;
+  }
+  return dr;
+}
+
+// res(A, B) for top-aligned A (deg da) and B (deg db), da >= db >= 1, nonzero
+// leading coefficients, ANY degree pattern of the remainder sequence (the
+// structured inputs whose subresultant coefficients vanish identically: every
+// image of F(x, y^2) drops the degree by two).  The reference's recursion
+// (modpoly.py:138-152) with division-free remainders: prem(A, B) = lb^e rem(A, B),
+// e = da - db + 1, so res(A, B) = (-1)^(da db) lb^(da - dr) res(B, rem)
+//                              = (-1)^(da db) lb^(da - dr - e db) res(B, prem).
+// Two register arrays swap roles in a loop written twice (static indices only).
+template <int MAXD>
+__device__ __forceinline__ uint32_t resultant_anydeg(uint32_t (&A)[MAXD + 1], int da, uint32_t (&B)[MAXD + 1], int db,
+                                                     bool neg, const Prime& P) {
+  const uint32_t p = P.p;
+  const uint32_t one = redc(P.r2, P);  // R mod p
+  uint32_t num = one, den = one;       // Montgomery form
+  for (;;) {
+    // dividend A (deg da), divisor B (deg db >= 1)
+    {
+      const uint32_t lb = red4(B[0], p);
+      const uint32_t lbm = to_mont(lb, P), lbc = comp_from_mont(lbm, P);
+      const int e = da - db + 1;
+      const int dr = prem_any<MAXD>(A, B, da, db, lb, lbc, P);
+      if (dr < 0) return 0u;  // a common factor
+      neg ^= (bool)(da & db & 1);
+      num = mmul(num, mpow(lbm, da - dr, one, P), P);
+      den = mmul(den, mpow(lbm, e * db, one, P), P);
+      da = dr;
+      if (da == 0) {  // res(B, c) = c^db
+        num = mmul(num, mpow(to_mont(red4(A[0], p), P), db, one, P), P);
+        break;
+      }
+    }
+    // dividend B (deg db), divisor A (deg da >= 1)
+    {
+      const uint32_t lb = red4(A[0], p);
+      const uint32_t lbm = to_mont(lb, P), lbc = comp_from_mont(lbm, P);
+      const int e = db - da + 1;
+      const int dr = prem_any<MAXD>(B, A, db, da, lb, lbc, P);
+      if (dr < 0) return 0u;
+      neg ^= (bool)(da & db & 1);
+      num = mmul(num, mpow(lbm, db - dr, one, P), P);
+      den = mmul(den, mpow(lbm, e * da, one, P), P);
+      db = dr;
+      if (db == 0) {
+        num = mmul(num, mpow(to_mont(red4(B[0], p), P), da, one, P), P);
+        break;
+      }
+    }
+  }
+  // num / den in the Montgomery domain (Fermat inverse), then leave it
+  uint32_t inv = one, b = den;
+  uint32_t ex = p - 2;
+  while (ex) {
+    if (ex & 1) inv = mmul(inv, b, P);
+    ex >>= 1;
+    if (ex) b = mmul(b, b, P);
+  }
+  const uint32_t r = redc((uint64_t)mmul(num, inv, P), P);
+  return neg ? neg_mod(r, p) : r;
+}
+
 // Lazy Shoup-Horner evaluation of a residue polynomial c[0..deg] at x: [0, 3p)
 __device__ __forceinline__ uint32_t horner_lazy(const uint32_t* c, int deg, uint32_t x, uint32_t xc, uint32_t p) {
   if (deg < 0) return 0u;

@@ -19,6 +19,9 @@ CONFIGS = {
     "cfg3": (24, 64, "fy"),
     "cfg4": (40, 64, "pair"),
     "cfg5": (64, 256, "pair"),
+    # structured (not a BASELINE config): f = F(x, y^2), g = G(x, y^2), total degree 40, 64-bit -- every
+    # image's remainder sequence drops the y-degree by 2 (systematically non-generic)
+    "sparse": (40, 64, "even"),
 }
 
 
@@ -27,6 +30,19 @@ def random_dense_terms(rng: random.Random, d: int, bits: int) -> dict:
     terms = {}
     for i in range(d + 1):
         for j in range(d + 1 - i):
+            c = 0
+            while c == 0:
+                c = rng.randint(-hi, hi)
+            terms[(i, j)] = c
+    return terms
+
+
+def random_even_terms(rng: random.Random, d: int, bits: int) -> dict:
+    """Dense in x and y^2: every x^i y^(2j) with i + 2j <= d."""
+    hi = (1 << bits) - 1
+    terms = {}
+    for i in range(d + 1):
+        for j in range(0, d + 1 - i, 2):
             c = 0
             while c == 0:
                 c = rng.randint(-hi, hi)
@@ -49,5 +65,8 @@ def make_pair(config: str, seed: int = 0):
     f = random_dense_terms(rng, d, bits)
     if kind == "fy":
         return f, diff_y(f)
+    if kind == "even":
+        rng = random.Random(seed)
+        return random_even_terms(rng, d, bits), random_even_terms(rng, d, bits)
     g = random_dense_terms(rng, d, bits)
     return f, g

@@ -487,3 +487,18 @@ def test_c_abi_rejects_bad_arguments():
     # still usable afterwards
     from paper_1201_1548_b200 import modpoly
     assert modpoly.biv_resultant({(2, 0): 1, (0, 2): 1, (0, 0): -1}, {(0, 1): 2}) == [-4, 0, 4]
+
+
+def test_structured_even_y_inputs(mp, oracle_mod):
+    """f = F(x, y^2), g = G(x, y^2): every image's remainder sequence drops the
+    degree by two (non-generic), so the images take the general path; small sizes
+    against the oracle, the 'sparse' bench configuration (d = 40) by specialisation."""
+    from paper_1201_1548_b200.synth import make_pair, random_even_terms
+    rng = random.Random(12)
+    for d, bits in ((6, 10), (10, 40), (14, 64)):
+        f, g = random_even_terms(rng, d, bits), random_even_terms(rng, d, bits)
+        for var in ("y", "x"):
+            assert mp.biv_resultant(f, g, var) == oracle_mod.biv_resultant(f, g, var)
+    f, g = make_pair("sparse", 0)
+    res = mp.biv_resultant(f, g, "y")
+    _specialisation_check(mp, oracle_mod, f, g, res, random.Random(40), trials=4)
