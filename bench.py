@@ -597,6 +597,8 @@ def run_ours(args):
             modpoly.biv_resultant(F, G, "y")
             pt.append(time.perf_counter() - t0)
         e_ms = 1e3 * statistics.median(et)
+        # share of the images the register kernel handed to the fallback (last C-ABI call)
+        fb, nimg = _lib.last_fallback()
         e2e = {"value": 1e3 / e_ms, "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(pk.limbs.nbytes + pk.degs.nbytes + 4 * len(p1.gens)),
                "d2h_bytes_per_step": int(hout.nbytes + 4),
@@ -604,6 +606,8 @@ def run_ours(args):
                "python_api_ms": 1e3 * statistics.median(pt),
                "python_api_note": "modpoly.biv_resultant incl. packing, planning, int conversion"}
 
+    if sharded:
+        fb, nimg = 0, 0  # (the sharded step's kernels run through ckb_dev_modular_images)
     if rank == 0:
         dfs = [len(c) - 1 for c in fc]
         dgs = [len(c) - 1 for c in gc]
@@ -614,13 +618,6 @@ def run_ours(args):
         # ideal time of this product mix at the measured peaks of its two forms
         t_ideal = p_shoup / (float(peak[3]) * 1e12) + p_mont / (float(peak[4]) * 1e12)
         mix_peak = img_prod / t_ideal / 1e12
-        # share of the images the register kernel handed to the general warp kernel
-        _lib.check(lib.ckb_dev_biv_resultant(
-            backend.d_limbs.data_ptr(), pk.C, pk.L, backend.d_degs.data_ptr(), _lib.ptr(backend.h_degs),
-            pk.m, pk.n, pk.dfx, pk.dgx, _lib.ptr(hp_all), _lib.ptr(hg_all), K, N, LW, d_out1.data_ptr()
-            if d_out1 is not None else d_out.data_ptr(), backend.d_status.data_ptr(), stream.cuda_stream),
-            "ckb_dev_biv_resultant")
-        fb, nimg = _lib.last_fallback()
         traffic = None
         try:
             with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as fh:
@@ -643,8 +640,9 @@ def run_ours(args):
                                         f"primes/{world}, all-to-all, CRT coefficients/{world}")),
             "images_per_s": images * 1e3 / ms_per_step,
             "fallback": {"images": fb, "of": nimg, "share": fb / max(1, nimg),
-                         "note": "images whose remainder sequence is not generic: recomputed by the general "
-                                 "warp kernel (k_images_fallback)"},
+                         "note": "images whose remainder sequence is not generic, recomputed one thread per "
+                                 "image by the any-degree elimination (k_images_fallback_reg); structured inputs "
+                                 "(an interior y-coefficient identically zero) run it in the register kernel itself"},
             "stages_ms": stages,
             "stages_note": ("CUDA events between the stages of one single-GPU pipeline call (timing mode: no graph)"
                             + ("" if world == 1 else "; measured on rank 0's GPU alone")),

@@ -304,6 +304,56 @@ __global__ void __launch_bounds__(NT, ALIGNED ? 1 : (EX ? exact_minb(MAXD) : img
   a.values[(size_t)pi * a.N + idx] = v;
 }
 
+// The images the register kernel could not finish (a remainder sequence that is
+// not generic), one THREAD per image: evaluation of every y-coefficient at the
+// image's point straight from the residues (Horner, the warp's threads mostly
+// share a prime, so the coefficient loads are broadcasts) and the any-degree
+// elimination in registers (resultant_anydeg).  A grid of resident CTAs strides
+// over the list; an empty list (the usual case) costs one short launch.
+template <int MAXD>
+__global__ void __launch_bounds__(128) k_images_fallback_reg(ImageArgs a) {
+  pdl_wait();
+  const uint32_t count = *a.fail_count;
+  const bool sw = a.m < a.n;
+  const int da = sw ? a.n : a.m, db = sw ? a.m : a.n;
+  const int offG = (a.m + 1) * (a.dfx + 1);
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += gridDim.x * blockDim.x) {
+    const uint32_t flat = a.fail_list[idx];
+    const int pi = (int)(flat / (uint32_t)a.N);
+    const Prime P = a.primes[pi];
+    const uint32_t p = P.p;
+    const uint32_t c = a.cval[pi];
+    const int loc = (int)(flat - (uint32_t)pi * (uint32_t)a.N), S = a.N / a.M;
+    const uint32_t* om = a.om + (size_t)pi * 4 * S;
+    uint32_t x = shoup(a.yq[(size_t)pi * a.M + loc / S], om[loc % S], om[S + loc % S], p);  // w^j g^u
+    if (c != 1u) x = shoup(x, c, shoup_comp(c, P), p);
+    const uint32_t xc = shoup_comp(x, P);
+    const uint32_t* res = a.red + (size_t)pi * a.C;
+    uint32_t A[MAXD + 1], B[MAXD + 1];
+#pragma unroll
+    for (int i = 0; i <= MAXD; ++i) {
+      // top-aligned: A[i] = (y-coefficient of degree da - i)(x); f is A unless swapped
+      uint32_t va = 0u, vb = 0u;
+      if (i <= da) {
+        const int j = da - i;
+        const uint32_t* cf = sw ? res + offG + j * (a.dgx + 1) : res + j * (a.dfx + 1);
+        const int dg = a.degs[sw ? a.m + 1 + j : j];
+        for (int e = dg; e >= 0; --e) va = add_mod(shoup(va, x, xc, p), cf[e], p);
+      }
+      if (i <= db) {
+        const int j = db - i;
+        const uint32_t* cg = sw ? res + j * (a.dfx + 1) : res + offG + j * (a.dgx + 1);
+        const int dg = a.degs[sw ? j : a.m + 1 + j];
+        for (int e = dg; e >= 0; --e) vb = add_mod(shoup(vb, x, xc, p), cg[e], p);
+      }
+      A[i] = va;
+      B[i] = vb;
+    }
+    const bool neg = sw && ((a.m * a.n) & 1);
+    a.values[flat] = resultant_anydeg<MAXD>(A, da, B, db, neg, P);
+  }
+}
+
 #define CKB_MAXD_LIST(X) X(4) X(8) X(12) X(16) X(24) X(32) X(40) X(48) X(56) X(64)
 
 static int images_sw(int maxd) {
@@ -496,6 +546,20 @@ static int images_exact(int maxd, int m, int n) {
   return db == maxd ? 1 : db == maxd - 1 ? 2 : 0;
 }
 
+// the failed images of the register kernel: thread per image (CKB_FALLBACK_WARP=1: the warp kernel)
+static void launch_fallback_reg(int maxd, const ImageArgs& a, cudaStream_t st) {
+  static int warp = -1;
+  if (warp < 0) {
+    const char* e = getenv("CKB_FALLBACK_WARP");
+    warp = e ? atoi(e) : 0;
+  }
+  if (warp) return launch_images_fallback(a, st);
+#define FB(D) \
+  if (maxd == D) launch_pdl(k_images_fallback_reg<D>, dim3(2 * 148), dim3(128), 0, st, a);
+  CKB_MAXD_LIST(FB)
+#undef FB
+}
+
 void launch_images(const ImageArgs& a, cudaStream_t st, bool structured) {
   const int maxd = images_maxd(a.m, a.n);
   const int ex = structured ? 3 : images_exact(maxd, a.m, a.n);
@@ -515,7 +579,7 @@ void launch_images(const ImageArgs& a, cudaStream_t st, bool structured) {
   }
     LAUNCH_AL(56) LAUNCH_AL(64)
 #undef LAUNCH_AL
-    launch_images_fallback(a, st);
+    launch_fallback_reg(maxd, a, st);
     return;
   }
   dim3 grid((unsigned)(((size_t)a.K * a.N + IMG_THREADS - 1) / IMG_THREADS));
@@ -533,7 +597,7 @@ void launch_images(const ImageArgs& a, cudaStream_t st, bool structured) {
   }
   CKB_MAXD_LIST(LAUNCH)
 #undef LAUNCH
-  launch_images_fallback(a, st);
+  launch_fallback_reg(maxd, a, st);
 }
 
 }  // namespace ckb
