@@ -15,6 +15,7 @@
 #include "ckb_choose.cuh"
 #include "ckb_resultant.cuh"
 #include "ckb_ntt.cuh"
+#include "ckb_images.cuh"
 
 namespace ckb {
 
@@ -30,42 +31,6 @@ constexpr int img_minb(int maxd) { return maxd >= 56 ? CKB_IMG_MINB_BIG : CKB_IM
 #define CKB_IMG_THREADS 128
 #endif
 constexpr int IMG_THREADS = CKB_IMG_THREADS;
-
-constexpr int POLY = 8;  // polyphase factor S: one 8-lane group per coset {w^j y_u}
-
-namespace {
-__device__ __forceinline__ uint32_t img_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void img_mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void img_mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void img_mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void img_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-}  // namespace
-
-// shared-memory row width of the transposed, top-aligned residue tables.  An
-// odd number of 16-byte chunks per row makes the 8 rows read by one lane
-// group (x-powers r + 8e', r < 8) fall in disjoint banks.
-template <int MAXD>
-struct ImgLayout {
-  static constexpr int NCH = (MAXD + 4) / 4;                   // chunks of 4 registers
-  static constexpr int SW = ((NCH & 1) ? NCH : NCH + 1) * 4;   // words per x-power row
-};
 
 // NT = threads (images) per CTA; ALIGNED: grid (ceil(N/NT), K), a CTA never
 // straddles primes (one staged table: the register-heavy buckets fit more CTAs)
@@ -560,9 +525,27 @@ static void launch_fallback_reg(int maxd, const ImageArgs& a, cudaStream_t st) {
 #undef FB
 }
 
+// paired lanes (ckb_images_pair.cu) when the launch is too small to fill the
+// machine: below PAIR_WARPS warps of images per scheduler (CKB_IMG_PAIR=0/1: never/always)
+static bool images_use_pair(int maxd, const ImageArgs& a) {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("CKB_IMG_PAIR");
+    mode = e ? atoi(e) : -1;
+  }
+  if (mode == 0 || maxd < 8 || maxd > 48) return false;
+  if (mode == 1) return true;
+  const double warps = (double)a.K * a.N / 32.0;
+  return warps < 3.0 * 148 * 4;
+}
+
 void launch_images(const ImageArgs& a, cudaStream_t st, bool structured) {
   const int maxd = images_maxd(a.m, a.n);
   const int ex = structured ? 3 : images_exact(maxd, a.m, a.n);
+  if (ex != 3 && images_use_pair(maxd, a) && launch_images_pair(maxd, ex, a, st)) {
+    launch_fallback_reg(maxd, a, st);
+    return;
+  }
   if (images_aligned(maxd)) {
     constexpr int NTA = 64;
     ImageArgs b = a;
