@@ -22,7 +22,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr"]
 SOURCES = ["ckb_capi.cu", "ckb_plan.cu", "ckb_images.cu", "ckb_interp.cu", "ckb_crt.cu", "ckb_gcd.cu", "ckb_general.cu",
            "ckb_peak.cu", "ckb_psc.cu", "ckb_crt_mma.cu",
-           "ckb_descartes.cu", "ckb_bivgcd.cu", "ckb_images_pair.cu"]
+           "ckb_descartes.cu", "ckb_bivgcd.cu"]
 HEADERS = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")] + \
     [os.path.join(REPO, "include", "curvekit_b200.h")]
 

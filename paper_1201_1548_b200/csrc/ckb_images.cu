@@ -525,27 +525,9 @@ static void launch_fallback_reg(int maxd, const ImageArgs& a, cudaStream_t st) {
 #undef FB
 }
 
-// paired lanes (ckb_images_pair.cu) when the launch is too small to fill the
-// machine: below PAIR_WARPS warps of images per scheduler (CKB_IMG_PAIR=0/1: never/always)
-static bool images_use_pair(int maxd, const ImageArgs& a) {
-  static int mode = -2;
-  if (mode == -2) {
-    const char* e = getenv("CKB_IMG_PAIR");
-    mode = e ? atoi(e) : -1;
-  }
-  if (mode == 0 || maxd < 8 || maxd > 48) return false;
-  if (mode == 1) return true;
-  const double warps = (double)a.K * a.N / 32.0;
-  return warps < 3.0 * 148 * 4;
-}
-
 void launch_images(const ImageArgs& a, cudaStream_t st, bool structured) {
   const int maxd = images_maxd(a.m, a.n);
   const int ex = structured ? 3 : images_exact(maxd, a.m, a.n);
-  if (ex != 3 && images_use_pair(maxd, a) && launch_images_pair(maxd, ex, a, st)) {
-    launch_fallback_reg(maxd, a, st);
-    return;
-  }
   if (images_aligned(maxd)) {
     constexpr int NTA = 64;
     ImageArgs b = a;

@@ -1,6 +1,5 @@
-// Helpers shared by the images kernels (ckb_images.cu: one lane per image;
-// ckb_images_pair.cu: two lanes per image): the polyphase factor, the staged
-// table layout and the mbarrier / bulk-copy primitives of the table staging.
+// Helpers of the images kernels (ckb_images.cu): the polyphase factor, the
+// staged table layout and the mbarrier / bulk-copy primitives of the table staging.
 #pragma once
 #include <cstdint>
 

@@ -119,8 +119,6 @@ void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes,
 // fast generic kernel followed by the general warp kernel on its fail list
 void launch_images(const ImageArgs& a, cudaStream_t st, bool structured = false);
 void launch_images_fallback(const ImageArgs& a, cudaStream_t st);
-// two lanes per image (ckb_images_pair.cu) for launches below ~3 warps per scheduler; false: no such bucket
-bool launch_images_pair(int maxd, int ex, const ImageArgs& a, cudaStream_t st);
 
 // batch of independent univariate resultants (modpoly.py:156-161)
 // fa/gb: [B][W] padded low-first coefficients; degrees da/db; per-pair prime index
