@@ -527,7 +527,14 @@ static void launch_fallback_reg(int maxd, const ImageArgs& a, cudaStream_t st) {
 
 void launch_images(const ImageArgs& a, cudaStream_t st, bool structured) {
   const int maxd = images_maxd(a.m, a.n);
-  const int ex = structured ? 3 : images_exact(maxd, a.m, a.n);
+  int ex = structured ? 3 : images_exact(maxd, a.m, a.n);
+  // below ~2.5 warps of images per scheduler (one prime shard of cfg4 at 8 GPUs) the
+  // unrolled chains stall on instruction fetch (ncu: 4.4 no-instruction stalls per
+  // issue at 8 warps/SM); the compact exit sweeps measured faster there (68 -> 62 us)
+  if (ex == 1 || ex == 2) {
+    const double warps = (double)a.K * a.N / 32.0;
+    if (warps < 2.5 * 148 * 4) ex = 0;
+  }
   if (images_aligned(maxd)) {
     constexpr int NTA = 64;
     ImageArgs b = a;

@@ -24,6 +24,7 @@ from paper_1201_1548_b200.synth import make_pair  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg4")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--worlds", default="1,2,4,8")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -50,7 +51,7 @@ def timed(fn):
     return float(np.median(ts))
 
 
-for world in (1, 2, 4, 8):
+for world in [int(w) for w in args.worlds.split(",")]:
     plan = plan_sharded(fc, gc, F.total_degree(), G.total_degree(), world)
     be = CudaBackend(fc, gc, dev)
     primes, gens = plan.shard(0)
