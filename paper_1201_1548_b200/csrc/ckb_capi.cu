@@ -950,9 +950,8 @@ int res_enqueue(const uint32_t* limbs, int C, int L, const int16_t* degs, int m,
     if ((r = modular_stage(d_limbs, C, L, d_degs, degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N, d_coeffs,
                            d_status, st, &ce->t)))
       return r;
-    launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
+    g.launches += launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
     stage_mark(st);
-    g.launches += 2;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(dst_out, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(ho + 4 * (size_t)N * LW, d_status, 4, cudaMemcpyDeviceToHost, st));
@@ -1196,8 +1195,7 @@ int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* 
     key_push(key, primes, 4 * (size_t)K);
     rc = graphed(key, st, [&]() -> int {
       if (ws > 0) {
-        launch_crt(v.ce->t, v.recv, ws, v.out, v.crtS, st);
-        g.launches += 3;
+        g.launches += launch_crt(v.ce->t, v.recv, ws, v.out, v.crtS, st);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(dst_out + (size_t)a0[s2] * LW, v.out, 4 * (size_t)ws * LW, cudaMemcpyDeviceToHost, st));
       }
@@ -1292,8 +1290,7 @@ int ckb_crt_lift(const uint32_t* residues, int K, int N, const uint32_t* primes,
   CK(cudaMemcpyAsync(d_res, residues, 4 * (size_t)K * N, cudaMemcpyHostToDevice, st));
   uint32_t* d_crtS;
   if ((rc = dbuf("crtS", crt_scratch_words(K, N, LW), &d_crtS))) return rc;
-  launch_crt(ce->t, d_res, N, d_out, d_crtS, st);
-  g.launches += 2;
+  g.launches += launch_crt(ce->t, d_res, N, d_out, d_crtS, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, d_out, 4 * (size_t)N * LW, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1592,8 +1589,7 @@ int ckb_dev_crt(const uint32_t* d_coeffs, int K, int N, const uint32_t* primes, 
                                (uint64_t)st};
   key_push(key, primes, 4 * (size_t)K);
   return graphed(key, st, [&]() -> int {
-    launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
-    g.launches += 3;
+    g.launches += launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st);
     CK(cudaGetLastError());
     return 0;
   });
@@ -1626,9 +1622,8 @@ int ckb_dev_biv_resultant(const uint32_t* d_limbs, int C, int L, const int16_t* 
     if ((r = modular_stage(d_limbs, C, L, d_degs, h_degs, m, n, dfx, dgx, ce->d_primes, primes, gens, K, N,
                            d_coeffs, d_status, st, &ce->t)))
       return r;
-    launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
+    g.launches += launch_crt(ce->t, d_coeffs, N, d_out, d_crtS, st, true);
     stage_mark(st);
-    g.launches += 2;
     CK(cudaGetLastError());
     return 0;
   });
@@ -1748,9 +1743,9 @@ int ckb_descartes_variations_batch(int handle, const uint32_t* aw, int AL, const
   uint32_t* d_dscr = nullptr;
   if (pl.direct && (rc = dbuf("desc.direct", desc_direct_scratch_words(K, d.n, B), &d_dscr))) return rc;
   launch_desc_shift(d.d_primes, pl, d.d_res, d_aw, AL, d_ld, B, d_c, d_dscr, st);
-  launch_crt(ce->t, d_c, (int)NB, d_out, d_crtS, st);
+  g.launches += launch_crt(ce->t, d_c, (int)NB, d_out, d_crtS, st);
   launch_desc_signs(d_out, N, LW, B, d_v, st);
-  g.launches += 5;
+  g.launches += pl.direct ? 4 : 2;  // the shift (3 direct kernels or 1), the sign count
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(variations, d_v, 4 * (size_t)B, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
