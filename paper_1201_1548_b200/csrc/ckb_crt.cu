@@ -232,184 +232,8 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uns
   }
 }
 
-// ---------------------------------------------------------------------------
-// Small lifts in ONE launch (few coefficients: cfg2, cfg3, a shard's block at
-// 4-8 GPUs, where the tensor-core GEMM + carry pair costs ~15-20 us of launch
-// and pipeline latency for a microsecond of work): one CTA per coefficient,
-// its warps splitting the primes.  X = sum_i y_i (M/p_i) is accumulated per
-// 32-bit limb as two 64-bit sums over the 16-bit halves of M/p_i (products
-// < 2^46, sums < 2^59 for K < 8192), warp 0 folds the partial sums, forms
-// q = round(sum_i y_i / p_i) and runs the same signed carry chain as
-// k_crt_carry on the 128-bit limb values (LW <= 256: one 8-limb block per lane).
-// ---------------------------------------------------------------------------
-constexpr int CRT_SMALL_WARPS = 4;
-__global__ void __launch_bounds__(32 * CRT_SMALL_WARPS) k_crt_small(CrtTables T, int N,
-                                                                    const uint32_t* __restrict__ src, int input_is_y,
-                                                                    uint32_t* __restrict__ out) {
-  __shared__ unsigned long long sa[CRT_SMALL_WARPS][256], sb[CRT_SMALL_WARPS][256];
-  __shared__ double sq[CRT_SMALL_WARPS];
-  const int k = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = T.K, LW = T.LW, KC = (K + 31) / 32;
-  const int l0 = lane * 8;
-  pdl_wait();
-  unsigned long long A[8], B[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) A[j] = B[j] = 0ull;
-  double qs = 0.0;
-  for (int i = warp; i < K; i += CRT_SMALL_WARPS) {
-    uint32_t yi;
-    if (input_is_y) {
-      yi = src[crt_a_word(i, k, KC)];
-    } else {
-      const uint32_t p = T.p[i];
-      yi = red1(shoup_lazy(src[(size_t)i * N + k], T.c[i], T.cc[i], p), p);
-    }
-    qs = fma((double)yi, T.pinvd[i], qs);  // every lane the same value
-    const uint32_t* row = T.Mi + (size_t)i * LW;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (l0 + j < LW) {
-        const uint32_t m = row[l0 + j];
-        A[j] += (unsigned long long)yi * (m & 0xffffu);
-        B[j] += (unsigned long long)yi * (m >> 16);
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    sa[warp][l0 + j] = A[j];
-    sb[warp][l0 + j] = B[j];
-  }
-  if (lane == 0) sq[warp] = qs;
-  __syncthreads();
-  if (warp != 0) return;
-  qs = 0.0;
-  for (int w = 0; w < CRT_SMALL_WARPS; ++w) qs += sq[w];
-  // the 128-bit limb sums S_l = A_l + B_l 2^16
-  unsigned long long s_lo[8];
-  long long s_hi[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    unsigned long long a = 0, b = 0;
-    for (int w = 0; w < CRT_SMALL_WARPS; ++w) {
-      a += sa[w][l0 + j];
-      b += sb[w][l0 + j];
-    }
-    const unsigned long long lo = a + (b << 16);
-    s_lo[j] = lo;
-    s_hi[j] = (long long)((b >> 48) + (lo < a ? 1ull : 0ull));
-  }
-  const unsigned FULL = 0xffffffffu;
-  const unsigned long long q = (unsigned long long)llrint(qs);
-  const bool ambk = fabs((qs - floor(qs)) - 0.5) < 1e-3;
-  uint32_t* ok = out + (size_t)k * LW;
-  uint32_t o[8];
-  I128 c = {0, 0};
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int l = l0 + j;
-    unsigned long long slo = 0, qm = 0;
-    long long shi = 0;
-    if (l < LW) {
-      slo = s_lo[j];
-      shi = s_hi[j];
-      qm = q * (unsigned long long)T.Ml[l];
-    }
-    I128 t;
-    t.lo = slo - qm;
-    t.hi = shi - (long long)(slo < qm);
-    t = add128(t, c.hi, c.lo);
-    o[j] = (uint32_t)t.lo;
-    c.lo = (t.lo >> 32) | ((unsigned long long)t.hi << 32);
-    c.hi = t.hi >> 32;
-  }
-  // carry-ins along the lanes (the fixed-point scheme of k_crt_carry, one chunk)
-  const unsigned long long seg_lo = (unsigned long long)o[0] | ((unsigned long long)o[1] << 32);
-  bool ones = true, zeros = true;
-#pragma unroll
-  for (int j = 2; j < 8; ++j) {
-    ones &= (o[j] == 0xffffffffu);
-    zeros &= (o[j] == 0u);
-  }
-  long long my_cin = 0;
-  long long co = (long long)c.lo;
-  for (int it = 0; it < 33; ++it) {
-    const long long up = __shfl_up_sync(FULL, co, 1);
-    const long long cin = (lane == 0) ? 0ll : up;
-    const unsigned long long u = seg_lo + (unsigned long long)cin;
-    const long long kappa = (cin >= 0) ? (long long)(u < seg_lo) : -(long long)(u > seg_lo);
-    long long delta = 0;
-    if (kappa == 1 && ones) delta = 1;
-    if (kappa == -1 && zeros) delta = -1;
-    const long long nco = (long long)c.lo + delta;
-    const bool changed = nco != co;
-    co = nco;
-    my_cin = cin;
-    if (!__any_sync(FULL, changed)) break;
-  }
-  {
-    const unsigned long long u = seg_lo + (unsigned long long)my_cin;
-    long long kappa = (my_cin >= 0) ? (long long)(u < seg_lo) : -(long long)(u > seg_lo);
-    o[0] = (uint32_t)u;
-    o[1] = (uint32_t)(u >> 32);
-#pragma unroll
-    for (int j = 2; j < 8; ++j) {
-      const long long v = (long long)o[j] + kappa;
-      o[j] = (uint32_t)v;
-      kappa = v >> 32;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (l0 + j < LW) ok[l0 + j] = o[j];
-  if (ambk) {  // exactness guard, as in k_crt_carry
-    __syncwarp();
-    __threadfence_block();
-    if (lane == 0) {
-      long long br = 0;
-      for (int l = 0; l < LW; ++l) {
-        const long long v = (long long)ok[l] - (long long)T.Mh[l] - (l == 0 ? 1 : 0) + br;
-        br = v >> 32;
-      }
-      const bool x_top_neg = (int32_t)ok[LW - 1] < 0;
-      const bool gt = !x_top_neg && br >= 0;
-      long long cr = 0;
-      for (int l = 0; l < LW; ++l) {
-        const long long v = (long long)ok[l] + (long long)T.Mh[l] + cr;
-        cr = v >> 32;
-      }
-      const bool lt = x_top_neg && cr == 0;
-      if (gt || lt) {
-        long long cc = 0;
-        for (int l = 0; l < LW; ++l) {
-          const long long v = (long long)ok[l] + (gt ? -(long long)T.Ml[l] : (long long)T.Ml[l]) + cc;
-          ok[l] = (uint32_t)v;
-          cc = v >> 32;
-        }
-      }
-    }
-  }
-}
-
-static bool crt_small_wanted(const CrtTables& t, int N) {
-  static int mode = -2;
-  if (mode == -2) {
-    const char* e = getenv("CKB_CRT_SMALL");
-    mode = e ? atoi(e) : -1;
-  }
-  if (t.LW > 256 || mode == 0) return false;
-  if (mode == 1) return true;
-  // the fused kernel's critical path is one CTA's sweep over all primes; below ~one
-  // resident wave of coefficient CTAs it beats the GEMM + carry pair
-  return N <= 1200 && (double)t.K * t.LW <= 60000.0;
-}
-
 int launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
                cudaStream_t st, bool input_is_y) {
-  if (crt_small_wanted(t, N)) {
-    launch_pdl(k_crt_small, dim3(N), dim3(32 * CRT_SMALL_WARPS), 0, st, t, N, coeffs, input_is_y ? 1 : 0, out);
-    return 1;
-  }
   // scratch (cudaMalloc-aligned): S [N][LWp] u64 | y (A layout)
   const int LWp = (t.LW + 31) / 32 * 32;
   unsigned long long* S = reinterpret_cast<unsigned long long*>(scratch);

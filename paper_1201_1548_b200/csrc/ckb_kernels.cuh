@@ -189,7 +189,7 @@ void launch_crt_btable(int K, int LW, const uint32_t* Mi, uint32_t* Bt, cudaStre
 void launch_crt_mma(const CrtTables& t, const uint32_t* y, int N, unsigned long long* S, cudaStream_t st);
 // coeffs [K][N] residues (or, input_is_y, y in the A layout) -> out [N][LW];
 // scratch >= crt_scratch_words
-// returns the number of kernels launched (1: the fused small-N kernel; 2-3: GEMM + carry)
+// returns the number of kernels launched (GEMM + carry, plus the premultiplication unless input_is_y)
 int launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
                 cudaStream_t st, bool input_is_y = false);
 size_t crt_scratch_words(int K, int N, int LW);  // scratch size for launch_crt
