@@ -502,3 +502,18 @@ def test_structured_even_y_inputs(mp, oracle_mod):
     f, g = make_pair("sparse", 0)
     res = mp.biv_resultant(f, g, "y")
     _specialisation_check(mp, oracle_mod, f, g, res, random.Random(40), trials=4)
+
+
+def test_cfg5_full_golden(mp):
+    """cfg5 (d = 64, 256-bit, ~1,100 primes): the whole resultant against the pinned
+    oracle's (tests/golden/make_oracle_golden.py, 30 min on 8 threads): sha256 of
+    repr(R), degree, bit length, and R modulo three 61-bit primes."""
+    from paper_1201_1548_b200.synth import make_pair
+    gold = load_golden("cfg5_full.json.gz")
+    f, g = make_pair("cfg5", 0)
+    got = mp.biv_resultant(f, g, "y")
+    assert len(got) - 1 == gold["degree"] == 4096
+    assert max(abs(c).bit_length() for c in got) == gold["max_bits"]
+    for q, want in gold["mod_fingerprint"].items():
+        assert [c % int(q) for c in got] == want
+    assert hashlib.sha256(repr(got).encode()).hexdigest() == gold["sha256_repr"]
