@@ -48,7 +48,11 @@ constexpr int exact_minb(int maxd) {
   return CKB_IMG_MINB_EX ? CKB_IMG_MINB_EX : maxd <= 24 ? 4 : maxd <= 32 ? 3 : maxd <= 40 ? 4 : maxd <= 48 ? 3 : img_minb(maxd);
 }
 template <int MAXD, int NT = IMG_THREADS, bool ALIGNED = false, int EX = 0>
-__global__ void __launch_bounds__(NT, ALIGNED ? 1 : (EX ? exact_minb(MAXD) : img_minb(MAXD))) k_images(ImageArgs a) {
+#ifndef CKB_ALIGN_MINB_EX
+#define CKB_ALIGN_MINB_EX 1
+#endif
+__global__ void __launch_bounds__(NT, ALIGNED ? ((EX == 1 || EX == 2) ? CKB_ALIGN_MINB_EX : 1)
+                                              : (EX ? exact_minb(MAXD) : img_minb(MAXD))) k_images(ImageArgs a) {
   using LY = ImgLayout<MAXD>;
   constexpr int NCH = LY::NCH, SW = LY::SW;
   extern __shared__ __align__(16) uint32_t sm[];
@@ -487,7 +491,10 @@ static bool images_aligned(int maxd) {
 // the kernel for a bucket: the exactly unrolled chains only up to MAXD 48 (at
 // 56 / 64 they exceed the register file and spill; the run-time exit sweep
 // measured faster there: cfg5 images 10.42 -> 9.97 ms)
-constexpr int EXACT_MAXD = 48;
+#ifndef CKB_EXACT_MAXD
+#define CKB_EXACT_MAXD 48
+#endif
+constexpr int EXACT_MAXD = CKB_EXACT_MAXD;
 template <int D, int NT, bool AL>
 static void (*images_kernel(int ex))(ImageArgs) {
   if (ex == 3) return k_images<D, NT, AL, 3>;
