@@ -19,15 +19,15 @@ count = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 rng = random.Random(seed)
 
 
-def rnd_poly(dy, dx, bits, dens):
+def rnd_poly(dy, dx, bits, dens, ystep=1):
     t = {}
-    for j in range(dy + 1):
+    for j in range(0, dy + 1, ystep):  # ystep > 1: F(x, y^ystep), structured (non-generic) sequences
         for i in range(dx + 1):
             if rng.random() < dens:
                 c = rng.randint(-(2 ** bits), 2 ** bits)
                 if c:
                     t[(i, j)] = c
-    t[(rng.randint(0, dx), dy)] = rng.choice([-1, 1]) * rng.randint(1, 2 ** bits)  # keep deg_y
+    t[(rng.randint(0, dx), dy - dy % ystep)] = rng.choice([-1, 1]) * rng.randint(1, 2 ** bits)  # keep deg_y
     return t
 
 
@@ -39,7 +39,8 @@ for it in range(count):
     dfx, dgx = rng.randint(0, 25), rng.randint(0, 25)
     bits = rng.choice([4, 10, 32, 64, 100, 200])
     dens = rng.choice([0.2, 0.5, 1.0])
-    f, g = rnd_poly(m, dfx, bits, dens), rnd_poly(n, dgx, bits, dens)
+    ystep = rng.choice([1, 1, 1, 2, 3])
+    f, g = rnd_poly(m, dfx, bits, dens, ystep), rnd_poly(n, dgx, bits, dens, ystep)
     var = rng.choice("xy")
     got = mp.biv_resultant(f, g, var)
     want = oracle.biv_resultant(f, g, var)
