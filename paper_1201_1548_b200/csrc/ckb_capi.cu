@@ -207,7 +207,7 @@ int get_crt(const uint32_t* primes, int K, int LW, CrtEntry** out) {
       return 0;
     }
   }
-  if (g.crt.size() >= 8) {  // evict least recently used
+  if (g.crt.size() >= 64) {  // evict least recently used (an entry is ~1-25 MB)
     size_t v = 0;
     for (size_t i = 1; i < g.crt.size(); ++i)
       if (g.crt[i].last_use < g.crt[v].last_use) v = i;
@@ -356,9 +356,15 @@ struct PlanEntry {
   InterpPlan pl;
   void* blob = nullptr;
   void* ab = nullptr;  // tensor-core interpolation matrix (polyphase plans), or nullptr
+  size_t bytes = 0;
   uint64_t last_use = 0;
 };
 std::vector<PlanEntry> g_plans_[kMaxCtx];
+// plans are input independent (like FFT plans) and rebuilt cold in 5-40 ms: a
+// Bisolve-style caller with many distinct (primes, N) keeps up to kPlanMax of
+// them, within kPlanBytes of HBM per device (a cfg4 plan is ~40 MB)
+constexpr size_t kPlanMax = 32;
+constexpr size_t kPlanBytes = (size_t)8 << 30;
 #define g_plans (g_plans_[g_ci])
 
 // Nfull points per prime, polyphase factor S (1 or 8): the interpolation plan
@@ -378,7 +384,12 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
   const uint32_t L = 1u << logL;
   for (int i = 0; i < K; ++i)
     if ((primes[i] - 1) % L) return fail("pipeline primes must be 1 mod the NTT length (use PRIMES30)", -2);
-  if (g_plans.size() >= 4) {
+  auto plan_bytes = [&]() {
+    size_t t = 0;
+    for (auto& e : g_plans) t += e.bytes;
+    return t;
+  };
+  while (!g_plans.empty() && (g_plans.size() >= kPlanMax || plan_bytes() > kPlanBytes)) {
     size_t v = 0;
     for (size_t i = 1; i < g_plans.size(); ++i)
       if (g_plans[i].last_use < g_plans[v].last_use) v = i;
@@ -403,6 +414,7 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
   const size_t words =
       kn * 10 + kn1 * 3 + kh * 4 + kl * 4 + (size_t)K * 5 + (size_t)K * 4 * S + (S > 1 ? 2 * (size_t)S * kn : 0) + 256;
   CK(cudaMalloc(&e.blob, 4 * words));
+  e.bytes = 4 * words;
   uint32_t* b = (uint32_t*)e.blob;
   // every table 16-byte aligned (the interpolation stages them with 16-byte cp.async)
   auto take = [&](size_t n) { uint32_t* r = b; b += (n + 3) & ~(size_t)3; return r; };
@@ -449,6 +461,7 @@ int get_plan(const uint32_t* primes, const uint32_t* gens, int K, int Nfull, int
     const size_t ab = interp_mma_bytes(K, N, &kch, &mt);
     if (S > 1 && !(env && env[0] == '0') && kch <= 16 && ab <= ((size_t)512 << 20)) {
       CK(cudaMalloc(&e.ab, ab));
+      e.bytes += ab;
       pl.Ab = (uint8_t*)e.ab;
       launch_interp_lagrange(d_primes, pl, pl.Ab, g.stream);
     }
@@ -500,7 +513,7 @@ int graphed(const std::vector<uint64_t>& key, cudaStream_t st, F&& body) {
     ge->epoch = g.epoch;
   }
   if (!ge) {
-    if (g_graphs.size() >= 16) {
+    if (g_graphs.size() >= 64) {
       size_t v = 0;
       for (size_t i = 1; i < g_graphs.size(); ++i)
         if (g_graphs[i].last_use < g_graphs[v].last_use) v = i;
