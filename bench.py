@@ -406,6 +406,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     os.environ["CKB_DEVICE"] = str(local)
     sharded = world > 1 or args.sharded  # --sharded: the N > 1 code path on one rank (tests it)
+    if sharded and "RANK" not in os.environ:  # --sharded without torchrun: a one-rank group
+        os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0", "MASTER_ADDR": "127.0.0.1",
+                           "MASTER_PORT": os.environ.get("MASTER_PORT", "29533")})
     if sharded:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
