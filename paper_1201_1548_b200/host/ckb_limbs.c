@@ -15,7 +15,9 @@
  * 30-bit digits (_PyLong_FromDigits copies and normalises them): O(limbs),
  * no per-byte loop (_PyLong_FromByteArray costs ~1 us per 5,000-bit
  * coefficient; this ~0.1 us). */
-static PyObject* limbs_to_long(const uint32_t* c, Py_ssize_t len, digit* dg) {
+/* the magnitude's digits into dg (room for len * 32 / 30 + 2), returns the
+ * normalised digit count; *neg = sign (no Python API: runs without the GIL) */
+static Py_ssize_t limbs_to_digits(const uint32_t* c, Py_ssize_t len, digit* dg, int* negp) {
   const int neg = (int)(c[len - 1] >> 31);
   /* magnitude = (c ^ flip) + carry0, negated on the fly for a negative value */
   const uint32_t flip = neg ? 0xffffffffu : 0u;
@@ -56,8 +58,8 @@ static PyObject* limbs_to_long(const uint32_t* c, Py_ssize_t len, digit* dg) {
   }
   if (bits > 0) dg[nd++] = (digit)(acc & PyLong_MASK);
   while (nd > 0 && dg[nd - 1] == 0) --nd;
-  if (nd == 0) return PyLong_FromLong(0);
-  return (PyObject*)_PyLong_FromDigits(neg, nd, dg);
+  *negp = neg;
+  return nd;
 }
 #endif
 
@@ -77,36 +79,65 @@ static PyObject* limbs_to_ints(PyObject* self, PyObject* args) {
   }
   const uint32_t* w = (const uint32_t*)view.buf;
 #ifdef CKB_FAST_DIGITS
-  digit* dg = (digit*)PyMem_Malloc(sizeof(digit) * (size_t)(lw * 32 / PyLong_SHIFT + 2));
-  if (!dg) {
+  /* pass 1: one int object per coefficient, allocated for the largest digit
+   * count its limbs allow; pass 2 (GIL released): the digits written straight
+   * into the objects (no staging buffer, no copy), then normalised.  The
+   * objects are not visible to Python until the list is returned.  (Worker
+   * threads for pass 2 measured erratic on CPU-quota'd hosts: not used.) */
+  Py_ssize_t* lens = (Py_ssize_t*)PyMem_Malloc(sizeof(Py_ssize_t) * (size_t)(n ? n : 1));
+  if (!lens) {
     Py_DECREF(out);
     PyBuffer_Release(&view);
     return PyErr_NoMemory();
   }
-#endif
   for (Py_ssize_t k = 0; k < n; ++k) {
     const uint32_t* c = w + k * lw;
     Py_ssize_t len = lw;
     const uint32_t ext = (c[lw - 1] >> 31) ? 0xffffffffu : 0u;
-    /* drop limbs that only repeat the sign, keeping the sign bit in the top one */
     while (len > 1 && c[len - 1] == ext && ((c[len - 2] >> 31) ? 0xffffffffu : 0u) == ext) --len;
-#ifdef CKB_FAST_DIGITS
-    PyObject* v = limbs_to_long(c, len, dg);
-#else
-    PyObject* v = _PyLong_FromByteArray((const unsigned char*)c, (size_t)(4 * len), 1, 1);
-#endif
+    lens[k] = len;
+    PyObject* v;
+    if (len == 1 && c[0] == 0u) {
+      v = PyLong_FromLong(0);
+      lens[k] = 0;  /* nothing to fill */
+    } else {
+      v = (PyObject*)_PyLong_New(len * 32 / PyLong_SHIFT + 2);
+    }
     if (!v) {
-#ifdef CKB_FAST_DIGITS
-      PyMem_Free(dg);
-#endif
+      PyMem_Free(lens);
       Py_DECREF(out);
       PyBuffer_Release(&view);
       return NULL;
     }
     PyList_SET_ITEM(out, k, v);
   }
-#ifdef CKB_FAST_DIGITS
-  PyMem_Free(dg);
+  PyObject** items = ((PyListObject*)out)->ob_item;
+  Py_BEGIN_ALLOW_THREADS
+  for (Py_ssize_t k = 0; k < n; ++k) {
+    if (!lens[k]) continue;
+    PyLongObject* v = (PyLongObject*)items[k];
+    int neg = 0;
+    const Py_ssize_t nd = limbs_to_digits(w + k * lw, lens[k], v->long_value.ob_digit, &neg);
+    /* lv_tag = digit count << 3 | sign (0: positive, 1: zero, 2: negative) */
+    v->long_value.lv_tag = nd ? ((uintptr_t)nd << 3) | (neg ? 2u : 0u) : 1u;
+    if (!nd) v->long_value.ob_digit[0] = 0;
+  }
+  Py_END_ALLOW_THREADS
+  PyMem_Free(lens);
+#else
+  for (Py_ssize_t k = 0; k < n; ++k) {
+    const uint32_t* c = w + k * lw;
+    Py_ssize_t len = lw;
+    const uint32_t ext = (c[lw - 1] >> 31) ? 0xffffffffu : 0u;
+    while (len > 1 && c[len - 1] == ext && ((c[len - 2] >> 31) ? 0xffffffffu : 0u) == ext) --len;
+    PyObject* v = _PyLong_FromByteArray((const unsigned char*)c, (size_t)(4 * len), 1, 1);
+    if (!v) {
+      Py_DECREF(out);
+      PyBuffer_Release(&view);
+      return NULL;
+    }
+    PyList_SET_ITEM(out, k, v);
+  }
 #endif
   PyBuffer_Release(&view);
   return out;

@@ -267,3 +267,19 @@ def test_host_mod_list_matches_python():
     xs = [rng.randint(-2 ** 6000, 2 ** 6000) for _ in range(300)] + [0, 1, -1, 2 ** 30, -(2 ** 30), 2 ** 64 - 1]
     for p in (2, 3, 7, 1073692673, 2147483647, 4294967291):
         assert mod_list(xs, p) == [x % p for x in xs]
+
+
+def test_host_limbs_to_ints_round_trip():
+    """The output conversion (digits written straight into the int objects):
+    random big ints of both signs and the edge cases of the two's-complement
+    sign handling (0, +-1, +-2^k, -2^k exactly, all-ones limbs)."""
+    import random as _r
+    from paper_1201_1548_b200.planner import ints_to_limbs, limbs_to_ints
+    rng = _r.Random(9)
+    vals = [rng.randint(-2 ** 5400, 2 ** 5400) for _ in range(200)]
+    vals += [0, 1, -1, 2, -2, 2 ** 29, 2 ** 30, -(2 ** 30), 2 ** 31, -(2 ** 31), 2 ** 32 - 1, -(2 ** 32),
+             2 ** 64, -(2 ** 64), (1 << 5000) - 1, -(1 << 5000), -(1 << 5000) + 1, 123456789]
+    limbs, L = ints_to_limbs(vals)
+    assert limbs_to_ints(limbs, len(vals), L) == vals
+    limbs, L = ints_to_limbs(vals, L + 3)  # extra sign-extension limbs
+    assert limbs_to_ints(limbs, len(vals), L) == vals
