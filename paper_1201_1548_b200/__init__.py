@@ -48,6 +48,7 @@ _ORIGINALS = {}
 
 def _bindings():
     """(module, name, replacement) for every rebinding install() makes."""
+    import importlib
     from . import bisolve as our_bisolve
     from . import bivpoly as our_bivpoly
     from . import modpoly as ours
@@ -66,6 +67,13 @@ def _bindings():
             ("curvekit.bisolve", "int_gcd_uni", ours.int_gcd_uni),
             ("curvekit.bisolve", "gcd_biv", our_bivpoly.gcd_biv),
             ("curvekit.bisolve", "biproject", our_bisolve.biproject)]
+    # the other direction: while installed, the engine raises and returns the
+    # reference's own exception and value types (UnluckyPrime, modpoly.py:23-24;
+    # ModPoly :80-93; ResidueSystem :258-261; ModularSubresultantProfile :421-425),
+    # so callers' `except UnluckyPrime` / isinstance / == checks behave as before
+    ref = importlib.import_module("curvekit.modpoly")
+    out += [("paper_1201_1548_b200.modpoly", name, getattr(ref, name))
+            for name in ("UnluckyPrime", "ModPoly", "ResidueSystem", "ModularSubresultantProfile")]
     return out
 
 
