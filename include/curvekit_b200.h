@@ -60,6 +60,10 @@ int ckb_init_devices(int n, const int* devices);
 /* Images of the last res_y pipeline call that left the register kernel for the
  * general warp kernel (non-generic remainder sequences), and all its images. */
 int ckb_last_fallback(unsigned long long* fallback, unsigned long long* images);
+
+/* Diagnostics of the last ckb_biv_resultant call: host microseconds from entry
+ * until the work was enqueued, and waiting for it to finish (us[0], us[1]). */
+int ckb_host_times(float* us, int max);
 int ckb_devices(int* n_contexts, int* nccl);
 
 /* ckb_biv_resultant over the first G contexts (primes sharded, SURVEY §8e

@@ -25,6 +25,7 @@ EXPORTS = (
     "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release", "ckb_biv_gcd_images",
     "ckb_biv_resultant_batch", "ckb_descartes_variations_batch", "ckb_set_graphs",
     "ckb_init_devices", "ckb_devices", "ckb_biv_resultant_multi", "ckb_subres_profile", "ckb_last_fallback",
+    "ckb_host_times",
 )
 
 _P = ctypes.c_void_p
@@ -64,6 +65,7 @@ _SIGS = {
     "ckb_biv_gcd_images": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P]),
     "ckb_init_devices": (_I, [_I, _P]),
     "ckb_last_fallback": (_I, [_P, _P]),
+    "ckb_host_times": (_I, [_P, _I]),
     "ckb_subres_profile": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, _P, _I, _I, _I, ctypes.c_uint32, _P]),
     "ckb_devices": (_I, [_P, _P]),
     "ckb_biv_resultant_multi": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _P, _P]),

@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -83,6 +84,7 @@ struct Ctx {
 // works on context 0 unless the multi-device call has switched g_ci.
 constexpr int kMaxCtx = 8;
 Ctx g_ctxs[kMaxCtx];
+float g_host_times[2] = {0.f, 0.f};
 int g_ci = 0;     // current context
 int g_nctx = 0;   // contexts initialised by ckb_init_devices (1 after ckb_init)
 #define g (g_ctxs[g_ci])
@@ -1002,6 +1004,7 @@ extern "C" {
 int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
                       const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, uint32_t* out,
                       uint32_t* status, float* device_ms) {
+  const auto t0 = std::chrono::steady_clock::now();
   std::lock_guard<std::mutex> lk(g_mu);
   int rc;
   if ((rc = ensure_ready())) return rc;
@@ -1010,7 +1013,11 @@ int ckb_biv_resultant(const uint32_t* limbs, int C, int L, const int16_t* degs, 
   CK(cudaEventRecord(g.ev0, st));
   if ((rc = res_enqueue(limbs, C, L, degs, m, n, dfx, dgx, primes, gens, K, N, LW, out, st, 0, &pd))) return rc;
   CK(cudaEventRecord(g.ev1, st));
+  const auto t1 = std::chrono::steady_clock::now();
   if ((rc = spin_event(g.ev1))) return rc;
+  const auto t2 = std::chrono::steady_clock::now();
+  g_host_times[0] = std::chrono::duration<float, std::micro>(t1 - t0).count();
+  g_host_times[1] = std::chrono::duration<float, std::micro>(t2 - t1).count();
   const uint32_t s = res_finish(pd);
   if (status) *status = s;
   if (device_ms) CK(cudaEventElapsedTime(device_ms, g.ev0, g.ev1));
@@ -1798,6 +1805,14 @@ int ckb_set_graphs(int on) {
   const char* e = getenv("CKB_NO_GRAPHS");
   g.graphs = on != 0 && !(e && e[0] == '1');
   return 0;
+}
+
+int ckb_host_times(float* us, int max) {
+  // diagnostics of the last ckb_biv_resultant call: host microseconds from entry
+  // to the work enqueued (checks, staging, graph launch), and waiting for it
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (int i = 0; i < max && i < 2; ++i) us[i] = g_host_times[i];
+  return 2;
 }
 
 int ckb_set_timing(int on) {
