@@ -71,7 +71,10 @@ def _bindings():
     # reference's own exception and value types (UnluckyPrime, modpoly.py:23-24;
     # ModPoly :80-93; ResidueSystem :258-261; ModularSubresultantProfile :421-425),
     # so callers' `except UnluckyPrime` / isinstance / == checks behave as before
-    ref = importlib.import_module("curvekit.modpoly")
+    try:
+        ref = importlib.import_module("curvekit.modpoly")
+    except ImportError:
+        return out
     out += [("paper_1201_1548_b200.modpoly", name, getattr(ref, name))
             for name in ("UnluckyPrime", "ModPoly", "ResidueSystem", "ModularSubresultantProfile")]
     return out
