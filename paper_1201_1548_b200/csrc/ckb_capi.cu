@@ -655,9 +655,7 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   else
     launch_images(a, st, structured_input(h_degs, m, n));
   stage_mark(st);
-  uint8_t* d_ixb = nullptr;
-  if (pl.Ab && (rc = dbuf("ixb", interp_mma_scratch_bytes(pl), &d_ixb))) return rc;
-  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr, d_ixb);
+  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr);
   stage_mark(st);
   // reduce (+ choose when merged), [choose], images (general: iota + warp kernel), fallback, interpolation
   g.launches += general ? 5 : (merged ? 4 : 5);

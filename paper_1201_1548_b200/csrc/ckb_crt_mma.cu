@@ -244,7 +244,7 @@ void launch_crt_mma(const CrtTables& t, const uint32_t* y, int N, unsigned long 
 // D[(k,a)][(r,b)] = sum_u A_a X_b < M 255^2 < 2^25, recombined mod p in the
 // epilogue.  A is input-independent: built once per plan (bytes in the
 // no-swizzle K-major core-matrix layout, like the CRT tables) and streamed by
-// the bulk-copy engine; X is built per call by k_interp_xprep.
+// the bulk-copy engine; X is built per call in shared memory by each CTA.
 // ===========================================================================
 namespace {
 constexpr uint32_t IDESC_N32 = (2u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -348,18 +348,6 @@ __device__ __forceinline__ void interp_x_bytes(const Prime& P, int pi, int u, co
 __device__ __forceinline__ uint32_t inv8_mod(const Prime& P) {  // ((p + 1) / 2)^3 = 1/8
   const uint32_t h = (P.p + 1u) >> 1;
   return mul_mod(mul_mod(h, h, P), h, P);
-}
-
-// per call: X bytes (phase separation and weights) for every prime and point
-// (standalone form; k_interp_mma builds them in shared memory itself)
-__global__ void k_interp_xprep(const Prime* __restrict__ primes, InterpPlan plan, const uint32_t* __restrict__ values,
-                               const uint32_t* __restrict__ cval, int KCH, uint8_t* __restrict__ Bb) {
-  const int pi = blockIdx.y, u = blockIdx.x * blockDim.x + threadIdx.x, M = plan.N, S = plan.S;
-  pdl_wait();  // the images' values
-  if (u >= KCH * 32) return;
-  const Prime P = primes[pi];
-  const uint32_t c = cval[pi];
-  interp_x_bytes(P, pi, u, plan, values, c, c != 1u ? inv_mod(c, P) : 1u, inv8_mod(P), Bb + (size_t)pi * KCH * IB_TILE);
 }
 
 // per call: the product, one CTA per (M-tile of 32 coefficients, prime); the
@@ -474,10 +462,9 @@ void launch_interp_lagrange(const Prime* primes, const InterpPlan& plan, uint8_t
 }
 
 void launch_interp_mma(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
-                       uint32_t* coeffs, uint8_t* Bb, cudaStream_t st, const uint32_t* crt_c) {
+                       uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c) {
   int KCH, MT;
   interp_mma_bytes(plan.K, plan.N, &KCH, &MT);
-  (void)Bb;  // X is built in shared memory by k_interp_mma (k_interp_xprep: the standalone form)
   const size_t smem = (size_t)KCH * (IA_TILE + IB_TILE) + 64;
   static size_t attr = 0;
   if (smem > attr) {

@@ -332,9 +332,9 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
 }
 
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
-                   uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c, const uint32_t* crt_cc, uint8_t* ixb) {
-  if (plan.S > 1 && plan.Ab && ixb) {  // the tensor-core product with the plan's inverse Vandermonde
-    launch_interp_mma(plan, primes, values, cval, coeffs, ixb, st, crt_c);
+                   uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c, const uint32_t* crt_cc) {
+  if (plan.S > 1 && plan.Ab) {  // the tensor-core product with the plan's inverse Vandermonde
+    launch_interp_mma(plan, primes, values, cval, coeffs, st, crt_c);
     return;
   }
   size_t smem = (size_t)plan.L * 4 * 3;  // data + 4 twiddle tables of L/2

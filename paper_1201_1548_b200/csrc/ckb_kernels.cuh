@@ -130,17 +130,16 @@ void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t*
 // values at the planned points -> coeffs [K][Nfull] (canonical residues); with
 // crt_c (polyphase plans only) each prime's row is pre-multiplied by crt_c[i]
 // for the explicit CRT (then launch_crt must be told the input is already y)
-// ixb: per-call scratch of interp_mma_scratch_bytes(plan): with plan.Ab set, the
+// with plan.Ab set (polyphase plans whose inverse Vandermonde fits) the
 // interpolation runs as a tensor-core product (ckb_crt_mma.cu) instead of NTTs
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
                    uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c = nullptr,
-                   const uint32_t* crt_cc = nullptr, uint8_t* ixb = nullptr);
+                   const uint32_t* crt_cc = nullptr);
 // tensor-core interpolation (ckb_crt_mma.cu): plan bytes (KCH K-chunks, MT M-tiles), plan build, per-call launch
 size_t interp_mma_bytes(int K, int M, int* KCH, int* MT);
-inline size_t interp_mma_scratch_bytes(const InterpPlan& pl) { return (size_t)pl.K * ((pl.N + 31) / 32) * 32 * 32; }
 void launch_interp_lagrange(const Prime* primes, const InterpPlan& plan, uint8_t* Ab, cudaStream_t st);
 void launch_interp_mma(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
-                       uint32_t* coeffs, uint8_t* Bb, cudaStream_t st, const uint32_t* crt_c);
+                       uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c);
 
 // ---- K5: explicit CRT + symmetric lift to two's-complement limbs -----------
 struct CrtTables {
