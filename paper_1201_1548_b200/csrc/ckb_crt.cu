@@ -98,13 +98,21 @@ __device__ __forceinline__ I128 add128(I128 a, long long bhi, unsigned long long
 }
 
 // S: the tensor-core limb sums (u64 [N][LWp], ckb_crt_mma.cu); y in the A layout.
+// out may be page-locked host memory (mapped): the limbs then travel to the host
+// as the kernel writes them, each warp store one contiguous 128-byte run.
+// status_src -> status_dst (optional): the pipeline's status word, final once
+// the grids this one waits on have completed.
 __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const unsigned long long* __restrict__ S,
                                                    const uint32_t* __restrict__ y, int LWp,
-                                                   uint32_t* __restrict__ out) {
+                                                   uint32_t* __restrict__ out, const uint32_t* status_src,
+                                                   uint32_t* status_dst) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = blockIdx.x * 4 + warp;
+  __shared__ uint32_t stage[4][256];
+  uint32_t* so = stage[warp];
   // pdl_launch();  (implicit at exit: measured better)
   pdl_wait();
+  if (status_dst && blockIdx.x == 0 && threadIdx.x == 0) *status_dst = *status_src;
   if (k >= N) return;
   const unsigned FULL = 0xffffffffu;
   const int LW = T.LW;
@@ -196,9 +204,14 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uns
         kappa = v >> 32;
       }
     }
+    // through shared memory: lane-contiguous stores instead of a stride of 8 limbs
+#pragma unroll
+    for (int j = 0; j < 8; ++j) so[lane * 8 + j] = o[j];
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (l0 + j < LW) ok[l0 + j] = o[j];
+      if (c0 + j * 32 + lane < LW) ok[c0 + j * 32 + lane] = so[j * 32 + lane];
+    __syncwarp();
     cin_lo = (unsigned long long)run;  // carry out of lane 31 = into the next chunk
   }
   // Exactness guard (never taken when M > 4 bound): fold x into
@@ -233,7 +246,7 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtTables T, int N, const uns
 }
 
 int launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
-               cudaStream_t st, bool input_is_y) {
+               cudaStream_t st, bool input_is_y, const uint32_t* status_src, uint32_t* status_dst) {
   // scratch (cudaMalloc-aligned): S [N][LWp] u64 | y (A layout)
   const int LWp = (t.LW + 31) / 32 * 32;
   unsigned long long* S = reinterpret_cast<unsigned long long*>(scratch);
@@ -244,7 +257,7 @@ int launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out,
     y = yb;
   }
   launch_crt_mma(t, y, N, S, st);
-  launch_pdl(k_crt_carry, dim3((N + 3) / 4), dim3(128), 0, st, t, N, S, y, LWp, out);
+  launch_pdl(k_crt_carry, dim3((N + 3) / 4), dim3(128), 0, st, t, N, S, y, LWp, out, status_src, status_dst);
   return input_is_y ? 2 : 3;
 }
 

@@ -186,11 +186,12 @@ void launch_desc_signs(const uint32_t* limbs, int N, int LW, int B, int32_t* res
 size_t crt_btable_bytes(int K, int LW);
 void launch_crt_btable(int K, int LW, const uint32_t* Mi, uint32_t* Bt, cudaStream_t st);
 void launch_crt_mma(const CrtTables& t, const uint32_t* y, int N, unsigned long long* S, cudaStream_t st);
-// coeffs [K][N] residues (or, input_is_y, y in the A layout) -> out [N][LW];
-// scratch >= crt_scratch_words
+// coeffs [K][N] residues (or, input_is_y, y in the A layout) -> out [N][LW] (device or mapped
+// page-locked host memory); scratch >= crt_scratch_words; status_src -> status_dst when given
 // returns the number of kernels launched (GEMM + carry, plus the premultiplication unless input_is_y)
 int launch_crt(const CrtTables& t, const uint32_t* coeffs, int N, uint32_t* out, uint32_t* scratch,
-                cudaStream_t st, bool input_is_y = false);
+               cudaStream_t st, bool input_is_y = false, const uint32_t* status_src = nullptr,
+               uint32_t* status_dst = nullptr);
 size_t crt_scratch_words(int K, int N, int LW);  // scratch size for launch_crt
 // M/p_i limbs [K][LW] and c_i = (M/p_i)^-1 mod p_i (+ Shoup companions) from M's limbs; bad |= 1 on repeated primes
 void launch_crt_tables(const uint32_t* primes, int K, const uint32_t* M, int LW, uint32_t* Mi, uint32_t* c,
