@@ -13,7 +13,11 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("CKB_LIB") or os.path.join(HERE, "libcurvekit_b200.so")  # CKB_LIB: tuning variants
+# CKB_LIB: tuning / checking variants (a relative path is taken from the repository root, so
+# subprocesses with another working directory load the same library)
+LIB_PATH = os.environ.get("CKB_LIB") or os.path.join(HERE, "libcurvekit_b200.so")
+if not os.path.isabs(LIB_PATH):
+    LIB_PATH = os.path.join(os.path.dirname(HERE), LIB_PATH)
 
 # every symbol include/curvekit_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (

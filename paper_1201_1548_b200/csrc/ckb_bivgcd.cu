@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(32 * BG_WARPS) k_biv_gcd_images(const uint32_t
                                                                   uint32_t* __restrict__ out, int Wo,
                                                                   int32_t* __restrict__ odeg) {
   extern __shared__ uint32_t sm[];
+  CKB_SMEM_POISON(sm);
   const int W = (m > n ? m : n) + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int img = blockIdx.x * BG_WARPS + warp;

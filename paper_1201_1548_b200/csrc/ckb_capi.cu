@@ -112,6 +112,19 @@ struct DescHandle {
 };
 std::vector<DescHandle> g_desc;
 
+// CKB_POISON=1 (checking runs; also disables graphs): every scratch buffer is
+// filled with a poison byte each time a call fetches it (alternating 0xA5 /
+// 0xFF between fetches), so a kernel reading scratch no earlier kernel of the
+// same call wrote changes the result and fails the parity tests
+int poison_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CKB_POISON");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 int dev_buf(const char* name, size_t bytes, void** out) {
   Buf& b = g.dev[g.ns + name];
   if (b.n < bytes) {
@@ -122,6 +135,12 @@ int dev_buf(const char* name, size_t bytes, void** out) {
     size_t want = bytes + bytes / 4 + 256;
     CK(cudaMalloc(&b.p, want));
     b.n = want;
+  }
+  if (poison_mode()) {
+    static unsigned n = 0;
+    CK(cudaStreamSynchronize(g.stream));
+    CK(cudaMemset(b.p, (n++ & 1) ? 0xFF : 0xA5, b.n));
+    CK(cudaDeviceSynchronize());
   }
   *out = b.p;
   return 0;
@@ -684,7 +703,7 @@ int init_ctx(int idx, int device) {
   g.device = device;
   {
     const char* e = getenv("CKB_NO_GRAPHS");
-    g.graphs = !(e && e[0] == '1');
+    g.graphs = !(e && e[0] == '1') && !poison_mode();
     const char* q = getenv("CKB_NO_PDL");
     ckb::g_pdl = !(q && q[0] == '1');
   }
@@ -1833,7 +1852,7 @@ int ckb_host_free(void* p) {
 int ckb_set_graphs(int on) {
   std::lock_guard<std::mutex> lk(g_mu);
   const char* e = getenv("CKB_NO_GRAPHS");
-  g.graphs = on != 0 && !(e && e[0] == '1');
+  g.graphs = on != 0 && !(e && e[0] == '1') && !poison_mode();
   return 0;
 }
 

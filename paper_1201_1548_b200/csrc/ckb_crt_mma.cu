@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_crt_mma(int N, int KC, const uin
                                                         const uint8_t* __restrict__ Bt, int LWp,
                                                         unsigned long long* __restrict__ S) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  CKB_SMEM_POISON(smem);
   uint8_t* sA = smem;                      // [STAGES][CHUNK]
   uint8_t* sB = smem + STAGES * CHUNK;     // [STAGES][CHUNK]
   // full[STAGES], done[STAGES], then `fin` (one phase: every MMA of the tile retired)
@@ -358,6 +359,7 @@ __global__ void __launch_bounds__(128, 1) k_interp_mma(const Prime* __restrict__
                                                        int KCH, int MT, const uint32_t* __restrict__ cval,
                                                        uint32_t* __restrict__ coeffs, const uint32_t* __restrict__ crt_c) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  CKB_SMEM_POISON(smem);
   uint8_t* sA = smem;                        // [KCH][16 KB]
   uint8_t* sB = smem + (size_t)KCH * IA_TILE;  // [KCH][4 KB]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)KCH * IB_TILE);

@@ -51,6 +51,7 @@ __device__ void desc_scan_mul(uint32_t* buf, int n, const Prime& P, uint32_t* sh
 __global__ void __launch_bounds__(DT) k_desc_plan(const Prime* __restrict__ primes, const uint32_t* __restrict__ gens,
                                                   DescPlan pl) {
   extern __shared__ uint32_t sm[];  // [L] work, [DT] scan scratch
+  CKB_SMEM_POISON(sm);
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, n = pl.n, L = pl.L, half = L >> 1;
   // direct mode (degrees beyond the NTT): the scans run in a global slice
   uint32_t* buf = pl.direct ? pl.Vf + (size_t)pi * (n + 1) : sm;
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(DT) k_desc_shift(const Prime* __restrict__ pri
                                                    int AL, const int32_t* __restrict__ lds,
                                                    uint32_t* __restrict__ outs) {
   extern __shared__ uint32_t sm[];  // X [L], Y [L], (TWS) twiddles 4 x [L/2]
+  CKB_SMEM_POISON(sm);
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x, n = pl.n, L = pl.L, half = L >> 1;
   const int b = blockIdx.y, B = gridDim.y;
   const uint32_t* aw = aws + (size_t)b * 2 * AL;

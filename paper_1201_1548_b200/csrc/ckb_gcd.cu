@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(GCD_THREADS) k_gcd_mod(const uint32_t* __restr
                                                          const int32_t* __restrict__ pidx, uint32_t* __restrict__ out,
                                                          int Wo, int32_t* __restrict__ odeg, uint32_t* __restrict__ gs) {
   extern __shared__ uint32_t sm_[];
+  CKB_SMEM_POISON(sm_);
   __shared__ int s_da, s_db, s_swap;
   __shared__ uint32_t s_la, s_lb;
   const int b = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(INTERP_THREADS) k_interp_points(const uint32_t
                                                                uint32_t* __restrict__ out, uint32_t* __restrict__ gs,
                                                                int xstride) {
   extern __shared__ uint32_t sm_[];
+  CKB_SMEM_POISON(sm_);
   __shared__ InterpShared S;
   const int b = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const int n = ns[b];

@@ -68,6 +68,7 @@ __device__ uint32_t warp_resultant(uint32_t* a, int la, uint32_t* b, int lb, uin
 // recompute the fast kernel's failed images
 __global__ void k_images_fallback(ImageArgs a, int W) {
   extern __shared__ uint32_t sm[];
+  CKB_SMEM_POISON(sm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint32_t* fa = sm + (size_t)warp * 3 * W;  // one warp per failed image
   uint32_t* gb = fa + W;
@@ -133,6 +134,7 @@ __global__ void k_uni_resultant(const uint32_t* __restrict__ fa, const int32_t* 
                                 const Prime* __restrict__ primes, const int32_t* __restrict__ pidx,
                                 uint32_t* __restrict__ out, uint32_t* __restrict__ gs) {
   extern __shared__ uint32_t sm[];
+  CKB_SMEM_POISON(sm);
   const int b = blockIdx.x, lane = threadIdx.x;
   // operands in shared memory, or (degrees beyond it) in a global scratch slice per pair
   uint32_t* x = gs ? gs + (size_t)b * 3 * W : sm;

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(NT, ALIGNED ? ((EX == 1 || EX == 2) ? CKB_ALIG
   using LY = ImgLayout<MAXD>;
   constexpr int NCH = LY::NCH, SW = LY::SW;
   extern __shared__ __align__(16) uint32_t sm[];
+  CKB_SMEM_POISON(sm);
   const bool sw = a.m < a.n;  // reference swaps so that deg a >= deg b
   const int da = sw ? a.n : a.m, db = sw ? a.m : a.n;
   const int16_t* Adeg = a.degs + (sw ? a.m + 1 : 0);

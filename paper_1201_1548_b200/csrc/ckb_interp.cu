@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(NTT_THREADS) k_plan_twiddles(const Prime* __re
 // plan, part 2: DIF transforms of the chirp q^C(m,2) (m < 2N-1) and of M~_{u+1} (u < N)
 __global__ void __launch_bounds__(NTT_THREADS) k_plan_transforms(const Prime* __restrict__ primes, InterpPlan plan) {
   extern __shared__ uint32_t buf[];
+  CKB_SMEM_POISON(buf);
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pi];
   const uint32_t p = P.p;
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(NTT_THREADS) k_interp(InterpPlan plan, const P
                                                         const uint32_t* __restrict__ cval,
                                                         uint32_t* __restrict__ coeffs) {
   extern __shared__ uint32_t buf[];  // [L] data, then 4 x [L/2] twiddle tables
+  CKB_SMEM_POISON(buf);
   const int pi = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pi];
   const uint32_t p = P.p;
@@ -207,6 +209,7 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
                                                               const uint32_t* __restrict__ crt_cc) {
   // shared: [L] data (one pad word per 8, sidx) | W, Wc, Wi, Wic [L/2 each] | Hf, Hfc, Mf, Mfc [L each] | sS, sSc [Mp each]
   extern __shared__ __align__(16) uint32_t buf[];
+  CKB_SMEM_POISON(buf);
   const int S = plan.S;
   const int pi = blockIdx.x / S, r = blockIdx.x % S, tid = threadIdx.x, T = blockDim.x;
   const Prime P = primes[pi];

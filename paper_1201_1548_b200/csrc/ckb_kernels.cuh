@@ -18,6 +18,28 @@ namespace ckb {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 extern bool g_pdl;  // CKB_NO_PDL=1 disables the attribute (A/B measurements)
+
+// Checking builds (-DCKB_POISON_SMEM, tools/build_variants.py; compute-sanitizer is closed on
+// this GPU pool): every kernel with dynamic shared memory first fills all of it with a poison
+// word, so reading a word that no thread and no bulk copy wrote surfaces as a parity failure.
+// The proxy fence orders the poison stores before the CTA's own bulk copies / tensor-core reads.
+#ifdef CKB_POISON_SMEM
+#define CKB_SMEM_POISON(base)                                                                   \
+  do {                                                                                          \
+    uint32_t nb_;                                                                               \
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(nb_));                               \
+    uint32_t* w_ = reinterpret_cast<uint32_t*>(base);                                           \
+    const uint32_t t_ = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);    \
+    const uint32_t nt_ = blockDim.x * blockDim.y * blockDim.z;                                  \
+    for (uint32_t i_ = t_; i_ < nb_ / 4; i_ += nt_) w_[i_] = 0xA5A5A5A5u;                       \
+    __syncthreads();                                                                            \
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");                             \
+  } while (0)
+#else
+#define CKB_SMEM_POISON(base) \
+  do {                        \
+  } while (0)
+#endif
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(32 * PSC_WARPS) k_psc_prs(const uint32_t* __re
                                                            const uint32_t* __restrict__ pts, int npts,
                                                            uint32_t* __restrict__ out, uint8_t* __restrict__ valid) {
   extern __shared__ uint32_t sm[];
+  CKB_SMEM_POISON(sm);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int j = blockIdx.x * PSC_WARPS + w;
   const int stride = 3 * (m + 1) + 2 * (n + 3);
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(1024) k_gcd_chain(const uint32_t* __restrict__
                                                    int W, int n, Prime P, int* __restrict__ chain,
                                                    uint32_t* __restrict__ status) {
   extern __shared__ uint32_t sm[];
+  CKB_SMEM_POISON(sm);
   __shared__ int s_len;
   const int tid = threadIdx.x, T = blockDim.x;
   const uint32_t p = P.p;
