@@ -68,7 +68,7 @@ def build_host(force: bool = False) -> str:
     src = os.path.join(HERE, "host", "ckb_limbs.c")
     dst = os.path.join(HERE, "ckb_limbs" + sysconfig.get_config_var("EXT_SUFFIX"))
     if force or not os.path.exists(dst) or os.path.getmtime(dst) < os.path.getmtime(src):
-        cmd = ["gcc", "-O3", "-shared", "-fPIC", "-I" + sysconfig.get_paths()["include"], src, "-o", dst]
+        cmd = ["gcc", "-O3", "-shared", "-fPIC", "-I" + sysconfig.get_paths()["include"], src, "-o", dst, "-lm"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"host helper build failed:\n{r.stderr}")

@@ -7,7 +7,9 @@
  * part of the compute path.) */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <math.h>
 #include <stdint.h>
+#include <string.h>
 
 #if PY_VERSION_HEX >= 0x030C0000 && PY_VERSION_HEX < 0x030E0000 && PyLong_SHIFT == 30
 #define CKB_FAST_DIGITS 1
@@ -15,48 +17,57 @@
  * 30-bit digits (_PyLong_FromDigits copies and normalises them): O(limbs),
  * no per-byte loop (_PyLong_FromByteArray costs ~1 us per 5,000-bit
  * coefficient; this ~0.1 us). */
+/* digit of the magnitude at bit offset `bit` (bounds-checked) */
+static inline digit digit_at(const uint32_t* a, Py_ssize_t len, Py_ssize_t bit) {
+  const Py_ssize_t w = bit >> 5;
+  const int o = (int)(bit & 31);
+  uint64_t v = (uint64_t)a[w] >> o;
+  if (w + 1 < len) v |= (uint64_t)a[w + 1] << (32 - o);
+  return (digit)(v & PyLong_MASK);
+}
+
 /* the magnitude's digits into dg (room for len * 32 / 30 + 2), returns the
- * normalised digit count; *neg = sign (no Python API: runs without the GIL) */
-static Py_ssize_t limbs_to_digits(const uint32_t* c, Py_ssize_t len, digit* dg, int* negp) {
+ * normalised digit count; *neg = sign; mag: scratch of len + 2 words (no
+ * Python API: runs without the GIL).  Each digit is one unaligned 64-bit load,
+ * a shift and a mask; a negative value's magnitude (~c + 1: zero below the
+ * lowest nonzero limb, its negation there, ~c above -- no carry chain) is
+ * formed in the scratch first. */
+static Py_ssize_t limbs_to_digits(const uint32_t* c, Py_ssize_t len, digit* dg, int* negp, uint32_t* mag) {
   const int neg = (int)(c[len - 1] >> 31);
-  /* magnitude = (c ^ flip) + carry0, negated on the fly for a negative value */
-  const uint32_t flip = neg ? 0xffffffffu : 0u;
-  uint64_t carry = neg ? 1u : 0u;
-  Py_ssize_t nd = 0;
-  Py_ssize_t i = 0;
-  /* 15 limbs = 480 bits = 16 digits: a fixed shift pattern the compiler unrolls */
-  for (; i + 15 <= len; i += 15) {
-    uint32_t s[15];
-#pragma GCC unroll 15
-    for (int k = 0; k < 15; ++k) {
-      const uint64_t v = (uint64_t)(c[i + k] ^ flip) + carry;
-      s[k] = (uint32_t)v;
-      carry = v >> 32;
-    }
-    digit* d = dg + nd;
-#pragma GCC unroll 16
-    for (int t = 0; t < 16; ++t) {
-      const int bit = 30 * t, w = bit >> 5, o = bit & 31;
-      uint64_t v = (uint64_t)s[w] >> o;
-      if (o > 2 && w + 1 < 15) v |= (uint64_t)s[w + 1] << (32 - o);
-      d[t] = (digit)(v & PyLong_MASK);
-    }
-    nd += 16;
+  const uint32_t* src = c;
+  if (neg) {
+    Py_ssize_t f = 0;
+    while (c[f] == 0u) ++f; /* a negative value has a nonzero limb */
+    for (Py_ssize_t k = 0; k < f; ++k) mag[k] = 0u;
+    mag[f] = 0u - c[f];
+    for (Py_ssize_t k = f + 1; k < len; ++k) mag[k] = ~c[k];
+    mag[len] = 0u;
+    mag[len + 1] = 0u;
+    src = mag;
   }
-  uint64_t acc = 0;
-  int bits = 0;
-  for (; i < len; ++i) {
-    const uint64_t v = (uint64_t)(c[i] ^ flip) + carry;
-    carry = v >> 32;
-    acc |= (uint64_t)(uint32_t)v << bits;
-    bits += 32;
-    while (bits >= PyLong_SHIFT) {
-      dg[nd++] = (digit)(acc & PyLong_MASK);
-      acc >>= PyLong_SHIFT;
-      bits -= PyLong_SHIFT;
-    }
+  const Py_ssize_t nd0 = (len * 32 + PyLong_SHIFT - 1) / PyLong_SHIFT;
+  /* digits whose 8-byte window lies inside the limbs (all of them with the padded scratch) */
+  const Py_ssize_t lim = neg ? 4 * len + 8 : 4 * len;
+  const unsigned char* bytes = (const unsigned char*)src;
+  /* four digits = 120 bits = 15 bytes: windows at byte offsets 0, 3, 7, 11 of
+   * each 15-byte group, shifted by 0, 6, 4, 2 bits (PyLong_SHIFT == 30) */
+  Py_ssize_t q = 0;
+  const Py_ssize_t nq = nd0 / 4;
+  for (; q < nq && 15 * q + 11 + 8 <= lim; ++q) {
+    const unsigned char* g = bytes + 15 * q;
+    uint64_t x0, x1, x2, x3;
+    memcpy(&x0, g, 8);
+    memcpy(&x1, g + 3, 8);
+    memcpy(&x2, g + 7, 8);
+    memcpy(&x3, g + 11, 8);
+    digit* d = dg + 4 * q;
+    d[0] = (digit)(x0 & PyLong_MASK);
+    d[1] = (digit)((x1 >> 6) & PyLong_MASK);
+    d[2] = (digit)((x2 >> 4) & PyLong_MASK);
+    d[3] = (digit)((x3 >> 2) & PyLong_MASK);
   }
-  if (bits > 0) dg[nd++] = (digit)(acc & PyLong_MASK);
+  for (Py_ssize_t t = 4 * q; t < nd0; ++t) dg[t] = digit_at(src, len, (Py_ssize_t)PyLong_SHIFT * t);
+  Py_ssize_t nd = nd0;
   while (nd > 0 && dg[nd - 1] == 0) --nd;
   *negp = neg;
   return nd;
@@ -112,17 +123,25 @@ static PyObject* limbs_to_ints(PyObject* self, PyObject* args) {
     PyList_SET_ITEM(out, k, v);
   }
   PyObject** items = ((PyListObject*)out)->ob_item;
+  uint32_t* mag = (uint32_t*)PyMem_RawMalloc(sizeof(uint32_t) * (size_t)(lw + 2));
+  if (!mag) {
+    PyMem_Free(lens);
+    Py_DECREF(out);
+    PyBuffer_Release(&view);
+    return PyErr_NoMemory();
+  }
   Py_BEGIN_ALLOW_THREADS
   for (Py_ssize_t k = 0; k < n; ++k) {
     if (!lens[k]) continue;
     PyLongObject* v = (PyLongObject*)items[k];
     int neg = 0;
-    const Py_ssize_t nd = limbs_to_digits(w + k * lw, lens[k], v->long_value.ob_digit, &neg);
+    const Py_ssize_t nd = limbs_to_digits(w + k * lw, lens[k], v->long_value.ob_digit, &neg, mag);
     /* lv_tag = digit count << 3 | sign (0: positive, 1: zero, 2: negative) */
     v->long_value.lv_tag = nd ? ((uintptr_t)nd << 3) | (neg ? 2u : 0u) : 1u;
     if (!nd) v->long_value.ob_digit[0] = 0;
   }
   Py_END_ALLOW_THREADS
+  PyMem_RawFree(mag);
   PyMem_Free(lens);
 #else
   for (Py_ssize_t k = 0; k < n; ++k) {
@@ -167,35 +186,57 @@ typedef struct {
   int norm_ok;
 } GridSide;
 
-static int key_ij(PyObject* key, int swap, long* i, long* j) {
-  if (!PyTuple_CheckExact(key) || PyTuple_GET_SIZE(key) != 2) return 0;
-  PyObject* a = PyTuple_GET_ITEM(key, 0);
-  PyObject* b = PyTuple_GET_ITEM(key, 1);
-  if (!PyLong_CheckExact(a) || !PyLong_CheckExact(b)) return 0;
-  const long x = PyLong_AsLong(a), y = PyLong_AsLong(b);
-  if ((x == -1 || y == -1) && PyErr_Occurred()) {
+/* one term: borrowed coefficient (the dicts outlive the call), exponents */
+typedef struct {
+  PyObject* v;
+  int32_t i, j;
+} Ent;
+
+/* small non-negative int (an exponent); 0 = not a plain int in range */
+static int small_exp(PyObject* o, long* x) {
+  if (!PyLong_CheckExact(o)) return 0;
+#if PY_VERSION_HEX >= 0x030C0000
+  if (PyUnstable_Long_IsCompact((PyLongObject*)o)) {
+    *x = (long)PyUnstable_Long_CompactValue((PyLongObject*)o);
+    return *x >= 0 && *x <= 1000000;
+  }
+  return 0;
+#else
+  *x = PyLong_AsLong(o);
+  if (*x == -1 && PyErr_Occurred()) {
     PyErr_Clear();
     return 0;
   }
-  if (x < 0 || y < 0 || x > 1000000 || y > 1000000) return 0;
-  *i = swap ? y : x;
-  *j = swap ? x : y;
-  return 1;
+  return *x >= 0 && *x <= 1000000;
+#endif
 }
 
-/* pass 1: shape, degrees, 1-norms and the widest coefficient; 0 = not plain */
-static int scan_side(PyObject* terms, int swap, GridSide* s, size_t* maxbits) {
-  Py_ssize_t pos = 0;
+/* pass 1 (the only walk of the dict): nonzero terms into an array with shape,
+ * degrees, 1-norms and the widest coefficient; 0 = not plain, -1 = no memory */
+static int scan_side(PyObject* terms, int swap, GridSide* s, size_t* maxbits, Ent** ents, Py_ssize_t* nent) {
+  Py_ssize_t pos = 0, n = 0;
   PyObject *k, *v;
   long i, j, maxj = -1, maxi = -1;
   s->td = -1;
+  Ent* e = (Ent*)PyMem_Malloc(sizeof(Ent) * (size_t)(PyDict_GET_SIZE(terms) + 1));
+  if (!e) return -1;
+  *ents = e;
   while (PyDict_Next(terms, &pos, &k, &v)) {
-    if (!PyLong_CheckExact(v) || !key_ij(k, swap, &i, &j)) return 0;
+    if (!PyLong_CheckExact(v) || !PyTuple_CheckExact(k) || PyTuple_GET_SIZE(k) != 2) return 0;
+    long a, b;
+    if (!small_exp(PyTuple_GET_ITEM(k, 0), &a) || !small_exp(PyTuple_GET_ITEM(k, 1), &b)) return 0;
     if (_PyLong_Sign(v) == 0) continue;
+    i = swap ? b : a;
+    j = swap ? a : b;
+    e[n].v = v;
+    e[n].i = (int32_t)i;
+    e[n].j = (int32_t)j;
+    ++n;
     if (j > maxj) maxj = j;
     if (i > maxi) maxi = i;
     if (i + j > s->td) s->td = i + j;
   }
+  *nent = n;
   s->rows = maxj + 1;
   s->dx = maxi < 0 ? 0 : maxi;
   s->deg = (int16_t*)PyMem_Malloc(sizeof(int16_t) * (size_t)(s->rows > 0 ? s->rows : 1));
@@ -203,45 +244,73 @@ static int scan_side(PyObject* terms, int swap, GridSide* s, size_t* maxbits) {
   if (!s->deg || !s->norm) return -1;
   for (Py_ssize_t r = 0; r < s->rows; ++r) s->deg[r] = -1;
   s->norm_ok = 1;
-  pos = 0;
-  while (PyDict_Next(terms, &pos, &k, &v)) {
-    key_ij(k, swap, &i, &j);
-    if (_PyLong_Sign(v) == 0) continue;
-    if (i > s->deg[j]) s->deg[j] = (int16_t)i;
-    const size_t nb = _PyLong_NumBits(v);
+  for (Py_ssize_t t = 0; t < n; ++t) {
+    const int32_t ti = e[t].i, tj = e[t].j;
+    if (ti > s->deg[tj]) s->deg[tj] = (int16_t)ti;
+    const size_t nb = _PyLong_NumBits(e[t].v);
     if (nb > *maxbits) *maxbits = nb;
     if (s->norm_ok) {
-      const double d = PyLong_AsDouble(v);
+      const double d = PyLong_AsDouble(e[t].v);
       if (d == -1.0 && PyErr_Occurred()) {
         PyErr_Clear();
         s->norm_ok = 0;
       } else {
-        s->norm[j] += d < 0 ? -d : d;
+        s->norm[tj] += d < 0 ? -d : d;
       }
     }
   }
   return 1;
 }
 
-/* pass 2: every nonzero coefficient into its grid slot */
-static int write_side(PyObject* terms, int swap, Py_ssize_t dx, Py_ssize_t L, unsigned char* base) {
-  Py_ssize_t pos = 0;
-  PyObject *k, *v;
-  long i, j;
-  while (PyDict_Next(terms, &pos, &k, &v)) {
-    key_ij(k, swap, &i, &j);
-    if (_PyLong_Sign(v) == 0) continue;
-    unsigned char* dst = base + ((size_t)j * (size_t)(dx + 1) + (size_t)i) * (size_t)(4 * L);
-#if PY_VERSION_HEX >= 0x030D0000
-    if (_PyLong_AsByteArray((PyLongObject*)v, dst, (size_t)(4 * L), 1, 1, 1) < 0) return 0;
+/* one coefficient as L two's-complement little-endian u32 limbs (dst zeroed;
+ * the caller sized L for the widest magnitude plus a sign bit) */
+static int put_limbs(PyObject* v, unsigned char* dst, Py_ssize_t L) {
+#ifdef CKB_FAST_DIGITS
+  const uintptr_t tag = ((PyLongObject*)v)->long_value.lv_tag;
+  const Py_ssize_t nd = (Py_ssize_t)(tag >> 3);
+  const int neg = (tag & 3) == 2;
+  const digit* d = ((PyLongObject*)v)->long_value.ob_digit;
+  uint32_t* w = (uint32_t*)dst;
+  uint64_t acc = 0;
+  int bits = 0;
+  Py_ssize_t k = 0;
+  for (Py_ssize_t t = 0; t < nd; ++t) {
+    acc |= (uint64_t)d[t] << bits;
+    bits += PyLong_SHIFT;
+    if (bits >= 32) {
+      if (k < L) w[k] = (uint32_t)acc;
+      ++k;
+      acc >>= 32;
+      bits -= 32;
+    }
+  }
+  if (bits > 0 && k < L) w[k] = (uint32_t)acc;
+  if (neg) { /* two's complement: invert, add one */
+    uint64_t cy = 1;
+    for (Py_ssize_t t = 0; t < L; ++t) {
+      const uint64_t x = (uint64_t)(uint32_t)~w[t] + cy;
+      w[t] = (uint32_t)x;
+      cy = x >> 32;
+    }
+  }
+  return 1;
+#elif PY_VERSION_HEX >= 0x030D0000
+  return _PyLong_AsByteArray((PyLongObject*)v, dst, (size_t)(4 * L), 1, 1, 1) >= 0;
 #else
-    if (_PyLong_AsByteArray((PyLongObject*)v, dst, (size_t)(4 * L), 1, 1) < 0) return 0;
+  return _PyLong_AsByteArray((PyLongObject*)v, dst, (size_t)(4 * L), 1, 1) >= 0;
 #endif
+}
+
+/* pass 2: every nonzero coefficient into its grid slot */
+static int write_side(const Ent* e, Py_ssize_t n, Py_ssize_t dx, Py_ssize_t L, unsigned char* base) {
+  for (Py_ssize_t t = 0; t < n; ++t) {
+    unsigned char* dst = base + ((size_t)e[t].j * (size_t)(dx + 1) + (size_t)e[t].i) * (size_t)(4 * L);
+    if (!put_limbs(e[t].v, dst, L)) return 0;
   }
   return 1;
 }
 
-static PyObject* lead_row(PyObject* terms, int swap, long row, int16_t deg) {
+static PyObject* lead_row(const Ent* e, Py_ssize_t n, long row, int16_t deg) {
   PyObject* out = PyList_New(deg + 1);
   if (!out) return NULL;
   PyObject* zero = PyLong_FromLong(0);
@@ -250,14 +319,10 @@ static PyObject* lead_row(PyObject* terms, int swap, long row, int16_t deg) {
     PyList_SET_ITEM(out, t, zero);
   }
   Py_DECREF(zero);
-  Py_ssize_t pos = 0;
-  PyObject *k, *v;
-  long i, j;
-  while (PyDict_Next(terms, &pos, &k, &v)) {
-    key_ij(k, swap, &i, &j);
-    if (j != row || _PyLong_Sign(v) == 0) continue;
-    Py_INCREF(v);
-    PyList_SetItem(out, i, v); /* steals v, releases the zero */
+  for (Py_ssize_t t = 0; t < n; ++t) {
+    if (e[t].j != row) continue;
+    Py_INCREF(e[t].v);
+    PyList_SetItem(out, e[t].i, e[t].v); /* steals v, releases the zero */
   }
   return out;
 }
@@ -277,10 +342,12 @@ static PyObject* terms_grid(PyObject* self, PyObject* args) {
   if (!PyArg_ParseTuple(args, "OOp", &tf, &tg, &swap)) return NULL;
   if (!PyDict_CheckExact(tf) || !PyDict_CheckExact(tg)) Py_RETURN_NONE;
   GridSide f = {0}, g = {0};
+  Ent *ef = NULL, *eg = NULL;
+  Py_ssize_t nf = 0, ng = 0;
   size_t maxbits = 0;
   PyObject* ret = NULL;
-  int okf = scan_side(tf, swap, &f, &maxbits);
-  int okg = okf == 1 ? scan_side(tg, swap, &g, &maxbits) : okf;
+  int okf = scan_side(tf, swap, &f, &maxbits, &ef, &nf);
+  int okg = okf == 1 ? scan_side(tg, swap, &g, &maxbits, &eg, &ng) : okf;
   if (okf < 0 || okg < 0) {
     PyErr_NoMemory();
     goto done;
@@ -297,7 +364,7 @@ static PyObject* terms_grid(PyObject* self, PyObject* args) {
     if (!limbs) goto done;
     unsigned char* buf = (unsigned char*)PyBytes_AS_STRING(limbs);
     memset(buf, 0, (size_t)(C * L * 4));
-    if (!write_side(tf, swap, f.dx, L, buf) || !write_side(tg, swap, g.dx, L, buf + (size_t)cf * L * 4)) {
+    if (!write_side(ef, nf, f.dx, L, buf) || !write_side(eg, ng, g.dx, L, buf + (size_t)cf * L * 4)) {
       Py_DECREF(limbs);
       goto done;
     }
@@ -309,8 +376,8 @@ static PyObject* terms_grid(PyObject* self, PyObject* args) {
     memcpy(PyBytes_AS_STRING(degs), f.deg, (size_t)f.rows * 2);
     memcpy(PyBytes_AS_STRING(degs) + f.rows * 2, g.deg, (size_t)g.rows * 2);
     PyObject* norms = norms_list(&f, &g);
-    PyObject* lcf = lead_row(tf, swap, (long)(f.rows - 1), f.deg[f.rows - 1]);
-    PyObject* lcg = lead_row(tg, swap, (long)(g.rows - 1), g.deg[g.rows - 1]);
+    PyObject* lcf = lead_row(ef, nf, (long)(f.rows - 1), f.deg[f.rows - 1]);
+    PyObject* lcg = lead_row(eg, ng, (long)(g.rows - 1), g.deg[g.rows - 1]);
     if (norms && lcf && lcg)
       ret = Py_BuildValue("(NnnnnnllNNNN)", limbs, L, f.rows - 1, g.rows - 1, f.dx, g.dx, f.td, g.td, degs, norms,
                           lcf, lcg);
@@ -323,6 +390,8 @@ static PyObject* terms_grid(PyObject* self, PyObject* args) {
     }
   }
 done:
+  PyMem_Free(ef);
+  PyMem_Free(eg);
   PyMem_Free(f.deg);
   PyMem_Free(f.norm);
   PyMem_Free(g.deg);
@@ -392,7 +461,68 @@ static PyObject* mod_list(PyObject* self, PyObject* args) {
   return out;
 }
 
+/* planner.log2_bound_from_norms in one C pass (host planning of every call):
+ * the reference's column-sum bound, the Hadamard column bound and the row
+ * bound of the Sylvester matrix from the per-row 1-norms (doubles); window
+ * sums taken directly (all terms positive, no prefix-sum cancellation). */
+static PyObject* norms_log2_bound(PyObject* self, PyObject* args) {
+  PyObject *af, *ag;
+  if (!PyArg_ParseTuple(args, "OO", &af, &ag)) return NULL;
+  PyObject* sf = PySequence_Fast(af, "norms_log2_bound: expected sequences of floats");
+  if (!sf) return NULL;
+  PyObject* sg = PySequence_Fast(ag, "norms_log2_bound: expected sequences of floats");
+  if (!sg) {
+    Py_DECREF(sf);
+    return NULL;
+  }
+  const Py_ssize_t lf = PySequence_Fast_GET_SIZE(sf), lg = PySequence_Fast_GET_SIZE(sg);
+  double* v = (double*)PyMem_Malloc(sizeof(double) * (size_t)(lf + lg + 1));
+  PyObject* ret = NULL;
+  if (!v) {
+    PyErr_NoMemory();
+    goto out;
+  }
+  for (Py_ssize_t i = 0; i < lf + lg; ++i) {
+    PyObject* o = i < lf ? PySequence_Fast_GET_ITEM(sf, i) : PySequence_Fast_GET_ITEM(sg, i - lf);
+    v[i] = PyFloat_AsDouble(o);
+    if (v[i] == -1.0 && PyErr_Occurred()) goto out;
+  }
+  {
+    const double* nf = v;
+    const double* ng = v + lf;
+    const Py_ssize_t m = lf - 1, n = lg - 1; /* y-degrees */
+    double ref = 0.0, col = 0.0, sf2 = 0.0, sg2 = 0.0;
+    for (Py_ssize_t i = 0; i <= m; ++i) sf2 += nf[i] * nf[i];
+    for (Py_ssize_t i = 0; i <= n; ++i) sg2 += ng[i] * ng[i];
+    /* column t (0 <= t < m + n): f rows i with t - n < i <= t, g rows with t - m < i <= t */
+    for (Py_ssize_t t = 0; t < m + n; ++t) {
+      double s1 = 0.0, s2 = 0.0;
+      for (Py_ssize_t i = (t - n + 1 > 0 ? t - n + 1 : 0); i <= t && i <= m; ++i) {
+        s1 += nf[i];
+        s2 += nf[i] * nf[i];
+      }
+      for (Py_ssize_t i = (t - m + 1 > 0 ? t - m + 1 : 0); i <= t && i <= n; ++i) {
+        s1 += ng[i];
+        s2 += ng[i] * ng[i];
+      }
+      ref += log2(s1 > 1.0 ? s1 : 1.0);
+      col += 0.5 * log2(s2 > 1.0 ? s2 : 1.0);
+    }
+    const double row = 0.5 * ((double)n * log2(sf2 > 1.0 ? sf2 : 1.0) + (double)m * log2(sg2 > 1.0 ? sg2 : 1.0));
+    double b = ref < row ? ref : row;
+    if (col < b) b = col;
+    ret = PyFloat_FromDouble(b);
+  }
+out:
+  PyMem_Free(v);
+  Py_DECREF(sf);
+  Py_DECREF(sg);
+  return ret;
+}
+
 static PyMethodDef methods[] = {
+    {"norms_log2_bound", norms_log2_bound, METH_VARARGS,
+     "(norms_f, norms_g) -> log2 of the Sylvester coefficient bound from the per-row 1-norms"},
     {"mod_list", mod_list, METH_VARARGS, "(ints, p) -> [c mod p for c in ints] (canonical residues)"},
     {"limbs_to_ints", limbs_to_ints, METH_VARARGS, "[N][LW] two's-complement u32 limbs -> list of ints"},
     {"terms_grid", terms_grid, METH_VARARGS,

@@ -110,6 +110,8 @@ def log2_bound_from_norms(nf, ng) -> float:
     directly (all terms positive: relative error <= (m + n) eps, no prefix-sum
     cancellation), so the result is within ~1e-12 bits of the exact one, far
     inside the planner's one-bit margin."""
+    if _ckb_limbs is not None and hasattr(_ckb_limbs, "norms_log2_bound"):
+        return _ckb_limbs.norms_log2_bound(nf, ng)  # the same sums in one C pass
     nf = np.asarray(nf, dtype=np.float64)
     ng = np.asarray(ng, dtype=np.float64)
     m, n = len(nf) - 1, len(ng) - 1
@@ -127,6 +129,12 @@ def choose_primes_log2(bound_log2: float, lcf, lcg, start: int = 0, table=PRIMES
     A prime annihilates a leading y-coefficient polynomial (modpoly.py:378-379)
     iff it divides the gcd of that polynomial's coefficients, so the scan tests
     two integers per prime (none at all when both gcds are 1, the usual case)."""
+    primes, gens, _ = _choose_primes(bound_log2, lcf, lcg, start, table)
+    return primes.tolist(), gens.tolist()
+
+
+def _choose_primes(bound_log2: float, lcf, lcg, start: int = 0, table=PRIMES30):
+    """choose_primes_log2 as (uint32 primes, uint32 generators, log2 of their product)."""
     from math import gcd
     target = bound_log2 + 3.0
     gf, gg = gcd(*lcf), gcd(*lcg)
@@ -139,7 +147,7 @@ def choose_primes_log2(bound_log2: float, lcf, lcg, start: int = 0, table=PRIMES
                                               | (_mod_many(gg, parr[start:k]) == 0)).any()):
         if k > len(table):
             raise ArithmeticError("prime table exhausted in resultant computation")
-        return parr[start:k].tolist(), garr[start:k].tolist()
+        return parr[start:k].astype(np.uint32), garr[start:k].astype(np.uint32), cum[k] - cum[start]
     primes, gens = [], []
     acc = 0.0
     i = start
@@ -154,7 +162,7 @@ def choose_primes_log2(bound_log2: float, lcf, lcg, start: int = 0, table=PRIMES
         gens.append(g)
         acc += logs[i]
         i += 1
-    return primes, gens
+    return np.array(primes, dtype=np.uint32), np.array(gens, dtype=np.uint32), acc
 
 
 _LOG2 = {}
@@ -267,14 +275,12 @@ def plan_packed(pk: Packed, start: int = 0) -> Plan:
 
 
 def _plan(blog: float, N: int, lcf, lcg, start: int) -> Plan:
-    from math import log2
-    primes, gens = choose_primes_log2(blog, lcf, lcg, start)
+    primes, gens, lsum = _choose_primes(blog, lcf, lcg, start)
     # bit length of the modulus (LW words must hold M): the float sum is within
     # ~1e-12 of log2 M; rounding it up by 1e-6 can only add a spare word
-    mbits = int(sum(log2(p) for p in primes) + 1e-6) + 1
+    mbits = int(lsum + 1e-6) + 1
     LW = (mbits + 31) // 32
-    return Plan(np.array(primes, dtype=np.uint32), np.array(gens, dtype=np.uint32), N, LW,
-                int(blog) + 1, mbits)
+    return Plan(primes, gens, N, LW, int(blog) + 1, mbits)
 
 
 def limbs_to_ints(buf: np.ndarray, N: int, LW: int) -> list:

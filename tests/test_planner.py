@@ -208,6 +208,9 @@ def test_pack_terms_matches_coeffs_path():
     from paper_1201_1548_b200.synth import make_pair
     rng = random.Random(5)
     cases = [make_pair(c, 0) for c in ("cfg1", "cfg2", "cfg4")]
+    # limb-boundary magnitudes (the digit repacking and the sign word): +-2^k, +-(2^k - 1), 2^k + 1
+    edge = [s * (2 ** k + d) for k in (29, 30, 31, 32, 60, 62, 63, 64, 90, 96) for d in (-1, 0, 1) for s in (1, -1)]
+    cases.append(({(i % 5, i // 5): c for i, c in enumerate(edge)}, {(0, 1): 1, (2, 0): -(2 ** 64)}))
     for _ in range(40):
         f, g = {}, {}
         for t in (f, g):
@@ -283,3 +286,19 @@ def test_host_limbs_to_ints_round_trip():
     assert limbs_to_ints(limbs, len(vals), L) == vals
     limbs, L = ints_to_limbs(vals, L + 3)  # extra sign-extension limbs
     assert limbs_to_ints(limbs, len(vals), L) == vals
+
+
+def test_host_limbs_to_ints_every_width():
+    """The grouped digit extraction (four 30-bit digits per 15 bytes, a bounds-checked
+    tail) at every limb count 1..40, values filling the whole width, both signs."""
+    import random as _r
+    from paper_1201_1548_b200 import planner
+    rng = _r.Random(3)
+    for L in range(1, 41):
+        vals = [0, -1, 1, -(1 << (32 * L - 1)), (1 << (32 * L - 1)) - 1]
+        for _ in range(40):
+            b = rng.randint(1, 32 * L - 1)
+            vals.append(rng.randint(-(1 << b) + 1, (1 << b) - 1))
+            vals.append(-(1 << rng.randint(0, 32 * L - 1)))
+        buf, _ = planner.ints_to_limbs(vals, L)
+        assert planner.limbs_to_ints(buf, len(vals), L) == vals, L
