@@ -379,7 +379,7 @@ def run_devices(args, devices):
             "vs_baseline": None, "dtype": "u32 (mod p < 2^30), exact integers", "data": "synthetic",
             "config": dict(cfg, primes=K, points_per_prime=N, out_words=LW, devices=list(devices),
                            parallelism=f"one process, {G} device contexts: primes/{G}, "
-                                       f"{'NCCL' if _lib.uses_nccl() else 'peer-copy'} exchange, CRT coefficients/{G}",
+                                       f"{_lib.last_exchange()} exchange, CRT coefficients/{G}",
                            l2="inputs from page-locked host memory every step (H2D + D2H inside the timed call)"),
             "value_note": "device time per call incl. its H2D/D2H (CUDA events per context, max over contexts)",
             "cold_first_call_ms": t_cold * 1e3, "clocks": clk.summary(), "gpu_launches": launches,

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CKB_ABI_VERSION 5
+#define CKB_ABI_VERSION 6
 #define CKB_STATUS_REPLAN 1 /* a prime had no admissible evaluation points: re-plan without it */
 
 int ckb_abi_version(void);
@@ -66,12 +66,20 @@ int ckb_last_fallback(unsigned long long* fallback, unsigned long long* images);
 int ckb_host_times(float* us, int max);
 int ckb_devices(int* n_contexts, int* nccl);
 
+/* How the last ckb_biv_resultant_multi call exchanged residues: 0 one context,
+ * 1 peer stores from the interpolation epilogue, 2 NCCL send/recv, 3 peer copies. */
+int ckb_last_exchange(void);
+
 /* ckb_biv_resultant over the first G contexts (primes sharded, SURVEY §8e
  * option B): context d runs the modular stages for its contiguous block of
  * K/G primes; one exchange gives every context all K residues of its block of
  * ceil(N/G) coefficients; each lifts its block by CRT and writes its rows of
- * `out`.  Same arguments, result and status as ckb_biv_resultant; device_ms is
- * the maximum over the contexts. */
+ * `out`.  When every context can reach every other's memory (peer access over
+ * NVLink, or contexts sharing a device) the exchange is folded into the
+ * interpolation: its epilogue stores each residue straight into the owning
+ * context's CRT input (CKB_EXCHANGE=nccl / copy: the separate step).  Same
+ * arguments, result and status as ckb_biv_resultant; device_ms is the maximum
+ * over the contexts. */
 int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* degs, int m, int n, int dfx, int dgx,
                             const uint32_t* primes, const uint32_t* gens, int K, int N, int LW, int G, uint32_t* out,
                             uint32_t* status, float* device_ms);

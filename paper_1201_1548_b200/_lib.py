@@ -29,6 +29,7 @@ EXPORTS = (
     "ckb_descartes_prepare", "ckb_descartes_variations", "ckb_descartes_release", "ckb_biv_gcd_images",
     "ckb_biv_resultant_batch", "ckb_descartes_variations_batch", "ckb_set_graphs",
     "ckb_init_devices", "ckb_devices", "ckb_biv_resultant_multi", "ckb_subres_profile", "ckb_last_fallback",
+    "ckb_last_exchange",
     "ckb_host_times",
 )
 
@@ -69,6 +70,7 @@ _SIGS = {
     "ckb_biv_gcd_images": (_I, [_P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P]),
     "ckb_init_devices": (_I, [_I, _P]),
     "ckb_last_fallback": (_I, [_P, _P]),
+    "ckb_last_exchange": (_I, []),
     "ckb_host_times": (_I, [_P, _I]),
     "ckb_subres_profile": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, _P, _I, _I, _I, ctypes.c_uint32, _P]),
     "ckb_devices": (_I, [_P, _P]),
@@ -161,6 +163,11 @@ def last_fallback() -> tuple:
     a, b = ctypes.c_ulonglong(0), ctypes.c_ulonglong(0)
     check(lib().ckb_last_fallback(ctypes.byref(a), ctypes.byref(b)), "ckb_last_fallback")
     return int(a.value), int(b.value)
+
+
+def last_exchange() -> str:
+    """How the last multi-device res_y exchanged residues."""
+    return {0: "none", 1: "peer-store", 2: "nccl", 3: "peer-copy"}.get(int(lib().ckb_last_exchange()), "?")
 
 
 def uses_nccl() -> bool:

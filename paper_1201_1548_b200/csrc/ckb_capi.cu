@@ -610,7 +610,7 @@ bool structured_input(const int16_t* h_degs, int m, int n) {
 int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, const int16_t* h_degs, int m,
                   int n, int dfx, int dgx, const Prime* d_primes, const uint32_t* h_primes, const uint32_t* h_gens,
                   int K, int N, uint32_t* d_coeffs, uint32_t* d_status, cudaStream_t st,
-                  const CrtTables* crt = nullptr) {
+                  const CrtTables* crt = nullptr, const PeerOut* po = nullptr) {
   // with crt: the output rows are the explicit CRT's y = coeff (M/p_i)^-1 mod p_i
   for (int i = 0; i < K; ++i)
     if (h_primes[i] >= (1u << 30)) return fail("pipeline primes must be below 2^30", -2);
@@ -674,7 +674,7 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   else
     launch_images(a, st, structured_input(h_degs, m, n));
   stage_mark(st);
-  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr);
+  launch_interp(pl, d_primes, d_vals, d_cval, d_coeffs, st, crt ? crt->c : nullptr, crt ? crt->cc : nullptr, po);
   stage_mark(st);
   // reduce (+ choose when merged), [choose], images (general: iota + warp kernel), fallback, interpolation
   g.launches += general ? 5 : (merged ? 4 : 5);
@@ -771,9 +771,11 @@ struct Exchange {
   NcclApi api;
   ncclComm_t comms[kMaxCtx] = {};
   int n = 0;
-  cudaEvent_t ready[kMaxCtx] = {};  // phase 1 done on context d (peer-copy exchange)
+  cudaEvent_t ready[kMaxCtx] = {};  // phase 1 done on context d (peer-copy / peer-store exchange)
+  bool peer_all = false;             // every context can store into every other context's memory
 };
 Exchange g_x;
+int g_last_exchange = 0;  // last multi-device call: 0 one context, 1 peer stores, 2 NCCL, 3 peer copies
 
 bool load_nccl(NcclApi& a) {
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
@@ -808,18 +810,25 @@ int setup_exchange(int n, const int* devices) {
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < i; ++j)
       if (devices[i] == devices[j]) distinct = false;
-  if (!distinct) return 0;
-  for (int i = 0; i < n; ++i) {  // NVLink peer access both ways (the peer-copy exchange)
+  // NVLink peer access both ways between distinct devices (the peer-store / peer-copy
+  // exchange); contexts sharing a device reach each other's memory directly
+  g_x.peer_all = true;
+  for (int i = 0; i < n; ++i) {
     CK(cudaSetDevice(devices[i]));
     for (int j = 0; j < n; ++j) {
+      if (devices[i] == devices[j]) continue;
       int can = 0;
-      if (i != j && cudaDeviceCanAccessPeer(&can, devices[i], devices[j]) == cudaSuccess && can) {
+      if (cudaDeviceCanAccessPeer(&can, devices[i], devices[j]) == cudaSuccess && can) {
         const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
         cudaGetLastError();
+      } else {
+        cudaGetLastError();
+        g_x.peer_all = false;
       }
     }
   }
+  if (!distinct) return 0;
   const char* off = getenv("CKB_NO_NCCL");
   if (!(off && off[0] == '1') && load_nccl(g_x.api)) {
     NC(g_x.api.CommInitAll(g_x.comms, n, devices));
@@ -898,6 +907,8 @@ int ckb_shutdown(void) {
   g_nctx = 0;
   return 0;
 }
+
+int ckb_last_exchange(void) { return g_last_exchange; }
 
 int ckb_last_fallback(unsigned long long* fallback, unsigned long long* images) {
   // images of the last pipeline call (context 0) that the register kernel handed
@@ -1179,7 +1190,7 @@ int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* 
     if ((rc = dbuf("m.degs", nd, &v.degs))) return rc;
     if ((rc = dbuf("m.coeffs", (size_t)kd * N, &v.coeffs))) return rc;
     if ((rc = dbuf("m.send", (size_t)kd * N, &v.send))) return rc;
-    if ((rc = dbuf("m.recv", (size_t)K * wd, &v.recv))) return rc;
+    if ((rc = dbuf("m.recv", std::max((size_t)K * wd, crt_a_words(K, wd)), &v.recv))) return rc;
     if ((rc = dbuf("m.out", (size_t)wd * LW, &v.out))) return rc;
     if ((rc = dbuf("m.status", 4, &v.status))) return rc;
     if ((rc = dbuf("m.crtS", crt_scratch_words(K, wd, LW), &v.crtS))) return rc;
@@ -1188,6 +1199,11 @@ int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* 
     InterpPlan pl;
     if ((rc = get_plan(primes + k0[d], gens + k0[d], kd, N, 8, &pl))) return rc;
   }
+  // the exchange: folded into the interpolation's stores when every context can
+  // reach every other's memory (CKB_EXCHANGE=nccl / copy: the separate step)
+  const char* xm = getenv("CKB_EXCHANGE");
+  const bool fused = G > 1 && g_x.peer_all && !(xm && (strcmp(xm, "nccl") == 0 || strcmp(xm, "copy") == 0));
+  g_last_exchange = G < 2 ? 0 : fused ? 1 : g_x.nccl ? 2 : 3;
   // phase 1 (each context's launches replayed as one CUDA graph after the first calls)
   for (int d = 0; d < G; ++d) {
     g_ci = d;
@@ -1202,6 +1218,19 @@ int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* 
     key_push(key, degs, 2 * nd);
     key_push(key, primes + k0[d], 4 * (size_t)kd);
     key_push(key, gens + k0[d], 4 * (size_t)kd);
+    PeerOut po{};
+    CrtTables ct = v.ce->t;  // this context's rows of the CRT premultipliers
+    if (fused) {
+      po.G = G;
+      po.nc = (N + G - 1) / G;
+      po.KC = (K + 31) / 32;
+      po.k0 = k0[d];
+      for (int s2 = 0; s2 < G; ++s2) po.dst[s2] = dv[s2].recv;
+      ct.c += k0[d];
+      ct.cc += k0[d];
+    }
+    key.push_back(fused ? 1u : 0u);
+    for (int s2 = 0; s2 < G && fused; ++s2) key.push_back((uint64_t)po.dst[s2]);
     rc = graphed(key, st, [&]() -> int {
       int r;
       CK(cudaMemcpyAsync(v.limbs, src_limbs, 4 * nl, cudaMemcpyHostToDevice, st));
@@ -1209,8 +1238,9 @@ int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* 
       CK(cudaMemsetAsync(v.status, 0, 4, st));
       g.nsev = 0;
       if ((r = modular_stage(v.limbs, C, L, v.degs, degs, m, n, dfx, dgx, v.primes, primes + k0[d], gens + k0[d], kd,
-                             N, v.coeffs, v.status, st)))
+                             N, v.coeffs, v.status, st, fused ? &ct : nullptr, fused ? &po : nullptr)))
         return r;
+      if (fused) return 0;  // the y values are already in every context's CRT input
       for (int s2 = 0; s2 < G; ++s2) {  // column block s2 -> contiguous [K_d][w_s2] at K_d a_s2
         const int ws = a0[s2 + 1] - a0[s2];
         if (ws > 0)
@@ -1220,10 +1250,17 @@ int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* 
       return 0;
     });
     if (rc) return rc;
-    if (!g_x.nccl) CK(cudaEventRecord(g_x.ready[d], st));
+    if (fused || !g_x.nccl) CK(cudaEventRecord(g_x.ready[d], st));
   }
   // the exchange
-  if (g_x.nccl) {
+  if (fused) {
+    for (int s2 = 0; s2 < G; ++s2) {  // each CRT waits for every context's stores into its input
+      g_ci = s2;
+      CK(cudaSetDevice(g.device));
+      for (int d = 0; d < G; ++d)
+        if (d != s2) CK(cudaStreamWaitEvent(g.stream, g_x.ready[d], 0));
+    }
+  } else if (g_x.nccl) {
     NC(g_x.api.GroupStart());
     for (int d = 0; d < G; ++d) {
       const int kd = k0[d + 1] - k0[d], wd = a0[d + 1] - a0[d];
@@ -1260,11 +1297,11 @@ int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* 
     const int ws = a0[s2 + 1] - a0[s2];
     Dev& v = dv[s2];
     std::vector<uint64_t> key = {6, (uint64_t)G, (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)dst_out,
-                                 (uint64_t)h_status};
+                                 (uint64_t)h_status, fused ? 1u : 0u};
     key_push(key, primes, 4 * (size_t)K);
     rc = graphed(key, st, [&]() -> int {
       if (ws > 0) {
-        g.launches += launch_crt(v.ce->t, v.recv, ws, v.out, v.crtS, st);
+        g.launches += launch_crt(v.ce->t, v.recv, ws, v.out, v.crtS, st, fused);  // fused: input is y already
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(dst_out + (size_t)a0[s2] * LW, v.out, 4 * (size_t)ws * LW, cudaMemcpyDeviceToHost, st));
       }

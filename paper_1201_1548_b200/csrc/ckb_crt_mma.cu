@@ -357,7 +357,8 @@ __global__ void __launch_bounds__(128, 1) k_interp_mma(const Prime* __restrict__
                                                        const uint8_t* __restrict__ Ab,
                                                        const uint32_t* __restrict__ values,
                                                        int KCH, int MT, const uint32_t* __restrict__ cval,
-                                                       uint32_t* __restrict__ coeffs, const uint32_t* __restrict__ crt_c) {
+                                                       uint32_t* __restrict__ coeffs, const uint32_t* __restrict__ crt_c,
+                                                       PeerOut po) {
   extern __shared__ __align__(1024) uint8_t smem[];
   CKB_SMEM_POISON(smem);
   uint8_t* sA = smem;                        // [KCH][16 KB]
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(128, 1) k_interp_mma(const Prime* __restrict__
     if (idx >= Nfull) continue;
     const uint32_t res = shoup(out[r], sc, scc, p);
     if (crt_c)
-      coeffs[crt_a_word(pi, idx, KC)] = res;
+      store_y(coeffs, po, pi, idx, KC, res);  // CRT A layout (peer contexts' inputs with po)
     else
       coeffs[(size_t)pi * Nfull + idx] = res;
   }
@@ -464,7 +465,9 @@ void launch_interp_lagrange(const Prime* primes, const InterpPlan& plan, uint8_t
 }
 
 void launch_interp_mma(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
-                       uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c) {
+                       uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c, const PeerOut* po) {
+  PeerOut pv = po ? *po : PeerOut{};
+  if (!po) pv.G = 0;
   int KCH, MT;
   interp_mma_bytes(plan.K, plan.N, &KCH, &MT);
   const size_t smem = (size_t)KCH * (IA_TILE + IB_TILE) + 64;
@@ -474,7 +477,7 @@ void launch_interp_mma(const InterpPlan& plan, const Prime* primes, const uint32
     attr = smem;
   }
   launch_pdl(k_interp_mma, dim3(MT, plan.K), dim3(128), smem, st, primes, plan, (const uint8_t*)plan.Ab, values,
-             KCH, MT, cval, coeffs, crt_c);
+             KCH, MT, cval, coeffs, crt_c, pv);
 }
 
 }  // namespace ckb

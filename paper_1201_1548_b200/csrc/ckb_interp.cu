@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
                                                               const uint32_t* __restrict__ cval,
                                                               uint32_t* __restrict__ coeffs,
                                                               const uint32_t* __restrict__ crt_c,
-                                                              const uint32_t* __restrict__ crt_cc) {
+                                                              const uint32_t* __restrict__ crt_cc, PeerOut po) {
   // shared: [L] data (one pad word per 8, sidx) | W, Wc, Wi, Wic [L/2 each] | Hf, Hfc, Mf, Mfc [L each] | sS, sSc [Mp each]
   extern __shared__ __align__(16) uint32_t buf[];
   CKB_SMEM_POISON(buf);
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
     uint32_t res = shoup(buf[sidx<true>(M - 1 + k)], fin, finc, p);
     if (c != 1u) res = mul_mod(res, pow_mod(cS, (uint64_t)k, P), P);
     if (crt_c)
-      coeffs[crt_a_word(pi, idx, KC)] = res;  // straight into the CRT GEMM's A layout
+      store_y(coeffs, po, pi, idx, KC, res);  // straight into the CRT GEMM's A layout (peer contexts' with po)
     else
       out[idx] = res;
   }
@@ -335,11 +335,14 @@ __global__ void __launch_bounds__(POLY_THREADS) k_interp_poly(InterpPlan plan, c
 }
 
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
-                   uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c, const uint32_t* crt_cc) {
+                   uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c, const uint32_t* crt_cc,
+                   const PeerOut* po) {
   if (plan.S > 1 && plan.Ab) {  // the tensor-core product with the plan's inverse Vandermonde
-    launch_interp_mma(plan, primes, values, cval, coeffs, st, crt_c);
+    launch_interp_mma(plan, primes, values, cval, coeffs, st, crt_c, po);
     return;
   }
+  PeerOut pv = po ? *po : PeerOut{};
+  if (!po) pv.G = 0;
   size_t smem = (size_t)plan.L * 4 * 3;  // data + 4 twiddle tables of L/2
   if (plan.S == 1) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -364,12 +367,12 @@ void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* 
       if (smem > 48 * 1024)                                                                                   \
         cudaFuncSetAttribute(k_interp_poly<TT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       launch_pdl(k_interp_poly<TT, true>, dim3(plan.K * plan.S), dim3(TT), smem, st, plan, primes, values, cval,  \
-                 coeffs, crt_c, crt_cc);                                                                      \
+                 coeffs, crt_c, crt_cc, pv);                                                                  \
     } else {                                                                                                  \
       if (smem > 48 * 1024)                                                                                   \
         cudaFuncSetAttribute(k_interp_poly<TT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       launch_pdl(k_interp_poly<TT, false>, dim3(plan.K * plan.S), dim3(TT), smem, st, plan, primes, values, cval, \
-                 coeffs, crt_c, crt_cc);                                                                      \
+                 coeffs, crt_c, crt_cc, pv);                                                                  \
     }                                                                                                         \
   }
     POLY_LAUNCH(32) POLY_LAUNCH(64) POLY_LAUNCH(128) POLY_LAUNCH(256)

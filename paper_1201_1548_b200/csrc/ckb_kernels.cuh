@@ -148,20 +148,23 @@ void launch_uni_resultant(const uint32_t* fa, const int32_t* da, const uint32_t*
                           const Prime* primes, const int32_t* pidx, int B, uint32_t* out, uint32_t* gs,
                           cudaStream_t st);  // gs: null = operands in shared memory, else 3 W words per pair
 
+struct PeerOut;  // below (multi-device res_y)
+
 // ---- K4: interpolation at the planned points (modpoly.py:164-185) -----------
 // values at the planned points -> coeffs [K][Nfull] (canonical residues); with
 // crt_c (polyphase plans only) each prime's row is pre-multiplied by crt_c[i]
 // for the explicit CRT (then launch_crt must be told the input is already y)
 // with plan.Ab set (polyphase plans whose inverse Vandermonde fits) the
 // interpolation runs as a tensor-core product (ckb_crt_mma.cu) instead of NTTs
+// (po: the peer stores of PeerOut; requires crt_c)
 void launch_interp(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
                    uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c = nullptr,
-                   const uint32_t* crt_cc = nullptr);
+                   const uint32_t* crt_cc = nullptr, const PeerOut* po = nullptr);
 // tensor-core interpolation (ckb_crt_mma.cu): plan bytes (KCH K-chunks, MT M-tiles), plan build, per-call launch
 size_t interp_mma_bytes(int K, int M, int* KCH, int* MT);
 void launch_interp_lagrange(const Prime* primes, const InterpPlan& plan, uint8_t* Ab, cudaStream_t st);
 void launch_interp_mma(const InterpPlan& plan, const Prime* primes, const uint32_t* values, const uint32_t* cval,
-                       uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c);
+                       uint32_t* coeffs, cudaStream_t st, const uint32_t* crt_c, const PeerOut* po);
 
 // ---- K5: explicit CRT + symmetric lift to two's-complement limbs -----------
 struct CrtTables {
@@ -184,6 +187,30 @@ __host__ __device__ __forceinline__ size_t crt_a_word(int i, int n, int KC) {
   return tile * 4096 + ((n & 127) >> 3) * 256 + ((i & 31) >> 2) * 32 + (n & 7) * 4 + (i & 3);
 }
 inline size_t crt_a_words(int K, int N) { return (size_t)((N + 127) / 128) * ((K + 31) / 32) * 4096; }
+// ---- multi-device res_y: the all-to-all folded into the interpolation -------
+// Context d interpolates its block of primes; coefficient idx belongs to context
+// s = idx / nc, whose CRT needs it from every prime.  With PeerOut set, the
+// interpolation's epilogue stores each y value (already premultiplied for the
+// explicit CRT) straight into context s's CRT input -- in that context's HBM, over
+// NVLink (peer access) when s lives on another GPU -- at its A-layout position
+// (global prime k0 + pi, local coefficient idx - s nc): the exchange step disappears
+// and the transfer overlaps the interpolation tile by tile.
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+  uint32_t* dst[kMaxPeers];  // per destination context: its CRT input, A layout over all K primes
+  int G;                     // destination contexts (0: plain store into coeffs)
+  int nc;                    // coefficients per destination block
+  int KC;                    // (K_total + 31) / 32 of the destination layout
+  int k0;                    // global index of this context's first prime
+};
+__device__ __forceinline__ void store_y(uint32_t* coeffs, const PeerOut& po, int pi, int idx, int KC, uint32_t v) {
+  if (po.G) {
+    const int s = idx / po.nc;
+    po.dst[s][crt_a_word(po.k0 + pi, idx - s * po.nc, po.KC)] = v;
+  } else {
+    coeffs[crt_a_word(pi, idx, KC)] = v;
+  }
+}
 // ---- Descartes sign-variation test (ckb_descartes.cu) -----------------------
 struct DescPlan {
   int K, n, L, logL;       // primes, degree, NTT length >= 2n+1

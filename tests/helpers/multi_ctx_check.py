@@ -47,4 +47,5 @@ for _ in range(3):  # eager, captured, replayed
     got = modpoly.biv_resultant(f, g, "y")
     assert hashlib.sha256(repr(got).encode()).hexdigest() == gold["sha256_repr"]
 report["launches"] = _lib.launch_count() - launches0
+report["exchange"] = _lib.last_exchange()
 print(json.dumps(report))

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version():
     from paper_1201_1548_b200 import _lib
-    assert _lib.load().ckb_abi_version() == 5
+    assert _lib.load().ckb_abi_version() == 6
 
 
 def test_no_cpu_fallback_without_library(tmp_path):

@@ -14,22 +14,30 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("devices", ["0,0", "0,0,0", "0,0,0,0,0,0,0,0"])
-def test_multi_context_resultants_bit_exact(devices):
+@pytest.mark.parametrize("devices,exchange", [("0,0", None), ("0,0,0", None), ("0,0,0,0,0,0,0,0", None),
+                                              ("0,0,0", "copy")])
+def test_multi_context_resultants_bit_exact(devices, exchange):
+    """Default: the exchange folded into the interpolation (every context stores its
+    residues straight into the owning context's CRT input); CKB_EXCHANGE=copy: the
+    separate peer-copy step."""
     env = dict(os.environ, CKB_DEVICES=devices)
     env.pop("CKB_GPUS", None)
+    env.pop("CKB_EXCHANGE", None)
+    if exchange:
+        env["CKB_EXCHANGE"] = exchange
     r = subprocess.run([sys.executable, os.path.join(HERE, "helpers", "multi_ctx_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     rep = json.loads(r.stdout.strip().splitlines()[-1])
     assert rep["contexts"] == len(devices.split(",")) and rep["launches"] > 0
-    assert rep["nccl"] is False  # one physical device: the peer-copy exchange
+    assert rep["nccl"] is False  # one physical device: no NCCL communicators
+    assert rep["exchange"] == ("peer-copy" if exchange == "copy" else "peer-store"), rep
 
 
 def test_multi_abi_declared():
     from paper_1201_1548_b200 import _lib
     lib = _lib.load()
-    for name in ("ckb_init_devices", "ckb_devices", "ckb_biv_resultant_multi"):
+    for name in ("ckb_init_devices", "ckb_devices", "ckb_biv_resultant_multi", "ckb_last_exchange"):
         assert hasattr(lib, name)
 
 
