@@ -71,6 +71,27 @@ def test_random_vs_oracle(mp, oracle_mod):
             assert mp.biv_resultant(f, g, var) == oracle_mod.biv_resultant(f, g, var)
 
 
+def test_wide_coefficients_and_thin_shapes_vs_oracle(mp, oracle_mod):
+    """Coefficients of 600-3,000 bits (more than 16 limbs: the reduction's general limb
+    loop, in K1 and in the point-scale role), pure-y polynomials (x-degree 0), y-degree 1
+    on either side, and very unequal y-degrees, both variables."""
+    rng = random.Random(91)
+    cases = []
+    for bits in (600, 1500, 3000):
+        f = {(i, j): rng.randint(-2 ** bits, 2 ** bits) or 1 for i in range(4) for j in range(4 - i)}
+        g = {(i, j): rng.randint(-2 ** bits, 2 ** bits) or 1 for i in range(3) for j in range(3 - i)}
+        cases.append((f, g))
+    cases.append(({(0, j): rng.randint(-99, 99) or 1 for j in range(7)}, {(2, 1): 5, (0, 0): -3}))   # x-degree 0
+    cases.append(({(1, 1): 7, (3, 0): 2}, {(i, j): rng.randint(-9, 9) or 1 for i in range(5) for j in range(9)}))
+    cases.append(({(i, 1): rng.randint(-2 ** 40, 2 ** 40) or 1 for i in range(12)},
+                  {(0, 1): 1, (5, 0): -(2 ** 70)}))                                                  # m = n = 1
+    cases.append(({(i, j): rng.randint(-2 ** 20, 2 ** 20) or 1 for i in range(3) for j in range(31)},
+                  {(1, 2): 3, (0, 0): 1}))                                                          # 30 vs 2
+    for f, g in cases:
+        for var in ("y", "x"):
+            assert mp.biv_resultant(f, g, var) == oracle_mod.biv_resultant(f, g, var), (len(f), len(g), var)
+
+
 def test_cfg2_golden(mp):
     from paper_1201_1548_b200.synth import make_pair
     gold = load_golden("cfg2_seed0.json.gz")
