@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(128) k_images_fallback_reg(ImageArgs a) {
   }
 }
 
-#define CKB_MAXD_LIST(X) X(4) X(8) X(12) X(16) X(24) X(32) X(40) X(48) X(56) X(64)
+#define CKB_MAXD_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(32) X(40) X(48) X(56) X(64)
 
 static int images_sw(int maxd) {
 #define SWOF(D) \
@@ -541,7 +541,9 @@ void launch_images(const ImageArgs& a, cudaStream_t st, bool structured) {
   // issue at 8 warps/SM); the compact exit sweeps measured faster there (68 -> 62 us)
   if (ex == 1 || ex == 2) {
     const double warps = (double)a.K * a.N / 32.0;
-    if (warps < 2.5 * 148 * 4) ex = 0;
+    // (buckets <= 24 keep it: their chains are short enough for the instruction
+    // cache -- cfg2, bucket 20 at one warp per scheduler: images 23.0 -> 21.2 us)
+    if (warps < 2.5 * 148 * 4 && maxd > 24) ex = 0;
   }
   if (images_aligned(maxd)) {
     constexpr int NTA = 64;
