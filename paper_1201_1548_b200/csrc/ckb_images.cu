@@ -19,6 +19,8 @@
 
 namespace ckb {
 
+static int fallback_warp();
+
 #ifndef CKB_IMG_MINB
 #define CKB_IMG_MINB 1
 #endif
@@ -286,7 +288,10 @@ __global__ void __launch_bounds__(128) k_images_fallback_reg(ImageArgs a) {
   const uint32_t count = *a.fail_count;
   const bool sw = a.m < a.n;
   const int da = sw ? a.n : a.m, db = sw ? a.m : a.n;
-  const int offG = (a.m + 1) * (a.dfx + 1);
+  constexpr int SW = ImgLayout<MAXD>::SW;
+  const int dmax = max(a.dfx, a.dgx);
+  const int rows = POLY * (dmax / POLY + 1);
+  const int TW = 2 * rows * SW;
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += gridDim.x * blockDim.x) {
     const uint32_t flat = a.fail_list[idx];
     const int pi = (int)(flat / (uint32_t)a.N);
@@ -298,23 +303,21 @@ __global__ void __launch_bounds__(128) k_images_fallback_reg(ImageArgs a) {
     uint32_t x = shoup(a.yq[(size_t)pi * a.M + loc / S], om[loc % S], om[S + loc % S], p);  // w^j g^u
     if (c != 1u) x = shoup(x, c, shoup_comp(c, P), p);
     const uint32_t xc = shoup_comp(x, P);
-    const uint32_t* res = a.red + (size_t)pi * a.C;
+    // the residues from K1's tables: TA[e][i] = coefficient of x^e in A's y-coefficient of degree da - i
+    const uint32_t* TA = a.tab + (size_t)pi * TW;
+    const uint32_t* TB = TA + (size_t)rows * SW;
     uint32_t A[MAXD + 1], B[MAXD + 1];
 #pragma unroll
     for (int i = 0; i <= MAXD; ++i) {
       // top-aligned: A[i] = (y-coefficient of degree da - i)(x); f is A unless swapped
       uint32_t va = 0u, vb = 0u;
       if (i <= da) {
-        const int j = da - i;
-        const uint32_t* cf = sw ? res + offG + j * (a.dgx + 1) : res + j * (a.dfx + 1);
-        const int dg = a.degs[sw ? a.m + 1 + j : j];
-        for (int e = dg; e >= 0; --e) va = add_mod(shoup(va, x, xc, p), cf[e], p);
+        const int dg = a.degs[sw ? a.m + 1 + da - i : da - i];
+        for (int e = dg; e >= 0; --e) va = add_mod(shoup(va, x, xc, p), TA[e * SW + i], p);
       }
       if (i <= db) {
-        const int j = db - i;
-        const uint32_t* cg = sw ? res + j * (a.dfx + 1) : res + offG + j * (a.dgx + 1);
-        const int dg = a.degs[sw ? j : a.m + 1 + j];
-        for (int e = dg; e >= 0; --e) vb = add_mod(shoup(vb, x, xc, p), cg[e], p);
+        const int dg = a.degs[sw ? db - i : a.m + 1 + db - i];
+        for (int e = dg; e >= 0; --e) vb = add_mod(shoup(vb, x, xc, p), TB[e * SW + i], p);
       }
       A[i] = va;
       B[i] = vb;
@@ -341,24 +344,28 @@ size_t images_tab_words(int m, int n, int dfx, int dgx) {
   return (size_t)2 * rows * images_sw(maxd);
 }
 
-// K1 for the pipeline, coefficient-major: a thread loads ONE input coefficient's
-// limbs into registers and reduces them modulo a block of RT_PRIMES primes
-// (per-prime constants staged in shared memory), writing each residue to
-// red[pi][c] (coalesced) and to its slot of the images kernel's table layout
-// TA[e][i] / TB[e][i] = coefficient of x^e in the y-coefficient of degree d - i
-// of A / B (A the higher y-degree input).  The padding of the tables is zeroed
-// by a memset first.  (One thread per table entry re-derived the per-prime
-// constants and paid an L2 round trip per entry: 157 us at cfg5.)
+// K1 for the pipeline, table-major: each CTA owns RT_ROWS rows (x-powers e) of
+// one side's table TA[e][i] / TB[e][i] (= coefficient of x^e in the
+// y-coefficient of degree d - i of A / B, A the higher y-degree input) for a
+// block of RT_PRIMES primes (per-prime constants staged in shared memory).  A
+// thread takes one entry (e, i): it gathers that coefficient's limbs (or writes
+// the zero padding) and reduces them modulo every prime of the block, so the
+// table stores are consecutive words across the warp -- no memset, no
+// scattered 4-byte stores (the coefficient-major K1 it replaces issued one L2
+// sector write per residue: 1.04 M sector writes at cfg4, now 0.15 M).
+// red[pi][c] (coefficient order) is written only when k_choose_c or the warp
+// fallback kernel will read it (write_red); the register fallback reads the tables.
 constexpr int RT_PRIMES = 8;
+constexpr int RT_ROWS = 4;
 constexpr int RT_LC_MAX = 256;  // leading-coefficient x-degrees the merged choose role stages
-// Roles by CTA index: the first nred CTAs reduce (coefficient block x prime
+// Roles by CTA index: the first nred CTAs reduce (row block x side x prime
 // block); the K CTAs after them each choose one prime's point scale
 // (choose_c_prime), reducing the two leading coefficients straight from the
 // limbs — so the separate k_choose_c launch disappears from the pipeline.
 template <int LMAX>
 __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__ limbs, int C, int L,
                                                     const Prime* __restrict__ primes, int K, int m, int n, int dfx,
-                                                    int dgx, int rows, int SW, int rt, int cb, int nred,
+                                                    int dgx, int rows, int SW, int nrb, int nred, int write_red,
                                                     uint32_t* __restrict__ red, uint32_t* __restrict__ tab,
                                                     InterpPlan plan, int lcf_off, int lcf_deg, int lcg_off,
                                                     int lcg_deg, uint32_t* __restrict__ cval, uint32_t* status) {
@@ -368,6 +375,10 @@ __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__
   if ((int)blockIdx.x >= nred) {  // choose role
     __shared__ uint32_t lc[2 * RT_LC_MAX];
     const int pi = blockIdx.x - nred;
+#ifdef K1_NOCHOOSE
+    if (threadIdx.x == 0) cval[pi] = 1u;  // timing experiments only (tools/build_variants.py)
+    return;
+#endif
     const Prime P = primes[pi];
     for (int i = threadIdx.x; i <= lcf_deg + 1 + lcg_deg; i += blockDim.x) {
       const int c = i <= lcf_deg ? lcf_off + i : lcg_off + (i - lcf_deg - 1);
@@ -378,47 +389,51 @@ __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__
                    status);
     return;
   }
-  const int c = (blockIdx.x % cb) * blockDim.x + threadIdx.x;
-  const int p0 = (blockIdx.x / cb) * rt, np = min(rt, K - p0);
+  const int rb = blockIdx.x % nrb, side = (blockIdx.x / nrb) & 1, pg = blockIdx.x / (2 * nrb);
+  const int p0 = pg * RT_PRIMES, np = min(RT_PRIMES, K - p0);
   const int TW = 2 * rows * SW;
   if (threadIdx.x < np) {
     const Prime P = primes[p0 + threadIdx.x];
     ps[threadIdx.x] = P;
     kc[threadIdx.x] = limbs_mod_const(L, P);
   }
-  uint32_t w[LMAX > 0 ? LMAX : 1];
-  int entry = 0;
-  bool neg = false;
-  const bool live = c < C;
-  if (live) {
-#pragma unroll
-    for (int l = 0; l < LMAX; ++l) {
-      w[l] = (l < L) ? limbs[(size_t)c * L + l] : 0u;
-      if (l == L - 1) neg = w[l] >> 31;
-    }
-    const int cf = (m + 1) * (dfx + 1);
-    const bool isf = c < cf;
-    const int cc = isf ? c : c - cf, str = isf ? dfx + 1 : dgx + 1;
-    const int j = cc / str, e = cc - j * str;
-    const bool isA = isf != (m < n);  // A = g when swapped (the reference swaps so that deg a >= deg b)
-    entry = (isA ? 0 : rows * SW) + e * SW + ((isf ? m : n) - j);
-  }
+  // side 0 = A: f unless the reference swaps (deg_y g > deg_y f)
+  const bool isf = (side == 0) != (m < n);
+  const int deg = isf ? m : n, dx = isf ? dfx : dgx;
+  const int cbase = isf ? 0 : (m + 1) * (dfx + 1);
   __syncthreads();
-  if (!live) return;
-  for (int q = 0; q < np; ++q) {
-    const uint32_t p = ps[q].p;
-    const LimbModConst k = kc[q];
-    uint32_t r = 0;
-    if (LMAX > 0) {
+  const int e0 = rb * RT_ROWS;
+  uint32_t* tbase = tab + (size_t)side * rows * SW + (size_t)e0 * SW;
+  for (int t = threadIdx.x; t < RT_ROWS * SW; t += blockDim.x) {
+    const int e = e0 + t / SW, i = t - (t / SW) * SW;
+    const bool live = i <= deg && e <= dx;
+    const int c = live ? cbase + (deg - i) * (dx + 1) + e : 0;
+    uint32_t w[LMAX > 0 ? LMAX : 1];
+    bool neg = false;
+    if (LMAX > 0 && live) {
 #pragma unroll
-      for (int l = LMAX - 1; l >= 0; --l)
-        if (l < L) r = add_mod(shoup(r, k.R1, k.R1c, p), mod_word(w[l], k.onec, p), p);
-      if (neg) r = sub_mod(r, k.big, p);
-    } else {  // very wide coefficients: limbs straight from global memory
-      r = limbs_mod(limbs + (size_t)c * L, L, ps[q]);
+      for (int l = 0; l < LMAX; ++l) {
+        w[l] = (l < L) ? limbs[(size_t)c * L + l] : 0u;
+        if (l == L - 1) neg = w[l] >> 31;
+      }
     }
-    red[(size_t)(p0 + q) * C + c] = r;
-    tab[(size_t)(p0 + q) * TW + entry] = r;
+    for (int q = 0; q < np; ++q) {
+      uint32_t r = 0;
+      if (live) {
+        const uint32_t p = ps[q].p;
+        if (LMAX > 0) {
+          const LimbModConst k = kc[q];
+#pragma unroll
+          for (int l = LMAX - 1; l >= 0; --l)
+            if (l < L) r = add_mod(shoup(r, k.R1, k.R1c, p), mod_word(w[l], k.onec, p), p);
+          if (neg) r = sub_mod(r, k.big, p);
+        } else {  // very wide coefficients: limbs straight from global memory
+          r = limbs_mod(limbs + (size_t)c * L, L, ps[q]);
+        }
+        if (write_red) red[(size_t)(p0 + q) * C + c] = r;
+      }
+      tbase[(size_t)(p0 + q) * TW + t] = r;
+    }
   }
 }
 
@@ -429,20 +444,18 @@ void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes,
                        int lcf_deg, int lcg_off, int lcg_deg, uint32_t* cval, uint32_t* status) {
   const int maxd = images_maxd(m, n);
   const int dmax = dfx > dgx ? dfx : dgx;
-  const int rows = POLY * (dmax / POLY + 1);
+  const int rows = POLY * (dmax / POLY + 1);  // a multiple of RT_ROWS
   const int SW = images_sw(maxd);
-  const int TW = 2 * rows * SW;
-  cudaMemsetAsync(tab, 0, (size_t)K * TW * 4, st);
-  // primes per CTA: up to RT_PRIMES, fewer when that would leave the grid under ~2 CTAs per SM
-  const int cb = (C + 127) / 128;
-  const int rt = std::max(1, std::min(RT_PRIMES, cb * K / 296));
-  const int nred = cb * ((K + rt - 1) / rt);
+  const int nrb = rows / RT_ROWS;
+  const int nred = ((K + RT_PRIMES - 1) / RT_PRIMES) * 2 * nrb;
   const int nch = plan ? K : 0;  // + one choose CTA per prime
+  // red: for k_choose_c (no choose role) and the warp fallback kernel (CKB_FALLBACK_WARP=1)
+  const int write_red = (!plan || fallback_warp()) ? 1 : 0;
   InterpPlan pl = plan ? *plan : InterpPlan{};
   const dim3 grid(nred + nch);
-#define RT_LAUNCH(LM)                                                                                             \
-  launch_pdl(k_reduce_tab<LM>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, rt, cb, \
-             nred, red, tab, pl, lcf_off, lcf_deg, lcg_off, lcg_deg, cval, status)
+#define RT_LAUNCH(LM)                                                                                          \
+  launch_pdl(k_reduce_tab<LM>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, nrb, \
+             nred, write_red, red, tab, pl, lcf_off, lcf_deg, lcg_off, lcg_deg, cval, status)
   if (L <= 4)
     RT_LAUNCH(4);
   else if (L <= 8)
@@ -520,13 +533,16 @@ static int images_exact(int maxd, int m, int n) {
 }
 
 // the failed images of the register kernel: thread per image (CKB_FALLBACK_WARP=1: the warp kernel)
-static void launch_fallback_reg(int maxd, const ImageArgs& a, cudaStream_t st) {
+static int fallback_warp() {
   static int warp = -1;
   if (warp < 0) {
     const char* e = getenv("CKB_FALLBACK_WARP");
     warp = e ? atoi(e) : 0;
   }
-  if (warp) return launch_images_fallback(a, st);
+  return warp;
+}
+static void launch_fallback_reg(int maxd, const ImageArgs& a, cudaStream_t st) {
+  if (fallback_warp()) return launch_images_fallback(a, st);
 #define FB(D) \
   if (maxd == D) launch_pdl(k_images_fallback_reg<D>, dim3(2 * 148), dim3(128), 0, st, a);
   CKB_MAXD_LIST(FB)
