@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__
                                                     InterpPlan plan, int lcf_off, int lcf_deg, int lcg_off,
                                                     int lcg_deg, uint32_t* __restrict__ cval, uint32_t* status) {
   __shared__ Prime ps[RT_PRIMES];
-  __shared__ LimbModConst kc[RT_PRIMES];
+  __shared__ LimbModFast kc[RT_PRIMES];
   pdl_wait();
   if ((int)blockIdx.x >= nred) {  // choose role
     __shared__ uint32_t lc[2 * RT_LC_MAX];
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__
   if (threadIdx.x < np) {
     const Prime P = primes[p0 + threadIdx.x];
     ps[threadIdx.x] = P;
-    kc[threadIdx.x] = limbs_mod_const(L, P);
+    kc[threadIdx.x] = limbs_mod_fast_const(L, P);
   }
   // side 0 = A: f unless the reference swaps (deg_y g > deg_y f)
   const bool isf = (side == 0) != (m < n);
@@ -422,10 +422,16 @@ __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__
       if (live) {
         const uint32_t p = ps[q].p;
         if (LMAX > 0) {
-          const LimbModConst k = kc[q];
+          const LimbModFast k = kc[q];
+          constexpr int NB = (LMAX + 2) / 3;  // blocks of three limbs, top block first
 #pragma unroll
-          for (int l = LMAX - 1; l >= 0; --l)
-            if (l < L) r = add_mod(shoup(r, k.R1, k.R1c, p), mod_word(w[l], k.onec, p), p);
+          for (int b = NB - 1; b >= 0; --b) {
+            if (3 * b < L) {
+              const uint32_t v = mod3_fast(w[3 * b], 3 * b + 1 < LMAX ? w[3 * b + 1] : 0u,
+                                           3 * b + 2 < LMAX ? w[3 * b + 2] : 0u, k, p);
+              r = (3 * b + 3 < L) ? add_mod(shoup(r, k.c96, k.c96c, p), v, p) : v;
+            }
+          }
           if (neg) r = sub_mod(r, k.big, p);
         } else {  // very wide coefficients: limbs straight from global memory
           r = limbs_mod(limbs + (size_t)c * L, L, ps[q]);

@@ -112,6 +112,38 @@ __device__ __forceinline__ uint32_t limbs_mod_k(const uint32_t* w, int L, uint32
   return r;
 }
 
+// Faster per-prime form for K1 (p < 2^30): three limbs at a time as ONE 64-bit sum
+// w0 a0 + w1 a1 + w2 a2 (a_l = 2^(32(l+1)) mod p, i.e. 2^(32 l) in Montgomery form,
+// so the sum is < 3 * 2^32 * p) and one Montgomery reduction into (0, 4p) -- about a
+// quarter of the Shoup-Horner instructions per limb; blocks of three limbs are
+// combined by Horner in 2^96.
+struct LimbModFast {
+  uint32_t a0, a1, a2, c96, c96c, big, pinv;
+};
+__device__ __forceinline__ LimbModFast limbs_mod_fast_const(int L, const Prime& P) {
+  LimbModFast k;
+  const uint32_t p = P.p;
+  const uint32_t R1 = redc(P.r2, P), R1c = shoup_comp(R1, P);  // 2^32 mod p
+  k.a0 = R1;
+  k.a1 = shoup(k.a0, R1, R1c, p);
+  k.a2 = shoup(k.a1, R1, R1c, p);
+  k.c96 = k.a2;  // 2^96 mod p
+  k.c96c = shoup_comp(k.c96, P);
+  uint32_t big = 1u % p;
+  for (int l = 0; l < L; ++l) big = shoup(big, R1, R1c, p);
+  k.big = big;  // 2^(32 L) mod p
+  k.pinv = P.pinv;
+  return k;
+}
+__device__ __forceinline__ uint32_t mod3_fast(uint32_t w0, uint32_t w1, uint32_t w2, const LimbModFast& k,
+                                              uint32_t p) {
+  const uint64_t t = (uint64_t)w0 * k.a0 + (uint64_t)w1 * k.a1 + (uint64_t)w2 * k.a2;
+  const uint32_t m = (uint32_t)t * k.pinv;
+  uint32_t u = (uint32_t)(t >> 32) + p - __umulhi(m, p);  // in (0, 4p)
+  u = u >= 2 * p ? u - 2 * p : u;
+  return u >= p ? u - p : u;
+}
+
 // residue mod p of a two's-complement integer of L little-endian 32-bit limbs
 __device__ __forceinline__ uint32_t limbs_mod(const uint32_t* w, int L, const Prime& P) {
   const uint32_t p = P.p;
