@@ -375,10 +375,6 @@ __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__
   if ((int)blockIdx.x >= nred) {  // choose role
     __shared__ uint32_t lc[2 * RT_LC_MAX];
     const int pi = blockIdx.x - nred;
-#ifdef K1_NOCHOOSE
-    if (threadIdx.x == 0) cval[pi] = 1u;  // timing experiments only (tools/build_variants.py)
-    return;
-#endif
     const Prime P = primes[pi];
     for (int i = threadIdx.x; i <= lcf_deg + 1 + lcg_deg; i += blockDim.x) {
       const int c = i <= lcf_deg ? lcf_off + i : lcg_off + (i - lcf_deg - 1);
