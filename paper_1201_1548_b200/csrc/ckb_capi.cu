@@ -751,11 +751,14 @@ void shutdown_ctx() {
 }
 
 // ---- the residue exchange between device contexts --------------
-// Distinct devices: NCCL point-to-point over NVLink (ncclCommInitAll: one
-// communicator per device in this process), loaded with dlopen so the library
-// itself has no NCCL dependency on single-GPU hosts.  Contexts sharing a device
-// (a correctness configuration for one-GPU machines) or a host without NCCL:
-// peer copies ordered by events.
+// Default: folded into the interpolation (PeerOut): every context stores its
+// residues straight into the owning context's CRT input -- over NVLink peer
+// access between distinct devices, plainly when contexts share a device -- and
+// each CRT waits on the other contexts' events.  Without peer access (or with
+// CKB_EXCHANGE=nccl|copy) a separate step: NCCL point-to-point (ncclCommInitAll:
+// one communicator per device in this process, loaded with dlopen so the
+// library has no NCCL dependency on single-GPU hosts) or peer copies ordered by
+// events.
 struct NcclApi {
   void* h = nullptr;
   ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
