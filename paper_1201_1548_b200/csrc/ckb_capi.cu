@@ -1302,9 +1302,28 @@ int ckb_biv_resultant_multi(const uint32_t* limbs, int C, int L, const int16_t* 
     std::vector<uint64_t> key = {6, (uint64_t)G, (uint64_t)K, (uint64_t)N, (uint64_t)LW, (uint64_t)dst_out,
                                  (uint64_t)h_status, fused ? 1u : 0u};
     key_push(key, primes, 4 * (size_t)K);
+    // zero copy as in ckb_biv_resultant: the carry kernel writes this block's rows and the status
+    // word straight into the page-locked destination (blocks <= 4 MB)
+    uint32_t *z_out = nullptr, *z_status = nullptr;
+    if (ws > 0 && zero_copy_on() && 4 * (size_t)ws * LW <= ((size_t)4 << 20)) {
+      void *zo = nullptr, *zs = nullptr;
+      if (cudaHostGetDevicePointer(&zo, dst_out + (size_t)a0[s2] * LW, 0) == cudaSuccess &&
+          cudaHostGetDevicePointer(&zs, h_status + s2, 0) == cudaSuccess) {
+        z_out = (uint32_t*)zo;
+        z_status = (uint32_t*)zs;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    key.push_back(z_out ? 1u : 0u);
     rc = graphed(key, st, [&]() -> int {
+      if (z_out) {  // fused: the input is y already
+        g.launches += launch_crt(v.ce->t, v.recv, ws, z_out, v.crtS, st, fused, v.status, z_status);
+        CK(cudaGetLastError());
+        return 0;
+      }
       if (ws > 0) {
-        g.launches += launch_crt(v.ce->t, v.recv, ws, v.out, v.crtS, st, fused);  // fused: input is y already
+        g.launches += launch_crt(v.ce->t, v.recv, ws, v.out, v.crtS, st, fused);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(dst_out + (size_t)a0[s2] * LW, v.out, 4 * (size_t)ws * LW, cudaMemcpyDeviceToHost, st));
       }
