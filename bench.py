@@ -605,7 +605,7 @@ def run_ours(args):
         e2e = {"value": 1e3 / e_ms, "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(pk.limbs.nbytes + pk.degs.nbytes + 4 * len(p1.gens)),
                "d2h_bytes_per_step": int(hout.nbytes + 4),
-               "path": "ckb_biv_resultant (C-ABI, page-locked host buffers, copies in the timed region)",
+               "path": "ckb_biv_resultant (C-ABI, page-locked host buffers: H2D of the input and the result written into host memory by the CRT carry kernel (zero copy), both inside the timed region)",
                "python_api_ms": 1e3 * statistics.median(pt),
                "python_api_note": "modpoly.biv_resultant incl. packing, planning, int conversion"}
 
