@@ -1,3 +1,4 @@
+# Record of a rejected experiment (profiles/r02/*_rejected.txt): its knob was removed with the code; see git history.
 timeout 900 python -m pytest tests -q -x -m gpu > gpurun_out/crt_t.txt 2>&1; echo suite=$?; tail -1 gpurun_out/crt_t.txt
 CKB_CRT_SMALL=1 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m gpu > gpurun_out/crt_t2.txt 2>&1; echo forced=$?; tail -1 gpurun_out/crt_t2.txt
 for v in 0 -1; do echo "== CKB_CRT_SMALL=$v"; CKB_CRT_SMALL=$v timeout 300 python tools/shard_timing.py --reps 10 2>&1 | sed 's/CRT of all.*stages/stages/';

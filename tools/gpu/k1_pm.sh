@@ -1,3 +1,4 @@
+# Record of a rejected experiment (profiles/r02/*_rejected.txt): its knob was removed with the code; see git history.
 # A/B of the K1 layouts: prime-major table build (default) vs coefficient-major + memset
 set -x
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/k1_suite.txt 2>&1; tail -3 gpurun_out/k1_suite.txt
