@@ -14,17 +14,22 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("devices,exchange", [("0,0", None), ("0,0,0", None), ("0,0,0,0,0,0,0,0", None),
-                                              ("0,0,0", "copy")])
-def test_multi_context_resultants_bit_exact(devices, exchange):
+@pytest.mark.parametrize("devices,exchange,zero_copy", [("0,0", None, True), ("0,0,0", None, True),
+                                                        ("0,0,0,0,0,0,0,0", None, True), ("0,0,0", "copy", True),
+                                                        ("0,0,0,0", None, False)])
+def test_multi_context_resultants_bit_exact(devices, exchange, zero_copy):
     """Default: the exchange folded into the interpolation (every context stores its
-    residues straight into the owning context's CRT input); CKB_EXCHANGE=copy: the
-    separate peer-copy step."""
+    residues straight into the owning context's CRT input) and each context's rows
+    written into the page-locked result by its carry kernel; CKB_EXCHANGE=copy: the
+    separate peer-copy step; CKB_ZERO_COPY=0: D2H copies of the rows."""
     env = dict(os.environ, CKB_DEVICES=devices)
     env.pop("CKB_GPUS", None)
     env.pop("CKB_EXCHANGE", None)
+    env.pop("CKB_ZERO_COPY", None)
     if exchange:
         env["CKB_EXCHANGE"] = exchange
+    if not zero_copy:
+        env["CKB_ZERO_COPY"] = "0"
     r = subprocess.run([sys.executable, os.path.join(HERE, "helpers", "multi_ctx_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
