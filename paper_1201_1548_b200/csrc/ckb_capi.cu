@@ -630,8 +630,7 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
   if ((rc = dbuf("cval", (size_t)K, &d_cval))) return rc;
   uint32_t* d_fail;
   if ((rc = dbuf("fail", (size_t)K * NI + 1, &d_fail))) return rc;
-  // zero the fail counter first so the kernels below run back to back (PDL)
-  if (!general) CK(cudaMemsetAsync(d_fail + (size_t)K * NI, 0, 4, st));
+  // the fail counter is zeroed by K1 (the images kernel runs after K1 completes)
   stage_mark(st);
   const int lcf_off = m * (dfx + 1), lcg_off = (m + 1) * (dfx + 1) + n * (dgx + 1);
   const bool merged = !general && reduce_tab_chooses(h_degs[m], h_degs[m + 1 + n]);
@@ -639,9 +638,10 @@ int modular_stage(const uint32_t* d_limbs, int C, int L, const int16_t* d_degs, 
     launch_reduce(d_limbs, C, L, d_primes, K, d_red, st);
   else if (merged)  // K1 and the point scales in one launch
     launch_reduce_tab(d_limbs, C, L, d_primes, K, m, n, dfx, dgx, d_red, d_tab, st, &pl, lcf_off, h_degs[m],
-                      lcg_off, h_degs[m + 1 + n], d_cval, d_status);
+                      lcg_off, h_degs[m + 1 + n], d_cval, d_status, d_fail + (size_t)K * NI);
   else
-    launch_reduce_tab(d_limbs, C, L, d_primes, K, m, n, dfx, dgx, d_red, d_tab, st);
+    launch_reduce_tab(d_limbs, C, L, d_primes, K, m, n, dfx, dgx, d_red, d_tab, st, nullptr, 0, 0, 0, 0, nullptr,
+                      nullptr, d_fail + (size_t)K * NI);
   stage_mark(st);
   if (!merged)
     launch_choose_c(d_primes, pl, d_red, C, lcf_off, h_degs[m], lcg_off, h_degs[m + 1 + n], d_cval, d_status, st);

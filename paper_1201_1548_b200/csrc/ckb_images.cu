@@ -368,10 +368,13 @@ __global__ void __launch_bounds__(128) k_reduce_tab(const uint32_t* __restrict__
                                                     int dgx, int rows, int SW, int nrb, int nred, int write_red,
                                                     uint32_t* __restrict__ red, uint32_t* __restrict__ tab,
                                                     InterpPlan plan, int lcf_off, int lcf_deg, int lcg_off,
-                                                    int lcg_deg, uint32_t* __restrict__ cval, uint32_t* status) {
+                                                    int lcg_deg, uint32_t* __restrict__ cval, uint32_t* status,
+                                                    uint32_t* zero_word) {
   __shared__ Prime ps[RT_PRIMES];
   __shared__ LimbModFast kc[RT_PRIMES];
   pdl_wait();
+  // the images kernel's fail counter (it runs after this grid completes): no memset node
+  if (zero_word && blockIdx.x == 0 && threadIdx.x == 0) *zero_word = 0u;
   if ((int)blockIdx.x >= nred) {  // choose role
     __shared__ uint32_t lc[2 * RT_LC_MAX];
     const int pi = blockIdx.x - nred;
@@ -443,7 +446,8 @@ bool reduce_tab_chooses(int lcf_deg, int lcg_deg) { return lcf_deg + lcg_deg + 2
 
 void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes, int K, int m, int n, int dfx,
                        int dgx, uint32_t* red, uint32_t* tab, cudaStream_t st, const InterpPlan* plan, int lcf_off,
-                       int lcf_deg, int lcg_off, int lcg_deg, uint32_t* cval, uint32_t* status) {
+                       int lcf_deg, int lcg_off, int lcg_deg, uint32_t* cval, uint32_t* status,
+                       uint32_t* zero_word) {
   const int maxd = images_maxd(m, n);
   const int dmax = dfx > dgx ? dfx : dgx;
   const int rows = POLY * (dmax / POLY + 1);  // a multiple of RT_ROWS
@@ -457,7 +461,7 @@ void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes,
   const dim3 grid(nred + nch);
 #define RT_LAUNCH(LM)                                                                                          \
   launch_pdl(k_reduce_tab<LM>, grid, dim3(128), 0, st, limbs, C, L, primes, K, m, n, dfx, dgx, rows, SW, nrb, \
-             nred, write_red, red, tab, pl, lcf_off, lcf_deg, lcg_off, lcg_deg, cval, status)
+             nred, write_red, red, tab, pl, lcf_off, lcf_deg, lcg_off, lcg_deg, cval, status, zero_word)
   if (L <= 4)
     RT_LAUNCH(4);
   else if (L <= 8)

@@ -137,7 +137,7 @@ bool reduce_tab_chooses(int lcf_deg, int lcg_deg);
 void launch_reduce_tab(const uint32_t* limbs, int C, int L, const Prime* primes, int K, int m, int n, int dfx,
                        int dgx, uint32_t* red, uint32_t* tab, cudaStream_t st, const InterpPlan* plan = nullptr,
                        int lcf_off = 0, int lcf_deg = 0, int lcg_off = 0, int lcg_deg = 0, uint32_t* cval = nullptr,
-                       uint32_t* status = nullptr);
+                       uint32_t* status = nullptr, uint32_t* zero_word = nullptr);  // zero_word: set to 0 by K1
 // fast generic kernel followed by the general warp kernel on its fail list
 void launch_images(const ImageArgs& a, cudaStream_t st, bool structured = false);
 void launch_images_fallback(const ImageArgs& a, cudaStream_t st);
