@@ -302,3 +302,23 @@ def test_host_limbs_to_ints_every_width():
             vals.append(-(1 << rng.randint(0, 32 * L - 1)))
         buf, _ = planner.ints_to_limbs(vals, L)
         assert planner.limbs_to_ints(buf, len(vals), L) == vals, L
+
+
+def test_host_limbs_to_ints_split_path():
+    """Results of >= 1 M limbs are filled by two threads (host/ckb_limbs.c): the same ints
+    as the pure-Python conversion, with both signs and every limb width around the split."""
+    import numpy as np
+    from paper_1201_1548_b200 import planner
+    rng = np.random.default_rng(7)
+    N, LW = 8193, 140
+    buf = rng.integers(0, 2 ** 32, size=N * LW, dtype=np.uint64).astype(np.uint32)
+    buf[5 * LW:6 * LW] = 0                      # zero
+    buf[7 * LW:8 * LW] = 0xFFFFFFFF             # -1
+    got = planner.limbs_to_ints(buf, N, LW)
+    saved = planner._ckb_limbs
+    planner._ckb_limbs = None
+    try:
+        want = planner.limbs_to_ints(buf, N, LW)
+    finally:
+        planner._ckb_limbs = saved
+    assert got == want
