@@ -278,11 +278,23 @@ __device__ __forceinline__ void shift_up(uint32_t (&D)[MAXD + 1]) {
 
 // one pseudo-remainder of the dividend D (deg dd) by V (deg dv >= 1), D <- prem(D, V)
 // by e = dd - dv + 1 single eliminations, then the leading zeros shifted out;
-// returns the remainder's degree (-1: zero remainder)
+// returns the remainder's degree (-1: zero remainder).  An elimination whose
+// quotient term is zero (lc(D) = 0 in every converged lane: the y -> y^2
+// structured inputs have one per remainder) only shifts D instead of scaling it
+// by lb: the remainder is then prem / lb^skip, which the caller's power of lb
+// absorbs (res(V, c R) = c^deg V res(V, R)); *skip counts those steps.
 template <int MAXD>
 __device__ __forceinline__ int prem_any(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int dd, int dv,
-                                        uint32_t lb, uint32_t lbc, const Prime& P) {
-  for (int s = 0; s <= dd - dv; ++s) step1<MAXD>(D, V, dd - s, lb, lbc, P);
+                                        uint32_t lb, uint32_t lbc, const Prime& P, int* skip) {
+  *skip = 0;
+  for (int s = 0; s <= dd - dv; ++s) {
+    if (__all_sync(__activemask(), red4(D[0], P.p) == 0u)) {
+      shift_up<MAXD>(D);
+      ++*skip;
+    } else {
+      step1<MAXD>(D, V, dd - s, lb, lbc, P);
+    }
+  }
   int dr = dv - 1;
   while (dr >= 0 && red4(D[0], P.p) == 0u) {
     shift_up<MAXD>(D);
@@ -310,12 +322,13 @@ __device__ __forceinline__ uint32_t resultant_anydeg(uint32_t (&A)[MAXD + 1], in
     {
       const uint32_t lb = red4(B[0], p);
       const uint32_t lbm = to_mont(lb, P), lbc = comp_from_mont(lbm, P);
+      int skip;
       const int e = da - db + 1;
-      const int dr = prem_any<MAXD>(A, B, da, db, lb, lbc, P);
+      const int dr = prem_any<MAXD>(A, B, da, db, lb, lbc, P, &skip);
       if (dr < 0) return 0u;  // a common factor
       neg ^= (bool)(da & db & 1);
       num = mmul(num, mpow(lbm, da - dr, one, P), P);
-      den = mmul(den, mpow(lbm, e * db, one, P), P);
+      den = mmul(den, mpow(lbm, (e - skip) * db, one, P), P);
       da = dr;
       if (da == 0) {  // res(B, c) = c^db
         num = mmul(num, mpow(to_mont(red4(A[0], p), P), db, one, P), P);
@@ -326,12 +339,13 @@ __device__ __forceinline__ uint32_t resultant_anydeg(uint32_t (&A)[MAXD + 1], in
     {
       const uint32_t lb = red4(A[0], p);
       const uint32_t lbm = to_mont(lb, P), lbc = comp_from_mont(lbm, P);
+      int skip;
       const int e = db - da + 1;
-      const int dr = prem_any<MAXD>(B, A, db, da, lb, lbc, P);
+      const int dr = prem_any<MAXD>(B, A, db, da, lb, lbc, P, &skip);
       if (dr < 0) return 0u;
       neg ^= (bool)(da & db & 1);
       num = mmul(num, mpow(lbm, db - dr, one, P), P);
-      den = mmul(den, mpow(lbm, e * da, one, P), P);
+      den = mmul(den, mpow(lbm, (e - skip) * da, one, P), P);
       db = dr;
       if (db == 0) {
         num = mmul(num, mpow(to_mont(red4(B[0], p), P), da, one, P), P);
