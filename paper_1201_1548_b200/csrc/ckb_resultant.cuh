@@ -287,6 +287,42 @@ template <int MAXD>
 __device__ __forceinline__ int prem_any(uint32_t (&D)[MAXD + 1], const uint32_t (&V)[MAXD + 1], int dd, int dv,
                                         uint32_t lb, uint32_t lbc, const Prime& P, int* skip) {
   *skip = 0;
+  // two-term quotient with a vanishing middle term in every converged lane (degree drop 2 of a
+  // y -> y^2 input): both eliminations fused into one pass of three products per output,
+  //   D'[i] = lb^2 D[i+3] - lb la V[i+3] - l2 V[i+1],  l2 = lb D[2] - la V[2],
+  // the same values as the single steps with the middle one skipped (multipliers in
+  // Montgomery form so mont3 returns them exactly, lazily in (0, 4p))
+  if (dd - dv == 2 && dv >= 1 && MAXD >= 3) {
+    const uint32_t p = P.p;
+    const uint32_t la = red4(D[0], p);
+    const bool mid0 = mul_mod(lb, red4(D[1], p), P) == mul_mod(la, red4(V[1], p), P);
+    if (__all_sync(__activemask(), mid0)) {
+      const uint32_t l2 = sub_mod(mul_mod(lb, red4(D[2], p), P), mul_mod(la, red4(V[2], p), P), p);
+      const uint32_t w1m = to_mont(mul_mod(lb, lb, P), P);
+      const uint32_t w2m = to_mont(neg_mod(mul_mod(lb, la, P), p), P);
+      const uint32_t w3m = to_mont(neg_mod(l2, p), P);
+#pragma unroll
+      for (int c = 0; c < (MAXD + 3) / 4; ++c) {
+        if (4 * c <= dd) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int i = 4 * c + k;
+            if (i < MAXD - 2) D[i] = mont3(D[i + 3], w1m, V[i + 3], w2m, V[i + 1], w3m, P.pinv, p);
+          }
+        }
+      }
+      D[MAXD - 2] = 0u;  // beyond the new nominal degree dd - 3
+      D[MAXD - 1] = 0u;
+      D[MAXD] = 0u;
+      *skip = 1;
+      int dr = dv - 1;
+      while (dr >= 0 && red4(D[0], p) == 0u) {
+        shift_up<MAXD>(D);
+        --dr;
+      }
+      return dr;
+    }
+  }
   for (int s = 0; s <= dd - dv; ++s) {
     if (__all_sync(__activemask(), red4(D[0], P.p) == 0u)) {
       shift_up<MAXD>(D);
