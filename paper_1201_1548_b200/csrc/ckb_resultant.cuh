@@ -363,8 +363,13 @@ __device__ __forceinline__ uint32_t resultant_anydeg(uint32_t (&A)[MAXD + 1], in
       const int dr = prem_any<MAXD>(A, B, da, db, lb, lbc, P, &skip);
       if (dr < 0) return 0u;  // a common factor
       neg ^= (bool)(da & db & 1);
-      num = mmul(num, mpow(lbm, da - dr, one, P), P);
-      den = mmul(den, mpow(lbm, (e - skip) * db, one, P), P);
+      {  // lb^(da - dr) / lb^((e - skip) db): one power, into num or den by the exponent's sign
+        const int x = (da - dr) - (e - skip) * db;
+        if (x >= 0)
+          num = mmul(num, mpow(lbm, x, one, P), P);
+        else
+          den = mmul(den, mpow(lbm, -x, one, P), P);
+      }
       da = dr;
       if (da == 0) {  // res(B, c) = c^db
         num = mmul(num, mpow(to_mont(red4(A[0], p), P), db, one, P), P);
@@ -380,8 +385,13 @@ __device__ __forceinline__ uint32_t resultant_anydeg(uint32_t (&A)[MAXD + 1], in
       const int dr = prem_any<MAXD>(B, A, db, da, lb, lbc, P, &skip);
       if (dr < 0) return 0u;
       neg ^= (bool)(da & db & 1);
-      num = mmul(num, mpow(lbm, db - dr, one, P), P);
-      den = mmul(den, mpow(lbm, (e - skip) * da, one, P), P);
+      {
+        const int x = (db - dr) - (e - skip) * da;
+        if (x >= 0)
+          num = mmul(num, mpow(lbm, x, one, P), P);
+        else
+          den = mmul(den, mpow(lbm, -x, one, P), P);
+      }
       db = dr;
       if (db == 0) {
         num = mmul(num, mpow(to_mont(red4(B[0], p), P), da, one, P), P);
